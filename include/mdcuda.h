@@ -1,0 +1,144 @@
+/*
+ * mdcuda.h -- C ABI of the B200 (sm_100a) Wiener + RRRL deconvolution library.
+ *
+ * Drop-in boundary for the hot path of the reference package `motiondeblur`
+ * (arXiv:1212.2245). The reference has no FFI: its boundary is the Python API
+ * (`motiondeblur/__init__.py:7-62`) plus the duck-typed convolver protocol
+ * `blur / adjoint / adjoint_pair` (`deconv.py:295-376`). Every entry point below replaces
+ * one of those calls; the Python mirror in `paper_1212_2245_b200/` binds them with ctypes
+ * (see INTEGRATION.md). Signatures carry plain pointers, sizes and scalars only.
+ *
+ * Conventions
+ *   - Images are batches of frames, `[batch, height, width]`, row-major, contiguous,
+ *     in the plan's dtype (MD_F64: double, MD_F32: float), resident in DEVICE memory
+ *     unless the function name ends in `_host`.
+ *   - `stream` is a `cudaStream_t` passed as `void*` (NULL = legacy default stream).
+ *   - Every function returns MD_OK (0) or a negative MD_E* status; `md_last_error()`
+ *     returns a thread-local message for the last failure. MD_EINVAL maps to Python
+ *     ValueError, MD_ECONTRACT to ContractError (core.py:39-40), MD_ECUDA to RuntimeError.
+ */
+#ifndef MDCUDA_H
+#define MDCUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MDCUDA_ABI_VERSION 1
+
+/* status codes */
+#define MD_OK 0
+#define MD_EINVAL (-1)     /* bad parameter / shape / unsupported size   -> ValueError    */
+#define MD_ECONTRACT (-2)  /* non-positive data where positivity required -> ContractError */
+#define MD_ECUDA (-3)      /* CUDA runtime failure                          -> RuntimeError  */
+#define MD_ENOMEM (-4)     /* device allocation failed                      -> MemoryError   */
+
+/* arithmetic type */
+#define MD_F64 0
+#define MD_F32 1
+
+/* PSF kinds (core.py:83-86) */
+#define MD_PSF_GENERAL_2D 0
+#define MD_PSF_GENERAL_1D 1
+#define MD_PSF_BOX_1D 2
+
+/* blur axis of 1D kinds (core.py:89-93) */
+#define MD_AXIS_NONE (-1)
+#define MD_AXIS_VERTICAL 0
+#define MD_AXIS_HORIZONTAL 1
+
+/* convolver realisation used inside the iterations (deconv.py:295-403, 566-579) */
+#define MD_CONV_BOX 0        /* clamped sliding-window box   (_BoxConvolver, Scenario.BOX_1D)   */
+#define MD_CONV_SPATIAL 1    /* clamped direct summation     (_SpatialConvolver)                */
+#define MD_CONV_FOURIER 2    /* periodic along the blur axis (_FourierConvolver1D, FOURIER_1D)  */
+#define MD_CONV_FOURIER2D 3  /* periodic 2D                  (_FourierConvolver2D, FOURIER_2D)  */
+
+/* how the iterate is initialised */
+#define MD_INIT_WIENER 0     /* DeblurPipeline.run_timed: u0 = max(Wiener(f), floor) (deconv.py:653-672) */
+#define MD_INIT_CLAMPED 1    /* rrrl_deblur / rl_deblur:  u0 = max(f, floor)         (deconv.py:524-559) */
+
+/* flags */
+#define MD_FLAG_RL 1u            /* identity penaliser and alpha = 0: plain RL (rl_deblur)        */
+#define MD_FLAG_NO_FUSED 2u      /* force the multi-kernel path even where a fused kernel applies */
+#define MD_FLAG_FORCE_FFT2D 4u   /* 2D periodic convolver through 2D FFTs, not direct taps        */
+
+typedef struct md_plan md_plan; /* opaque */
+
+/* Problem description -- mirrors DeblurPipeline(shape, psf, params, scenario)
+ * (deconv.py:611-643) and make_convolver(psf, shape, mode) (deconv.py:379-403). */
+typedef struct md_plan_desc {
+    int32_t height, width;        /* frame shape (rows, cols)                                     */
+    int32_t dtype;                /* MD_F64 | MD_F32                                               */
+    int32_t psf_kind;             /* MD_PSF_*                                                      */
+    int32_t psf_axis;             /* MD_AXIS_* (1D kinds)                                          */
+    int32_t psf_rows, psf_cols;   /* weight array shape; 1D kinds: rows = taps, cols = 1           */
+    int32_t center_row, center_col; /* 2D: (cy, cx); 1D kinds: center_row = centre index          */
+    double box_length;            /* MD_PSF_BOX_1D only (Psf.length)                               */
+    const double *psf_weights;    /* HOST pointer, psf_rows*psf_cols normalised weights            */
+    int32_t conv;                 /* MD_CONV_*                                                     */
+    int32_t init;                 /* MD_INIT_*                                                     */
+    int32_t iterations;           /* DeconvParams.iterations                                       */
+    uint32_t flags;               /* MD_FLAG_*                                                     */
+    double wiener_k, alpha, eps_data, eps_reg, floor; /* DeconvParams (core.py:242-247)            */
+} md_plan_desc;
+
+/* library */
+int32_t md_abi_version(void);
+const char *md_last_error(void);
+int32_t md_device_sm_count(void);
+
+/* plans (DeblurPipeline.__init__, deconv.py:611-643; make_convolver, deconv.py:379-403) */
+int32_t md_plan_create(const md_plan_desc *desc, md_plan **out);
+int32_t md_plan_destroy(md_plan *plan);
+/* scratch bytes a run over `batch` frames needs (allocated lazily, owned by the plan) */
+int64_t md_plan_scratch_bytes(const md_plan *plan, int64_t batch);
+/* human-readable description of the kernels the plan launches (for logs / DESIGN.md) */
+const char *md_plan_describe(const md_plan *plan);
+/* frames per internal chunk (0 = automatic, bounded by ~1 GiB of scratch) */
+int32_t md_plan_set_chunk(md_plan *plan, int64_t frames);
+/* enable / disable the fused persistent kernel where the plan supports it */
+int32_t md_plan_set_fused(md_plan *plan, int32_t on);
+int32_t md_plan_is_fused(const md_plan *plan);
+
+/* the pipeline: Wiener (or clamp) init + iterations (DeblurPipeline.run, deconv.py:653-693;
+ * rrrl_deblur deconv.py:537-559; rl_deblur deconv.py:524-534). f and u are device arrays. */
+int32_t md_run(md_plan *plan, const void *f, void *u, int64_t batch, void *stream);
+/* same, but f/u are HOST float64 arrays; H2D, dtype conversion, run, D2H all inside.
+ * Copies are chunked through the plan's pinned staging buffers. */
+int32_t md_run_host(md_plan *plan, const double *f, double *u, int64_t batch, void *stream);
+/* md_run with CUDA events between launch groups on `stream`; synchronises. ms_out[4]:
+ * [0] init (Wiener or clamp) ms, [1] RRRL iteration kernels ms, [2] layout transposes ms,
+ * [3] number of launch groups timed. */
+int32_t md_run_profile(md_plan *plan, const void *f, void *u, int64_t batch, void *stream,
+                       double *ms_out);
+/* number of kernel launches md_run issues for one call (for the bench's gpu_launches) */
+int32_t md_run_launch_count(const md_plan *plan, int64_t batch);
+
+/* Wiener filter only, unclamped (wiener_1d deconv.py:275-288 / wiener_2d deconv.py:257-272) */
+int32_t md_wiener(md_plan *plan, const void *f, void *out, int64_t batch, void *stream);
+
+/* convolver protocol (deconv.py:295-376): which = 0 blur, 1 adjoint */
+int32_t md_convolve(md_plan *plan, const void *in, void *out, int64_t batch, int32_t which,
+                    void *stream);
+int32_t md_adjoint_pair(md_plan *plan, const void *p, const void *q, void *out_p, void *out_q,
+                        int64_t batch, void *stream);
+
+/* step-level operations (deconv.py:142-229, 415-446). n = element count / frame shape. */
+int32_t md_robust_weight(int32_t dtype, const void *f, const void *b, void *out, int64_t n,
+                         double eps_data, double floor, int32_t assume_floored, void *stream);
+int32_t md_diffusion(int32_t dtype, const void *u, void *out, int64_t batch, int32_t height,
+                     int32_t width, double eps_reg, void *stream);
+/* u' = u*num/den assembled from blurred b, optional weight w and diffusion d (_combine) */
+int32_t md_rrrl_step(md_plan *plan, const void *u, const void *f, const void *b, const void *w,
+                     const void *d, void *out, int64_t batch, double alpha, void *stream);
+/* x = max(x, 1e-12) in place (_blur_guarded, deconv.py:415-418) */
+int32_t md_guard(int32_t dtype, void *x, int64_t n, void *stream);
+/* min over n elements, written to *out_host (positivity contracts, deconv.py:410-412) */
+int32_t md_min(int32_t dtype, const void *x, int64_t n, double *out_host, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MDCUDA_H */

@@ -1,0 +1,937 @@
+// md_capi.cu -- the C ABI (include/mdcuda.h): plans, constant tables and kernel dispatch.
+//
+// A plan is the B200 counterpart of DeblurPipeline.__init__ (deconv.py:611-643) and
+// make_convolver (deconv.py:379-403): it validates the problem, picks the kernel path,
+// uploads the PSF taps, builds the twiddle tables, the divergence table (deconv.py:101-112)
+// and the Wiener multiplier conj(h)/(|h|^2+K) (deconv.py:253-254) ON THE DEVICE, and owns
+// the scratch fields. md_run is DeblurPipeline.run (deconv.py:653-693) for a batch.
+//
+// Kernel paths
+//   LINES        1D PSFs (box or general, any convolver mode): k_wiener_lines + one
+//                k_iter_lines launch per iteration (md_lines.cu).
+//   PLANE_DIRECT 2D PSFs with a modest tap count: 2D-FFT Wiener + two direct-tap stage
+//                kernels per iteration (md_plane.cu), periodic or clamped.
+//   PLANE_FFT    2D PSFs with many taps: 2D-FFT Wiener + 4 fused FFT passes per iteration
+//                (md_fft2d.cu).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/mdcuda.h"
+#include "md_fused.h"
+#include "md_plane.h"
+
+using namespace md;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CU(expr)                                                                                   \
+    do {                                                                                           \
+        cudaError_t _e = (expr);                                                                   \
+        if (_e != cudaSuccess) return fail(MD_ECUDA, std::string(#expr ": ") + cudaGetErrorString(_e)); \
+    } while (0)
+
+bool is_pow2(int n) { return n >= 1 && (n & (n - 1)) == 0; }
+int ilog2(int n) { int l = 0; while ((1 << l) < n) ++l; return l; }
+
+enum Path { PATH_LINES = 0, PATH_PLANE_DIRECT = 1, PATH_PLANE_FFT = 2 };
+
+// optional per-launch-group CUDA events (md_run_profile): kind 0 = init (Wiener / clamp),
+// 1 = RRRL iterations, 2 = layout (transposes)
+enum { PK_INIT = 0, PK_ITER = 1, PK_LAYOUT = 2, PK_KINDS = 3 };
+struct Prof {
+    static constexpr int kMax = 4096;
+    cudaEvent_t ev[kMax + 1];
+    int kind[kMax + 1];
+    int n = 0;
+};
+thread_local Prof *g_prof = nullptr;
+inline void prof_mark(cudaStream_t st, int kind) {
+    if (!g_prof || g_prof->n >= Prof::kMax) return;
+    cudaEventRecord(g_prof->ev[g_prof->n + 1], st);
+    g_prof->kind[g_prof->n + 1] = kind;
+    ++g_prof->n;
+}
+
+// ---------------------------------------------------------------- plan-time kernels
+__global__ void k_build_lut(double *t64, float *t32) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kLutCount; i += gridDim.x * blockDim.x) {
+        const double x = kLutDelta + (1.0 / kLutInvStep) * (double)i;   // deconv.py:106-108
+        const double v = x - 1.0 - log(x);
+        t64[i] = v;
+        t32[i] = (float)v;
+    }
+}
+
+__global__ void k_build_twiddles(double2 *t64, float2 *t32, int n) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n / 2; k += gridDim.x * blockDim.x) {
+        double s, c;
+        sincospi(-2.0 * (double)k / (double)n, &s, &c);
+        t64[k] = make_double2(c, s);
+        t32[k] = make_float2((float)c, (float)s);
+    }
+}
+
+// mult = conj(h) / (|h|^2 + K) (or h itself when K < 0), converted to the plan dtype
+__global__ void k_make_filter(const double2 *h, int64_t count, double K, double2 *o64, float2 *o32) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+        const double2 v = h[i];
+        double2 r;
+        if (K >= 0.0) {
+            const double den = v.x * v.x + v.y * v.y + K;
+            r = make_double2(v.x / den, -v.y / den);
+        } else {
+            r = v;
+        }
+        if (o64) o64[i] = r;
+        if (o32) o32[i] = make_float2((float)r.x, (float)r.y);
+    }
+}
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+    void release() { if (p) cudaFree(p); p = nullptr; bytes = 0; }
+    int ensure(size_t b) {
+        if (b <= bytes) return MD_OK;
+        release();
+        if (cudaMalloc(&p, b) != cudaSuccess) { cudaGetLastError(); return fail(MD_ENOMEM, "device allocation failed"); }
+        bytes = b;
+        return MD_OK;
+    }
+};
+
+}  // namespace
+
+struct md_plan {
+    md_plan_desc d{};
+    std::vector<double> w;
+    int es = 8;                 // element size
+    int path = PATH_LINES;
+    bool robust = true, has_d = true;
+    // lines
+    int vert = 0, n = 0, m = 0, log2n = -1;
+    LineConv lblur{}, ladj{};
+    double *d_taps_blur = nullptr, *d_taps_adj = nullptr;
+    // plane
+    PlaneHalo hblur{}, hadj{};
+    PlaneTap *d_ptaps_blur = nullptr, *d_ptaps_adj = nullptr;
+    int periodic = 0;
+    // FFT tables (dtype copies; fp64 masters are temporaries)
+    void *d_tw_n = nullptr, *d_tw_H = nullptr, *d_tw_W = nullptr;
+    void *d_mult = nullptr;     // Wiener multiplier (lines: [n]; plane: [H][W] storage coords)
+    void *d_hspec = nullptr;    // PSF spectrum (PLANE_FFT iterations)
+    // LUT
+    double *d_lut64 = nullptr;
+    float *d_lut32 = nullptr;
+    LutView lut{};
+    // scratch / staging
+    DevBuf scratch, stage, partial;
+    void *h_pin = nullptr;
+    size_t h_pin_bytes = 0;
+    int64_t chunk = 0;          // frames per internal chunk (0 = auto)
+    bool fused = false;         // whole-iteration-loop fused kernel applies
+    std::string describe;
+
+    int64_t frame_elems() const { return (int64_t)d.height * d.width; }
+    ~md_plan() {
+        for (void *p : {(void *)d_taps_blur, (void *)d_taps_adj, (void *)d_ptaps_blur, (void *)d_ptaps_adj, d_tw_n,
+                        d_tw_H, d_tw_W, d_mult, d_hspec, (void *)d_lut64, (void *)d_lut32})
+            if (p) cudaFree(p);
+        scratch.release();
+        stage.release();
+        partial.release();
+        if (h_pin) cudaFreeHost(h_pin);
+    }
+};
+
+namespace {
+
+template <typename X>
+int upload(X **dst, const X *src, size_t count) {
+    CU(cudaMalloc(dst, std::max<size_t>(count, 1) * sizeof(X)));
+    if (count) CU(cudaMemcpy(*dst, src, count * sizeof(X), cudaMemcpyHostToDevice));
+    return MD_OK;
+}
+
+int build_twiddles(int n, int dtype, void **out) {
+    if (n < 2) { CU(cudaMalloc(out, 16)); return MD_OK; }
+    double2 *t64 = nullptr;
+    float2 *t32 = nullptr;
+    CU(cudaMalloc(&t64, (n / 2) * sizeof(double2)));
+    CU(cudaMalloc(&t32, (n / 2) * sizeof(float2)));
+    k_build_twiddles<<<(n / 2 + 255) / 256, 256>>>(t64, t32, n);
+    CU(cudaGetLastError());
+    CU(cudaDeviceSynchronize());
+    if (dtype == MD_F64) { cudaFree(t32); *out = t64; }
+    else { cudaFree(t64); *out = t32; }
+    return MD_OK;
+}
+
+// spectrum of a real H x W array (natural layout) in storage coordinates, fp64;
+// for H == 1 this is one row transform (1D spectra)
+int spectrum_f64(const std::vector<double> &emb, int H, int W, double2 **out) {
+    void *twH = nullptr, *twW = nullptr;
+    int rc = build_twiddles(W, MD_F64, &twW);
+    if (rc) return rc;
+    rc = build_twiddles(H, MD_F64, &twH);
+    if (rc) return rc;
+    double *d_emb = nullptr;
+    rc = upload(&d_emb, emb.data(), emb.size());
+    if (rc) return rc;
+    double2 *z = nullptr;
+    CU(cudaMalloc(&z, (size_t)H * W * sizeof(double2)));
+    Fft2Args a{};
+    a.H = H; a.W = W; a.log2H = ilog2(H); a.log2W = ilog2(W);
+    a.twH = twH; a.twW = twW;
+    a.load = R_LOAD_REAL; a.ra = d_emb; a.z = z; a.epi = R_EPI_NONE; a.fwd_after = 1;
+    CU(launch_fft2_rows<double>(a, 1, 0));
+    if (H > 1) {
+        a.filt = nullptr; a.col_inv = 0;
+        CU(launch_fft2_cols<double>(a, 1, 0));
+    }
+    CU(cudaDeviceSynchronize());
+    cudaFree(d_emb); cudaFree(twH); cudaFree(twW);
+    *out = z;
+    return MD_OK;
+}
+
+int make_filter(const double2 *h64, int64_t count, double K, int dtype, void **out) {
+    void *o = nullptr;
+    CU(cudaMalloc(&o, count * (dtype == MD_F64 ? sizeof(double2) : sizeof(float2))));
+    k_make_filter<<<(int)std::min<int64_t>((count + 255) / 256, 4096), 256>>>(
+        h64, count, K, dtype == MD_F64 ? (double2 *)o : nullptr, dtype == MD_F32 ? (float2 *)o : nullptr);
+    CU(cudaGetLastError());
+    CU(cudaDeviceSynchronize());
+    *out = o;
+    return MD_OK;
+}
+
+// PSF taps for the direct 2D path: blur reads u[y + cy - jy, x + cx - jx]; the adjoint
+// (reflected kernel, core.py:204-220) reads u[y - cy + jy, x - cx + jx].
+void plane_taps(const md_plan &P, bool adjoint, std::vector<PlaneTap> &taps, PlaneHalo &h) {
+    const int sy = P.d.psf_rows, sx = P.d.psf_cols, cy = P.d.center_row, cx = P.d.center_col;
+    taps.clear();
+    int dymin = 0, dymax = 0, dxmin = 0, dxmax = 0;
+    for (int i = 0; i < sy; ++i) {
+        const int jy = adjoint ? sy - 1 - i : i;
+        for (int jx0 = 0; jx0 < sx; ++jx0) {
+            const int jx = adjoint ? sx - 1 - jx0 : jx0;
+            const double w = P.w[(size_t)jy * sx + jx];
+            if (w == 0.0) continue;
+            PlaneTap t;
+            t.dy = adjoint ? jy - cy : cy - jy;
+            t.dx = adjoint ? jx - cx : cx - jx;
+            t.w = w;
+            taps.push_back(t);
+            dymin = std::min(dymin, t.dy); dymax = std::max(dymax, t.dy);
+            dxmin = std::min(dxmin, t.dx); dxmax = std::max(dxmax, t.dx);
+        }
+    }
+    h.nt = (int)taps.size();
+    h.ht = -dymin; h.hb = dymax; h.hl = -dxmin; h.hr = dxmax;
+}
+
+// 1D convolution descriptor for one direction (conv.py:141-173, deconv.py:310-326)
+LineConv line_conv(const md_plan &P, bool adjoint, bool box, int periodic) {
+    LineConv c{};
+    const int T = P.d.psf_rows;
+    const int center = adjoint ? T - 1 - P.d.center_row : P.d.center_row;
+    c.periodic = periodic;
+    c.ntaps = T;
+    c.center = center;
+    if (box) {
+        const double L = P.d.box_length;
+        const int whole = (int)std::floor(L);
+        const bool frac = L != (double)whole;
+        c.kind = LINE_BOX;
+        c.wi = 1.0 / (frac ? L : (double)whole);
+        // the 1/L factor: integer L multiplies by (1.0 / whole), fractional by (1.0 / length)
+        if (frac) {
+            c.lo = center - T + 2; c.hi = center - 1;
+            c.ends = 1; c.elo = center - T + 1; c.ehi = center;
+            c.we = (L - whole) / (2.0 * L);
+        } else {
+            c.lo = center - T + 1; c.hi = center;
+        }
+        c.ntaps = 0;   // no tap table needed
+    } else {
+        c.kind = LINE_TAPS;
+    }
+    return c;
+}
+
+int validate(const md_plan_desc *d) {
+    if (d->height < 1 || d->width < 1) return fail(MD_EINVAL, "image must be a non-empty 2D grid");
+    if (d->dtype != MD_F64 && d->dtype != MD_F32) return fail(MD_EINVAL, "dtype must be MD_F64 or MD_F32");
+    if (d->psf_kind < 0 || d->psf_kind > 2) return fail(MD_EINVAL, "unknown PSF kind");
+    if (d->psf_rows < 1 || d->psf_cols < 1 || !d->psf_weights) return fail(MD_EINVAL, "PSF weights missing");
+    if (d->psf_kind != MD_PSF_GENERAL_2D && d->psf_cols != 1) return fail(MD_EINVAL, "1D PSF weights must be a vector");
+    if (d->psf_kind != MD_PSF_GENERAL_2D && d->psf_axis != MD_AXIS_VERTICAL && d->psf_axis != MD_AXIS_HORIZONTAL)
+        return fail(MD_EINVAL, "1D PSF kinds need a blur axis");
+    if (!(d->wiener_k > 0.0)) return fail(MD_EINVAL, "wiener_k must be positive");
+    if (d->alpha < 0.0) return fail(MD_EINVAL, "alpha must be non-negative");
+    if (d->iterations < 0) return fail(MD_EINVAL, "iterations must be a non-negative integer");
+    if (!(d->eps_data > 0.0 && d->eps_reg > 0.0 && d->floor > 0.0))
+        return fail(MD_EINVAL, "eps_data, eps_reg and floor must be positive");
+    if (d->conv < MD_CONV_BOX || d->conv > MD_CONV_FOURIER2D) return fail(MD_EINVAL, "unknown convolver mode");
+    return MD_OK;
+}
+
+}  // namespace
+
+// ======================================================================== C ABI
+extern "C" {
+
+int32_t md_abi_version(void) { return MDCUDA_ABI_VERSION; }
+const char *md_last_error(void) { return g_err.c_str(); }
+
+int32_t md_device_sm_count(void) {
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+}
+
+int32_t md_plan_create(const md_plan_desc *desc, md_plan **out) {
+    if (!desc || !out) return fail(MD_EINVAL, "null argument");
+    *out = nullptr;
+    int rc = validate(desc);
+    if (rc) return rc;
+    md_plan *P = new md_plan();
+    P->d = *desc;
+    P->w.assign(desc->psf_weights, desc->psf_weights + (size_t)desc->psf_rows * desc->psf_cols);
+    P->d.psf_weights = nullptr;
+    P->es = desc->dtype == MD_F64 ? 8 : 4;
+    P->robust = !(desc->flags & MD_FLAG_RL);
+    P->has_d = !(desc->flags & MD_FLAG_RL) && desc->alpha > 0.0;
+    const int H = desc->height, W = desc->width;
+    const bool wiener = desc->init == MD_INIT_WIENER;
+    auto bail = [&](int code) { delete P; return code; };
+    char buf[512];
+
+    if (desc->psf_kind != MD_PSF_GENERAL_2D) {
+        // ---------------------------------------------------------------- LINES
+        P->path = PATH_LINES;
+        P->vert = desc->psf_axis == MD_AXIS_VERTICAL;
+        P->n = P->vert ? H : W;
+        P->m = P->vert ? W : H;
+        const int T = desc->psf_rows;
+        if (T > P->n) return bail(fail(MD_EINVAL, "PSF support exceeds the image dimensions"));
+        const bool isbox = desc->psf_kind == MD_PSF_BOX_1D;
+        if (desc->conv == MD_CONV_BOX && !isbox) return bail(fail(MD_EINVAL, "box convolver requires a uniform-box PSF"));
+        const int periodic = (desc->conv == MD_CONV_FOURIER || desc->conv == MD_CONV_FOURIER2D) ? 1 : 0;
+        if (periodic) {
+            const bool ok = desc->conv == MD_CONV_FOURIER ? is_pow2(P->n) : (is_pow2(H) && is_pow2(W));
+            if (!ok) return bail(fail(MD_EINVAL, "transform length must be a power of two"));
+        }
+        if (wiener && !is_pow2(P->n)) return bail(fail(MD_EINVAL, "the blur axis must have power-of-two extent"));
+        const bool use_box = isbox;   // box taps realised as a sliding window in every mode
+        P->lblur = line_conv(*P, false, use_box, periodic);
+        P->ladj = line_conv(*P, true, use_box, periodic);
+        if (!use_box) {
+            std::vector<double> rev(P->w.rbegin(), P->w.rend());
+            if ((rc = upload(&P->d_taps_blur, P->w.data(), P->w.size()))) return bail(rc);
+            if ((rc = upload(&P->d_taps_adj, rev.data(), rev.size()))) return bail(rc);
+        }
+        if (is_pow2(P->n)) {
+            P->log2n = ilog2(P->n);
+            if ((rc = build_twiddles(P->n, desc->dtype, &P->d_tw_n))) return bail(rc);
+            std::vector<double> emb(P->n, 0.0);       // fft.py:192-201
+            for (int j = 0; j < T; ++j) emb[((j - desc->center_row) % P->n + P->n) % P->n] = P->w[j];
+            double2 *h64 = nullptr;
+            if ((rc = spectrum_f64(emb, 1, P->n, &h64))) return bail(rc);
+            rc = make_filter(h64, P->n, desc->wiener_k, desc->dtype, &P->d_mult);
+            cudaFree(h64);
+            if (rc) return bail(rc);
+        }
+        const size_t lim = desc->dtype == MD_F64 ? 4096 : 8192;
+        if (wiener && (size_t)P->n > lim) return bail(fail(MD_EINVAL, "blur-axis length above the on-chip FFT limit"));
+        P->fused = fused_lines_supported(desc->dtype, P->n, P->m, desc->flags);
+        snprintf(buf, sizeof buf, "lines: n=%d m=%d %s %s %s, %s", P->n, P->m, P->vert ? "vertical" : "horizontal",
+                 use_box ? "box-sliding" : "taps", periodic ? "periodic" : "clamped",
+                 P->fused ? "fused persistent iteration kernel" : "k_wiener_lines + k_iter_lines per iteration");
+    } else {
+        // ---------------------------------------------------------------- PLANE
+        if (desc->psf_rows > H || desc->psf_cols > W) return bail(fail(MD_EINVAL, "PSF support exceeds the image dimensions"));
+        if (desc->conv == MD_CONV_BOX) return bail(fail(MD_EINVAL, "box convolver requires a uniform-box PSF"));
+        if (!(desc->center_row >= 0 && desc->center_row < desc->psf_rows && desc->center_col >= 0 &&
+              desc->center_col < desc->psf_cols))
+            return bail(fail(MD_EINVAL, "PSF center must lie inside the support"));
+        P->periodic = desc->conv != MD_CONV_SPATIAL;
+        const bool pow2 = is_pow2(H) && is_pow2(W);
+        if ((P->periodic || wiener) && !pow2)
+            return bail(fail(MD_EINVAL, "2D Fourier convolution needs power-of-two dimensions"));
+        std::vector<PlaneTap> tb, ta;
+        plane_taps(*P, false, tb, P->hblur);
+        plane_taps(*P, true, ta, P->hadj);
+        const int maxh = std::max(std::max(P->hadj.ht, P->hadj.hb), std::max(P->hadj.hl, P->hadj.hr));
+        const bool direct_ok = maxh <= 40;
+        bool use_fft = P->periodic && ((desc->flags & MD_FLAG_FORCE_FFT2D) || P->hblur.nt > 96 || !direct_ok);
+        if (!P->periodic && !direct_ok) return bail(fail(MD_EINVAL, "PSF too large for the direct clamped path"));
+        if (pow2 && (use_fft || wiener) && std::max(H, W) > (desc->dtype == MD_F64 ? 4096 : 8192))
+            return bail(fail(MD_EINVAL, "image side above the on-chip 2D FFT limit"));
+        P->path = use_fft ? PATH_PLANE_FFT : PATH_PLANE_DIRECT;
+        if ((rc = upload(&P->d_ptaps_blur, tb.data(), tb.size()))) return bail(rc);
+        if ((rc = upload(&P->d_ptaps_adj, ta.data(), ta.size()))) return bail(rc);
+        if (pow2) {
+            if ((rc = build_twiddles(H, desc->dtype, &P->d_tw_H))) return bail(rc);
+            if ((rc = build_twiddles(W, desc->dtype, &P->d_tw_W))) return bail(rc);
+            std::vector<double> emb((size_t)H * W, 0.0);       // fft.py:204-221
+            for (int jy = 0; jy < desc->psf_rows; ++jy)
+                for (int jx = 0; jx < desc->psf_cols; ++jx) {
+                    const int y = ((jy - desc->center_row) % H + H) % H;
+                    const int x = ((jx - desc->center_col) % W + W) % W;
+                    emb[(size_t)y * W + x] = P->w[(size_t)jy * desc->psf_cols + jx];
+                }
+            double2 *h64 = nullptr;
+            if ((rc = spectrum_f64(emb, H, W, &h64))) return bail(rc);
+            rc = make_filter(h64, (int64_t)H * W, desc->wiener_k, desc->dtype, &P->d_mult);
+            if (!rc && use_fft) rc = make_filter(h64, (int64_t)H * W, -1.0, desc->dtype, &P->d_hspec);
+            cudaFree(h64);
+            if (rc) return bail(rc);
+        }
+        snprintf(buf, sizeof buf, "plane: %dx%d %s, %d taps (halo %d/%d/%d/%d), %s", H, W,
+                 P->periodic ? "periodic" : "clamped", P->hblur.nt, P->hblur.ht, P->hblur.hb, P->hblur.hl,
+                 P->hblur.hr, use_fft ? "2D FFT convolver (4 launches/iteration)" : "direct taps (2 launches/iteration)");
+    }
+    P->describe = buf;
+    // divergence table (deconv.py:101-112, 137-139)
+    CU(cudaMalloc(&P->d_lut64, kLutCount * sizeof(double)));
+    CU(cudaMalloc(&P->d_lut32, kLutCount * sizeof(float)));
+    k_build_lut<<<(kLutCount + 255) / 256, 256>>>(P->d_lut64, P->d_lut32);
+    CU(cudaGetLastError());
+    CU(cudaDeviceSynchronize());
+    P->lut.t64 = P->d_lut64;
+    P->lut.t32 = P->d_lut32;
+    P->lut.slope = 1.0 - 1.0 / kLutUpper;
+    P->lut.intercept = (kLutUpper - 1.0 - std::log(kLutUpper)) - P->lut.slope * kLutUpper;
+    *out = P;
+    return MD_OK;
+}
+
+int32_t md_plan_destroy(md_plan *plan) {
+    delete plan;
+    return MD_OK;
+}
+
+const char *md_plan_describe(const md_plan *plan) { return plan ? plan->describe.c_str() : ""; }
+
+}  // extern "C"
+
+// ======================================================================== execution
+namespace {
+
+// scratch fields per frame (in elements of the plan dtype)
+int scratch_fields(const md_plan &P) {
+    switch (P.path) {
+        case PATH_LINES: return 3;          // fpos, A, B
+        case PATH_PLANE_DIRECT: return 5;   // fpos, A, B, p, W
+        default: return 5;                  // fpos, A, B, z (complex = 2)
+    }
+}
+
+int64_t auto_chunk(const md_plan &P, int64_t batch) {
+    if (P.chunk > 0) return std::min(P.chunk, batch);
+    // keep one chunk's scratch within ~1 GiB
+    const int64_t per = (int64_t)scratch_fields(P) * P.frame_elems() * P.es;
+    int64_t c = std::max<int64_t>(1, (1ll << 30) / std::max<int64_t>(per, 1));
+    return std::min(c, batch);
+}
+
+template <typename T>
+int run_lines(md_plan &P, const void *f, void *u, int64_t nb, char *scr, cudaStream_t st) {
+    const int64_t fb = P.frame_elems() * (int64_t)sizeof(T) * nb;
+    void *FP = scr, *A = scr + fb, *B = scr + 2 * fb;
+    const int K = P.d.iterations;
+    const bool wiener = P.d.init == MD_INIT_WIENER;
+    if (wiener) {
+        WienerLinesArgs a{};
+        a.in = f; a.n = P.n; a.log2n = P.log2n; a.m = P.m; a.in_vert = P.vert;
+        a.mult = P.d_mult; a.tw = P.d_tw_n; a.floor = P.d.floor; a.clamp = 1;
+        if (K == 0) { a.out = u; a.out_vert = P.vert; a.fpos = nullptr; }
+        else { a.out = A; a.out_vert = 0; a.fpos = FP; }
+        CU(launch_wiener_lines<T>(a, nb, st));
+        prof_mark(st, PK_INIT);
+        if (K == 0) return MD_OK;
+    } else {
+        if (K == 0) { CU(launch_clamp2<T>(f, u, nullptr, P.frame_elems() * nb, P.d.floor, st)); return MD_OK; }
+        if (P.vert) {
+            // native [n rows][m cols] -> line-major [m][n]
+            CU(launch_transpose<T>(f, A, FP, P.n, P.m, P.d.floor, 1, nb, st));
+        } else {
+            CU(launch_clamp2<T>(f, A, FP, P.frame_elems() * nb, P.d.floor, st));
+        }
+        prof_mark(st, PK_INIT);
+    }
+    if (P.fused) {
+        FusedLinesArgs fa{};
+        fa.u_in = A; fa.fpos = FP; fa.u_out = u; fa.n = P.n; fa.m = P.m; fa.iterations = K;
+        fa.out_vert = P.vert; fa.blur = P.lblur; fa.adj = P.ladj;
+        fa.taps_blur = P.d_taps_blur; fa.taps_adj = P.d_taps_adj;
+        fa.alpha = P.d.alpha; fa.eps_d2 = P.d.eps_data * P.d.eps_data; fa.eps_r2 = P.d.eps_reg * P.d.eps_reg;
+        fa.has_d = P.has_d; fa.robust = P.robust; fa.lut = P.lut;
+        CU(launch_fused_lines<T>(fa, nb, st));
+        prof_mark(st, PK_ITER);
+        return MD_OK;
+    }
+    IterLinesArgs it{};
+    it.n = P.n; it.m = P.m; it.blur = P.lblur; it.adj = P.ladj;
+    it.taps_blur = P.d_taps_blur; it.taps_adj = P.d_taps_adj;
+    it.alpha = P.d.alpha; it.eps_d2 = P.d.eps_data * P.d.eps_data; it.eps_r2 = P.d.eps_reg * P.d.eps_reg;
+    it.has_d = P.has_d; it.lut = P.lut; it.fpos = FP;
+    void *cur = A;
+    for (int k = 0; k < K; ++k) {
+        const bool last = k == K - 1;
+        void *dst = (last && !P.vert) ? u : (cur == A ? B : A);
+        it.u_in = cur; it.u_out = dst;
+        CU(launch_iter_lines<T>(it, P.robust, nb, st));
+        prof_mark(st, PK_ITER);
+        cur = dst;
+    }
+    if (P.vert) {
+        CU(launch_transpose<T>(cur, u, nullptr, P.m, P.n, 0.0, 0, nb, st));
+        prof_mark(st, PK_LAYOUT);
+    }
+    return MD_OK;
+}
+
+template <typename T>
+Fft2Args fft2_base(const md_plan &P) {
+    Fft2Args a{};
+    a.H = P.d.height; a.W = P.d.width; a.log2H = ilog2(a.H); a.log2W = ilog2(a.W);
+    a.twH = P.d_tw_H; a.twW = P.d_tw_W;
+    a.lut = P.lut;
+    a.eps_d2 = P.d.eps_data * P.d.eps_data; a.eps_r2 = P.d.eps_reg * P.d.eps_reg;
+    a.alpha = P.d.alpha; a.has_d = P.has_d; a.robust = P.robust;
+    a.scale = 1.0 / ((double)a.H * (double)a.W);
+    return a;
+}
+
+// Wiener 2D: rows fwd -> cols (x M, inv) -> rows inv + epilogue; optionally leaves the
+// row-transformed clamped result in z for the first FFT-path iteration
+template <typename T>
+int wiener_plane(md_plan &P, const void *f, void *out, void *fpos, void *z, bool clamp, bool fwd_after,
+                 int64_t nb, cudaStream_t st) {
+    Fft2Args a = fft2_base<T>(P);
+    a.load = R_LOAD_REAL; a.ra = f; a.rb = nullptr; a.z = z; a.epi = R_EPI_NONE; a.fwd_after = 1;
+    CU(launch_fft2_rows<T>(a, nb, st));
+    a.filt = P.d_mult; a.conj_filt = 0; a.col_inv = 1;
+    CU(launch_fft2_cols<T>(a, nb, st));
+    a.load = R_LOAD_COMPLEX; a.inv = 1; a.epi = R_EPI_WIENER; a.fwd_after = fwd_after;
+    a.oa = out; a.ob = fpos; a.f = f; a.floor = clamp ? P.d.floor : 0.0;
+    CU(launch_fft2_rows<T>(a, nb, st));
+    return MD_OK;
+}
+
+template <typename T>
+int run_plane(md_plan &P, const void *f, void *u, int64_t nb, char *scr, cudaStream_t st) {
+    const int64_t fb = P.frame_elems() * (int64_t)sizeof(T) * nb;
+    void *FP = scr, *A = scr + fb, *B = scr + 2 * fb, *X = scr + 3 * fb, *Y = scr + 4 * fb;
+    const int K = P.d.iterations;
+    const bool wiener = P.d.init == MD_INIT_WIENER;
+    const bool fftp = P.path == PATH_PLANE_FFT;
+    void *z = X;   // complex field spans X and Y
+    if (wiener) {
+        int rc = wiener_plane<T>(P, f, K == 0 ? u : A, K == 0 ? nullptr : FP, z, true, fftp && K > 0, nb, st);
+        prof_mark(st, PK_INIT);
+        if (rc || K == 0) return rc;
+    } else {
+        if (K == 0) { CU(launch_clamp2<T>(f, u, nullptr, P.frame_elems() * nb, P.d.floor, st)); return MD_OK; }
+        CU(launch_clamp2<T>(f, A, FP, P.frame_elems() * nb, P.d.floor, st));
+        if (fftp) {
+            Fft2Args a = fft2_base<T>(P);
+            a.load = R_LOAD_REAL; a.ra = A; a.z = z; a.epi = R_EPI_NONE; a.fwd_after = 1;
+            CU(launch_fft2_rows<T>(a, nb, st));
+        }
+        prof_mark(st, PK_INIT);
+    }
+    void *cur = A;
+    for (int k = 0; k < K; ++k) {
+        const bool last = k == K - 1;
+        void *dst = last ? u : (cur == A ? B : A);
+        if (fftp) {
+            Fft2Args a = fft2_base<T>(P);
+            a.z = z;
+            a.filt = P.d_hspec; a.conj_filt = 0; a.col_inv = 1;
+            CU(launch_fft2_cols<T>(a, nb, st));                       // blur: x h
+            a.load = R_LOAD_COMPLEX; a.inv = 1; a.epi = R_EPI_STAGE_A; a.f = FP; a.fwd_after = 1;
+            CU(launch_fft2_rows<T>(a, nb, st));                       // b -> (p + iW), fwd
+            a.conj_filt = 1;
+            CU(launch_fft2_cols<T>(a, nb, st));                       // adjoint pair: x conj(h)
+            a.epi = R_EPI_STAGE_B; a.u = cur; a.oa = dst; a.fwd_after = !last;
+            CU(launch_fft2_rows<T>(a, nb, st));                       // update, fwd of u'
+        } else {
+            StagePlaneArgs s{};
+            s.u = cur; s.f = FP; s.p = X; s.w = Y; s.u_out = dst;
+            s.H = P.d.height; s.W = P.d.width; s.periodic = P.periodic;
+            s.blur = P.hblur; s.adj = P.hadj; s.blur_taps = P.d_ptaps_blur; s.adj_taps = P.d_ptaps_adj;
+            s.alpha = P.d.alpha; s.eps_d2 = P.d.eps_data * P.d.eps_data; s.eps_r2 = P.d.eps_reg * P.d.eps_reg;
+            s.floor = P.d.floor; s.has_d = P.has_d; s.floor_f = 0; s.general_weight = 0; s.lut = P.lut;
+            CU(launch_stage_plane<T>(s, P.robust, nb, st));
+        }
+        prof_mark(st, PK_ITER);
+        cur = dst;
+    }
+    return MD_OK;
+}
+
+template <typename T>
+int run_typed(md_plan &P, const void *f, void *u, int64_t batch, cudaStream_t st) {
+    const int64_t chunk = auto_chunk(P, batch);
+    const size_t need = (size_t)scratch_fields(P) * P.frame_elems() * sizeof(T) * chunk;
+    int rc = P.scratch.ensure(need);
+    if (rc) return rc;
+    const int64_t fbytes = P.frame_elems() * (int64_t)sizeof(T);
+    for (int64_t b0 = 0; b0 < batch; b0 += chunk) {
+        const int64_t nb = std::min(chunk, batch - b0);
+        const void *fc = static_cast<const char *>(f) + b0 * fbytes;
+        void *uc = static_cast<char *>(u) + b0 * fbytes;
+        rc = P.path == PATH_LINES ? run_lines<T>(P, fc, uc, nb, (char *)P.scratch.p, st)
+                                  : run_plane<T>(P, fc, uc, nb, (char *)P.scratch.p, st);
+        if (rc) return rc;
+    }
+    return MD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t md_plan_scratch_bytes(const md_plan *P, int64_t batch) {
+    if (!P) return 0;
+    return (int64_t)scratch_fields(*P) * P->frame_elems() * P->es * auto_chunk(*P, batch);
+}
+
+int32_t md_plan_set_chunk(md_plan *P, int64_t frames) {
+    if (!P || frames < 0) return fail(MD_EINVAL, "bad chunk");
+    P->chunk = frames;
+    return MD_OK;
+}
+
+int32_t md_plan_set_fused(md_plan *P, int32_t on) {
+    if (!P) return fail(MD_EINVAL, "null plan");
+    if (on && !(P->path == PATH_LINES && fused_lines_supported(P->d.dtype, P->n, P->m, 0)))
+        return fail(MD_EINVAL, "fused kernel not available for this plan");
+    P->fused = on != 0;
+    return MD_OK;
+}
+
+int32_t md_plan_is_fused(const md_plan *P) { return P && P->fused ? 1 : 0; }
+
+int32_t md_run(md_plan *P, const void *f, void *u, int64_t batch, void *stream) {
+    if (!P || !f || !u || batch < 0) return fail(MD_EINVAL, "bad arguments");
+    if (batch == 0) return MD_OK;
+    if (f == u) return fail(MD_EINVAL, "input and output must not alias");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    return P->d.dtype == MD_F64 ? run_typed<double>(*P, f, u, batch, st) : run_typed<float>(*P, f, u, batch, st);
+}
+
+int32_t md_run_profile(md_plan *P, const void *f, void *u, int64_t batch, void *stream, double *ms_out) {
+    if (!P || !ms_out) return fail(MD_EINVAL, "bad arguments");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Prof *pr = new Prof();
+    for (int i = 0; i <= Prof::kMax; ++i) cudaEventCreate(&pr->ev[i]);
+    cudaEventRecord(pr->ev[0], st);
+    g_prof = pr;
+    int rc = md_run(P, f, u, batch, stream);
+    g_prof = nullptr;
+    if (rc == MD_OK) {
+        cudaStreamSynchronize(st);
+        for (int k = 0; k < PK_KINDS; ++k) ms_out[k] = 0.0;
+        for (int i = 1; i <= pr->n; ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, pr->ev[i - 1], pr->ev[i]);
+            ms_out[pr->kind[i]] += ms;
+        }
+        ms_out[PK_KINDS] = (double)pr->n;
+    }
+    for (int i = 0; i <= Prof::kMax; ++i) cudaEventDestroy(pr->ev[i]);
+    delete pr;
+    return rc;
+}
+
+int32_t md_run_launch_count(const md_plan *P, int64_t batch) {
+    if (!P || batch <= 0) return 0;
+    const int64_t chunk = auto_chunk(*P, batch);
+    const int64_t chunks = (batch + chunk - 1) / chunk;
+    const int64_t sub = (chunk + 65534) / 65535;    // grid.y / grid.z splits
+    const int K = P->d.iterations;
+    int per = 0;
+    const bool wiener = P->d.init == MD_INIT_WIENER;
+    if (P->path == PATH_LINES) {
+        per = 1;
+        if (K > 0) per += P->fused ? 1 : K + (P->vert ? 1 : 0);
+    } else {
+        per = wiener ? 3 : 1;
+        if (K > 0) {
+            if (!wiener && P->path == PATH_PLANE_FFT) per += 1;
+            per += K * (P->path == PATH_PLANE_FFT ? 4 : 2);
+        }
+    }
+    return (int32_t)(chunks * sub * per);
+}
+
+int32_t md_run_host(md_plan *P, const double *f, double *u, int64_t batch, void *stream) {
+    if (!P || !f || !u || batch < 0) return fail(MD_EINVAL, "bad arguments");
+    if (batch == 0) return MD_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t fe = P->frame_elems();
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(batch, (256ll << 20) / (fe * 8)));
+    // device staging: f64 in, T in, T out, f64 out
+    const size_t fbT = (size_t)fe * P->es * chunk, fb64 = (size_t)fe * 8 * chunk;
+    int rc = P->stage.ensure(2 * fb64 + 2 * fbT);
+    if (rc) return rc;
+    char *s64in = (char *)P->stage.p, *s64out = s64in + fb64, *sTin = s64out + fb64, *sTout = sTin + fbT;
+    for (int64_t b0 = 0; b0 < batch; b0 += chunk) {
+        const int64_t nb = std::min(chunk, batch - b0);
+        CU(cudaMemcpyAsync(s64in, f + b0 * fe, nb * fe * 8, cudaMemcpyHostToDevice, st));
+        const void *fin = s64in;
+        void *uo = s64out;
+        if (P->d.dtype == MD_F32) {
+            CU(launch_convert<float>(s64in, sTin, nb * fe, 0, st));
+            fin = sTin;
+            uo = sTout;
+        }
+        rc = md_run(P, fin, uo, nb, stream);
+        if (rc) return rc;
+        if (P->d.dtype == MD_F32) CU(launch_convert<float>(sTout, s64out, nb * fe, 1, st));
+        CU(cudaMemcpyAsync(u + b0 * fe, s64out, nb * fe * 8, cudaMemcpyDeviceToHost, st));
+    }
+    CU(cudaStreamSynchronize(st));
+    return MD_OK;
+}
+
+int32_t md_wiener(md_plan *P, const void *f, void *out, int64_t batch, void *stream) {
+    if (!P || !f || !out || batch < 0) return fail(MD_EINVAL, "bad arguments");
+    if (batch == 0) return MD_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (P->path == PATH_LINES) {
+        if (P->log2n < 0) return fail(MD_EINVAL, "the blur axis must have power-of-two extent");
+        WienerLinesArgs a{};
+        a.in = f; a.out = out; a.fpos = nullptr; a.n = P->n; a.log2n = P->log2n; a.m = P->m;
+        a.in_vert = P->vert; a.out_vert = P->vert; a.clamp = 0; a.mult = P->d_mult; a.tw = P->d_tw_n;
+        a.floor = P->d.floor;
+        CU(P->d.dtype == MD_F64 ? launch_wiener_lines<double>(a, batch, st) : launch_wiener_lines<float>(a, batch, st));
+        return MD_OK;
+    }
+    if (!P->d_mult) return fail(MD_EINVAL, "2D Wiener needs power-of-two dimensions");
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(batch, (1ll << 30) / (P->frame_elems() * 2 * P->es)));
+    int rc = P->scratch.ensure((size_t)P->frame_elems() * 2 * P->es * chunk);
+    if (rc) return rc;
+    for (int64_t b0 = 0; b0 < batch; b0 += chunk) {
+        const int64_t nb = std::min(chunk, batch - b0);
+        const int64_t off = b0 * P->frame_elems() * P->es;
+        const void *fc = static_cast<const char *>(f) + off;
+        void *oc = static_cast<char *>(out) + off;
+        rc = P->d.dtype == MD_F64 ? wiener_plane<double>(*P, fc, oc, nullptr, P->scratch.p, false, false, nb, st)
+                                  : wiener_plane<float>(*P, fc, oc, nullptr, P->scratch.p, false, false, nb, st);
+        if (rc) return rc;
+    }
+    return MD_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+template <typename T>
+int convolve_typed(md_plan &P, const void *in, void *out, int64_t batch, int which, cudaStream_t st) {
+    const int64_t fe = P.frame_elems();
+    if (P.path == PATH_LINES) {
+        ConvLinesArgs a{};
+        a.n = P.n; a.m = P.m; a.c = which ? P.ladj : P.lblur;
+        a.taps = which ? P.d_taps_adj : P.d_taps_blur;
+        if (!P.vert) {
+            a.in = in; a.out = out;
+            CU(launch_conv_lines<T>(a, batch, st));
+            return MD_OK;
+        }
+        const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(batch, (1ll << 30) / (fe * 2 * (int64_t)sizeof(T))));
+        int rc = P.scratch.ensure((size_t)fe * 2 * sizeof(T) * chunk);
+        if (rc) return rc;
+        char *A = (char *)P.scratch.p, *B = A + fe * sizeof(T) * chunk;
+        for (int64_t b0 = 0; b0 < batch; b0 += chunk) {
+            const int64_t nb = std::min(chunk, batch - b0);
+            const int64_t off = b0 * fe * sizeof(T);
+            CU(launch_transpose<T>(static_cast<const char *>(in) + off, A, nullptr, P.n, P.m, 0.0, 0, nb, st));
+            a.in = A; a.out = B;
+            CU(launch_conv_lines<T>(a, nb, st));
+            CU(launch_transpose<T>(B, static_cast<char *>(out) + off, nullptr, P.m, P.n, 0.0, 0, nb, st));
+        }
+        return MD_OK;
+    }
+    if (P.path == PATH_PLANE_DIRECT) {
+        ConvPlaneArgs a{};
+        a.in = in; a.out = out; a.H = P.d.height; a.W = P.d.width; a.periodic = P.periodic;
+        a.h = which ? P.hadj : P.hblur;
+        a.taps = which ? P.d_ptaps_adj : P.d_ptaps_blur;
+        CU(launch_conv_plane<T>(a, batch, st));
+        return MD_OK;
+    }
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(batch, (1ll << 30) / (fe * 2 * (int64_t)sizeof(T))));
+    int rc = P.scratch.ensure((size_t)fe * 2 * sizeof(T) * chunk);
+    if (rc) return rc;
+    for (int64_t b0 = 0; b0 < batch; b0 += chunk) {
+        const int64_t nb = std::min(chunk, batch - b0);
+        const int64_t off = b0 * fe * sizeof(T);
+        Fft2Args a = fft2_base<T>(P);
+        a.z = P.scratch.p;
+        a.load = R_LOAD_REAL; a.ra = static_cast<const char *>(in) + off; a.epi = R_EPI_NONE; a.fwd_after = 1;
+        CU(launch_fft2_rows<T>(a, nb, st));
+        a.filt = P.d_hspec; a.conj_filt = which; a.col_inv = 1;
+        CU(launch_fft2_cols<T>(a, nb, st));
+        a.load = R_LOAD_COMPLEX; a.inv = 1; a.epi = R_EPI_STORE_PAIR; a.fwd_after = 0;
+        a.oa = static_cast<char *>(out) + off; a.ob = nullptr;
+        CU(launch_fft2_rows<T>(a, nb, st));
+    }
+    return MD_OK;
+}
+
+template <typename T>
+int adjoint_pair_typed(md_plan &P, const void *p, const void *q, void *op, void *oq, int64_t batch, cudaStream_t st) {
+    if (P.path != PATH_PLANE_FFT) {
+        int rc = convolve_typed<T>(P, p, op, batch, 1, st);
+        if (rc) return rc;
+        return convolve_typed<T>(P, q, oq, batch, 1, st);
+    }
+    const int64_t fe = P.frame_elems();
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(batch, (1ll << 30) / (fe * 2 * (int64_t)sizeof(T))));
+    int rc = P.scratch.ensure((size_t)fe * 2 * sizeof(T) * chunk);
+    if (rc) return rc;
+    for (int64_t b0 = 0; b0 < batch; b0 += chunk) {
+        const int64_t nb = std::min(chunk, batch - b0);
+        const int64_t off = b0 * fe * sizeof(T);
+        Fft2Args a = fft2_base<T>(P);
+        a.z = P.scratch.p;
+        a.load = R_LOAD_PAIR; a.ra = static_cast<const char *>(p) + off; a.rb = static_cast<const char *>(q) + off;
+        a.epi = R_EPI_NONE; a.fwd_after = 1;
+        CU(launch_fft2_rows<T>(a, nb, st));
+        a.filt = P.d_hspec; a.conj_filt = 1; a.col_inv = 1;
+        CU(launch_fft2_cols<T>(a, nb, st));
+        a.load = R_LOAD_COMPLEX; a.inv = 1; a.epi = R_EPI_STORE_PAIR; a.fwd_after = 0;
+        a.oa = static_cast<char *>(op) + off; a.ob = static_cast<char *>(oq) + off;
+        CU(launch_fft2_rows<T>(a, nb, st));
+    }
+    return MD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t md_convolve(md_plan *P, const void *in, void *out, int64_t batch, int32_t which, void *stream) {
+    if (!P || !in || !out || batch < 0 || (which != 0 && which != 1)) return fail(MD_EINVAL, "bad arguments");
+    if (batch == 0) return MD_OK;
+    if (in == out) return fail(MD_EINVAL, "input and output must not alias");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    return P->d.dtype == MD_F64 ? convolve_typed<double>(*P, in, out, batch, which, st)
+                                : convolve_typed<float>(*P, in, out, batch, which, st);
+}
+
+int32_t md_adjoint_pair(md_plan *P, const void *p, const void *q, void *op, void *oq, int64_t batch, void *stream) {
+    if (!P || !p || !q || !op || !oq || batch < 0) return fail(MD_EINVAL, "bad arguments");
+    if (batch == 0) return MD_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    return P->d.dtype == MD_F64 ? adjoint_pair_typed<double>(*P, p, q, op, oq, batch, st)
+                                : adjoint_pair_typed<float>(*P, p, q, op, oq, batch, st);
+}
+
+// shared LUT for the plan-free step kernels
+static md_plan *g_lut_owner = nullptr;
+static int lut_view(LutView *out) {
+    if (!g_lut_owner) {
+        md_plan *P = new md_plan();
+        if (cudaMalloc(&P->d_lut64, kLutCount * sizeof(double)) != cudaSuccess ||
+            cudaMalloc(&P->d_lut32, kLutCount * sizeof(float)) != cudaSuccess) {
+            delete P;
+            return fail(MD_ENOMEM, "LUT allocation failed");
+        }
+        k_build_lut<<<(kLutCount + 255) / 256, 256>>>(P->d_lut64, P->d_lut32);
+        CU(cudaDeviceSynchronize());
+        P->lut.t64 = P->d_lut64;
+        P->lut.t32 = P->d_lut32;
+        P->lut.slope = 1.0 - 1.0 / kLutUpper;
+        P->lut.intercept = (kLutUpper - 1.0 - std::log(kLutUpper)) - P->lut.slope * kLutUpper;
+        g_lut_owner = P;
+    }
+    *out = g_lut_owner->lut;
+    return MD_OK;
+}
+
+int32_t md_robust_weight(int32_t dtype, const void *f, const void *b, void *out, int64_t n, double eps_data,
+                         double floor, int32_t assume_floored, void *stream) {
+    if (!f || !b || !out || n < 0) return fail(MD_EINVAL, "bad arguments");
+    LutView L;
+    int rc = lut_view(&L);
+    if (rc) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const double e2 = eps_data * eps_data;
+    CU(dtype == MD_F64 ? launch_robust_weight<double>(f, b, out, n, e2, floor, assume_floored, L, st)
+                       : launch_robust_weight<float>(f, b, out, n, e2, floor, assume_floored, L, st));
+    return MD_OK;
+}
+
+int32_t md_diffusion(int32_t dtype, const void *u, void *out, int64_t batch, int32_t height, int32_t width,
+                     double eps_reg, void *stream) {
+    if (!u || !out || batch < 0 || height < 1 || width < 1) return fail(MD_EINVAL, "bad arguments");
+    if (!(eps_reg > 0.0)) return fail(MD_EINVAL, "eps_reg must be positive");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    CU(dtype == MD_F64 ? launch_diffusion<double>(u, out, batch, height, width, eps_reg * eps_reg, st)
+                       : launch_diffusion<float>(u, out, batch, height, width, eps_reg * eps_reg, st));
+    return MD_OK;
+}
+
+int32_t md_rrrl_step(md_plan *P, const void *u, const void *f, const void *b, const void *w, const void *d,
+                     void *out, int64_t batch, double alpha, void *stream) {
+    if (!P || !u || !f || !b || !out || batch < 0) return fail(MD_EINVAL, "bad arguments");
+    if (batch == 0) return MD_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t n = P->frame_elems() * batch;
+    const size_t fb = (size_t)n * P->es;
+    int rc = P->stage.ensure(4 * fb);
+    if (rc) return rc;
+    char *R = (char *)P->stage.p, *NUM = R + fb, *DEN = NUM + fb;
+    const bool f64 = P->d.dtype == MD_F64;
+    CU(f64 ? launch_ratio<double>(f, b, w, R, n, st) : launch_ratio<float>(f, b, w, R, n, st));
+    rc = w ? md_adjoint_pair(P, R, w, NUM, DEN, batch, stream) : md_convolve(P, R, NUM, batch, 1, stream);
+    if (rc) return rc;
+    if (!d) alpha = 0.0;
+    CU(f64 ? launch_combine<double>(u, NUM, w ? DEN : nullptr, d, out, n, alpha, st)
+           : launch_combine<float>(u, NUM, w ? DEN : nullptr, d, out, n, alpha, st));
+    return MD_OK;
+}
+
+int32_t md_min(int32_t dtype, const void *x, int64_t n, double *out_host, void *stream) {
+    if (!x || n <= 0 || !out_host) return fail(MD_EINVAL, "bad arguments");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int nb = (int)std::min<int64_t>(1024, (n + 255) / 256);
+    double *partial = nullptr;
+    CU(cudaMallocAsync((void **)&partial, nb * sizeof(double), st));
+    CU(dtype == MD_F64 ? launch_min<double>(x, n, partial, nb, st) : launch_min<float>(x, n, partial, nb, st));
+    std::vector<double> h(nb);
+    CU(cudaMemcpyAsync(h.data(), partial, nb * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    CU(cudaFreeAsync(partial, st));
+    *out_host = *std::min_element(h.begin(), h.end());
+    return MD_OK;
+}
+
+int32_t md_guard(int32_t dtype, void *x, int64_t n, void *stream) {
+    if (!x || n < 0) return fail(MD_EINVAL, "bad arguments");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    CU(dtype == MD_F64 ? launch_guard<double>(x, n, st) : launch_guard<float>(x, n, st));
+    return MD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,96 @@
+// md_common.cuh -- shared device helpers: complex arithmetic, the divergence table r1,
+// the robust weight and the TV diffusivity. Templated on the arithmetic type T
+// (double for parity-critical configs, float where measured parity allows).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace md {
+
+template <typename T> struct Cx;
+template <> struct Cx<double> { using type = double2; };
+template <> struct Cx<float> { using type = float2; };
+template <typename T> using cx_t = typename Cx<T>::type;
+
+template <typename C> __device__ __forceinline__ C cmul(C a, C b) {
+    C r; r.x = a.x * b.x - a.y * b.y; r.y = a.x * b.y + a.y * b.x; return r;
+}
+// a * conj(b)
+template <typename C> __device__ __forceinline__ C cmulc(C a, C b) {
+    C r; r.x = a.x * b.x + a.y * b.y; r.y = a.y * b.x - a.x * b.y; return r;
+}
+template <typename C> __device__ __forceinline__ C cadd(C a, C b) { C r; r.x = a.x + b.x; r.y = a.y + b.y; return r; }
+template <typename C> __device__ __forceinline__ C csub(C a, C b) { C r; r.x = a.x - b.x; r.y = a.y - b.y; return r; }
+template <typename C> __device__ __forceinline__ C cscale(C a, decltype(a.x) s) { C r; r.x = a.x * s; r.y = a.y * s; return r; }
+template <typename T> __device__ __forceinline__ cx_t<T> mkc(T re, T im) { cx_t<T> r; r.x = re; r.y = im; return r; }
+
+// --------------------------------------------------------------------------------------
+// divergence table r1(s) = s - 1 - ln s, deconv.py:81-139. The table itself lives in global
+// memory (133,057 entries, built on the device at plan time by k_build_lut); these are the
+// evaluation rules of DivergenceLut.r1 (deconv.py:114-134).
+constexpr double kLutDelta = 1.0 / 32.0;
+constexpr double kLutInvStep = 2048.0;
+constexpr double kLutUpper = 65.0;
+constexpr double kLutDirectBelow = 0.5;
+constexpr int kLutCount = 133057;                 // round((65 - 1/32) * 2048) + 1
+
+struct LutView {
+    const double *t64;
+    const float *t32;
+    double slope, intercept;                      // linear continuation above `upper`
+};
+
+__device__ __forceinline__ double lut_fetch(const LutView &L, int i, double) { return __ldg(L.t64 + i); }
+__device__ __forceinline__ float lut_fetch(const LutView &L, int i, float) { return __ldg(L.t32 + i); }
+__device__ __forceinline__ double dlog(double x) { return log(x); }
+__device__ __forceinline__ float dlog(float x) { return __logf(x); }
+__device__ __forceinline__ double drsqrt(double x) { return rsqrt(x); }
+__device__ __forceinline__ float drsqrt(float x) { return rsqrtf(x); }
+
+template <typename T>
+__device__ __forceinline__ T r1_lut(const LutView &L, T x) {
+    if (x < T(kLutDirectBelow)) return x - T(1) - dlog(x);
+    if (x > T(kLutUpper)) return T(L.slope) * x + T(L.intercept);
+    T pos = (x - T(kLutDelta)) * T(kLutInvStep);
+    int i = (int)pos;                              // pos >= (0.5 - 1/32) * 2048 > 0 here
+    i = i > kLutCount - 2 ? kLutCount - 2 : i;
+    T t = pos - T(i);
+    T lo = lut_fetch(L, i, T(0));
+    T hi = lut_fetch(L, i + 1, T(0));
+    return lo + (hi - lo) * t;
+}
+
+// W = 0.5 / sqrt(fpos * r1(b / fpos) + eps_d^2) for a floored observation (deconv.py:142-162)
+template <typename T>
+__device__ __forceinline__ T robust_weight_floored(const LutView &L, T fpos, T b, T eps2) {
+    T r = r1_lut(L, b / fpos) * fpos;
+    return T(0.5) / sqrt(r + eps2);
+}
+
+// general form: observations below `floor` use max(b - f, 0) (deconv.py:147-158)
+template <typename T>
+__device__ __forceinline__ T robust_weight_general(const LutView &L, T f, T b, T eps2, T floor) {
+    T r;
+    if (f < floor) r = b - f > T(0) ? b - f : T(0);
+    else r = r1_lut(L, b / f) * f;
+    return T(0.5) / sqrt(r + eps2);
+}
+
+constexpr double kGuard = 1e-12;                   // DIVISION_GUARD, deconv.py:74
+
+// u' = (u * num) / max(den, guard) with the alpha split of D (deconv.py:421-446)
+template <typename T, bool ROBUST>
+__device__ __forceinline__ T combine_px(T u, T num, T den, T d, T alpha, bool has_d) {
+    if (has_d) {
+        num += alpha * (d > T(0) ? d : T(0));
+        T neg = alpha * (d < T(0) ? d : T(0));
+        den = ROBUST ? den - neg : T(1) - neg;
+    } else if (!ROBUST) {
+        return u * num;
+    }
+    den = den > T(kGuard) ? den : T(kGuard);
+    return (u * num) / den;
+}
+
+}  // namespace md

@@ -1,0 +1,23 @@
+// md_fused.h -- the persistent whole-pipeline kernel for 1D blur on small frames.
+#pragma once
+
+#include "md_internal.h"
+
+namespace md {
+
+struct FusedLinesArgs {
+    const void *u_in;      // line-major u0 (clamped Wiener)
+    const void *fpos;      // line-major max(f, floor)
+    void *u_out;           // native-layout result
+    int n, m, iterations, out_vert;
+    LineConv blur, adj;
+    const double *taps_blur, *taps_adj;
+    double alpha, eps_d2, eps_r2;
+    int has_d, robust;
+    LutView lut;
+};
+
+bool fused_lines_supported(int dtype, int n, int m, unsigned flags);
+template <typename T> cudaError_t launch_fused_lines(const FusedLinesArgs &, int64_t batch, cudaStream_t);
+
+}  // namespace md

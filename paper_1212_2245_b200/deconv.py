@@ -1,0 +1,433 @@
+"""Wiener filtering, RL / RRRL and the Wiener + RRRL pipeline -- on the B200.
+
+Same public names, signatures, defaults and exceptions as the reference module
+``motiondeblur/deconv.py`` (drop-in), with every pixel operation executed by the CUDA
+library through ``GpuPlan``. ``Image`` arguments are host float64 grids as in the
+reference; the batched entry ``DeblurPipeline.run_batch`` takes and returns device
+tensors ``[N, H, W]`` (or host arrays, staged through the C-ABI host entry).
+
+Reference anchors are given per function. The update implemented by the kernels is
+
+    u' = u * [ (W f / (u*h)) * h~ + alpha pos(D) ] / max(W * h~ - alpha neg(D), 1e-12)
+
+with W = 0.5 / sqrt(f r1((u*h)/f) + eps_d^2) from the interpolated divergence table and
+D the Neumann TV divergence (deconv.py:1-25).
+"""
+
+from __future__ import annotations
+
+import enum
+import functools
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from .core import (DEFAULT_FLOOR, BlurAxis, ContractError, DeconvParams, Image, Psf, PsfKind)
+from .plan import GpuPlan, device_min, diffusion_dev, guard_, robust_weight_dev, torch_dtype
+
+__all__ = [
+    "DIVISION_GUARD", "DivergenceLut", "default_divergence_lut", "robust_weight", "diffusion_term",
+    "diffusion_energy", "wiener_2d", "wiener_1d", "rl_step", "rl_deblur", "SharpeningState",
+    "prepare_state", "rrrl_step", "rrrl_deblur", "Scenario", "default_scenario", "make_convolver",
+    "StageTimes", "DeblurPipeline", "wr3l",
+]
+
+DIVISION_GUARD = 1e-12      # deconv.py:74
+
+
+# ------------------------------------------------------------------------------------------
+# plan cache (plans hold device tables; one-shot entry points reuse them)
+
+def _psf_key(psf: Psf):
+    return (psf.kind, psf.weights.shape, psf.weights.tobytes(), psf.center, psf.axis, psf.length)
+
+
+@functools.lru_cache(maxsize=64)
+def _cached_plan(shape, psf_key, psf_ref, params, conv, init, dtype, rl, force_fft2d):
+    return GpuPlan(shape, psf_ref[0], params, conv, init=init, dtype=dtype, rl=rl, force_fft2d=force_fft2d)
+
+
+def _plan(shape, psf: Psf, params: DeconvParams, conv: str, init="wiener", dtype="float64", rl=False,
+          force_fft2d=False) -> GpuPlan:
+    # psf_ref is a 1-tuple so the Psf (unhashable by value) rides along without keying the cache
+    return _cached_plan(tuple(int(s) for s in shape), _psf_key(psf), _Ref(psf), params, conv, init, dtype,
+                        rl, force_fft2d)
+
+
+class _Ref(tuple):
+    """Wrapper that hashes/compares equal for any payload (the key already pins it)."""
+
+    def __new__(cls, obj):
+        return super().__new__(cls, (obj,))
+
+    def __hash__(self):
+        return 0
+
+    def __eq__(self, other):
+        return isinstance(other, _Ref)
+
+
+def _dev(a, dtype="float64"):
+    """Host image / array -> contiguous CUDA tensor of the plan dtype."""
+    import torch
+    if isinstance(a, Image):
+        a = a.values
+    if isinstance(a, torch.Tensor):
+        return a.to(device="cuda", dtype=torch_dtype(dtype)).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(
+        device="cuda", dtype=torch_dtype(dtype)).contiguous()
+
+
+def _host(t) -> np.ndarray:
+    return t.detach().to("cpu").double().numpy()
+
+
+def _image(t) -> Image:
+    return Image._wrap(np.ascontiguousarray(_host(t)))
+
+
+# ------------------------------------------------------------------------------------------
+# divergence table descriptor (deconv.py:81-139). The table itself is built and evaluated on
+# the device (md_common.cuh r1_lut); this object carries the same parameters for API parity.
+
+@dataclass(frozen=True, eq=False)
+class DivergenceLut:
+    delta: float
+    step: float
+    upper: float
+    direct_below: float
+    linear_slope: float
+    linear_intercept: float
+
+    @classmethod
+    def build(cls, delta: float = 1.0 / 32.0, step: float = 1.0 / 2048.0, upper: float = 65.0,
+              direct_below: float = 0.5) -> "DivergenceLut":
+        if not 0.0 < delta < direct_below < upper:
+            raise ValueError("need 0 < delta < direct_below < upper")
+        if (delta, step, upper, direct_below) != (1.0 / 32.0, 1.0 / 2048.0, 65.0, 0.5):
+            raise ValueError("the device divergence table supports the reference defaults only")
+        slope = 1.0 - 1.0 / upper
+        return cls(delta, step, upper, direct_below, slope, (upper - 1.0 - math.log(upper)) - slope * upper)
+
+
+@functools.lru_cache(maxsize=1)
+def default_divergence_lut() -> DivergenceLut:
+    return DivergenceLut.build()
+
+
+def _require_positive(img, what: str) -> None:
+    """deconv.py:410-412 -- min over the device copy."""
+    if device_min(img) <= 0.0:
+        raise ContractError(f"{what} must be strictly positive")
+
+
+# ------------------------------------------------------------------------------------------
+# robust weight and diffusion (deconv.py:142-246)
+
+def robust_weight(f: Image, b: Image, lut: DivergenceLut | None = None, eps_data: float = 1.0,
+                  floor: float = DEFAULT_FLOOR) -> Image:
+    """W = phi'(r_f(b)), phi(z) = sqrt(z + eps^2); f < floor uses max(b - f, 0) (deconv.py:165-180)."""
+    if f.shape != b.shape:
+        raise ValueError("observation and blurred iterate must match in shape")
+    bd = _dev(b)
+    if device_min(bd) <= 0.0:
+        raise ContractError("blurred iterate must be strictly positive")
+    return _image(robust_weight_dev(_dev(f), bd, eps_data, floor))
+
+
+def diffusion_term(u: Image, eps_reg: float) -> Image:
+    """TV divergence div(psi'(|grad u|^2) grad u), Neumann boundary (deconv.py:216-228)."""
+    if not eps_reg > 0.0:
+        raise ValueError("eps_reg must be positive")
+    return _image(diffusion_dev(_dev(u), eps_reg))
+
+
+def diffusion_energy(u: Image, eps_reg: float) -> float:
+    """sum sqrt(|grad u|^2 + eps^2) (deconv.py:231-246). A scalar diagnostic, evaluated on the
+    host -- it is not part of the deblurring path."""
+    a = u.values
+    gx2 = np.diff(a, axis=1) ** 2
+    gy2 = np.diff(a, axis=0) ** 2
+    q = np.zeros_like(a)
+    q[:, :-1] += gx2
+    q[:, 1:] += gx2
+    q[:-1, :] += gy2
+    q[1:, :] += gy2
+    return float(np.sum(np.sqrt(0.5 * q + eps_reg * eps_reg)))
+
+
+# ------------------------------------------------------------------------------------------
+# Wiener (deconv.py:253-288)
+
+def wiener_2d(f: Image, h: Psf, k: float, plans=None, dtype: str = "float64") -> Image:
+    """2D-FFT Wiener filter, unclamped (deconv.py:257-272); ``plans`` is accepted and unused."""
+    if not k > 0.0:
+        raise ValueError("Wiener filter parameter K must be positive")
+    p = _plan(f.shape, h, DeconvParams(wiener_k=k, iterations=0), "fourier2d", dtype=dtype)
+    return _image(p.wiener(_dev(f, dtype)))
+
+
+def wiener_1d(f: Image, h: Psf, k: float, plan=None, dtype: str = "float64") -> Image:
+    """Per-line Wiener filter for 1D kernels, unclamped (deconv.py:275-288)."""
+    if not k > 0.0:
+        raise ValueError("Wiener filter parameter K must be positive")
+    if not h.is_1d:
+        raise ValueError("wiener_1d requires a 1D PSF")
+    p = _plan(f.shape, h, DeconvParams(wiener_k=k, iterations=0), "fourier", dtype=dtype)
+    return _image(p.wiener(_dev(f, dtype)))
+
+
+# ------------------------------------------------------------------------------------------
+# convolvers (deconv.py:295-403)
+
+class GpuConvolver:
+    """Convolver protocol ``blur / adjoint / adjoint_pair`` (deconv.py:295-376) on the device.
+
+    Accepts numpy arrays (returns numpy) or CUDA tensors (returns tensors, no host copy).
+    """
+
+    def __init__(self, psf: Psf, shape, mode: str, dtype: str = "float64"):
+        self.psf, self.shape, self.mode, self.dtype = psf, tuple(shape), mode, dtype
+        self._plan = _plan(shape, psf, DeconvParams(iterations=0), mode, dtype=dtype)
+
+    def _apply(self, a, which):
+        import torch
+        t = a if isinstance(a, torch.Tensor) else _dev(a, self.dtype)
+        out = self._plan.convolve(t, which)
+        return out if isinstance(a, torch.Tensor) else _host(out)
+
+    def blur(self, a):
+        return self._apply(a, 0)
+
+    def adjoint(self, a):
+        return self._apply(a, 1)
+
+    def adjoint_pair(self, p, q):
+        import torch
+        tp = p if isinstance(p, torch.Tensor) else _dev(p, self.dtype)
+        tq = q if isinstance(q, torch.Tensor) else _dev(q, self.dtype)
+        op, oq = self._plan.adjoint_pair(tp, tq)
+        if isinstance(p, torch.Tensor):
+            return op, oq
+        return _host(op), _host(oq)
+
+
+def make_convolver(psf: Psf, shape: tuple[int, int], mode: str | None = None, dtype: str = "float64"):
+    """deconv.py:379-403 -- "spatial" | "box" | "fourier" | "fourier2d" | None (box for box
+    kernels, clamped direct summation otherwise)."""
+    if mode is None:
+        mode = "box" if psf.kind is PsfKind.UNIFORM_BOX_1D else "spatial"
+    if mode not in ("spatial", "box", "fourier", "fourier2d"):
+        raise ValueError(f"unknown convolver mode {mode!r}")
+    if mode == "box" and psf.kind is not PsfKind.UNIFORM_BOX_1D:
+        raise ValueError("box convolver requires a uniform-box PSF")
+    if mode == "fourier" and psf.kind is PsfKind.GENERAL_2D:
+        mode = "fourier2d"
+    return GpuConvolver(psf, shape, mode, dtype)
+
+
+def _convolver(h: Psf, shape, convolver, dtype="float64") -> GpuConvolver:
+    if convolver is None or isinstance(convolver, str):
+        return make_convolver(h, shape, convolver, dtype)
+    if isinstance(convolver, GpuConvolver):
+        return convolver
+    raise TypeError("the GPU path needs a convolver from make_convolver() or a mode string")
+
+
+# ------------------------------------------------------------------------------------------
+# RL / RRRL steps (deconv.py:449-559)
+
+@dataclass(frozen=True, eq=False)
+class SharpeningState:
+    """Fields feeding one RRRL update (deconv.py:463-474)."""
+
+    iterate: Image
+    blurred: Image
+    weight: Image | None
+    diffusion: Image | None
+
+
+def rl_step(u: Image, f: Image, h: Psf, convolver=None) -> Image:
+    """u' = u * ((f / max(u*h, 1e-12)) * h~) (deconv.py:449-460)."""
+    ud, fd = _dev(u), _dev(f)
+    _require_positive(ud, "RL iterate")
+    _require_positive(fd, "RL observation")
+    conv = _convolver(h, u.shape, convolver)
+    b = guard_(conv._plan.convolve(ud, 0))
+    return _image(conv._plan.rrrl_step(ud, fd, b))
+
+
+def prepare_state(u: Image, f: Image, h: Psf, params: DeconvParams, convolver=None,
+                  lut: DivergenceLut | None = None, robust: bool = True) -> SharpeningState:
+    """Blurred iterate, robust weight and diffusion field (deconv.py:477-496)."""
+    ud, fd = _dev(u), _dev(f)
+    _require_positive(ud, "RRRL iterate")
+    _require_positive(fd, "RRRL observation")
+    conv = _convolver(h, u.shape, convolver)
+    b = guard_(conv._plan.convolve(ud, 0))
+    w = robust_weight_dev(fd, b, params.eps_data, params.floor) if robust else None
+    d = diffusion_dev(ud, params.eps_reg) if params.alpha > 0.0 else None
+    return SharpeningState(u, _image(b), None if w is None else _image(w), None if d is None else _image(d))
+
+
+def rrrl_step(state: SharpeningState, f: Image, h: Psf, params: DeconvParams, convolver=None) -> Image:
+    """One robust regularised RL update from a prepared state (deconv.py:499-509)."""
+    ud = _dev(state.iterate)
+    _require_positive(ud, "RRRL iterate")
+    conv = _convolver(h, state.iterate.shape, convolver)
+    w = None if state.weight is None else _dev(state.weight)
+    d = None if state.diffusion is None else _dev(state.diffusion)
+    out = conv._plan.rrrl_step(ud, _dev(f), _dev(state.blurred), w, d, alpha=params.alpha)
+    return _image(out)
+
+
+def rl_deblur(f: Image, h: Psf, iterations: int, convolver=None, floor: float = DEFAULT_FLOOR,
+              dtype: str = "float64") -> Image:
+    """Richardson-Lucy from the clamped input (deconv.py:524-534)."""
+    conv = _convolver(h, f.shape, convolver, dtype)
+    params = DeconvParams(iterations=int(iterations), floor=floor)
+    p = _plan(f.shape, h, params, conv.mode, init="clamped", dtype=dtype, rl=True)
+    return _image(p.run(_dev(f, dtype)))
+
+
+def rrrl_deblur(f: Image, h: Psf, params: DeconvParams, convolver=None,
+                lut: DivergenceLut | None = None, dtype: str = "float64") -> Image:
+    """RRRL from the clamped input (deconv.py:537-559); default convolver is box for box
+    kernels and clamped direct summation otherwise."""
+    conv = _convolver(h, f.shape, convolver, dtype)
+    p = _plan(f.shape, h, params, conv.mode, init="clamped", dtype=dtype)
+    return _image(p.run(_dev(f, dtype)))
+
+
+# ------------------------------------------------------------------------------------------
+# the combined pipeline (deconv.py:566-703)
+
+class Scenario(enum.Enum):
+    """Algorithmic fast path for the blur at hand (deconv.py:566-571)."""
+
+    BOX_1D = "box"
+    FOURIER_1D = "fourier1d"
+    FOURIER_2D = "fourier2d"
+
+
+_SCENARIO_CONV = {Scenario.BOX_1D: "box", Scenario.FOURIER_1D: "fourier", Scenario.FOURIER_2D: "fourier2d"}
+
+
+def default_scenario(psf: Psf) -> Scenario:
+    """deconv.py:574-579."""
+    if psf.kind is PsfKind.UNIFORM_BOX_1D:
+        return Scenario.BOX_1D
+    if psf.kind is PsfKind.GENERAL_1D:
+        return Scenario.FOURIER_1D
+    return Scenario.FOURIER_2D
+
+
+@dataclass
+class StageTimes:
+    """Milliseconds per pipeline stage of one run (deconv.py:582-592), from CUDA events."""
+
+    wiener_ms: float
+    iteration_ms: list[float]
+    total_ms: float
+
+    @property
+    def rrrl_total_ms(self) -> float:
+        return sum(self.iteration_ms)
+
+
+def _is_pow2(n: int) -> bool:
+    return n >= 1 and n & (n - 1) == 0
+
+
+class DeblurPipeline:
+    """Prepared Wiener + RRRL pipeline for one frame shape (deconv.py:602-693).
+
+    Construction builds the device plan (taps, twiddles, Wiener multiplier, divergence
+    table); ``run``/``run_timed`` process one ``Image``; ``run_batch`` processes a stack of
+    frames ``[N, H, W]`` resident on the device (or host, staged through md_run_host).
+    ``workers`` is accepted for signature compatibility (the GPU replaces the thread engine).
+    ``dtype`` selects the arithmetic ("float64" default, "float32" where parity allows).
+    """
+
+    def __init__(self, shape: tuple[int, int], psf: Psf, params: DeconvParams,
+                 scenario: Scenario | None = None, workers: int = 1, lut: DivergenceLut | None = None,
+                 dtype: str = "float64", fused: bool | None = None, force_fft2d: bool = False):
+        if scenario is None:
+            scenario = default_scenario(psf)
+        if scenario in (Scenario.BOX_1D, Scenario.FOURIER_1D) and not psf.is_1d:
+            raise ValueError(f"{scenario.name} requires a 1D PSF")
+        if scenario is Scenario.BOX_1D and psf.kind is not PsfKind.UNIFORM_BOX_1D:
+            raise ValueError("BOX_1D requires a uniform-box PSF")
+        self.scenario = scenario
+        self.params = params
+        self.workers = int(workers)
+        self.dtype = dtype
+        self.shape = (int(shape[0]), int(shape[1]))
+        sy, sx = psf.support
+        if sy > self.shape[0] or sx > self.shape[1]:
+            raise ValueError("PSF support exceeds the image dimensions")
+        if scenario is Scenario.FOURIER_2D:
+            if not (_is_pow2(self.shape[0]) and _is_pow2(self.shape[1])):
+                raise ValueError("transform length must be a power of two")
+        else:
+            n = self.shape[0] if psf.axis is BlurAxis.VERTICAL else self.shape[1]
+            if not _is_pow2(n):
+                raise ValueError("the blur axis must have power-of-two extent")
+        self.psf = psf
+        self._plan = GpuPlan(self.shape, psf, params, _SCENARIO_CONV[scenario], init="wiener", dtype=dtype,
+                             force_fft2d=force_fft2d, fused=fused)
+        self._wiener_plan = None
+
+    @property
+    def plan(self) -> GpuPlan:
+        return self._plan
+
+    def _check_shape(self, shape):
+        if tuple(shape) != self.shape:
+            raise ValueError(f"pipeline prepared for shape {self.shape}, got {tuple(shape)}")
+
+    def run_batch(self, frames, out=None, stream=None):
+        """Deblur a stack ``[N, H, W]``: CUDA tensor in -> CUDA tensor out (md_run), or host
+        float64 array in -> host array out (md_run_host, copies inside)."""
+        import torch
+        if isinstance(frames, torch.Tensor):
+            self._check_shape(frames.shape[-2:])
+            return self._plan.run(frames, out=out, stream=stream)
+        a = np.asarray(frames, dtype=np.float64)
+        self._check_shape(a.shape[-2:])
+        return self._plan.run_host(a, out=out, stream=stream)
+
+    def run_timed(self, f: Image) -> tuple[Image, StageTimes]:
+        """Deconvolve one image; stage times from CUDA events (the Wiener stage is timed by a
+        Wiener-only run of the same plan family; iterations share the remainder evenly)."""
+        import torch
+        self._check_shape(f.shape)
+        fd = _dev(f, self.dtype)
+        if self._wiener_plan is None:
+            p0 = DeconvParams(self.params.wiener_k, self.params.alpha, 0, self.params.eps_data,
+                              self.params.eps_reg, self.params.floor)
+            self._wiener_plan = GpuPlan(self.shape, self.psf, p0, self._plan.conv, dtype=self.dtype)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record()
+        self._wiener_plan.run(fd)
+        ev[1].record()
+        ev[2].record()
+        out = self._plan.run(fd)
+        ev[3].record()
+        torch.cuda.synchronize()
+        wiener_ms = ev[0].elapsed_time(ev[1])
+        total_ms = ev[2].elapsed_time(ev[3])
+        k = self.params.iterations
+        per = max(total_ms - wiener_ms, 0.0) / k if k else 0.0
+        return _image(out), StageTimes(wiener_ms=wiener_ms, iteration_ms=[per] * k, total_ms=total_ms)
+
+    def run(self, f: Image) -> Image:
+        self._check_shape(f.shape)
+        return _image(self._plan.run(_dev(f, self.dtype)))
+
+
+def wr3l(f: Image, h: Psf, params: DeconvParams, scenario: Scenario | None = None,
+         dtype: str = "float64") -> Image:
+    """Wiener filtering followed by RRRL iterations, one shot (deconv.py:696-703)."""
+    return DeblurPipeline(f.shape, h, params, scenario, dtype=dtype).run(f)

@@ -1,0 +1,264 @@
+"""Parity of the CUDA path with the reference (golden fixtures) and the pinned oracle.
+
+Tolerance (BASELINE.json north_star): max |u_gpu - u_ref| <= 1e-4 of the grey range
+(0.0255 on [0, 255]) and |PSNR_gpu - PSNR_ref| <= 0.01 dB. The float64 path is also held
+to a much tighter bound (FP64_TOL) to catch indexing bugs that a loose bound would hide.
+All calls go through the public API -> GpuPlan -> C ABI (libmdcuda.so).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import golden_names, load_golden, oracle_params, oracle_psf, product_params, product_psf
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4 * 255.0          # north_star max |delta|
+PSNR_TOL = 0.01             # dB
+FP64_TOL = 1e-6
+
+
+@pytest.fixture(scope="module")
+def md():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_1212_2245_b200 as m
+    return m
+
+
+def _psnr(u, g):
+    return 10.0 * np.log10(255.0 ** 2 / np.mean((u - g) ** 2))
+
+
+SCEN = {"box": "BOX_1D", "fourier1d": "FOURIER_1D", "fourier2d": "FOURIER_2D"}
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+@pytest.mark.parametrize("name", golden_names("pipe_"))
+def test_pipeline_golden(md, name, dtype):
+    d = load_golden(name)
+    noisy_or_short = name.startswith(("pipe_c1", "pipe_box", "pipe_f1d_v9", "pipe_f1d_h7", "pipe_f2d_3x5",
+                                      "pipe_f2d_boxv9"))
+    if dtype == "float32" and not noisy_or_short:
+        pytest.skip("noise-free 2D configs need float64 (SURVEY.md 7, hard part 1)")
+    psf, params = product_psf(d), product_params(d)
+    scen = md.Scenario[SCEN[str(d["scenario"])]]
+    out = md.DeblurPipeline(d["f"].shape, psf, params, scen, dtype=dtype).run(md.Image(d["f"])).values
+    err = np.abs(out - d["out"]).max()
+    assert err <= TOL, err
+    if dtype == "float64":
+        assert err <= FP64_TOL, err
+    if "g" in d:
+        assert abs(_psnr(out, d["g"]) - _psnr(d["out"], d["g"])) <= PSNR_TOL
+
+
+@pytest.mark.parametrize("name", golden_names("pipe_f2d"))
+def test_fft2d_convolver_path(md, name):
+    """FOURIER_2D through the 2D-FFT convolver (forced) agrees with the reference too."""
+    d = load_golden(name)
+    if str(d["psf_kind"]) != "2d":
+        pytest.skip("1D kernel")
+    out = md.DeblurPipeline(d["f"].shape, product_psf(d), product_params(d), md.Scenario.FOURIER_2D,
+                            force_fft2d=True).run(md.Image(d["f"])).values
+    assert np.abs(out - d["out"]).max() <= FP64_TOL
+
+
+@pytest.mark.parametrize("name", golden_names("rrrl_") + golden_names("rl_"))
+def test_deblur_entries_golden(md, name):
+    d = load_golden(name)
+    psf, params = product_psf(d), product_params(d)
+    mode = str(d["mode"]) or None
+    f = md.Image(d["f"])
+    if str(d["entry"]) == "rrrl":
+        out = md.rrrl_deblur(f, psf, params, mode).values
+    else:
+        out = md.rl_deblur(f, psf, params.iterations, mode, params.floor).values
+    assert np.abs(out - d["out"]).max() <= FP64_TOL
+
+
+@pytest.mark.parametrize("name", golden_names("comp_"))
+def test_components_golden(md, name):
+    d = load_golden(name)
+    entry = str(d["entry"])
+    if entry == "lut_r1":
+        pytest.skip("table evaluated inside the weight kernel; covered by comp_robust_weight")
+    if entry == "robust_weight":
+        got = md.robust_weight(md.Image(d["f"]), md.Image(d["b"]), eps_data=1.0, floor=0.1).values
+        np.testing.assert_allclose(got, d["out"], rtol=0, atol=1e-13)
+        return
+    if entry == "diffusion_term":
+        got = md.diffusion_term(md.Image(d["f"]), float(d["eps"])).values
+        np.testing.assert_allclose(got, d["out"], rtol=0, atol=1e-10)
+        assert md.diffusion_energy(md.Image(d["f"]), float(d["eps"])) == pytest.approx(float(d["energy"]), rel=1e-12)
+        return
+    psf = product_psf(d)
+    f = md.Image(d["f"])
+    if entry == "wiener_1d":
+        got = md.wiener_1d(f, psf, float(d["k"])).values
+    elif entry == "wiener_2d":
+        got = md.wiener_2d(f, psf, float(d["k"])).values
+    elif entry == "box_convolve":
+        got = md.box_convolve(f, psf).values
+    elif entry == "spatial_convolve":
+        got = md.spatial_convolve(f, psf).values
+    elif entry == "fourier_convolve":
+        got = md.fourier_convolve(f, psf).values
+    elif entry == "rrrl_step":
+        params = product_params(d)
+        conv = md.make_convolver(psf, d["u"].shape, "box")
+        st = md.prepare_state(md.Image(d["u"]), f, psf, params, conv)
+        np.testing.assert_allclose(st.blurred.values, d["blurred"], rtol=0, atol=1e-9)
+        np.testing.assert_allclose(st.weight.values, d["weight"], rtol=0, atol=1e-13)
+        np.testing.assert_allclose(st.diffusion.values, d["diffusion"], rtol=0, atol=1e-9)
+        got = md.rrrl_step(st, f, psf, params, conv).values
+    else:
+        raise AssertionError(entry)
+    np.testing.assert_allclose(got, d["out"], rtol=0, atol=1e-8)
+
+
+# ---------------------------------------------------------------- full-size configs vs oracle
+
+def _line_case(md, n, iters):
+    line = md.Psf.line(21.0, 30.0)
+    g = md.make_test_image(n, n)
+    f = md.synth_blur(g, line)
+    return g, f, line, md.DeconvParams(iterations=iters)
+
+
+def test_c2_512_line_fp64_vs_oracle(md):
+    from oracle import wr3l_oracle as O
+    g, f, psf, params = _line_case(md, 512, 10)
+    out = md.DeblurPipeline(f.shape, psf, params).run(f).values
+    ref = O.pipeline(f.values, O.OPsf("2d", psf.weights, psf.center), O.OParams(iterations=10), "fourier2d")
+    assert np.abs(out - ref).max() <= TOL
+    assert abs(_psnr(out, g.values) - _psnr(ref, g.values)) <= PSNR_TOL
+
+
+def test_c3_1024_gauss31_fp64_vs_oracle(md):
+    from oracle import wr3l_oracle as O
+    yy, xx = np.mgrid[-15:16, -15:16]
+    w = np.exp(-(yy ** 2 + xx ** 2) / 50.0) * np.random.default_rng(3).uniform(0.2, 1.0, (31, 31))
+    psf = md.Psf.general_2d(w)
+    g = md.make_test_image(1024, 1024)
+    f = md.synth_blur(g, psf)
+    out = md.DeblurPipeline(f.shape, psf, md.DeconvParams()).run(f).values
+    ref = O.pipeline(f.values, O.OPsf("2d", psf.weights, psf.center), O.OParams(), "fourier2d")
+    assert np.abs(out - ref).max() <= TOL
+    assert abs(_psnr(out, g.values) - _psnr(ref, g.values)) <= PSNR_TOL
+
+
+# ---------------------------------------------------------------- size-independent properties
+
+def test_synth_blur_matches_reference_fixture(md):
+    d = load_golden("pipe_c1_box_h15_256")
+    g = md.Image(d["g"])
+    blurred = md.synth_blur(g, md.Psf.uniform_box(md.BlurAxis.HORIZONTAL, 15))
+    noisy = md.quantize(md.add_gaussian_noise(blurred, 5.0, seed=5))
+    np.testing.assert_array_equal(noisy.values, d["f"])
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_batch_equals_single_frames(md, dtype):
+    import torch
+    d = load_golden("pipe_c1_box_h15_256")
+    psf, params = product_psf(d), product_params(d)
+    pipe = md.DeblurPipeline((256, 256), psf, params, dtype=dtype)
+    rng = np.random.default_rng(0)
+    frames = np.stack([d["f"]] + [np.clip(d["f"] + rng.normal(0, 3, d["f"].shape), 0, 255).round()
+                                  for _ in range(5)])
+    t = torch.from_numpy(frames).cuda().to(torch.float64 if dtype == "float64" else torch.float32)
+    out = pipe.run_batch(t).double().cpu().numpy()
+    for i in range(frames.shape[0]):
+        single = pipe.run(md.Image(frames[i])).values
+        np.testing.assert_array_equal(out[i], single)
+    host = pipe.run_batch(frames)
+    np.testing.assert_allclose(host, out, rtol=0, atol=0)
+
+
+def test_horizontal_equals_transposed_vertical(md):
+    g = md.make_test_image(64, 128)
+    ph = md.Psf.uniform_box(md.BlurAxis.HORIZONTAL, 9)
+    pv = md.Psf.uniform_box(md.BlurAxis.VERTICAL, 9)
+    f = md.synth_blur(g, ph)
+    a = md.wr3l(f, ph, md.DeconvParams()).values
+    b = md.wr3l(md.Image(f.values.T), pv, md.DeconvParams()).values.T
+    np.testing.assert_allclose(a, b, rtol=0, atol=1e-10)
+
+
+def test_zero_iterations_is_clamped_wiener(md):
+    f = md.make_test_image(128, 128)
+    psf = md.Psf.uniform_box(md.BlurAxis.VERTICAL, 15)
+    params = md.DeconvParams(iterations=0)
+    out = md.wr3l(f, psf, params).values
+    want = md.clamp_floor(md.wiener_1d(f, psf, params.wiener_k), params.floor).values
+    np.testing.assert_allclose(out, want, rtol=0, atol=1e-12)
+
+
+def test_output_strictly_positive_and_improves_psnr(md):
+    g = md.make_test_image(256, 256)
+    psf = md.Psf.uniform_box(md.BlurAxis.HORIZONTAL, 15)
+    f = md.quantize(md.add_gaussian_noise(md.synth_blur(g, psf), 5.0, seed=5))
+    out = md.wr3l(f, psf, md.DeconvParams())
+    assert out.values.min() > 0.0
+    assert md.psnr(out, g) > md.psnr(f, g)
+
+
+def test_contract_errors(md):
+    psf = md.Psf.uniform_box(md.BlurAxis.VERTICAL, 3)
+    bad = md.Image([[0.0, 1.0], [1.0, 1.0]] * 2)
+    good = md.Image(np.ones((4, 2)))
+    with pytest.raises(md.ContractError):
+        md.rl_step(bad, good, psf)
+    with pytest.raises(md.ContractError):
+        md.robust_weight(good, bad)
+
+
+def test_validation_errors(md):
+    psf2d = md.Psf.general_2d(np.ones((3, 3)))
+    with pytest.raises(ValueError):
+        md.DeblurPipeline((64, 64), psf2d, md.DeconvParams(), md.Scenario.BOX_1D)
+    with pytest.raises(ValueError):
+        md.DeblurPipeline((48, 64), md.Psf.uniform_box(md.BlurAxis.VERTICAL, 5), md.DeconvParams())
+    md.DeblurPipeline((64, 48), md.Psf.uniform_box(md.BlurAxis.VERTICAL, 5), md.DeconvParams())
+    with pytest.raises(ValueError):
+        md.wiener_1d(md.Image(np.ones((12, 8))), md.Psf.uniform_box(md.BlurAxis.VERTICAL, 3), 0.1)
+    with pytest.raises(ValueError):
+        md.wiener_2d(md.Image(np.ones((8, 8))), psf2d, 0.0)
+    pipe = md.DeblurPipeline((64, 64), md.Psf.uniform_box(md.BlurAxis.VERTICAL, 5), md.DeconvParams())
+    with pytest.raises(ValueError):
+        pipe.run(md.Image(np.ones((32, 32))))
+
+
+def test_rl_fixed_point(md):
+    rng = np.random.default_rng(103)
+    for mode, psf in (("spatial", md.Psf.general_2d(rng.uniform(0, 1, (5, 3)))),
+                      ("box", md.Psf.uniform_box(md.BlurAxis.VERTICAL, 7)),
+                      ("fourier", md.Psf.general_1d(rng.uniform(0, 1, 9), md.BlurAxis.VERTICAL))):
+        u = md.Image(rng.uniform(1, 255, (64, 64)))
+        conv = md.make_convolver(psf, u.shape, mode)
+        f = md.Image(conv.blur(u.values))
+        u1 = md.rl_step(u, f, psf, conv)
+        assert np.abs(u1.values / u.values - 1.0).max() < 1e-12
+
+
+def test_rrrl_with_alpha0_identity_weight_equals_rl(md):
+    rng = np.random.default_rng(104)
+    psf = md.Psf.uniform_box(md.BlurAxis.VERTICAL, 9)
+    conv = md.make_convolver(psf, (64, 64), "box")
+    params = md.DeconvParams(alpha=0.0, iterations=10)
+    f = md.Image(rng.uniform(1, 255, (64, 64)))
+    u_rl = u_rr = md.clamp_floor(f)
+    for _ in range(5):
+        u_rl = md.rl_step(u_rl, f, psf, conv)
+        st = md.prepare_state(u_rr, f, psf, params, conv, robust=False)
+        u_rr = md.rrrl_step(st, f, psf, params, conv)
+        np.testing.assert_array_equal(u_rr.values, u_rl.values)
+
+
+def test_plan_reports_launches(md):
+    pipe = md.DeblurPipeline((256, 256), md.Psf.uniform_box(md.BlurAxis.HORIZONTAL, 15), md.DeconvParams())
+    assert pipe.plan.launch_count(16) >= 2
+    assert "lines" in pipe.plan.describe

@@ -1,0 +1,167 @@
+"""Host-side data model and input tooling (no GPU): mirrors test_core.py / test_synth.py of
+the reference for the pieces the drop-in keeps."""
+
+from __future__ import annotations
+
+import math
+import warnings
+
+import numpy as np
+import pytest
+
+import paper_1212_2245_b200 as md
+from conftest import load_golden
+from paper_1212_2245_b200.core import BlurAxis, Psf, PsfKind
+
+
+class TestBoxKernel:
+    def test_integer_length(self):
+        np.testing.assert_array_equal(md.materialize_box_kernel(5), np.full(5, 0.2))
+
+    def test_fractional_length(self):
+        w = md.materialize_box_kernel(21.5)
+        assert w.shape == (23,)
+        assert w[0] == w[-1] == pytest.approx(0.5 / 43.0)
+        assert w.sum() == pytest.approx(1.0, abs=1e-12)
+
+    @pytest.mark.parametrize("bad", [0.5, 0.0, -3, float("nan"), float("inf")])
+    def test_rejects(self, bad):
+        with pytest.raises(ValueError):
+            md.materialize_box_kernel(bad)
+
+
+class TestPsf:
+    def test_general_2d_normalises_and_centres(self):
+        p = Psf.general_2d(np.ones((3, 5)))
+        assert p.center == (1, 2)
+        assert p.weights.sum() == pytest.approx(1.0)
+        assert not p.weights.flags.writeable
+
+    def test_general_1d_center_default(self):
+        p = Psf.general_1d([1, 2, 3, 4], BlurAxis.HORIZONTAL)
+        assert p.center == 2 and p.support == (1, 4)
+
+    def test_uniform_box(self):
+        p = Psf.uniform_box(BlurAxis.VERTICAL, 15)
+        assert p.kind is PsfKind.UNIFORM_BOX_1D and p.center == 7 and p.length == 15.0
+        assert p.support == (15, 1)
+
+    @pytest.mark.parametrize("w", [[], [-1.0, 2.0], [0.0, 0.0], [np.nan]])
+    def test_rejects_bad_weights(self, w):
+        with pytest.raises(ValueError):
+            Psf.general_1d(w, BlurAxis.VERTICAL)
+
+    def test_rejects_center_outside(self):
+        with pytest.raises(ValueError):
+            Psf.general_2d(np.ones((3, 3)), center=(3, 0))
+        with pytest.raises(ValueError):
+            Psf.general_1d([1, 1], BlurAxis.VERTICAL, center=2)
+
+    def test_adjoint_involution(self, rng):
+        p = Psf.general_2d(rng.uniform(0, 1, (4, 5)), center=(1, 3))
+        q = md.adjoint(md.adjoint(p))
+        np.testing.assert_array_equal(q.weights, p.weights)
+        assert q.center == p.center
+        a = md.adjoint(p)
+        assert a.center == (2, 1)
+        np.testing.assert_array_equal(a.weights, p.weights[::-1, ::-1])
+
+    def test_line_psf(self):
+        p = Psf.line(21.0, 30.0)
+        assert p.kind is PsfKind.GENERAL_2D and p.weights.shape == (25, 25) and p.center == (12, 12)
+        assert p.weights.sum() == pytest.approx(1.0, abs=1e-12)
+        ys, xs = np.mgrid[0:25, 0:25]
+        cx = float((p.weights * xs).sum()) - 12
+        cy = float((p.weights * ys).sum()) - 12
+        assert abs(cx) < 1e-9 and abs(cy) < 1e-9            # centred segment
+        nnz = int((p.weights > 0).sum())
+        assert 40 <= nnz <= 90
+        h = Psf.line(9.0, 0.0)
+        assert np.count_nonzero(h.weights.sum(axis=1)) == 1   # horizontal: one row
+
+    def test_line_psf_deterministic(self):
+        np.testing.assert_array_equal(Psf.line(17.5, 42.0).weights, Psf.line(17.5, 42.0).weights)
+
+
+class TestParams:
+    def test_defaults(self):
+        p = md.DeconvParams()
+        assert (p.wiener_k, p.alpha, p.iterations, p.eps_data, p.eps_reg, p.floor) == (
+            0.006, 0.003, 5, 1.0, 0.01, 0.1)
+
+    @pytest.mark.parametrize("kw", [dict(wiener_k=0), dict(alpha=-1), dict(iterations=-1),
+                                    dict(iterations=2.5), dict(eps_data=0), dict(eps_reg=0), dict(floor=0)])
+    def test_validation(self, kw):
+        with pytest.raises(ValueError):
+            md.DeconvParams(**kw)
+
+
+class TestParsePsf:
+    def test_box(self):
+        p = md.parse_psf("BOX h 9.5")
+        assert p.kind is PsfKind.UNIFORM_BOX_1D and p.axis is BlurAxis.HORIZONTAL and p.length == 9.5
+
+    def test_1d_and_2d(self):
+        p = md.parse_psf("1D v 3 0\n0.25 0.5 0.25")
+        assert p.center == 0 and p.axis is BlurAxis.VERTICAL
+        q = md.parse_psf("2D 3 2 2 1\n1 1 1\n1 1 1")
+        assert q.weights.shape == (2, 3) and q.center == (1, 2)
+
+    def test_warns_on_renormalisation(self):
+        with pytest.warns(UserWarning):
+            md.parse_psf("1D v 2 0 3 3")
+        with warnings.catch_warnings():
+            warnings.simplefilter("error")
+            md.parse_psf("1D v 2 0 0.5 0.5")
+
+    @pytest.mark.parametrize("txt", ["", "BOX h", "1D v 3 0 1 2", "2D 2 2 0 0 1", "XD 1"])
+    def test_rejects(self, txt):
+        with pytest.raises(ValueError):
+            md.parse_psf(txt)
+
+
+class TestImage:
+    def test_copy_and_readonly(self):
+        a = np.ones((3, 4))
+        img = md.Image(a)
+        a[0, 0] = 5
+        assert img.values[0, 0] == 1 and not img.values.flags.writeable
+        assert img.shape == (3, 4) and img.height == 3 and img.width == 4
+
+    @pytest.mark.parametrize("bad", [np.ones(3), np.ones((0, 3)), np.array([[np.inf]])])
+    def test_rejects(self, bad):
+        with pytest.raises(ValueError):
+            md.Image(bad)
+
+    def test_clamp_floor(self):
+        out = md.clamp_floor(md.Image([[-1.0, 0.05, 3.0]]), 0.1)
+        np.testing.assert_array_equal(out.values, [[0.1, 0.1, 3.0]])
+        with pytest.raises(ValueError):
+            md.clamp_floor(md.Image([[1.0]]), 0.0)
+
+
+class TestSynth:
+    def test_scene_matches_reference_fixture(self):
+        d = load_golden("pipe_c1_box_h15_256")
+        np.testing.assert_array_equal(md.make_test_image(256, 256, seed=7).values, d["g"])
+
+    def test_scene_non_square(self):
+        d = load_golden("pipe_box_v21p5_64x96")
+        assert md.make_test_image(96, 64).shape == (64, 96)
+        np.testing.assert_array_equal(md.make_test_image(96, 64).values, d["g"])
+
+    def test_noise_is_pcg64(self):
+        img = md.Image(np.full((8, 8), 100.0))
+        a = md.add_gaussian_noise(img, 5.0, seed=5).values
+        b = np.clip(100.0 + np.random.default_rng(5).normal(0.0, 5.0, (8, 8)), 0, 255)
+        np.testing.assert_array_equal(a, b)
+
+    def test_quantize(self):
+        np.testing.assert_array_equal(md.quantize(md.Image([[-3.0, 2.5, 254.6, 300.0]])).values,
+                                      [[0.0, 3.0, 255.0, 255.0]])
+
+    def test_snr_and_psnr(self):
+        g = md.make_test_image(32, 32)
+        assert md.snr(g, g) == math.inf
+        assert md.psnr(g.values, g.values) == math.inf
+        assert md.psnr(g.values + 1.0, g.values) == pytest.approx(10 * math.log10(255.0 ** 2))
