@@ -63,6 +63,7 @@ extern "C" {
 #define MD_FLAG_RL 1u            /* identity penaliser and alpha = 0: plain RL (rl_deblur)        */
 #define MD_FLAG_NO_FUSED 2u      /* force the multi-kernel path even where a fused kernel applies */
 #define MD_FLAG_FORCE_FFT2D 4u   /* 2D periodic convolver through 2D FFTs, not direct taps        */
+#define MD_FLAG_GENERIC_LINES 8u /* 1D blur: generic per-iteration line kernel, not the fast one  */
 
 typedef struct md_plan md_plan; /* opaque */
 

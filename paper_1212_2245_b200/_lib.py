@@ -21,7 +21,7 @@ MD_PSF_GENERAL_2D, MD_PSF_GENERAL_1D, MD_PSF_BOX_1D = 0, 1, 2
 MD_AXIS_NONE, MD_AXIS_VERTICAL, MD_AXIS_HORIZONTAL = -1, 0, 1
 MD_CONV_BOX, MD_CONV_SPATIAL, MD_CONV_FOURIER, MD_CONV_FOURIER2D = 0, 1, 2, 3
 MD_INIT_WIENER, MD_INIT_CLAMPED = 0, 1
-MD_FLAG_RL, MD_FLAG_NO_FUSED, MD_FLAG_FORCE_FFT2D = 1, 2, 4
+MD_FLAG_RL, MD_FLAG_NO_FUSED, MD_FLAG_FORCE_FFT2D, MD_FLAG_GENERIC_LINES = 1, 2, 4, 8
 
 
 class CudaUnavailable(RuntimeError):

@@ -22,6 +22,7 @@
 
 #include "../../include/mdcuda.h"
 #include "md_fused.h"
+#include "md_lines_fast.h"
 #include "md_plane.h"
 
 using namespace md;
@@ -115,7 +116,7 @@ struct DevBuf {
 
 struct md_plan {
     md_plan_desc d{};
-    std::vector<double> w;
+    std::vector<double> w, wrev;
     int es = 8;                 // element size
     int path = PATH_LINES;
     bool robust = true, has_d = true;
@@ -141,6 +142,7 @@ struct md_plan {
     size_t h_pin_bytes = 0;
     int64_t chunk = 0;          // frames per internal chunk (0 = auto)
     bool fused = false;         // whole-iteration-loop fused kernel applies
+    bool fast_lines = false;    // register-window iteration kernel applies
     std::string describe;
 
     int64_t frame_elems() const { return (int64_t)d.height * d.width; }
@@ -339,11 +341,13 @@ int32_t md_plan_create(const md_plan_desc *desc, md_plan **out) {
         const bool use_box = isbox;   // box taps realised as a sliding window in every mode
         P->lblur = line_conv(*P, false, use_box, periodic);
         P->ladj = line_conv(*P, true, use_box, periodic);
+        P->wrev.assign(P->w.rbegin(), P->w.rend());
         if (!use_box) {
-            std::vector<double> rev(P->w.rbegin(), P->w.rend());
             if ((rc = upload(&P->d_taps_blur, P->w.data(), P->w.size()))) return bail(rc);
-            if ((rc = upload(&P->d_taps_adj, rev.data(), rev.size()))) return bail(rc);
+            if ((rc = upload(&P->d_taps_adj, P->wrev.data(), P->wrev.size()))) return bail(rc);
         }
+        P->fast_lines = !(desc->flags & MD_FLAG_GENERIC_LINES) &&
+                        iter_fast_supported(desc->dtype, P->n, P->lblur, P->ladj);
         if (is_pow2(P->n)) {
             P->log2n = ilog2(P->n);
             if ((rc = build_twiddles(P->n, desc->dtype, &P->d_tw_n))) return bail(rc);
@@ -359,8 +363,10 @@ int32_t md_plan_create(const md_plan_desc *desc, md_plan **out) {
         if (wiener && (size_t)P->n > lim) return bail(fail(MD_EINVAL, "blur-axis length above the on-chip FFT limit"));
         P->fused = fused_lines_supported(desc->dtype, P->n, P->m, desc->flags);
         snprintf(buf, sizeof buf, "lines: n=%d m=%d %s %s %s, %s", P->n, P->m, P->vert ? "vertical" : "horizontal",
-                 use_box ? "box-sliding" : "taps", periodic ? "periodic" : "clamped",
-                 P->fused ? "fused persistent iteration kernel" : "k_wiener_lines + k_iter_lines per iteration");
+                 use_box ? "box" : "taps", periodic ? "periodic" : "clamped",
+                 P->fused ? "fused persistent iteration kernel"
+                          : (P->fast_lines ? "k_wiener_lines + k_iter_lines_fast per iteration"
+                                           : "k_wiener_lines + k_iter_lines per iteration"));
     } else {
         // ---------------------------------------------------------------- PLANE
         if (desc->psf_rows > H || desc->psf_cols > W) return bail(fail(MD_EINVAL, "PSF support exceeds the image dimensions"));
@@ -483,6 +489,27 @@ int run_lines(md_plan &P, const void *f, void *u, int64_t nb, char *scr, cudaStr
         fa.has_d = P.has_d; fa.robust = P.robust; fa.lut = P.lut;
         CU(launch_fused_lines<T>(fa, nb, st));
         prof_mark(st, PK_ITER);
+        return MD_OK;
+    }
+    if (P.fast_lines) {
+        IterFastDesc fd{};
+        fd.fpos = FP; fd.n = P.n; fd.m = P.m; fd.blur = P.lblur; fd.adj = P.ladj;
+        fd.taps_blur_host = P.w.data(); fd.taps_adj_host = P.wrev.data();
+        fd.alpha = P.d.alpha; fd.eps_d2 = P.d.eps_data * P.d.eps_data; fd.eps_r2 = P.d.eps_reg * P.d.eps_reg;
+        fd.has_d = P.has_d; fd.lut = P.lut;
+        void *cur = A;
+        for (int k = 0; k < K; ++k) {
+            const bool last = k == K - 1;
+            void *dst = (last && !P.vert) ? u : (cur == A ? B : A);
+            fd.u_in = cur; fd.u_out = dst;
+            CU(launch_iter_fast<T>(fd, P.robust, nb, st));
+            prof_mark(st, PK_ITER);
+            cur = dst;
+        }
+        if (P.vert) {
+            CU(launch_transpose<T>(cur, u, nullptr, P.m, P.n, 0.0, 0, nb, st));
+            prof_mark(st, PK_LAYOUT);
+        }
         return MD_OK;
     }
     IterLinesArgs it{};

@@ -1,0 +1,55 @@
+// md_linefast.cuh -- register-window building blocks for line (1D blur) kernels.
+//
+// A warp owns whole lines; lane s holds the 8 consecutive samples j = 8s .. 8s+7 of a line
+// ("segment"). Lines live in shared memory extended by a halo of HW samples on each side
+// (edge-replicated for the clamped convolvers, wrapped for the periodic ones) in a
+// "9-stride" layout -- one pad word after every 8 samples -- so that the 32 lanes of a warp,
+// whose segments start 8 samples apart, hit 32 distinct banks, and so that every element of
+// a lane's window sits at a COMPILE-TIME offset from the lane's base address. Convolutions
+// then need no index arithmetic at all: out[r] = sum_k w[k] * v[r + k], k in [-R, R], with
+// the dense tap vector w passed as kernel parameters (constant-bank FFMA operands).
+#pragma once
+
+#include "md_common.cuh"
+
+namespace md {
+
+constexpr int SEG = 8;
+
+template <int R> struct HaloOf { static constexpr int value = R <= 8 ? 8 : (R <= 16 ? 16 : 32); };
+
+// storage index of extended sample e (0 <= e < n + 2*HW)
+__host__ __device__ constexpr int xaddr(int e) { return e + (e >> 3); }
+__host__ __device__ constexpr int xline_len(int n, int hw) { return xaddr(n + 2 * hw) + 1; }
+
+// compile-time offset of element k (relative to the segment start) from the lane base
+__host__ __device__ constexpr int koff(int k) { return k + (k >= 0 ? k / 8 : -((-k + 7) / 8)); }
+
+template <typename T, int R> struct DenseTaps { T w[2 * R + 1]; };
+
+// fast reciprocal / reciprocal square root: MUFU for float, IEEE-accurate for double
+__device__ __forceinline__ float frcp(float x) { return __fdividef(1.0f, x); }
+__device__ __forceinline__ double frcp(double x) { return 1.0 / x; }
+__device__ __forceinline__ float frsqrt(float x) { return rsqrtf(x); }
+__device__ __forceinline__ double frsqrt(double x) { return 1.0 / sqrt(x); }
+__device__ __forceinline__ float flog(float x) { return __logf(x); }
+__device__ __forceinline__ double flog(double x) { return log(x); }
+
+// r1 by table interpolation with both extensions evaluated branch-free (deconv.py:114-134)
+template <typename T>
+__device__ __forceinline__ T r1_fast(const LutView &L, T x) {
+    const T xc = x < T(kLutUpper) ? x : T(kLutUpper);
+    T pos = (xc - T(kLutDelta)) * T(kLutInvStep);
+    pos = pos > T(0) ? pos : T(0);
+    int i = (int)pos;
+    i = i < kLutCount - 2 ? i : kLutCount - 2;
+    const T t = pos - T(i);
+    const T lo = lut_fetch(L, i, T(0));
+    const T hi = lut_fetch(L, i + 1, T(0));
+    T r = lo + (hi - lo) * t;
+    if (x > T(kLutUpper)) r = T(L.slope) * x + T(L.intercept);
+    if (x < T(kLutDirectBelow)) r = x - T(1) - flog(x);
+    return r;
+}
+
+}  // namespace md

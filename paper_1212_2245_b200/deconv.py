@@ -75,8 +75,10 @@ def _dev(a, dtype="float64"):
         a = a.values
     if isinstance(a, torch.Tensor):
         return a.to(device="cuda", dtype=torch_dtype(dtype)).contiguous()
-    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(
-        device="cuda", dtype=torch_dtype(dtype)).contiguous()
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if not a.flags.writeable:
+        a = a.copy()
+    return torch.from_numpy(a).to(device="cuda", dtype=torch_dtype(dtype)).contiguous()
 
 
 def _host(t) -> np.ndarray:
@@ -189,7 +191,7 @@ class GpuConvolver:
 
     def __init__(self, psf: Psf, shape, mode: str, dtype: str = "float64"):
         self.psf, self.shape, self.mode, self.dtype = psf, tuple(shape), mode, dtype
-        self._plan = _plan(shape, psf, DeconvParams(iterations=0), mode, dtype=dtype)
+        self._plan = _plan(shape, psf, DeconvParams(iterations=0), mode, init="clamped", dtype=dtype)
 
     def _apply(self, a, which):
         import torch
@@ -352,7 +354,8 @@ class DeblurPipeline:
 
     def __init__(self, shape: tuple[int, int], psf: Psf, params: DeconvParams,
                  scenario: Scenario | None = None, workers: int = 1, lut: DivergenceLut | None = None,
-                 dtype: str = "float64", fused: bool | None = None, force_fft2d: bool = False):
+                 dtype: str = "float64", fused: bool | None = None, force_fft2d: bool = False,
+                 generic_lines: bool = False):
         if scenario is None:
             scenario = default_scenario(psf)
         if scenario in (Scenario.BOX_1D, Scenario.FOURIER_1D) and not psf.is_1d:
@@ -376,7 +379,7 @@ class DeblurPipeline:
                 raise ValueError("the blur axis must have power-of-two extent")
         self.psf = psf
         self._plan = GpuPlan(self.shape, psf, params, _SCENARIO_CONV[scenario], init="wiener", dtype=dtype,
-                             force_fft2d=force_fft2d, fused=fused)
+                             force_fft2d=force_fft2d, fused=fused, generic_lines=generic_lines)
         self._wiener_plan = None
 
     @property

@@ -197,13 +197,26 @@ def test_zero_iterations_is_clamped_wiener(md):
     np.testing.assert_allclose(out, want, rtol=0, atol=1e-12)
 
 
-def test_output_strictly_positive_and_improves_psnr(md):
-    g = md.make_test_image(256, 256)
-    psf = md.Psf.uniform_box(md.BlurAxis.HORIZONTAL, 15)
-    f = md.quantize(md.add_gaussian_noise(md.synth_blur(g, psf), 5.0, seed=5))
+def test_output_strictly_positive_and_improves_snr(md):
+    """test_pipeline.py:57-69 of the reference."""
+    g = md.make_test_image(128, 128)
+    psf = md.Psf.uniform_box(md.BlurAxis.VERTICAL, 15)
+    f = md.synth_blur(g, psf)
     out = md.wr3l(f, psf, md.DeconvParams())
     assert out.values.min() > 0.0
-    assert md.psnr(out, g) > md.psnr(f, g)
+    assert md.snr(out, g) > md.snr(f, g)
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+@pytest.mark.parametrize("name", ["pipe_c1_box_h15_256", "pipe_box_v21p5_64x96", "pipe_f1d_v9_128x64",
+                                  "pipe_f1d_h7_64x128", "pipe_box_h15_alpha0_64"])
+def test_generic_line_kernel_golden(md, name, dtype):
+    """The generic (index-resolving) line kernel stays correct next to the fast one."""
+    d = load_golden(name)
+    scen = md.Scenario[SCEN[str(d["scenario"])]]
+    out = md.DeblurPipeline(d["f"].shape, product_psf(d), product_params(d), scen, dtype=dtype,
+                            generic_lines=True).run(md.Image(d["f"])).values
+    assert np.abs(out - d["out"]).max() <= (FP64_TOL if dtype == "float64" else TOL)
 
 
 def test_contract_errors(md):
