@@ -361,7 +361,7 @@ int32_t md_plan_create(const md_plan_desc *desc, md_plan **out) {
         }
         const size_t lim = desc->dtype == MD_F64 ? 4096 : 8192;
         if (wiener && (size_t)P->n > lim) return bail(fail(MD_EINVAL, "blur-axis length above the on-chip FFT limit"));
-        P->fused = fused_lines_supported(desc->dtype, P->n, P->m, desc->flags);
+        P->fused = P->fast_lines && fused_lines_supported(desc->dtype, P->n, P->m, desc->flags);
         snprintf(buf, sizeof buf, "lines: n=%d m=%d %s %s %s, %s", P->n, P->m, P->vert ? "vertical" : "horizontal",
                  use_box ? "box" : "taps", periodic ? "periodic" : "clamped",
                  P->fused ? "fused persistent iteration kernel"
@@ -484,7 +484,7 @@ int run_lines(md_plan &P, const void *f, void *u, int64_t nb, char *scr, cudaStr
         FusedLinesArgs fa{};
         fa.u_in = A; fa.fpos = FP; fa.u_out = u; fa.n = P.n; fa.m = P.m; fa.iterations = K;
         fa.out_vert = P.vert; fa.blur = P.lblur; fa.adj = P.ladj;
-        fa.taps_blur = P.d_taps_blur; fa.taps_adj = P.d_taps_adj;
+        fa.taps_blur_host = P.w.data(); fa.taps_adj_host = P.wrev.data();
         fa.alpha = P.d.alpha; fa.eps_d2 = P.d.eps_data * P.d.eps_data; fa.eps_r2 = P.d.eps_reg * P.d.eps_reg;
         fa.has_d = P.has_d; fa.robust = P.robust; fa.lut = P.lut;
         CU(launch_fused_lines<T>(fa, nb, st));
@@ -648,7 +648,7 @@ int32_t md_plan_set_chunk(md_plan *P, int64_t frames) {
 
 int32_t md_plan_set_fused(md_plan *P, int32_t on) {
     if (!P) return fail(MD_EINVAL, "null plan");
-    if (on && !(P->path == PATH_LINES && fused_lines_supported(P->d.dtype, P->n, P->m, 0)))
+    if (on && !(P->path == PATH_LINES && P->fast_lines && fused_lines_supported(P->d.dtype, P->n, P->m, 0)))
         return fail(MD_EINVAL, "fused kernel not available for this plan");
     P->fused = on != 0;
     return MD_OK;

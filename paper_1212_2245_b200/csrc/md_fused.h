@@ -1,4 +1,4 @@
-// md_fused.h -- the persistent whole-pipeline kernel for 1D blur on small frames.
+// md_fused.h -- the cluster-resident whole-iteration-loop kernel for 1D blur on small frames.
 #pragma once
 
 #include "md_internal.h"
@@ -11,7 +11,7 @@ struct FusedLinesArgs {
     void *u_out;           // native-layout result
     int n, m, iterations, out_vert;
     LineConv blur, adj;
-    const double *taps_blur, *taps_adj;
+    const double *taps_blur_host, *taps_adj_host;
     double alpha, eps_d2, eps_r2;
     int has_d, robust;
     LutView lut;

@@ -270,21 +270,6 @@ cudaError_t launch_iter_fast_t(const IterFastArgs<T, R> &a, bool robust, int64_t
     return cudaGetLastError();
 }
 
-template <typename T, int R>
-void fill_dense(DenseTaps<T, R> &d, const LineConv &c, const double *taps_host) {
-    for (int k = -R; k <= R; ++k) d.w[k + R] = T(0);
-    if (c.kind == LINE_BOX) {
-        for (int k = c.lo; k <= c.hi; ++k) d.w[k + R] = T(c.wi);
-        if (c.ends) {
-            d.w[c.elo + R] = T(c.we);
-            d.w[c.ehi + R] = T(c.we);
-        }
-    } else {
-        // out[j] = sum_t w[t] a[j + center - t]  ->  k = center - t
-        for (int t = 0; t < c.ntaps; ++t) d.w[c.center - t + R] = T(taps_host[t]);
-    }
-}
-
 int line_radius(const LineConv &c) {
     int lo, hi;
     if (c.kind == LINE_BOX) {

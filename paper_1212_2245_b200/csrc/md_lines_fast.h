@@ -32,6 +32,22 @@ struct IterFastDesc {
 };
 
 int line_radius(const LineConv &c);
+
+// dense tap vector over [-R, R] for one direction of a line convolution
+template <typename T, int R>
+void fill_dense(DenseTaps<T, R> &d, const LineConv &c, const double *taps_host) {
+    for (int k = -R; k <= R; ++k) d.w[k + R] = T(0);
+    if (c.kind == LINE_BOX) {
+        for (int k = c.lo; k <= c.hi; ++k) d.w[k + R] = T(c.wi);
+        if (c.ends) {
+            d.w[c.elo + R] = T(c.we);
+            d.w[c.ehi + R] = T(c.we);
+        }
+    } else {
+        // out[j] = sum_t w[t] a[j + center - t]  ->  k = center - t
+        for (int t = 0; t < c.ntaps; ++t) d.w[c.center - t + R] = T(taps_host[t]);
+    }
+}
 bool iter_fast_supported(int dtype, int n, const LineConv &blur, const LineConv &adj);
 template <typename T> cudaError_t launch_iter_fast(const IterFastDesc &, bool robust, int64_t batch, cudaStream_t);
 

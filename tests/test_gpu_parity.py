@@ -271,6 +271,39 @@ def test_rrrl_with_alpha0_identity_weight_equals_rl(md):
         np.testing.assert_array_equal(u_rr.values, u_rl.values)
 
 
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+@pytest.mark.parametrize("name", ["pipe_c1_box_h15_256", "pipe_box_v21p5_64x96", "pipe_f1d_v9_128x64",
+                                  "pipe_f1d_h7_64x128", "pipe_box_h15_alpha0_64", "pipe_f1d_box_v27_256"])
+def test_fused_cluster_kernel_matches_per_iteration_kernel(md, name, dtype):
+    """The cluster-resident kernel (DSMEM halo exchange) reproduces the per-iteration kernel
+    and the reference."""
+    d = load_golden(name)
+    scen = md.Scenario[SCEN[str(d["scenario"])]]
+    shape = d["f"].shape
+    on = md.DeblurPipeline(shape, product_psf(d), product_params(d), scen, dtype=dtype)
+    if not on.plan.fused:
+        pytest.skip(f"fused kernel not applicable: {on.plan.describe}")
+    off = md.DeblurPipeline(shape, product_psf(d), product_params(d), scen, dtype=dtype, fused=False)
+    a = on.run(md.Image(d["f"])).values
+    b = off.run(md.Image(d["f"])).values
+    np.testing.assert_allclose(a, b, rtol=0, atol=1e-9 if dtype == "float64" else 1e-3)
+    assert np.abs(a - d["out"]).max() <= (FP64_TOL if dtype == "float64" else TOL)
+
+
+def test_fused_batch_many_frames(md):
+    import torch
+    d = load_golden("pipe_c1_box_h15_256")
+    pipe = md.DeblurPipeline((256, 256), product_psf(d), product_params(d), dtype="float32")
+    assert pipe.plan.fused
+    frames = torch.from_numpy(np.stack([d["f"]] * 300)).cuda().float()
+    frames[7] += 3.0
+    out = pipe.run_batch(frames).double().cpu().numpy()
+    ref = pipe.run(md.Image(d["f"])).values
+    for i in (0, 1, 150, 299):
+        np.testing.assert_array_equal(out[i], ref)
+    assert np.abs(out[7] - ref).max() > 0.1
+
+
 def test_plan_reports_launches(md):
     pipe = md.DeblurPipeline((256, 256), md.Psf.uniform_box(md.BlurAxis.HORIZONTAL, 15), md.DeconvParams())
     assert pipe.plan.launch_count(16) >= 2
