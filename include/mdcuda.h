@@ -114,6 +114,15 @@ int32_t md_run_host(md_plan *plan, const double *f, double *u, int64_t batch, vo
  * [3] number of launch groups timed. */
 int32_t md_run_profile(md_plan *plan, const void *f, void *u, int64_t batch, void *stream,
                        double *ms_out);
+/* host frame types for md_run_host_ex */
+#define MD_IO_F64 0
+#define MD_IO_F32 1
+#define MD_IO_U8 2    /* 8-bit grey frames (camera / PGM capture), input only */
+/* md_run from HOST frames of type in_type to HOST results of type out_type. Chunks are
+ * pipelined over internal streams (H2D of chunk c+1 overlaps compute of chunk c and D2H of
+ * chunk c-1); pinned host buffers make the copies asynchronous. Synchronises `stream`. */
+int32_t md_run_host_ex(md_plan *plan, const void *f, int32_t in_type, void *u, int32_t out_type,
+                       int64_t batch, void *stream);
 /* number of kernel launches md_run issues for one call (for the bench's gpu_launches) */
 int32_t md_run_launch_count(const md_plan *plan, int64_t batch);
 

@@ -150,11 +150,16 @@ def r1(x: np.ndarray, lut: Lut | None = None) -> np.ndarray:
     below ``direct_below``, linear continuation above ``upper``."""
     lut = default_lut() if lut is None else lut
     x = np.asarray(x, dtype=np.float64)
-    t = (np.minimum(x, lut.upper) - lut.delta) * (1.0 / lut.step)
+    t = np.minimum(x, lut.upper)
+    t -= lut.delta
+    t *= 1.0 / lut.step
     i = np.clip(t.astype(np.int64), 0, lut.table.shape[0] - 2)
     t -= i
     lo = lut.table[i]
-    res = lo + (lut.table[i + 1] - lo) * t
+    res = lut.table[i + 1]
+    res -= lo
+    res *= t
+    res += lo
     above = x > lut.upper
     if above.any():
         res[above] = lut.slope * x[above] + lut.intercept
@@ -168,30 +173,42 @@ def r1(x: np.ndarray, lut: Lut | None = None) -> np.ndarray:
 def robust_weight(f, b, eps_data=1.0, floor=0.1, lut=None, floored=False):
     """deconv.py:142-162 (and the public wrapper 165-180 without its checks)."""
     if floored:
-        r = r1(b / f, lut) * f
+        r = r1(b / f, lut)
+        r *= f
     else:
         small = f < floor
         fs = np.where(small, 1.0, f)
         r = r1(b / fs, lut) * fs
         r = np.where(small, np.maximum(b - f, 0.0), r)
-    return 0.5 / np.sqrt(r + eps_data * eps_data)
+    r += eps_data * eps_data
+    np.sqrt(r, out=r)
+    np.divide(0.5, r, out=r)
+    return r
 
 
 def diffusion(u: np.ndarray, eps_reg: float) -> np.ndarray:
-    """deconv.py:187-213 -- TV divergence with Neumann boundary; x fluxes first."""
-    gx = np.diff(u, axis=1)
-    gy = np.diff(u, axis=0)
-    q = np.zeros_like(u)
-    q[:, 1:] += gx * gx
-    q[:, :-1] += gx * gx
-    q[1:, :] += gy * gy
-    q[:-1, :] += gy * gy
-    g = 0.5 / np.sqrt(0.5 * q + eps_reg * eps_reg)
+    """deconv.py:187-213 -- TV divergence with Neumann boundary; x fluxes first.
+    (In-place NumPy so that the CPU baseline costs what the reference costs.)"""
+    gx = u[:, 1:] - u[:, :-1]
+    gy = u[1:, :] - u[:-1, :]
+    gx2 = gx * gx
+    gy2 = gy * gy
+    g = np.zeros_like(u)
+    g[:, 1:] += gx2
+    g[:, :-1] += gx2
+    g[1:, :] += gy2
+    g[:-1, :] += gy2
+    g *= 0.5
+    g += eps_reg * eps_reg
+    np.sqrt(g, out=g)
+    np.divide(0.5, g, out=g)
     d = np.zeros_like(u)
-    fx = (g[:, 1:] + g[:, :-1]) * gx
+    fx = g[:, 1:] + g[:, :-1]
+    fx *= gx
     d[:, :-1] += fx
     d[:, 1:] -= fx
-    fy = (g[1:, :] + g[:-1, :]) * gy
+    fy = g[1:, :] + g[:-1, :]
+    fy *= gy
     d[:-1, :] += fy
     d[1:, :] -= fy
     return d
@@ -547,14 +564,24 @@ def combine(u, f, b, weight, diff, alpha, conv):
     if weight is None:
         num, den = conv.adjoint(ratio), None
     else:
-        num, den = conv.adjoint_pair(weight * ratio, weight)
+        ratio *= weight
+        num, den = conv.adjoint_pair(ratio, weight)
     if diff is not None and alpha != 0.0:
-        num = num + alpha * np.maximum(diff, 0.0)
-        neg = alpha * np.minimum(diff, 0.0)
-        den = 1.0 - neg if den is None else den - neg
+        pos = np.maximum(diff, 0.0)
+        pos *= alpha
+        num += pos
+        neg = np.minimum(diff, 0.0)
+        neg *= alpha
+        if den is None:
+            den = 1.0 - neg
+        else:
+            den -= neg
     if den is None:
         return u * num
-    return (u * num) / np.maximum(den, GUARD)
+    np.maximum(den, GUARD, out=den)
+    out = u * num
+    out /= den
+    return out
 
 
 def rrrl_iteration(u, fpos, conv, params: OParams, lut=None, robust=True):

@@ -21,6 +21,7 @@ MD_PSF_GENERAL_2D, MD_PSF_GENERAL_1D, MD_PSF_BOX_1D = 0, 1, 2
 MD_AXIS_NONE, MD_AXIS_VERTICAL, MD_AXIS_HORIZONTAL = -1, 0, 1
 MD_CONV_BOX, MD_CONV_SPATIAL, MD_CONV_FOURIER, MD_CONV_FOURIER2D = 0, 1, 2, 3
 MD_INIT_WIENER, MD_INIT_CLAMPED = 0, 1
+MD_IO_F64, MD_IO_F32, MD_IO_U8 = 0, 1, 2
 MD_FLAG_RL, MD_FLAG_NO_FUSED, MD_FLAG_FORCE_FFT2D, MD_FLAG_GENERIC_LINES = 1, 2, 4, 8
 
 
@@ -63,6 +64,7 @@ SIGNATURES = {
     "md_plan_is_fused": (_I32, [_P]),
     "md_run": (_I32, [_P, _P, _P, _I64, _P]),
     "md_run_host": (_I32, [_P, _P, _P, _I64, _P]),
+    "md_run_host_ex": (_I32, [_P, _P, _I32, _P, _I32, _I64, _P]),
     "md_run_launch_count": (_I32, [_P, _I64]),
     "md_run_profile": (_I32, [_P, _P, _P, _I64, _P, ctypes.POINTER(_D)]),
     "md_wiener": (_I32, [_P, _P, _P, _I64, _P]),

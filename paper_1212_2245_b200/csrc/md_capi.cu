@@ -51,15 +51,25 @@ enum Path { PATH_LINES = 0, PATH_PLANE_DIRECT = 1, PATH_PLANE_FFT = 2 };
 // 1 = RRRL iterations, 2 = layout (transposes)
 enum { PK_INIT = 0, PK_ITER = 1, PK_LAYOUT = 2, PK_KINDS = 3 };
 struct Prof {
-    static constexpr int kMax = 4096;
-    cudaEvent_t ev[kMax + 1];
-    int kind[kMax + 1];
+    std::vector<cudaEvent_t> ev;     // persistent per-thread pool (created once, reused)
+    std::vector<int> kind;
     int n = 0;
+    bool active = false;
+    cudaEvent_t get(int i) {
+        while ((int)ev.size() <= i) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            ev.push_back(e);
+            kind.push_back(0);
+        }
+        return ev[i];
+    }
 };
+thread_local Prof g_prof_pool;
 thread_local Prof *g_prof = nullptr;
 inline void prof_mark(cudaStream_t st, int kind) {
-    if (!g_prof || g_prof->n >= Prof::kMax) return;
-    cudaEventRecord(g_prof->ev[g_prof->n + 1], st);
+    if (!g_prof) return;
+    cudaEventRecord(g_prof->get(g_prof->n + 1), st);
     g_prof->kind[g_prof->n + 1] = kind;
     ++g_prof->n;
 }
@@ -99,6 +109,14 @@ __global__ void k_make_filter(const double2 *h, int64_t count, double K, double2
     }
 }
 
+// dst[k] = src[bitrev(k)] for complex elements of `es` bytes (bit-reversed -> natural order)
+__global__ void k_unbitrev(const unsigned char *src, unsigned char *dst, int n, int log2n, int es) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const int r = (int)(__brev((unsigned)k) >> (32 - log2n));
+        for (int b = 0; b < es; ++b) dst[(size_t)k * es + b] = src[(size_t)r * es + b];
+    }
+}
+
 struct DevBuf {
     void *p = nullptr;
     size_t bytes = 0;
@@ -131,6 +149,8 @@ struct md_plan {
     // FFT tables (dtype copies; fp64 masters are temporaries)
     void *d_tw_n = nullptr, *d_tw_H = nullptr, *d_tw_W = nullptr;
     void *d_mult = nullptr;     // Wiener multiplier (lines: [n]; plane: [H][W] storage coords)
+    void *d_mult_nat = nullptr; // lines: the same multiplier in natural frequency order
+    bool wiener_reg = false;    // register four-step FFT kernel for the line Wiener step
     void *d_hspec = nullptr;    // PSF spectrum (PLANE_FFT iterations)
     // LUT
     double *d_lut64 = nullptr;
@@ -141,6 +161,19 @@ struct md_plan {
     void *h_pin = nullptr;
     size_t h_pin_bytes = 0;
     int64_t chunk = 0;          // frames per internal chunk (0 = auto)
+    cudaStream_t hstream[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t ev_start = nullptr, ev_done[3] = {nullptr, nullptr, nullptr};
+    int ensure_host_streams() {
+        if (hstream[0]) return MD_OK;
+        for (int s = 0; s < 3; ++s) {
+            if (cudaStreamCreateWithFlags(&hstream[s], cudaStreamNonBlocking) != cudaSuccess ||
+                cudaEventCreateWithFlags(&ev_done[s], cudaEventDisableTiming) != cudaSuccess)
+                return fail(MD_ECUDA, "stream creation failed");
+        }
+        if (cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming) != cudaSuccess)
+            return fail(MD_ECUDA, "event creation failed");
+        return MD_OK;
+    }
     bool fused = false;         // whole-iteration-loop fused kernel applies
     bool fast_lines = false;    // register-window iteration kernel applies
     std::string describe;
@@ -148,12 +181,17 @@ struct md_plan {
     int64_t frame_elems() const { return (int64_t)d.height * d.width; }
     ~md_plan() {
         for (void *p : {(void *)d_taps_blur, (void *)d_taps_adj, (void *)d_ptaps_blur, (void *)d_ptaps_adj, d_tw_n,
-                        d_tw_H, d_tw_W, d_mult, d_hspec, (void *)d_lut64, (void *)d_lut32})
+                        d_tw_H, d_tw_W, d_mult, d_mult_nat, d_hspec, (void *)d_lut64, (void *)d_lut32})
             if (p) cudaFree(p);
         scratch.release();
         stage.release();
         partial.release();
         if (h_pin) cudaFreeHost(h_pin);
+        for (int s = 0; s < 3; ++s) {
+            if (hstream[s]) cudaStreamDestroy(hstream[s]);
+            if (ev_done[s]) cudaEventDestroy(ev_done[s]);
+        }
+        if (ev_start) cudaEventDestroy(ev_start);
     }
 };
 
@@ -358,10 +396,25 @@ int32_t md_plan_create(const md_plan_desc *desc, md_plan **out) {
             rc = make_filter(h64, P->n, desc->wiener_k, desc->dtype, &P->d_mult);
             cudaFree(h64);
             if (rc) return bail(rc);
+            const int ces = desc->dtype == MD_F64 ? 16 : 8;
+            CU(cudaMalloc(&P->d_mult_nat, (size_t)P->n * ces));
+            if (P->n > 1) {
+                k_unbitrev<<<(P->n + 255) / 256, 256>>>((const unsigned char *)P->d_mult, (unsigned char *)P->d_mult_nat,
+                                                        P->n, P->log2n, ces);
+            } else {
+                CU(cudaMemcpy(P->d_mult_nat, P->d_mult, ces, cudaMemcpyDeviceToDevice));
+            }
+            CU(cudaGetLastError());
+            CU(cudaDeviceSynchronize());
+            P->wiener_reg = !(desc->flags & MD_FLAG_GENERIC_LINES) && wiener_reg_supported(desc->dtype, P->n);
         }
         const size_t lim = desc->dtype == MD_F64 ? 4096 : 8192;
         if (wiener && (size_t)P->n > lim) return bail(fail(MD_EINVAL, "blur-axis length above the on-chip FFT limit"));
-        P->fused = P->fast_lines && fused_lines_supported(desc->dtype, P->n, P->m, desc->flags);
+        // default: the cluster kernel for float (measured faster); float64 keeps the
+        // per-iteration kernel (16-CTA clusters at one CTA per SM lose to it), opt-in via
+        // md_plan_set_fused
+        P->fused = desc->dtype == MD_F32 && P->fast_lines &&
+                   fused_lines_supported(desc->dtype, P->n, P->m, desc->flags);
         snprintf(buf, sizeof buf, "lines: n=%d m=%d %s %s %s, %s", P->n, P->m, P->vert ? "vertical" : "horizontal",
                  use_box ? "box" : "taps", periodic ? "periodic" : "clamped",
                  P->fused ? "fused persistent iteration kernel"
@@ -467,7 +520,12 @@ int run_lines(md_plan &P, const void *f, void *u, int64_t nb, char *scr, cudaStr
         a.mult = P.d_mult; a.tw = P.d_tw_n; a.floor = P.d.floor; a.clamp = 1;
         if (K == 0) { a.out = u; a.out_vert = P.vert; a.fpos = nullptr; }
         else { a.out = A; a.out_vert = 0; a.fpos = FP; }
-        CU(launch_wiener_lines<T>(a, nb, st));
+        if (P.wiener_reg) {
+            a.mult = P.d_mult_nat;
+            CU(launch_wiener_reg<T>(a, nb, st));
+        } else {
+            CU(launch_wiener_lines<T>(a, nb, st));
+        }
         prof_mark(st, PK_INIT);
         if (K == 0) return MD_OK;
     } else {
@@ -614,6 +672,15 @@ int run_plane(md_plan &P, const void *f, void *u, int64_t nb, char *scr, cudaStr
 }
 
 template <typename T>
+int run_chunk(md_plan &P, const void *f, void *u, int64_t nb, char *scr, cudaStream_t st) {
+    return P.path == PATH_LINES ? run_lines<T>(P, f, u, nb, scr, st) : run_plane<T>(P, f, u, nb, scr, st);
+}
+
+constexpr int kHostStreams = 3;
+inline size_t align_up(size_t b) { return (b + 255) & ~(size_t)255; }
+inline int io_bytes(int t) { return t == MD_IO_F64 ? 8 : (t == MD_IO_F32 ? 4 : 1); }
+
+template <typename T>
 int run_typed(md_plan &P, const void *f, void *u, int64_t batch, cudaStream_t st) {
     const int64_t chunk = auto_chunk(P, batch);
     const size_t need = (size_t)scratch_fields(P) * P.frame_elems() * sizeof(T) * chunk;
@@ -667,14 +734,14 @@ int32_t md_run(md_plan *P, const void *f, void *u, int64_t batch, void *stream) 
 int32_t md_run_profile(md_plan *P, const void *f, void *u, int64_t batch, void *stream, double *ms_out) {
     if (!P || !ms_out) return fail(MD_EINVAL, "bad arguments");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    Prof *pr = new Prof();
-    for (int i = 0; i <= Prof::kMax; ++i) cudaEventCreate(&pr->ev[i]);
-    cudaEventRecord(pr->ev[0], st);
+    Prof *pr = &g_prof_pool;
+    pr->n = 0;
+    cudaEventRecord(pr->get(0), st);
     g_prof = pr;
     int rc = md_run(P, f, u, batch, stream);
     g_prof = nullptr;
     if (rc == MD_OK) {
-        cudaStreamSynchronize(st);
+        cudaEventSynchronize(pr->ev[pr->n]);
         for (int k = 0; k < PK_KINDS; ++k) ms_out[k] = 0.0;
         for (int i = 1; i <= pr->n; ++i) {
             float ms = 0.f;
@@ -683,8 +750,6 @@ int32_t md_run_profile(md_plan *P, const void *f, void *u, int64_t batch, void *
         }
         ms_out[PK_KINDS] = (double)pr->n;
     }
-    for (int i = 0; i <= Prof::kMax; ++i) cudaEventDestroy(pr->ev[i]);
-    delete pr;
     return rc;
 }
 
@@ -709,34 +774,65 @@ int32_t md_run_launch_count(const md_plan *P, int64_t batch) {
     return (int32_t)(chunks * sub * per);
 }
 
-int32_t md_run_host(md_plan *P, const double *f, double *u, int64_t batch, void *stream) {
+int32_t md_run_host_ex(md_plan *P, const void *f, int32_t in_type, void *u, int32_t out_type, int64_t batch,
+                       void *stream) {
     if (!P || !f || !u || batch < 0) return fail(MD_EINVAL, "bad arguments");
+    if (in_type != MD_IO_F64 && in_type != MD_IO_F32 && in_type != MD_IO_U8) return fail(MD_EINVAL, "bad input type");
+    if (out_type != MD_IO_F64 && out_type != MD_IO_F32) return fail(MD_EINVAL, "bad output type");
     if (batch == 0) return MD_OK;
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaStream_t user = static_cast<cudaStream_t>(stream);
     const int64_t fe = P->frame_elems();
-    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(batch, (256ll << 20) / (fe * 8)));
-    // device staging: f64 in, T in, T out, f64 out
-    const size_t fbT = (size_t)fe * P->es * chunk, fb64 = (size_t)fe * 8 * chunk;
-    int rc = P->stage.ensure(2 * fb64 + 2 * fbT);
+    const int ib = io_bytes(in_type), ob = io_bytes(out_type);
+    // pipeline: chunk c runs H2D -> convert -> pipeline -> convert -> D2H on internal stream
+    // c % kHostStreams, so copies of one chunk overlap compute of the next
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(batch, std::max<int64_t>(1, (64ll << 20) / (fe * 8))));
+    int rc = P->ensure_host_streams();
     if (rc) return rc;
-    char *s64in = (char *)P->stage.p, *s64out = s64in + fb64, *sTin = s64out + fb64, *sTout = sTin + fbT;
-    for (int64_t b0 = 0; b0 < batch; b0 += chunk) {
+    const size_t in_b = (size_t)fe * ib * chunk, tin_b = (size_t)fe * P->es * chunk, tout_b = tin_b,
+                 out_b = (size_t)fe * ob * chunk;
+    const size_t scr_b = (size_t)scratch_fields(*P) * fe * P->es * chunk;
+    const size_t per = align_up(in_b) + align_up(tin_b) + align_up(tout_b) + align_up(out_b) + align_up(scr_b);
+    rc = P->stage.ensure(per * kHostStreams);
+    if (rc) return rc;
+    CU(cudaEventRecord(P->ev_start, user));
+    for (int s = 0; s < kHostStreams; ++s) CU(cudaStreamWaitEvent(P->hstream[s], P->ev_start, 0));
+    const int64_t saved_chunk = P->chunk;
+    P->chunk = chunk;
+    for (int64_t b0 = 0, c = 0; b0 < batch; b0 += chunk, ++c) {
         const int64_t nb = std::min(chunk, batch - b0);
-        CU(cudaMemcpyAsync(s64in, f + b0 * fe, nb * fe * 8, cudaMemcpyHostToDevice, st));
-        const void *fin = s64in;
-        void *uo = s64out;
-        if (P->d.dtype == MD_F32) {
-            CU(launch_convert<float>(s64in, sTin, nb * fe, 0, st));
-            fin = sTin;
-            uo = sTout;
+        const int s = (int)(c % kHostStreams);
+        cudaStream_t st = P->hstream[s];
+        char *base = (char *)P->stage.p + per * s;
+        char *din = base, *dtin = din + align_up(in_b), *dtout = dtin + align_up(tin_b),
+             *dout = dtout + align_up(tout_b), *dscr = dout + align_up(out_b);
+        CU(cudaMemcpyAsync(din, (const char *)f + b0 * fe * ib, nb * fe * ib, cudaMemcpyHostToDevice, st));
+        const void *fin = din;
+        if (in_type != (P->d.dtype == MD_F64 ? MD_IO_F64 : MD_IO_F32)) {
+            CU(P->d.dtype == MD_F64 ? launch_convert_in<double>(din, in_type, dtin, nb * fe, st)
+                                    : launch_convert_in<float>(din, in_type, dtin, nb * fe, st));
+            fin = dtin;
         }
-        rc = md_run(P, fin, uo, nb, stream);
-        if (rc) return rc;
-        if (P->d.dtype == MD_F32) CU(launch_convert<float>(sTout, s64out, nb * fe, 1, st));
-        CU(cudaMemcpyAsync(u + b0 * fe, s64out, nb * fe * 8, cudaMemcpyDeviceToHost, st));
+        const bool direct_out = out_type == (P->d.dtype == MD_F64 ? MD_IO_F64 : MD_IO_F32);
+        void *uo = direct_out ? (void *)dout : (void *)dtout;
+        rc = P->d.dtype == MD_F64 ? run_chunk<double>(*P, fin, uo, nb, dscr, st) : run_chunk<float>(*P, fin, uo, nb, dscr, st);
+        if (rc) { P->chunk = saved_chunk; return rc; }
+        if (!direct_out) {
+            CU(P->d.dtype == MD_F64 ? launch_convert_out<double>(dtout, dout, out_type, nb * fe, st)
+                                    : launch_convert_out<float>(dtout, dout, out_type, nb * fe, st));
+        }
+        CU(cudaMemcpyAsync((char *)u + b0 * fe * ob, dout, nb * fe * ob, cudaMemcpyDeviceToHost, st));
     }
-    CU(cudaStreamSynchronize(st));
+    P->chunk = saved_chunk;
+    for (int s = 0; s < kHostStreams; ++s) {
+        CU(cudaEventRecord(P->ev_done[s], P->hstream[s]));
+        CU(cudaStreamWaitEvent(user, P->ev_done[s], 0));
+    }
+    CU(cudaStreamSynchronize(user));
     return MD_OK;
+}
+
+int32_t md_run_host(md_plan *P, const double *f, double *u, int64_t batch, void *stream) {
+    return md_run_host_ex(P, f, MD_IO_F64, u, MD_IO_F64, batch, stream);
 }
 
 int32_t md_wiener(md_plan *P, const void *f, void *out, int64_t batch, void *stream) {
@@ -749,7 +845,13 @@ int32_t md_wiener(md_plan *P, const void *f, void *out, int64_t batch, void *str
         a.in = f; a.out = out; a.fpos = nullptr; a.n = P->n; a.log2n = P->log2n; a.m = P->m;
         a.in_vert = P->vert; a.out_vert = P->vert; a.clamp = 0; a.mult = P->d_mult; a.tw = P->d_tw_n;
         a.floor = P->d.floor;
-        CU(P->d.dtype == MD_F64 ? launch_wiener_lines<double>(a, batch, st) : launch_wiener_lines<float>(a, batch, st));
+        if (P->wiener_reg) {
+            a.mult = P->d_mult_nat;
+            CU(P->d.dtype == MD_F64 ? launch_wiener_reg<double>(a, batch, st) : launch_wiener_reg<float>(a, batch, st));
+        } else {
+            CU(P->d.dtype == MD_F64 ? launch_wiener_lines<double>(a, batch, st)
+                                    : launch_wiener_lines<float>(a, batch, st));
+        }
         return MD_OK;
     }
     if (!P->d_mult) return fail(MD_EINVAL, "2D Wiener needs power-of-two dimensions");

@@ -54,6 +54,8 @@ struct ConvLinesArgs {
 };
 
 template <typename T> cudaError_t launch_wiener_lines(const WienerLinesArgs &, int64_t, cudaStream_t);
+bool wiener_reg_supported(int dtype, int n);
+template <typename T> cudaError_t launch_wiener_reg(const WienerLinesArgs &, int64_t, cudaStream_t);
 template <typename T> cudaError_t launch_iter_lines(const IterLinesArgs &, bool robust, int64_t, cudaStream_t);
 template <typename T> cudaError_t launch_conv_lines(const ConvLinesArgs &, int64_t, cudaStream_t);
 template <typename T> cudaError_t launch_transpose(const void *in, void *out, void *out_clamped, int rows,

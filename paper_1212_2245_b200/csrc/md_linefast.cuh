@@ -27,12 +27,25 @@ __host__ __device__ constexpr int koff(int k) { return k + (k >= 0 ? k / 8 : -((
 
 template <typename T, int R> struct DenseTaps { T w[2 * R + 1]; };
 
-// fast reciprocal / reciprocal square root: MUFU for float, IEEE-accurate for double
-__device__ __forceinline__ float frcp(float x) { return __fdividef(1.0f, x); }
+// fast reciprocal / reciprocal square root / log: one MUFU op for float (operands here are
+// positive normal numbers: b >= 1e-12, fpos >= floor, q + eps^2 > 0), IEEE-accurate for double
+__device__ __forceinline__ float frcp(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
 __device__ __forceinline__ double frcp(double x) { return 1.0 / x; }
-__device__ __forceinline__ float frsqrt(float x) { return rsqrtf(x); }
+__device__ __forceinline__ float frsqrt(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
 __device__ __forceinline__ double frsqrt(double x) { return 1.0 / sqrt(x); }
-__device__ __forceinline__ float flog(float x) { return __logf(x); }
+__device__ __forceinline__ float flog(float x) {
+    float r;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r * 0.69314718055994531f;
+}
 __device__ __forceinline__ double flog(double x) { return log(x); }
 
 // r1 by table interpolation with both extensions evaluated branch-free (deconv.py:114-134)

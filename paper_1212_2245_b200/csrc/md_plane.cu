@@ -284,6 +284,25 @@ __global__ void k_convert(const void *__restrict__ in, void *__restrict__ out, i
     }
 }
 
+template <typename T>
+__global__ void k_convert_in(const void *__restrict__ in, int in_type, T *__restrict__ out, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        T v;
+        if (in_type == 2) v = T(static_cast<const unsigned char *>(in)[i]);
+        else if (in_type == 1) v = T(static_cast<const float *>(in)[i]);
+        else v = T(static_cast<const double *>(in)[i]);
+        out[i] = v;
+    }
+}
+
+template <typename T>
+__global__ void k_convert_out(const T *__restrict__ in, void *__restrict__ out, int out_type, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        if (out_type == 1) static_cast<float *>(out)[i] = (float)in[i];
+        else static_cast<double *>(out)[i] = (double)in[i];
+    }
+}
+
 // --------------------------------------------------------------------------------------
 // launchers
 
@@ -398,6 +417,18 @@ cudaError_t launch_convert(const void *in, void *out, int64_t n, int to_double, 
     return cudaGetLastError();
 }
 
+template <typename T>
+cudaError_t launch_convert_in(const void *in, int in_type, void *out, int64_t n, cudaStream_t st) {
+    k_convert_in<T><<<ew_blocks(n), 256, 0, st>>>(in, in_type, static_cast<T *>(out), n);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_convert_out(const void *in, void *out, int out_type, int64_t n, cudaStream_t st) {
+    k_convert_out<T><<<ew_blocks(n), 256, 0, st>>>(static_cast<const T *>(in), out, out_type, n);
+    return cudaGetLastError();
+}
+
 #define MD_INST(T)                                                                                      \
     template cudaError_t launch_stage_plane<T>(const StagePlaneArgs &, bool, int64_t, cudaStream_t);     \
     template cudaError_t launch_conv_plane<T>(const ConvPlaneArgs &, int64_t, cudaStream_t);             \
@@ -410,7 +441,9 @@ cudaError_t launch_convert(const void *in, void *out, int64_t n, int to_double, 
                                            void *, int64_t, double, cudaStream_t);                      \
     template cudaError_t launch_guard<T>(void *, int64_t, cudaStream_t);                                \
     template cudaError_t launch_min<T>(const void *, int64_t, double *, int, cudaStream_t);             \
-    template cudaError_t launch_convert<T>(const void *, void *, int64_t, int, cudaStream_t);
+    template cudaError_t launch_convert<T>(const void *, void *, int64_t, int, cudaStream_t);          \
+    template cudaError_t launch_convert_in<T>(const void *, int, void *, int64_t, cudaStream_t);       \
+    template cudaError_t launch_convert_out<T>(const void *, void *, int, int64_t, cudaStream_t);
 MD_INST(double)
 MD_INST(float)
 #undef MD_INST

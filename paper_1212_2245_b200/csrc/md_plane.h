@@ -52,6 +52,9 @@ template <typename T> cudaError_t launch_combine(const void *u, const void *num,
 template <typename T> cudaError_t launch_guard(void *x, int64_t n, cudaStream_t);
 template <typename T> cudaError_t launch_min(const void *x, int64_t n, double *partial, int nblocks, cudaStream_t);
 template <typename T> cudaError_t launch_convert(const void *in, void *out, int64_t n, int to_double, cudaStream_t);
+// host-frame type conversion: in_type / out_type are MD_IO_F64 (0), MD_IO_F32 (1), MD_IO_U8 (2)
+template <typename T> cudaError_t launch_convert_in(const void *in, int in_type, void *out, int64_t n, cudaStream_t);
+template <typename T> cudaError_t launch_convert_out(const void *in, void *out, int out_type, int64_t n, cudaStream_t);
 
 // ---- 2D FFT (md_fft2d.cu) ----
 // row-pass epilogues

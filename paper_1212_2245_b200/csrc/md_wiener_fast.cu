@@ -1,0 +1,236 @@
+// md_wiener_fast.cu -- per-line Wiener filter with a register-resident four-step FFT.
+//
+// Replaces apply_column_filter(a, conj(h)/(|h|^2+K)) (fft.py:236-258, deconv.py:253-254,
+// 666-672) for line lengths n = S*S (S = 8, 16, 32). Two lines ride in one complex
+// transform (real / imaginary part, as in the reference). For j = j1 + S*j2 and
+// k = k2 + S*k1:
+//   forward  : thread j1: S-point DFT over j2 (registers) -> x W_n^{j1 k2} -> smem transpose
+//              thread k2: S-point DFT over j1 (registers) -> X[k2 + S k1]
+//   filter   : X *= M[k]                                    (registers)
+//   inverse  : thread k2: inverse DFT over k1 -> x W_n^{-j1 k2} -> smem transpose
+//              thread j1: inverse DFT over k2 -> x'[j1 + S j2] / n
+// so a line pair costs two shared-memory transposes and no global round trip.
+#include "md_internal.h"
+
+namespace md {
+
+// cos / sin of 2*pi*k/32, k = 0..31 (compile-time twiddles for S <= 32)
+__device__ constexpr double kC32[32] = {
+    1.0, 0.98078528040323043, 0.92387953251128674, 0.83146961230254524, 0.70710678118654757,
+    0.55557023301960218, 0.38268343236508978, 0.19509032201612825, 0.0, -0.19509032201612825,
+    -0.38268343236508978, -0.55557023301960218, -0.70710678118654757, -0.83146961230254524,
+    -0.92387953251128674, -0.98078528040323043, -1.0, -0.98078528040323043, -0.92387953251128674,
+    -0.83146961230254524, -0.70710678118654757, -0.55557023301960218, -0.38268343236508978,
+    -0.19509032201612825, 0.0, 0.19509032201612825, 0.38268343236508978, 0.55557023301960218,
+    0.70710678118654757, 0.83146961230254524, 0.92387953251128674, 0.98078528040323043};
+
+template <int S> __host__ __device__ constexpr int bitrev(int x) {
+    int r = 0;
+    for (int b = 1; b < S; b <<= 1) {
+        r = (r << 1) | (x & 1);
+        x >>= 1;
+    }
+    return r;
+}
+
+// in-register S-point DFT, natural order in and out; INV uses conjugate twiddles (unscaled)
+template <typename T, int S, bool INV>
+__device__ __forceinline__ void dft_reg(cx_t<T> (&v)[S]) {
+    using C = cx_t<T>;
+    C w[S];
+#pragma unroll
+    for (int i = 0; i < S; ++i) w[i] = v[bitrev<S>(i)];
+#pragma unroll
+    for (int half = 1; half < S; half <<= 1) {
+#pragma unroll
+        for (int g = 0; g < S; g += 2 * half) {
+#pragma unroll
+            for (int k = 0; k < half; ++k) {
+                // twiddle exp(-+ 2 pi i k / (2 half)) = index k * (32 / (2 half)) of the 32-table
+                const int ti = k * (32 / (2 * half));
+                const T c = T(kC32[ti]);
+                const T s = INV ? T(kC32[(ti + 24) & 31]) : -T(kC32[(ti + 24) & 31]);   // sin = cos(x - pi/2)
+                C a = w[g + k], b = w[g + k + half];
+                C t;
+                if (k == 0) {
+                    t = b;
+                } else if (4 * k == 2 * half) {          // quarter turn: -i (fwd) / +i (inv)
+                    t = INV ? mkc<T>(-b.y, b.x) : mkc<T>(b.y, -b.x);
+                } else {
+                    t = mkc<T>(b.x * c - b.y * s, b.x * s + b.y * c);
+                }
+                w[g + k] = cadd(a, t);
+                w[g + k + half] = csub(a, t);
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < S; ++i) v[i] = w[i];
+}
+
+template <typename T, int S>
+__global__ void __launch_bounds__(256)
+k_wiener_lines_reg(WienerLinesArgs a) {
+    using C = cx_t<T>;
+    constexpr int N = S * S;
+    constexpr int PB = 256 / S;                 // line pairs per block
+    constexpr int TS = S + 1;                   // transpose row stride (padding)
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C *tw = reinterpret_cast<C *>(smem_raw);    // W_n^k, k < N
+    C *tr = tw + N;                             // PB transposes of S x TS
+    const int m = a.m;
+    const int64_t fr = blockIdx.y;
+    const int64_t fsz = (int64_t)N * m;
+    const T *in = static_cast<const T *>(a.in) + fr * fsz;
+    T *out = static_cast<T *>(a.out) + fr * fsz;
+    T *fpos = a.fpos ? static_cast<T *>(a.fpos) + fr * fsz : nullptr;
+    const T floor = T(a.floor);
+    const C *twg = static_cast<const C *>(a.tw);
+    for (int k = threadIdx.x; k < N; k += blockDim.x) {
+        // the plan table holds W_n^k for k < n/2; the rest is its negation
+        const C t = twg[k & (N / 2 - 1)];
+        tw[k] = k < N / 2 ? t : mkc<T>(-t.x, -t.y);
+    }
+    const int t = threadIdx.x;
+    // thread -> (pair p, lane-in-pair q); vertical input: p fastest for coalescing
+    const int p = a.in_vert ? t % PB : t / S;
+    const int q = a.in_vert ? t / PB : t % S;
+    const int pair = blockIdx.x * PB + p;
+    const int l0 = 2 * pair, l1 = 2 * pair + 1;
+    const bool v0 = l0 < m, v1 = l1 < m;
+    C *T2 = tr + p * (S * TS + 1);             // +1: spread pairs over banks
+
+    // ---- load x[q + S j2] (q = j1), fpos
+    C v[S];
+#pragma unroll
+    for (int j2 = 0; j2 < S; ++j2) {
+        const int j = q + S * j2;
+        T x0 = T(0), x1 = T(0);
+        if (a.in_vert) {
+            if (v0) x0 = in[(int64_t)j * m + l0];
+            if (v1) x1 = in[(int64_t)j * m + l1];
+        } else {
+            if (v0) x0 = in[(int64_t)l0 * N + j];
+            if (v1) x1 = in[(int64_t)l1 * N + j];
+        }
+        v[j2] = mkc<T>(x0, x1);
+        if (fpos && !a.in_vert) {
+            if (v0) fpos[(int64_t)l0 * N + j] = x0 > floor ? x0 : floor;
+            if (v1) fpos[(int64_t)l1 * N + j] = x1 > floor ? x1 : floor;
+        }
+    }
+    __syncthreads();                            // twiddle table ready
+    // ---- forward: DFT over j2, twiddle W_n^{j1 k2}, transpose
+    dft_reg<T, S, false>(v);
+#pragma unroll
+    for (int k2 = 0; k2 < S; ++k2) T2[k2 * TS + q] = cmul(v[k2], tw[(q * k2) & (N - 1)]);
+    __syncthreads();
+    // thread q = k2 now: DFT over j1
+#pragma unroll
+    for (int j1 = 0; j1 < S; ++j1) v[j1] = T2[q * TS + j1];
+    dft_reg<T, S, false>(v);
+    // ---- filter X[k2 + S k1] *= M (M stored in natural order for this kernel)
+    const C *mult = static_cast<const C *>(a.mult);
+#pragma unroll
+    for (int k1 = 0; k1 < S; ++k1) v[k1] = cmul(v[k1], __ldg(mult + q + S * k1));
+    // ---- inverse: DFT^-1 over k1, twiddle W_n^{-j1 k2}, transpose back
+    dft_reg<T, S, true>(v);
+#pragma unroll
+    for (int j1 = 0; j1 < S; ++j1) T2[q * TS + j1] = cmulc(v[j1], tw[(q * j1) & (N - 1)]);
+    __syncthreads();
+#pragma unroll
+    for (int k2 = 0; k2 < S; ++k2) v[k2] = T2[k2 * TS + q];
+    dft_reg<T, S, true>(v);
+    const T inv_n = T(1) / T(N);
+    // ---- store x'[q + S j2]
+    if (!a.in_vert && !a.out_vert) {
+#pragma unroll
+        for (int j2 = 0; j2 < S; ++j2) {
+            const int j = q + S * j2;
+            T y0 = v[j2].x * inv_n, y1 = v[j2].y * inv_n;
+            if (a.clamp) { y0 = y0 > floor ? y0 : floor; y1 = y1 > floor ? y1 : floor; }
+            if (v0) out[(int64_t)l0 * N + j] = y0;
+            if (v1) out[(int64_t)l1 * N + j] = y1;
+        }
+        return;
+    }
+    if (a.in_vert && a.out_vert) {
+#pragma unroll
+        for (int j2 = 0; j2 < S; ++j2) {
+            const int j = q + S * j2;
+            T y0 = v[j2].x * inv_n, y1 = v[j2].y * inv_n;
+            if (a.clamp) { y0 = y0 > floor ? y0 : floor; y1 = y1 > floor ? y1 : floor; }
+            if (v0) out[(int64_t)j * m + l0] = y0;
+            if (v1) out[(int64_t)j * m + l1] = y1;
+        }
+        return;
+    }
+    // vertical input -> line-major output (and fpos): stage the pair through shared memory so
+    // that consecutive threads write consecutive samples of a line
+    __syncthreads();
+    T *st = reinterpret_cast<T *>(tr);          // PB pairs x 2 lines x N reals (fits: PB*S*TS complex)
+#pragma unroll
+    for (int j2 = 0; j2 < S; ++j2) {
+        const int j = q + S * j2;
+        T y0 = v[j2].x * inv_n, y1 = v[j2].y * inv_n;
+        if (a.clamp) { y0 = y0 > floor ? y0 : floor; y1 = y1 > floor ? y1 : floor; }
+        st[(2 * p) * N + j] = y0;
+        st[(2 * p + 1) * N + j] = y1;
+    }
+    __syncthreads();
+    const int lbase = 2 * blockIdx.x * PB;
+    for (int idx = threadIdx.x; idx < 2 * PB * N; idx += blockDim.x) {
+        const int li = idx / N, j = idx - li * N;
+        if (lbase + li < m) out[(int64_t)(lbase + li) * N + j] = st[idx];
+    }
+    if (fpos) {
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < 2 * PB * N; idx += blockDim.x) {
+            const int j = idx / (2 * PB), li = idx - j * (2 * PB);
+            if (lbase + li < m) st[li * N + j] = in[(int64_t)j * m + lbase + li];
+        }
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < 2 * PB * N; idx += blockDim.x) {
+            const int li = idx / N, j = idx - li * N;
+            const T x = st[idx];
+            if (lbase + li < m) fpos[(int64_t)(lbase + li) * N + j] = x > floor ? x : floor;
+        }
+    }
+}
+
+template <typename T, int S>
+cudaError_t launch_wiener_reg_t(const WienerLinesArgs &a, int64_t batch, cudaStream_t st) {
+    constexpr int PB = 256 / S;
+    const size_t smem = (size_t)(S * S + PB * (S * (S + 1) + 1)) * sizeof(cx_t<T>);
+    cudaError_t e = cudaFuncSetAttribute(k_wiener_lines_reg<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    const int groups = (a.m + 2 * PB - 1) / (2 * PB);
+    const int64_t fb = (int64_t)a.n * a.m * sizeof(T);
+    for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
+        const int nb = (int)((batch - b0) < 65535 ? (batch - b0) : 65535);
+        WienerLinesArgs ab = a;
+        ab.in = static_cast<const char *>(a.in) + b0 * fb;
+        ab.out = static_cast<char *>(a.out) + b0 * fb;
+        if (a.fpos) ab.fpos = static_cast<char *>(a.fpos) + b0 * fb;
+        k_wiener_lines_reg<T, S><<<dim3(groups, nb), 256, smem, st>>>(ab);
+    }
+    return cudaGetLastError();
+}
+
+bool wiener_reg_supported(int dtype, int n) {
+    if (n == 64 || n == 256) return true;
+    return n == 1024 && dtype == 1;              // 32 complex registers per thread: float only
+}
+
+template <typename T>
+cudaError_t launch_wiener_reg(const WienerLinesArgs &a, int64_t batch, cudaStream_t st) {
+    if (a.n == 64) return launch_wiener_reg_t<T, 8>(a, batch, st);
+    if (a.n == 256) return launch_wiener_reg_t<T, 16>(a, batch, st);
+    return launch_wiener_reg_t<T, 32>(a, batch, st);
+}
+
+template cudaError_t launch_wiener_reg<double>(const WienerLinesArgs &, int64_t, cudaStream_t);
+template cudaError_t launch_wiener_reg<float>(const WienerLinesArgs &, int64_t, cudaStream_t);
+
+}  // namespace md

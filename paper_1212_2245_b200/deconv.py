@@ -390,16 +390,17 @@ class DeblurPipeline:
         if tuple(shape) != self.shape:
             raise ValueError(f"pipeline prepared for shape {self.shape}, got {tuple(shape)}")
 
-    def run_batch(self, frames, out=None, stream=None):
+    def run_batch(self, frames, out=None, stream=None, out_dtype=np.float64):
         """Deblur a stack ``[N, H, W]``: CUDA tensor in -> CUDA tensor out (md_run), or host
-        float64 array in -> host array out (md_run_host, copies inside)."""
+        array in (uint8 camera frames, float32 or float64) -> host array out (float64 by
+        default, float32 on request), copies pipelined inside the C ABI (md_run_host_ex)."""
         import torch
         if isinstance(frames, torch.Tensor):
             self._check_shape(frames.shape[-2:])
             return self._plan.run(frames, out=out, stream=stream)
-        a = np.asarray(frames, dtype=np.float64)
+        a = np.asarray(frames)
         self._check_shape(a.shape[-2:])
-        return self._plan.run_host(a, out=out, stream=stream)
+        return self._plan.run_host(a, out=out, stream=stream, out_dtype=out_dtype)
 
     def run_timed(self, f: Image) -> tuple[Image, StageTimes]:
         """Deconvolve one image; stage times from CUDA events (the Wiener stage is timed by a

@@ -139,14 +139,25 @@ class GpuPlan:
         L.check(self.lib.md_run_profile(self._h, f.data_ptr(), out.data_ptr(), n, _stream_ptr(stream), ms))
         return {"init_ms": ms[0], "iter_ms": ms[1], "layout_ms": ms[2], "groups": int(ms[3])}
 
-    def run_host(self, f: np.ndarray, out: np.ndarray | None = None, stream=None) -> np.ndarray:
-        """Whole pipeline from HOST float64 frames, copies inside (md_run_host)."""
-        f = np.ascontiguousarray(f, dtype=np.float64)
+    _IO = {np.dtype(np.float64): L.MD_IO_F64, np.dtype(np.float32): L.MD_IO_F32, np.dtype(np.uint8): L.MD_IO_U8}
+
+    def run_host(self, f: np.ndarray, out: np.ndarray | None = None, stream=None,
+                 out_dtype=np.float64) -> np.ndarray:
+        """Whole pipeline from HOST frames (uint8 / float32 / float64) to HOST results
+        (float32 / float64), copies pipelined inside the C ABI (md_run_host_ex). Pinned
+        (page-locked) buffers make the copies asynchronous."""
+        f = np.asarray(f)
+        if f.dtype not in self._IO:
+            f = f.astype(np.float64)
+        f = np.ascontiguousarray(f)
         if f.shape[-2:] != self.shape:
             raise ValueError(f"plan prepared for shape {self.shape}, got {f.shape[-2:]}")
         n = 1 if f.ndim == 2 else int(np.prod(f.shape[:-2]))
-        out = np.empty_like(f) if out is None else out
-        L.check(self.lib.md_run_host(self._h, f.ctypes.data, out.ctypes.data, n, _stream_ptr(stream)))
+        out = np.empty(f.shape, dtype=out_dtype) if out is None else out
+        if out.dtype not in (np.float32, np.float64) or out.shape != f.shape or not out.flags.c_contiguous:
+            raise ValueError("out must be a C-contiguous float32/float64 array of the input's shape")
+        L.check(self.lib.md_run_host_ex(self._h, f.ctypes.data, self._IO[f.dtype], out.ctypes.data,
+                                        self._IO[out.dtype], n, _stream_ptr(stream)))
         return out
 
     def wiener(self, f, out=None, stream=None):

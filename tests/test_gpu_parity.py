@@ -280,14 +280,35 @@ def test_fused_cluster_kernel_matches_per_iteration_kernel(md, name, dtype):
     d = load_golden(name)
     scen = md.Scenario[SCEN[str(d["scenario"])]]
     shape = d["f"].shape
-    on = md.DeblurPipeline(shape, product_psf(d), product_params(d), scen, dtype=dtype)
-    if not on.plan.fused:
-        pytest.skip(f"fused kernel not applicable: {on.plan.describe}")
+    try:
+        on = md.DeblurPipeline(shape, product_psf(d), product_params(d), scen, dtype=dtype, fused=True)
+    except ValueError as exc:
+        pytest.skip(f"fused kernel not applicable: {exc}")
     off = md.DeblurPipeline(shape, product_psf(d), product_params(d), scen, dtype=dtype, fused=False)
     a = on.run(md.Image(d["f"])).values
     b = off.run(md.Image(d["f"])).values
     np.testing.assert_allclose(a, b, rtol=0, atol=1e-9 if dtype == "float64" else 1e-3)
     assert np.abs(a - d["out"]).max() <= (FP64_TOL if dtype == "float64" else TOL)
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_host_entry_io_types(md, dtype):
+    """md_run_host_ex: uint8 / float32 / float64 host frames, pipelined chunks, equal results."""
+    import torch
+    d = load_golden("pipe_c1_box_h15_256")
+    pipe = md.DeblurPipeline((256, 256), product_psf(d), product_params(d), dtype=dtype)
+    rng = np.random.default_rng(3)
+    frames = np.stack([np.clip(d["f"] + rng.normal(0, 4, d["f"].shape), 0, 255).round() for _ in range(37)])
+    dev = pipe.run_batch(torch.from_numpy(frames).cuda().to(torch.float64 if dtype == "float64"
+                                                              else torch.float32)).double().cpu().numpy()
+    pipe.plan.set_chunk(0)
+    a = pipe.run_batch(frames.astype(np.uint8), out_dtype=np.float32)
+    b = pipe.run_batch(frames.astype(np.float32))
+    c = pipe.run_batch(frames)
+    assert a.dtype == np.float32 and b.dtype == np.float64
+    np.testing.assert_allclose(c, dev, rtol=0, atol=0)
+    np.testing.assert_allclose(b, dev, rtol=0, atol=0)
+    np.testing.assert_allclose(a, dev.astype(np.float32), rtol=0, atol=0)
 
 
 def test_fused_batch_many_frames(md):
