@@ -5,25 +5,25 @@
                     [--config c1|c4] [--dtype float32|float64] [--batch B]
 
 One "step" = the whole pipeline (Wiener init + RRRL iterations) over one batch of B
-synthetic frames resident in HBM. ``value`` = frames/s over all ranks (weak scaling: B
-frames per GPU per step; frames are independent, no collective on the data path), timed
+synthetic 256x256 frames resident in HBM. ``value`` = frames/s over all ranks (weak scaling:
+B frames per GPU per step; frames are independent -- no collective on the data path), timed
 with CUDA events, max over ranks. ``e2e`` = the same metric through the public host-buffer
-entry (md_run_host: pinned float64 H2D + run + D2H inside the timed region).
-``--impl reference`` times the CPU oracle port of the reference algorithm on all host
-cores (one process per core), the CPU baseline arm.
+entry (DeblurPipeline.run_batch on pinned host arrays -> md_run_host_ex: H2D + run + D2H
+inside the timed region). ``--impl reference`` times the reference algorithm (the CPU
+oracle port, oracle/wr3l_oracle.py) on all host cores: the CPU-baseline arm.
 
 Workloads:
   c1  256x256, uniform horizontal box L=15, Gaussian noise sigma=5, Wiener + 5 RRRL
-      (BASELINE.json configs[0], the metric's 256^2 Wiener+RRRL frame).
-  c4  256x256 frames with a seeded 1/3 box / 1/3 general-1D / 1/3 2D-line mix (configs[3]);
-      each class runs as its own batch through its own plan.
+      (BASELINE.json configs[0]: the metric's 256^2 Wiener+RRRL frame). Default.
+  c4  256x256 frames over a bank of 48 PSFs: 16 uniform boxes (H/V, L in [5,31] incl.
+      fractional), 16 axis-aligned general 1D kernels, 16 2D kernels (12 lines at random
+      angles, L<=21, + 4 small dense kernels); sigma=5, Wiener + 5 RRRL (configs[3]).
 """
 
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import multiprocessing as mp
 import os
 import statistics
@@ -39,6 +39,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "deblurred frames/sec (256² Wiener+RRRL) per GPU & 8 GPUs; p50 ms/frame; % HBM roofline"
 H = W = 256
+PX = H * W
 
 
 def peaks() -> dict:
@@ -50,24 +51,148 @@ def peaks() -> dict:
         return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
 
 
-# ---------------------------------------------------------------------------------- inputs
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
 
-def c1_psf(md):
-    return md.Psf.uniform_box(md.BlurAxis.HORIZONTAL, 15)
+
+def noisy(blurred: np.ndarray, seed: int, sigma: float = 5.0) -> np.ndarray:
+    """quantize(add_gaussian_noise(., sigma, seed)) of synth.py:29-55 (PCG64)."""
+    n = blurred + np.random.default_rng(seed).normal(0.0, sigma, blurred.shape)
+    return np.clip(np.floor(np.clip(n, 0.0, 255.0) + 0.5), 0.0, 255.0)
 
 
-def make_frames(md, psf, count: int, distinct: int = 64, sigma: float = 5.0, seed0: int = 5) -> np.ndarray:
-    """``count`` float64 frames: the deterministic scene blurred on the GPU (clamped spatial
-    convolution), plus ``distinct`` PCG64 noise realisations, quantised, tiled to ``count``."""
-    g = md.make_test_image(W, H, seed=7)
-    blurred = md.synth_blur(g, psf, quantize_output=True).values
-    k = min(distinct, count)
-    base = np.empty((k, H, W))
-    for i in range(k):
-        noisy = blurred + np.random.default_rng(seed0 + i).normal(0.0, sigma, blurred.shape)
-        base[i] = np.clip(np.floor(np.clip(noisy, 0.0, 255.0) + 0.5), 0.0, 255.0)
-    reps = -(-count // k)
-    return np.tile(base, (reps, 1, 1))[:count]
+# ---------------------------------------------------------------------------------- workloads
+
+class C1:
+    """configs[0]: 256^2, horizontal box L=15, sigma=5, Wiener + 5 RRRL."""
+
+    name = "c1: 256x256 box L=15 horizontal, sigma=5, Wiener + 5 RRRL (BASELINE.json configs[0])"
+
+    def __init__(self, md, args):
+        self.md = md
+        self.psf = md.Psf.uniform_box(md.BlurAxis.HORIZONTAL, 15)
+        self.params = md.DeconvParams()
+        fused = None if args.fused == "auto" else args.fused == "on"
+        self.pipe = md.DeblurPipeline((H, W), self.psf, self.params, md.Scenario.BOX_1D, dtype=args.dtype,
+                                      fused=fused)
+        self.describe = self.pipe.plan.describe
+        self.fused = self.pipe.plan.fused
+        blurred = md.synth_blur(md.make_test_image(W, H, seed=7), self.psf).values
+        k = min(64, args.batch)
+        base = np.stack([noisy(blurred, 5 + i) for i in range(k)])
+        self.host = np.tile(base, (-(-args.batch // k), 1, 1))[:args.batch]
+        self.cpu_items = [("box", self.psf, base[i]) for i in range(k)]
+        self.latency_plan = self.pipe.plan
+
+    def run(self, f, u):
+        self.pipe.plan.run(f, out=u)
+
+    def run_profile(self, f, u) -> dict:
+        return self.pipe.plan.run_profile(f, out=u)
+
+    def e2e_set(self, nb):
+        return self.host[:nb], None
+
+    def run_host(self, hin, hout, ctx):
+        self.pipe.run_batch(hin, out=hout)
+
+    def launches(self, n) -> int:
+        return self.pipe.plan.launch_count(n)
+
+    def iter_bytes(self, n, esz) -> float:
+        """SURVEY 8(d) algorithmic bytes of the iteration stage for n frames (8 passes/it.)."""
+        return 8 * self.params.iterations * PX * esz * n
+
+
+def c4_bank(md, seed: int = 2026):
+    """48 PSFs: 16 boxes, 16 general 1D, 16 2D (12 lines + 4 small dense kernels)."""
+    rng = np.random.default_rng(seed)
+    bank, kinds = [], []
+    for i in range(16):
+        axis = md.BlurAxis.HORIZONTAL if i % 2 == 0 else md.BlurAxis.VERTICAL
+        L = float(rng.integers(5, 32)) + (0.5 if i % 4 == 3 else 0.0)
+        bank.append(md.Psf.uniform_box(axis, min(L, 31.0)))
+        kinds.append("box")
+    for i in range(16):
+        axis = md.BlurAxis.HORIZONTAL if i % 2 == 0 else md.BlurAxis.VERTICAL
+        taps = int(rng.integers(5, 18))
+        w = np.exp(-np.linspace(0.0, rng.uniform(0.5, 3.0), taps)) * rng.uniform(0.5, 1.0, taps)
+        bank.append(md.Psf.general_1d(w, axis, center=int(rng.integers(taps // 3, 2 * taps // 3 + 1))))
+        kinds.append("fourier1d")
+    for i in range(16):
+        if i < 12:
+            bank.append(md.Psf.line(float(rng.uniform(7.0, 21.0)), float(rng.uniform(0.0, 180.0))))
+        else:
+            s = int(rng.integers(3, 8))
+            bank.append(md.Psf.general_2d(rng.uniform(0.0, 1.0, (s, s))))
+        kinds.append("fourier2d")
+    return bank, kinds
+
+
+class C4:
+    """configs[3]: 256^2 frames over a 48-PSF bank, grouped by PSF."""
+
+    name = ("c4: 256x256 frames, 48-PSF bank (16 box H/V L 5-31 incl. fractional, 16 general 1D, "
+            "12 lines L<=21 at random angles + 4 small 2D), sigma=5, Wiener + 5 RRRL (BASELINE.json configs[3])")
+
+    def __init__(self, md, args):
+        from paper_1212_2245_b200.batch import PsfBankPipeline
+        self.md = md
+        self.params = md.DeconvParams()
+        self.bank, self.kinds = c4_bank(md)
+        self.pipe = PsfBankPipeline((H, W), self.bank, self.params, dtype=args.dtype)
+        nb = len(self.bank)
+        per = -(-args.batch // nb)
+        self.index = np.minimum(np.arange(args.batch) // per, nb - 1)
+        scenes = [md.make_test_image(W, H, seed=s).values for s in (7, 8, 9, 10)]
+        distinct = 8
+        frames = np.empty((args.batch, H, W))
+        self.cpu_items = []
+        for b, psf in enumerate(self.bank):
+            sel = np.nonzero(self.index == b)[0]
+            if sel.size == 0:
+                continue
+            blurred = [md.synth_blur(md.Image(scenes[j]), psf).values for j in range(4)]
+            base = [noisy(blurred[j % 4], 1000 * b + j) for j in range(distinct)]
+            for k, i in enumerate(sel):
+                frames[i] = base[k % distinct]
+            self.cpu_items.append((self.kinds[b], psf, base[0]))
+        self.host = frames
+        self.describe = "; ".join(sorted({p.plan.describe.split(",")[0] for p in self.pipe.pipes}))
+        self.fused = False
+        self.latency_plan = self.pipe.pipes[int(self.index[0])].plan
+
+    def run(self, f, u):
+        self.pipe.run(f, self.index, out=u)
+
+    def run_profile(self, f, u) -> dict:
+        tot = {"init_ms": 0.0, "iter_ms": 0.0, "layout_ms": 0.0, "groups": 0}
+        for b, s, e in self.pipe.groups(self.index):
+            p = self.pipe.pipes[b].plan.run_profile(f[s:e], out=u[s:e])
+            for k in tot:
+                tot[k] += p[k]
+        return tot
+
+    def e2e_set(self, nb):
+        sel = np.linspace(0, self.index.size - 1, nb).astype(np.int64)   # every PSF class, sorted
+        return self.host[sel], self.index[sel]
+
+    def run_host(self, hin, hout, ctx):
+        for b, s, e in self.pipe.groups(ctx):
+            self.pipe.pipes[b].run_batch(hin[s:e], out=hout[s:e])
+
+    def launches(self, n) -> int:
+        return self.pipe.launch_count(self.index[:n])
+
+    def iter_bytes(self, n, esz) -> float:
+        # 8 passes per iteration for every class (line / box / direct-tap convolvers)
+        return 8 * self.params.iterations * PX * esz * n
+
+
+WORKLOADS = {"c1": C1, "c4": C4}
 
 
 # ---------------------------------------------------------------------------------- clocks
@@ -80,7 +205,8 @@ class ClockSampler:
          "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
-        self.index, self.rows, self.proc = index, [], None
+        self.index, self.rows, self.stamps, self.proc = index, [], [], None
+        self.t_start = self.t_end = None
 
     def __enter__(self):
         try:
@@ -89,8 +215,12 @@ class ClockSampler:
                  "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 5.0:   # first sample before timing starts
+                time.sleep(0.02)
         except Exception:
             self.proc = None
+        self.t_start = time.time()
         return self
 
     def _read(self):
@@ -98,8 +228,11 @@ class ClockSampler:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) == 7:
                 self.rows.append(parts)
+                self.stamps.append(time.time())
 
     def __exit__(self, *exc):
+        self.t_end = time.time()
+        time.sleep(0.25)
         if self.proc:
             self.proc.terminate()
             try:
@@ -108,83 +241,85 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self) -> dict:
-        if not self.rows:
+        rows = [r for r, t in zip(self.rows, self.stamps)
+                if self.t_start is not None and self.t_start <= t <= (self.t_end or t) + 0.2]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [v for v in (num(r[0]) for r in rows) if v is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].replace(".", "").isdigit() else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": num(rows[0][1]),
+                "reasons": reasons, "samples": len(rows)}
 
 
 # ---------------------------------------------------------------------------------- CPU arm
 
-def _cpu_worker(args):
-    frames, kind = args
+def _cpu_worker(job):
+    """Time the oracle port of the reference pipeline on a list of (kind, psf-spec, frame)."""
     from oracle import wr3l_oracle as O
-    psf = O.make_psf("box", axis="h", length=15)
-    params = O.OParams()
     t0 = time.perf_counter()
-    for f in frames:
-        O.pipeline(f, psf, params, "box")
+    for kind, spec, f in job:
+        O.pipeline(f, spec, O.OParams(), kind)
     return time.perf_counter() - t0
 
 
-def cpu_rate(frames: np.ndarray, cores: int, per_core: int, pool=None) -> tuple[float, float]:
-    """frames/s of the oracle port (reference algorithm, float64) over ``cores`` processes."""
-    jobs = [(frames[(i * per_core + np.arange(per_core)) % len(frames)], "c1") for i in range(cores)]
-    own = pool is None
-    if own:
-        pool = mp.get_context("fork").Pool(cores)
+def oracle_spec(psf):
+    from oracle import wr3l_oracle as O
+    if psf.kind.value == "box":
+        return O.OPsf("box", np.asarray(psf.weights), int(psf.center), psf.axis.value, float(psf.length))
+    if psf.kind.value == "1d":
+        return O.OPsf("1d", np.asarray(psf.weights), int(psf.center), psf.axis.value)
+    return O.OPsf("2d", np.asarray(psf.weights), tuple(psf.center))
+
+
+def cpu_jobs(work, per_core: int, cores: int):
+    """Per-core frame lists with the workload's class mix."""
+    items = [(k, oracle_spec(p), f) for k, p, f in work.cpu_items]
+    return [[items[(c * per_core + i) % len(items)] for i in range(per_core)] for c in range(cores)]
+
+
+def cpu_rate(jobs, pool) -> tuple[float, float]:
     t0 = time.perf_counter()
     pool.map(_cpu_worker, jobs)
     wall = time.perf_counter() - t0
-    if own:
-        pool.close()
-        pool.join()
-    return cores * per_core / wall, wall
-
-
-def host_cores() -> int:
-    try:
-        return len(os.sched_getaffinity(0))
-    except Exception:
-        return os.cpu_count() or 1
+    return sum(len(j) for j in jobs) / wall, wall
 
 
 def run_reference(args, rank: int) -> None:
     """--impl reference: the reference algorithm (CPU oracle port) on all host cores."""
     if rank != 0:
         return
-    cores = host_cores()
-    per_core = args.cpu_frames_per_core
     import paper_1212_2245_b200 as md
-    frames = make_frames(md, c1_psf(md), 64)
+    args.batch = min(args.batch, 1024)
+    work = WORKLOADS[args.config](md, args)            # inputs only (GPU-synthesised blur)
+    cores = host_cores()
+    jobs = cpu_jobs(work, args.cpu_frames_per_core, cores)
     pool = mp.get_context("fork").Pool(cores)
     for _ in range(args.warmup):
-        cpu_rate(frames, cores, per_core, pool)
-    rates, walls = [], []
-    for _ in range(args.steps):
-        r, w = cpu_rate(frames, cores, per_core, pool)
-        rates.append(r)
-        walls.append(w)
+        cpu_rate(jobs, pool)
+    walls = [cpu_rate(jobs, pool)[1] for _ in range(args.steps)]
     pool.close()
     pool.join()
-    total_frames = cores * per_core * args.steps
-    value = total_frames / sum(walls)
+    per_step = sum(len(j) for j in jobs)
+    value = per_step * args.steps / sum(walls)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(walls) / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (deterministic scene, box blur, PCG64 noise)",
-        "config": {"workload": "c1: 256x256 box L=15 horizontal, sigma=5, Wiener + 5 RRRL",
-                   "frames_per_step": cores * per_core},
+        "data": "synthetic (deterministic scenes, GPU-synthesised blur, PCG64 sigma=5 noise, 8-bit)",
+        "config": {"workload": work.name, "frames_per_step": per_step},
         "cpu_baseline": {"value": value, "unit": "frames/s", "cores": cores, "kind": "port",
-                         "sample": f"{cores * per_core} frames per step, oracle/wr3l_oracle.pipeline "
-                                   f"(NumPy float64, reference radix-2 FFT), one process per core"},
+                         "sample": f"{per_step} frames per step through oracle/wr3l_oracle.pipeline (NumPy "
+                                   "float64, the reference's radix-2 FFT and cumsum box filter), one process "
+                                   "per host core"},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "p50_ms_per_frame": 1e3 * statistics.median(walls) / per_core,
+        "p50_ms_per_frame": 1e3 * statistics.median(walls) / args.cpu_frames_per_core,
     }
     print(json.dumps(line), flush=True)
 
@@ -194,26 +329,30 @@ def run_reference(args, rank: int) -> None:
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c1", choices=["c1"])
+    ap.add_argument("--config", default="c1", choices=sorted(WORKLOADS))
     ap.add_argument("--dtype", default="float32", choices=["float32", "float64"])
-    ap.add_argument("--batch", type=int, default=4096, help="frames per GPU per step")
+    ap.add_argument("--batch", type=int, default=None, help="frames per GPU per step")
     ap.add_argument("--e2e-batch", type=int, default=4096)
     ap.add_argument("--cpu-frames-per-core", type=int, default=24)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--fused", default="auto", choices=["auto", "on", "off"])
     args = ap.parse_args()
+    if args.batch is None:
+        args.batch = 4096 if args.config == "c1" else 16384
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    import torch
     if args.impl == "reference":
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
         run_reference(args, rank)
         return
 
-    import torch
     import torch.distributed as dist
 
     torch.cuda.set_device(local)
@@ -221,20 +360,15 @@ def main() -> None:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_1212_2245_b200 as md
 
-    psf = c1_psf(md)
-    params = md.DeconvParams()
-    fused = None if args.fused == "auto" else args.fused == "on"
-    pipe = md.DeblurPipeline((H, W), psf, params, md.Scenario.BOX_1D, dtype=args.dtype, fused=fused)
-    plan = pipe.plan
+    work = WORKLOADS[args.config](md, args)
     tdt = torch.float32 if args.dtype == "float32" else torch.float64
     esz = 4 if args.dtype == "float32" else 8
-    host = make_frames(md, psf, args.batch)
-    f = torch.from_numpy(host).to(device="cuda", dtype=tdt).contiguous()
+    f = torch.from_numpy(work.host).to(device="cuda", dtype=tdt).contiguous()
     u = torch.empty_like(f)
     stream = torch.cuda.current_stream()
 
     for _ in range(args.warmup):
-        plan.run(f, out=u)
+        work.run(f, u)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -244,7 +378,7 @@ def main() -> None:
         torch.cuda.synchronize()
         ev0.record(stream)
         for _ in range(args.steps):
-            p = plan.run_profile(f, out=u)          # CUDA events between launch groups, same stream
+            p = work.run_profile(f, u)              # CUDA events between launch groups, same stream
             for k in prof:
                 prof[k] += p[k]
         ev1.record(stream)
@@ -254,17 +388,15 @@ def main() -> None:
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     max_ms = float(t.item())
-    frames_total = args.batch * args.steps * world
-    value = frames_total / (max_ms / 1e3)
+    value = args.batch * args.steps * world / (max_ms / 1e3)
 
     # single-frame latency (p50 over 50 runs, batch = 1)
-    f1 = f[:1].clone()
-    u1 = torch.empty_like(f1)
+    f1, u1 = f[:1].clone(), torch.empty_like(f[:1])
     lat = []
     for i in range(60):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        plan.run(f1, out=u1)
+        work.latency_plan.run(f1, out=u1)
         b.record(stream)
         b.synchronize()
         if i >= 10:
@@ -275,17 +407,18 @@ def main() -> None:
     # region. Primary: the workload's native 8-bit frames in, float32 results out; also the
     # drop-in float64 -> float64 (reference Image semantics).
     def e2e_rate(in_dtype, out_dtype, nb):
-        hin = torch.from_numpy(host[:nb].astype(in_dtype)).pin_memory()
+        frames, ctx = work.e2e_set(nb)
+        hin = torch.from_numpy(np.ascontiguousarray(frames).astype(in_dtype)).pin_memory()
         hout = torch.empty(hin.shape, dtype=torch.from_numpy(np.zeros(1, out_dtype)).dtype).pin_memory()
         hin_np, hout_np = hin.numpy(), hout.numpy()
-        pipe.run_batch(hin_np, out=hout_np)
+        work.run_host(hin_np, hout_np, ctx)
         torch.cuda.synchronize()
-        steps = max(3, args.steps // 2)
+        steps = max(3, min(10, args.steps // 4))
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(steps):
-            pipe.run_batch(hin_np, out=hout_np)   # H2D + convert + run + convert + D2H, synchronous
+            work.run_host(hin_np, hout_np, ctx)  # H2D + convert + run + convert + D2H, synchronous
         el = time.perf_counter() - t0
         te = torch.tensor([el], device="cuda", dtype=torch.float64)
         if world > 1:
@@ -294,52 +427,51 @@ def main() -> None:
 
     nb = min(args.e2e_batch, args.batch)
     e2e_value, e2e_in, e2e_out = e2e_rate(np.uint8, np.float32, nb)
-    e2e64_value, e2e64_in, e2e64_out = e2e_rate(np.float64, np.float64, min(nb, 1024))
+    nb64 = min(nb, 1024)
+    e2e64_value, e2e64_in, e2e64_out = e2e_rate(np.float64, np.float64, nb64)
 
     if rank == 0:
         pk = peaks()
-        px = H * W
-        iters = params.iterations
-        # algorithmic bytes: 8 field passes per RRRL iteration, 2 for Wiener-1D
-        iter_bytes_total = 8 * px * esz * args.batch * iters * args.steps
-        if plan.fused:
-            iter_bytes_total = (2 + 8 * iters) * px * esz * args.batch * args.steps
-        achieved = iter_bytes_total / (prof["iter_ms"] / 1e3) / 1e9 if prof["iter_ms"] > 0 else None
+        iter_bytes = work.iter_bytes(args.batch, esz) * args.steps
+        achieved = iter_bytes / (prof["iter_ms"] / 1e3) / 1e9 if prof["iter_ms"] > 0 else None
         cpu = None
         if not args.no_cpu:
             cores = host_cores()
-            r, wall = cpu_rate(host[:64], cores, args.cpu_frames_per_core)
+            jobs = cpu_jobs(work, args.cpu_frames_per_core, cores)
+            pool = mp.get_context("fork").Pool(cores)
+            r, wall = cpu_rate(jobs, pool)
+            pool.close()
+            pool.join()
             cpu = {"value": r, "unit": "frames/s", "cores": cores, "kind": "port",
-                   "sample": f"{cores * args.cpu_frames_per_core} c1 frames ({wall:.1f} s wall) through "
-                             f"oracle/wr3l_oracle.pipeline (NumPy float64), one process per core"}
-        step_ms = max_ms / args.steps
+                   "sample": f"{sum(len(j) for j in jobs)} frames of this workload ({wall:.1f} s wall) through "
+                             "oracle/wr3l_oracle.pipeline (NumPy float64), one process per host core"}
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32" if args.dtype == "float32" else "f64",
-            "data": "synthetic (deterministic scene, GPU clamped box blur, PCG64 sigma=5 noise, 8-bit)",
-            "config": {"workload": "c1: 256x256 box L=15 horizontal, sigma=5, Wiener + 5 RRRL "
-                                   "(BASELINE.json configs[0])",
-                       "frames_per_gpu_per_step": args.batch, "parallelism": f"frame-sharded x{world}",
-                       "l2": f"inputs {args.batch * px * esz / 2**20:.0f} MiB per GPU > 126 MB L2",
-                       "plan": plan.describe},
+            "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32" if args.dtype == "float32" else "f64",
+            "data": "synthetic (deterministic scenes, GPU clamped-spatial blur, PCG64 sigma=5 noise, 8-bit)",
+            "config": {"workload": work.name, "frames_per_gpu_per_step": args.batch,
+                       "parallelism": f"frame-sharded x{world}",
+                       "l2": f"inputs {args.batch * PX * esz / 2**20:.0f} MiB per GPU > 126 MB L2",
+                       "plan": work.describe},
             "p50_ms_per_frame_batch1": statistics.median(lat),
             "stage_ms_per_step": {k: prof[k] / args.steps for k in ("init_ms", "iter_ms", "layout_ms")},
-            "roofline": {"bound": "hbm", "kernel": "RRRL iteration" + (" (fused)" if plan.fused else ""),
+            "roofline": {"bound": "hbm",
+                         "kernel": "RRRL iteration" + (" (fused cluster kernel)" if work.fused else ""),
                          "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": (achieved / pk["hbm_gbs"]) if achieved else None, "traffic": None,
                          "peak_source": pk["source"],
-                         "bytes_model": "SURVEY.md 8(d): 8 field passes per iteration x 65536 px x "
-                                        f"{esz} B per frame"},
+                         "bytes_model": "SURVEY.md 8(d): 8 field passes per RRRL iteration x 65536 px x "
+                                        f"{esz} B per frame; time = CUDA events around the iteration launches"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": e2e_in,
                     "d2h_bytes_per_step": e2e_out, "frames_per_step": nb,
                     "entry": "DeblurPipeline.run_batch(pinned uint8 frames) -> float32 results "
                              "(md_run_host_ex, copies pipelined over 3 streams)"},
             "e2e_f64": {"value": e2e64_value, "unit": "frames/s", "h2d_bytes_per_step": e2e64_in,
-                        "d2h_bytes_per_step": e2e64_out, "frames_per_step": min(nb, 1024),
+                        "d2h_bytes_per_step": e2e64_out, "frames_per_step": nb64,
                         "entry": "DeblurPipeline.run_batch(pinned float64) -> float64 (drop-in Image semantics)"},
-            "gpu_launches": plan.launch_count(args.batch) * args.steps,
+            "gpu_launches": work.launches(args.batch) * args.steps,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -329,3 +329,22 @@ def test_plan_reports_launches(md):
     pipe = md.DeblurPipeline((256, 256), md.Psf.uniform_box(md.BlurAxis.HORIZONTAL, 15), md.DeconvParams())
     assert pipe.plan.launch_count(16) >= 2
     assert "lines" in pipe.plan.describe
+
+
+def test_psf_bank_pipeline_matches_single_plans(md):
+    """configs[3]-style bank: unsorted per-frame PSF indices, each frame equals its own plan."""
+    import torch
+    from paper_1212_2245_b200.batch import PsfBankPipeline
+    bank = [md.Psf.uniform_box(md.BlurAxis.HORIZONTAL, 9.5), md.Psf.general_1d([1, 3, 2, 1], md.BlurAxis.VERTICAL),
+            md.Psf.line(11.0, 40.0)]
+    params = md.DeconvParams()
+    pipe = PsfBankPipeline((64, 64), bank, params, dtype="float64")
+    rng = np.random.default_rng(9)
+    g = md.make_test_image(64, 64)
+    idx = np.array([2, 0, 1, 1, 0, 2, 2])
+    frames = np.stack([md.quantize(md.add_gaussian_noise(md.synth_blur(g, bank[i]), 5.0, int(s))).values
+                       for s, i in enumerate(idx)])
+    out = pipe.run(torch.from_numpy(frames).cuda(), idx).cpu().numpy()
+    for k, i in enumerate(idx):
+        want = md.DeblurPipeline((64, 64), bank[i], params).run(md.Image(frames[k])).values
+        np.testing.assert_array_equal(out[k], want)

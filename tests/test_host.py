@@ -165,3 +165,13 @@ class TestSynth:
         assert md.snr(g, g) == math.inf
         assert md.psnr(g.values, g.values) == math.inf
         assert md.psnr(g.values + 1.0, g.values) == pytest.approx(10 * math.log10(255.0 ** 2))
+
+
+class TestPsfBankGrouping:
+    def test_groups_of_sorted_index(self):
+        from paper_1212_2245_b200.batch import PsfBankPipeline
+        g = PsfBankPipeline.groups(None, np.array([0, 0, 1, 3, 3, 3]))
+        assert g == [(0, 0, 2), (1, 2, 3), (3, 3, 6)]
+        assert PsfBankPipeline.groups(None, np.array([], dtype=np.int64)) == []
+        with pytest.raises(ValueError):
+            PsfBankPipeline.groups(None, np.array([1, 0]))
