@@ -23,6 +23,7 @@
 #include "../../include/mdcuda.h"
 #include "md_fused.h"
 #include "md_lines_fast.h"
+#include "md_plane_fast.h"
 #include "md_plane.h"
 
 using namespace md;
@@ -145,6 +146,8 @@ struct md_plan {
     // plane
     PlaneHalo hblur{}, hadj{};
     PlaneTap *d_ptaps_blur = nullptr, *d_ptaps_adj = nullptr;
+    std::vector<PlaneTap> htaps_blur, htaps_adj;
+    bool fast_plane = false;    // register-blocked direct-tap stage kernels apply
     int periodic = 0;
     // FFT tables (dtype copies; fp64 masters are temporaries)
     void *d_tw_n = nullptr, *d_tw_H = nullptr, *d_tw_W = nullptr;
@@ -443,6 +446,9 @@ int32_t md_plan_create(const md_plan_desc *desc, md_plan **out) {
         P->path = use_fft ? PATH_PLANE_FFT : PATH_PLANE_DIRECT;
         if ((rc = upload(&P->d_ptaps_blur, tb.data(), tb.size()))) return bail(rc);
         if ((rc = upload(&P->d_ptaps_adj, ta.data(), ta.size()))) return bail(rc);
+        P->htaps_blur = tb;
+        P->htaps_adj = ta;
+        P->fast_plane = !(desc->flags & MD_FLAG_GENERIC_LINES) && plane_fast_supported(P->hblur, P->hadj, desc->dtype);
         if (pow2) {
             if ((rc = build_twiddles(H, desc->dtype, &P->d_tw_H))) return bail(rc);
             if ((rc = build_twiddles(W, desc->dtype, &P->d_tw_W))) return bail(rc);
@@ -656,6 +662,14 @@ int run_plane(md_plan &P, const void *f, void *u, int64_t nb, char *scr, cudaStr
             CU(launch_fft2_cols<T>(a, nb, st));                       // adjoint pair: x conj(h)
             a.epi = R_EPI_STAGE_B; a.u = cur; a.oa = dst; a.fwd_after = !last;
             CU(launch_fft2_rows<T>(a, nb, st));                       // update, fwd of u'
+        } else if (P.fast_plane) {
+            PlaneFastDesc s{};
+            s.u = cur; s.f = FP; s.p = X; s.w = Y; s.u_out = dst;
+            s.H = P.d.height; s.W = P.d.width; s.periodic = P.periodic;
+            s.hb = P.hblur; s.ha = P.hadj; s.taps_blur = &P.htaps_blur; s.taps_adj = &P.htaps_adj;
+            s.alpha = P.d.alpha; s.eps_d2 = P.d.eps_data * P.d.eps_data; s.eps_r2 = P.d.eps_reg * P.d.eps_reg;
+            s.has_d = P.has_d; s.lut = P.lut;
+            CU(launch_plane_fast<T>(s, P.robust, nb, st));
         } else {
             StagePlaneArgs s{};
             s.u = cur; s.f = FP; s.p = X; s.w = Y; s.u_out = dst;

@@ -1,0 +1,43 @@
+// md_plane_fast.h -- interface of the register-blocked 2D direct-tap iteration stages.
+#pragma once
+
+#include <vector>
+
+#include "md_plane.h"
+
+namespace md {
+
+constexpr int kPlaneMaxTaps = 128;
+
+template <typename T, int MAXT> struct FastTaps {
+    int nt;
+    int off[MAXT];      // dy * tile_stride + dx
+    T w[MAXT];
+};
+
+template <typename T, int MAXT> struct PlaneFastArgs {
+    const T *u, *f;     // iterate, floored observation
+    T *p, *w, *u_out;
+    int H, W, periodic;
+    PlaneHalo hb, ha;
+    FastTaps<T, MAXT> tb, ta;
+    T alpha, eps_d2, eps_r2;
+    int has_d;
+    LutView lut;
+};
+
+struct PlaneFastDesc {
+    const void *u, *f;
+    void *p, *w, *u_out;
+    int H, W, periodic;
+    PlaneHalo hb, ha;
+    const std::vector<PlaneTap> *taps_blur, *taps_adj;   // host copies
+    double alpha, eps_d2, eps_r2;
+    int has_d;
+    LutView lut;
+};
+
+bool plane_fast_supported(const PlaneHalo &hb, const PlaneHalo &ha, int dtype);
+template <typename T> cudaError_t launch_plane_fast(const PlaneFastDesc &, bool robust, int64_t, cudaStream_t);
+
+}  // namespace md
