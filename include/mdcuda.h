@@ -64,6 +64,7 @@ extern "C" {
 #define MD_FLAG_NO_FUSED 2u      /* force the multi-kernel path even where a fused kernel applies */
 #define MD_FLAG_FORCE_FFT2D 4u   /* 2D periodic convolver through 2D FFTs, not direct taps        */
 #define MD_FLAG_GENERIC_LINES 8u /* 1D blur: generic per-iteration line kernel, not the fast one  */
+#define MD_FLAG_BIG_FFT 16u      /* 2D Wiener through the two-level FFT passes at any size        */
 
 typedef struct md_plan md_plan; /* opaque */
 
@@ -147,6 +148,27 @@ int32_t md_rrrl_step(md_plan *plan, const void *u, const void *f, const void *b,
 int32_t md_guard(int32_t dtype, void *x, int64_t n, void *stream);
 /* min over n elements, written to *out_host (positivity contracts, deconv.py:410-412) */
 int32_t md_min(int32_t dtype, const void *x, int64_t n, double *out_host, void *stream);
+
+/* ---- one image split into row slabs over ranks (c5; driver: paper_1212_2245_b200/slab.py).
+ * Plans must be 2D direct-tap plans created with MD_FLAG_BIG_FFT. Slab buffers hold the
+ * rank's rows plus `top`/`bottom` halo rows; pointers passed to md_slab_iterate point at the
+ * first OWN row (halo rows live before / after it). */
+/* halo depth in rows needed above / below a slab for one iteration */
+int32_t md_slab_halo(const md_plan *plan, int32_t *top, int32_t *bottom);
+/* device copy of the Wiener multiplier's storage columns [col0, col0+cols) (plan-owned) */
+int32_t md_slab_prepare(md_plan *plan, int32_t col0, int32_t cols, void **mult_block);
+/* two-level FFT along the rows of a [rows][W] complex slab (forward: optional real input) */
+int32_t md_slab_rows_fft(md_plan *plan, void *z, const void *real_in, int32_t rows, int32_t inv,
+                         double scale, void *stream);
+/* forward column transform, x multiplier block, inverse, on a [H][cols] complex block */
+int32_t md_slab_cols_filter(md_plan *plan, void *zc, int32_t cols, const void *mult_block,
+                            void *stream);
+/* u0 = max(Re z / (H W), floor), fpos = max(f, floor) for `rows` rows */
+int32_t md_slab_wiener_epilogue(md_plan *plan, const void *z, const void *f, void *u0,
+                                void *fpos, int32_t rows, void *stream);
+/* one RRRL iteration of a slab whose first own row is global row `row0` */
+int32_t md_slab_iterate(md_plan *plan, const void *u, const void *fpos, void *p, void *w,
+                        void *u_out, int32_t rows, int32_t row0, void *stream);
 
 #ifdef __cplusplus
 }

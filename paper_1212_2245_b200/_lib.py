@@ -22,7 +22,7 @@ MD_AXIS_NONE, MD_AXIS_VERTICAL, MD_AXIS_HORIZONTAL = -1, 0, 1
 MD_CONV_BOX, MD_CONV_SPATIAL, MD_CONV_FOURIER, MD_CONV_FOURIER2D = 0, 1, 2, 3
 MD_INIT_WIENER, MD_INIT_CLAMPED = 0, 1
 MD_IO_F64, MD_IO_F32, MD_IO_U8 = 0, 1, 2
-MD_FLAG_RL, MD_FLAG_NO_FUSED, MD_FLAG_FORCE_FFT2D, MD_FLAG_GENERIC_LINES = 1, 2, 4, 8
+MD_FLAG_RL, MD_FLAG_NO_FUSED, MD_FLAG_FORCE_FFT2D, MD_FLAG_GENERIC_LINES, MD_FLAG_BIG_FFT = 1, 2, 4, 8, 16
 
 
 class CudaUnavailable(RuntimeError):
@@ -75,6 +75,12 @@ SIGNATURES = {
     "md_rrrl_step": (_I32, [_P, _P, _P, _P, _P, _P, _P, _I64, _D, _P]),
     "md_guard": (_I32, [_I32, _P, _I64, _P]),
     "md_min": (_I32, [_I32, _P, _I64, ctypes.POINTER(_D), _P]),
+    "md_slab_halo": (_I32, [_P, ctypes.POINTER(_I32), ctypes.POINTER(_I32)]),
+    "md_slab_prepare": (_I32, [_P, _I32, _I32, ctypes.POINTER(_P)]),
+    "md_slab_rows_fft": (_I32, [_P, _P, _P, _I32, _I32, _D, _P]),
+    "md_slab_cols_filter": (_I32, [_P, _P, _I32, _P, _P]),
+    "md_slab_wiener_epilogue": (_I32, [_P, _P, _P, _P, _P, _I32, _P]),
+    "md_slab_iterate": (_I32, [_P, _P, _P, _P, _P, _P, _I32, _I32, _P]),
 }
 
 _lib = None

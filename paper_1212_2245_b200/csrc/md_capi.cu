@@ -24,6 +24,7 @@
 #include "md_fused.h"
 #include "md_lines_fast.h"
 #include "md_plane_fast.h"
+#include "md_fft_big.h"
 #include "md_plane.h"
 
 using namespace md;
@@ -118,6 +119,14 @@ __global__ void k_unbitrev(const unsigned char *src, unsigned char *dst, int n, 
     }
 }
 
+// scatter a direct-tap list into a zeroed H x W grid, centre at (0, 0), wrapped (fft.py:204-221)
+__global__ void k_embed_taps(double *z, int H, int W, const PlaneTap *taps, int nt) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
+        const int y = ((-taps[t].dy) % H + H) % H, x = ((-taps[t].dx) % W + W) % W;
+        z[(size_t)y * W + x] = taps[t].w;
+    }
+}
+
 struct DevBuf {
     void *p = nullptr;
     size_t bytes = 0;
@@ -148,6 +157,9 @@ struct md_plan {
     PlaneTap *d_ptaps_blur = nullptr, *d_ptaps_adj = nullptr;
     std::vector<PlaneTap> htaps_blur, htaps_adj;
     bool fast_plane = false;    // register-blocked direct-tap stage kernels apply
+    bool big = false;           // two-level FFT passes for the 2D Wiener step (large images)
+    BigAxis bigH{}, bigW{};
+    std::vector<void *> owned;  // extra device tables
     int periodic = 0;
     // FFT tables (dtype copies; fp64 masters are temporaries)
     void *d_tw_n = nullptr, *d_tw_H = nullptr, *d_tw_W = nullptr;
@@ -186,6 +198,7 @@ struct md_plan {
         for (void *p : {(void *)d_taps_blur, (void *)d_taps_adj, (void *)d_ptaps_blur, (void *)d_ptaps_adj, d_tw_n,
                         d_tw_H, d_tw_W, d_mult, d_mult_nat, d_hspec, (void *)d_lut64, (void *)d_lut32})
             if (p) cudaFree(p);
+        for (void *p : owned) cudaFree(p);
         scratch.release();
         stage.release();
         partial.release();
@@ -218,6 +231,21 @@ int build_twiddles(int n, int dtype, void **out) {
     CU(cudaDeviceSynchronize());
     if (dtype == MD_F64) { cudaFree(t32); *out = t64; }
     else { cudaFree(t64); *out = t32; }
+    return MD_OK;
+}
+
+int build_big_axis(int N, int dtype, BigAxis *ax, std::vector<void *> &owned) {
+    ax->N = N;
+    split_axis(N, &ax->N1, &ax->N2);
+    ax->l1 = ilog2(ax->N1);
+    ax->l2 = ilog2(ax->N2);
+    void *a = nullptr, *b = nullptr, *c = nullptr;
+    int rc = build_twiddles(N, dtype, &a);
+    if (!rc) rc = build_twiddles(ax->N1, dtype, &b);
+    if (!rc) rc = build_twiddles(ax->N2, dtype, &c);
+    if (rc) return rc;
+    owned.push_back(a); owned.push_back(b); owned.push_back(c);
+    ax->twN = a; ax->twN1 = b; ax->twN2 = c;
     return MD_OK;
 }
 
@@ -439,17 +467,45 @@ int32_t md_plan_create(const md_plan_desc *desc, md_plan **out) {
         plane_taps(*P, true, ta, P->hadj);
         const int maxh = std::max(std::max(P->hadj.ht, P->hadj.hb), std::max(P->hadj.hl, P->hadj.hr));
         const bool direct_ok = maxh <= 40;
+        const int lim = desc->dtype == MD_F64 ? 4096 : 8192;
+        P->big = pow2 && (std::max(H, W) > lim || (desc->flags & MD_FLAG_BIG_FFT)) && (P->periodic || wiener);
         bool use_fft = P->periodic && ((desc->flags & MD_FLAG_FORCE_FFT2D) || P->hblur.nt > 96 || !direct_ok);
         if (!P->periodic && !direct_ok) return bail(fail(MD_EINVAL, "PSF too large for the direct clamped path"));
-        if (pow2 && (use_fft || wiener) && std::max(H, W) > (desc->dtype == MD_F64 ? 4096 : 8192))
-            return bail(fail(MD_EINVAL, "image side above the on-chip 2D FFT limit"));
+        if (P->big && use_fft) {
+            if (!direct_ok || P->hblur.nt > kPlaneMaxTaps)
+                return bail(fail(MD_EINVAL, "image side above the on-chip 2D FFT limit for a dense PSF"));
+            use_fft = false;    // large images iterate with direct taps; only the Wiener step needs FFTs
+        }
+        if (std::max(H, W) > 65536) return bail(fail(MD_EINVAL, "transform length above 65536"));
         P->path = use_fft ? PATH_PLANE_FFT : PATH_PLANE_DIRECT;
         if ((rc = upload(&P->d_ptaps_blur, tb.data(), tb.size()))) return bail(rc);
         if ((rc = upload(&P->d_ptaps_adj, ta.data(), ta.size()))) return bail(rc);
         P->htaps_blur = tb;
         P->htaps_adj = ta;
         P->fast_plane = !(desc->flags & MD_FLAG_GENERIC_LINES) && plane_fast_supported(P->hblur, P->hadj, desc->dtype);
-        if (pow2) {
+        if (pow2 && P->big) {
+            BigAxis h64{}, w64{};
+            std::vector<void *> tmp;
+            if ((rc = build_big_axis(H, MD_F64, &h64, tmp)) || (rc = build_big_axis(W, MD_F64, &w64, tmp)) ||
+                (rc = build_big_axis(H, desc->dtype, &P->bigH, P->owned)) ||
+                (rc = build_big_axis(W, desc->dtype, &P->bigW, P->owned)))
+                return bail(rc);
+            double *emb = nullptr;
+            double2 *h64s = nullptr;
+            CU(cudaMalloc(&emb, (size_t)H * W * sizeof(double)));
+            CU(cudaMalloc(&h64s, (size_t)H * W * sizeof(double2)));
+            CU(cudaMemset(emb, 0, (size_t)H * W * sizeof(double)));
+            k_embed_taps<<<(tb.size() + 255) / 256, 256>>>(emb, H, W, P->d_ptaps_blur, (int)tb.size());
+            CU(cudaGetLastError());
+            CU(big_axis<double>(w64, h64s, H, W, 1, 0, emb, nullptr, nullptr, 0, 1.0, 1, 0));
+            CU(big_axis<double>(h64, h64s, H, W, 0, 0, nullptr, nullptr, nullptr, 0, 1.0, 1, 0));
+            CU(cudaDeviceSynchronize());
+            cudaFree(emb);
+            for (void *p : tmp) cudaFree(p);
+            rc = make_filter(h64s, (int64_t)H * W, desc->wiener_k, desc->dtype, &P->d_mult);
+            cudaFree(h64s);
+            if (rc) return bail(rc);
+        } else if (pow2) {
             if ((rc = build_twiddles(H, desc->dtype, &P->d_tw_H))) return bail(rc);
             if ((rc = build_twiddles(W, desc->dtype, &P->d_tw_W))) return bail(rc);
             std::vector<double> emb((size_t)H * W, 0.0);       // fft.py:204-221
@@ -468,7 +524,9 @@ int32_t md_plan_create(const md_plan_desc *desc, md_plan **out) {
         }
         snprintf(buf, sizeof buf, "plane: %dx%d %s, %d taps (halo %d/%d/%d/%d), %s", H, W,
                  P->periodic ? "periodic" : "clamped", P->hblur.nt, P->hblur.ht, P->hblur.hb, P->hblur.hl,
-                 P->hblur.hr, use_fft ? "2D FFT convolver (4 launches/iteration)" : "direct taps (2 launches/iteration)");
+                 P->hblur.hr, use_fft ? "2D FFT convolver (4 launches/iteration)"
+                                      : (P->big ? "two-level FFT Wiener, direct taps (2 launches/iteration)"
+                                                : "direct taps (2 launches/iteration)"));
     }
     P->describe = buf;
     // divergence table (deconv.py:101-112, 137-139)
@@ -614,6 +672,16 @@ Fft2Args fft2_base(const md_plan &P) {
 template <typename T>
 int wiener_plane(md_plan &P, const void *f, void *out, void *fpos, void *z, bool clamp, bool fwd_after,
                  int64_t nb, cudaStream_t st) {
+    if (P.big) {
+        const int H = P.d.height, W = P.d.width;
+        CU(big_axis<T>(P.bigW, z, H, W, 1, 0, f, nullptr, nullptr, 0, 1.0, nb, st));
+        CU(big_axis<T>(P.bigH, z, H, W, 0, 0, nullptr, nullptr, P.d_mult, 0, 1.0, nb, st));
+        CU(big_axis<T>(P.bigH, z, H, W, 0, 1, nullptr, nullptr, nullptr, 0, 1.0, nb, st));
+        CU(big_axis<T>(P.bigW, z, H, W, 1, 1, nullptr, nullptr, nullptr, 0, 1.0, nb, st));
+        CU(launch_big_wiener_epilogue<T>(z, f, out, fpos, (int64_t)H * W * nb, 1.0 / ((double)H * W), P.d.floor,
+                                         clamp ? 1 : 0, st));
+        return MD_OK;
+    }
     Fft2Args a = fft2_base<T>(P);
     a.load = R_LOAD_REAL; a.ra = f; a.rb = nullptr; a.z = z; a.epi = R_EPI_NONE; a.fwd_after = 1;
     CU(launch_fft2_rows<T>(a, nb, st));
@@ -1074,6 +1142,116 @@ int32_t md_guard(int32_t dtype, void *x, int64_t n, void *stream) {
     if (!x || n < 0) return fail(MD_EINVAL, "bad arguments");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     CU(dtype == MD_F64 ? launch_guard<double>(x, n, st) : launch_guard<float>(x, n, st));
+    return MD_OK;
+}
+
+}  // extern "C"
+
+// ======================================================================== row slabs (c5)
+// One image split into row slabs over ranks. The driver
+// (paper_1212_2245_b200/slab.py) moves halo rows (NCCL send/recv) and transposes the
+// spectrum (all-to-all); these entries are the per-rank compute.
+namespace {
+
+__global__ void k_copy_cols(const unsigned char *src, unsigned char *dst, int H, int W, int col0, int cols, int es) {
+    const int64_t n = (int64_t)H * cols;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t y = i / cols, x = i - y * cols;
+        const unsigned char *s = src + ((int64_t)y * W + col0 + x) * es;
+        unsigned char *d = dst + i * es;
+        for (int b = 0; b < es; ++b) d[b] = s[b];
+    }
+}
+
+int slab_check(const md_plan *P) {
+    if (!P) return fail(MD_EINVAL, "null plan");
+    if (P->path != PATH_PLANE_DIRECT || !P->big || !P->fast_plane)
+        return fail(MD_EINVAL, "slab execution needs a 2D direct-tap plan built with MD_FLAG_BIG_FFT");
+    return MD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t md_slab_halo(const md_plan *P, int32_t *top, int32_t *bottom) {
+    int rc = slab_check(P);
+    if (rc) return rc;
+    // stage A runs on rows [-adj.ht, S + adj.hb) and reads blur.ht / blur.hb more; TV needs 2
+    *top = std::max(P->hadj.ht + P->hblur.ht, 2);
+    *bottom = std::max(P->hadj.hb + P->hblur.hb, 2);
+    return MD_OK;
+}
+
+int32_t md_slab_prepare(md_plan *P, int32_t col0, int32_t cols, void **mult_block) {
+    int rc = slab_check(P);
+    if (rc) return rc;
+    if (col0 < 0 || cols < 1 || col0 + cols > P->d.width) return fail(MD_EINVAL, "bad column block");
+    const int ces = P->d.dtype == MD_F64 ? 16 : 8;
+    void *blk = nullptr;
+    CU(cudaMalloc(&blk, (size_t)P->d.height * cols * ces));
+    k_copy_cols<<<1024, 256>>>((const unsigned char *)P->d_mult, (unsigned char *)blk, P->d.height, P->d.width,
+                               col0, cols, ces);
+    CU(cudaGetLastError());
+    CU(cudaDeviceSynchronize());
+    P->owned.push_back(blk);
+    *mult_block = blk;
+    return MD_OK;
+}
+
+int32_t md_slab_rows_fft(md_plan *P, void *z, const void *real_in, int32_t rows, int32_t inv, double scale,
+                         void *stream) {
+    int rc = slab_check(P);
+    if (rc) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int W = P->d.width;
+    CU(P->d.dtype == MD_F64 ? big_axis<double>(P->bigW, z, rows, W, 1, inv, real_in, nullptr, nullptr, 0, scale, 1, st)
+                            : big_axis<float>(P->bigW, z, rows, W, 1, inv, real_in, nullptr, nullptr, 0, scale, 1, st));
+    return MD_OK;
+}
+
+int32_t md_slab_cols_filter(md_plan *P, void *zc, int32_t cols, const void *mult_block, void *stream) {
+    int rc = slab_check(P);
+    if (rc) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int H = P->d.height;
+    if (P->d.dtype == MD_F64) {
+        CU(big_axis<double>(P->bigH, zc, H, cols, 0, 0, nullptr, nullptr, mult_block, 0, 1.0, 1, st));
+        CU(big_axis<double>(P->bigH, zc, H, cols, 0, 1, nullptr, nullptr, nullptr, 0, 1.0, 1, st));
+    } else {
+        CU(big_axis<float>(P->bigH, zc, H, cols, 0, 0, nullptr, nullptr, mult_block, 0, 1.0, 1, st));
+        CU(big_axis<float>(P->bigH, zc, H, cols, 0, 1, nullptr, nullptr, nullptr, 0, 1.0, 1, st));
+    }
+    return MD_OK;
+}
+
+int32_t md_slab_wiener_epilogue(md_plan *P, const void *z, const void *f, void *u0, void *fpos, int32_t rows,
+                                void *stream) {
+    int rc = slab_check(P);
+    if (rc) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t n = (int64_t)rows * P->d.width;
+    const double scale = 1.0 / ((double)P->d.height * P->d.width);
+    CU(P->d.dtype == MD_F64 ? launch_big_wiener_epilogue<double>(z, f, u0, fpos, n, scale, P->d.floor, 1, st)
+                            : launch_big_wiener_epilogue<float>(z, f, u0, fpos, n, scale, P->d.floor, 1, st));
+    return MD_OK;
+}
+
+int32_t md_slab_iterate(md_plan *P, const void *u, const void *fpos, void *p, void *w, void *u_out, int32_t rows,
+                        int32_t row0, void *stream) {
+    int rc = slab_check(P);
+    if (rc) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    PlaneFastDesc s{};
+    s.u = u; s.f = fpos; s.p = p; s.w = w; s.u_out = u_out;     // all point at own row 0 of haloed buffers
+    s.H = rows; s.W = P->d.width; s.periodic = P->periodic;
+    s.slab = 1; s.gy0 = row0; s.Hg = P->d.height;
+    s.row_a0 = -P->hadj.ht; s.rows_a = rows + P->hadj.ht + P->hadj.hb;
+    s.hb = P->hblur; s.ha = P->hadj; s.taps_blur = &P->htaps_blur; s.taps_adj = &P->htaps_adj;
+    s.alpha = P->d.alpha; s.eps_d2 = P->d.eps_data * P->d.eps_data; s.eps_r2 = P->d.eps_reg * P->d.eps_reg;
+    s.has_d = P->has_d; s.lut = P->lut;
+    CU(P->d.dtype == MD_F64 ? launch_plane_fast<double>(s, P->robust, 1, st)
+                            : launch_plane_fast<float>(s, P->robust, 1, st));
     return MD_OK;
 }
 

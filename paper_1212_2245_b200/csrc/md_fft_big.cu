@@ -1,0 +1,183 @@
+// md_fft_big.cu -- two-level ("four-step") FFT passes for transform lengths beyond one
+// block's shared memory (the 16384^2 single-image config), and for the
+// column transforms of a row slab's all-to-all-transposed block.
+//
+// A length-N transform along an axis, N = N1 * N2 with j = j1 + N1 j2, runs as two passes,
+// each a batch of short sub-transforms staged through shared memory:
+//   F1: for each j1, DIF over j2 (stride N1)   -> position j1 + N1 p holds k2 = rev(p);
+//       multiply by W_N^{j1 rev(p)}
+//   F2: for each p,  DIF over j1 (stride 1)    -> position q + N1 p holds k = rev(p) + N2 rev(q)
+// and the inverse undoes them in reverse order (DIT, conjugate twiddles). The spectrum is
+// held in this "storage order"; filters computed by the same passes line up with it, so no
+// permutation is ever executed (fft.py:87-117 convention: unnormalised forward, 1/N inverse).
+//
+// Generic line geometry: line (a, b) starts at a*sa + b*sb and has L elements at stride es;
+// a block transforms G lines with consecutive b.
+#include "md_fft.cuh"
+#include "md_fft_big.h"
+
+namespace md {
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_subfft(SubFftArgs a) {
+    using C = cx_t<T>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C *s = reinterpret_cast<C *>(smem_raw);
+    const int L = 1 << a.log2L, G = a.G, ls = L + 1;
+    const int blocks_b = (a.B + G - 1) / G;
+    const int ai = blockIdx.x / blocks_b, b0 = (blockIdx.x - ai * blocks_b) * G;
+    const int64_t fr = blockIdx.y;
+    C *z = static_cast<C *>(a.z) + fr * a.frame;
+    const T *ra = a.ra ? static_cast<const T *>(a.ra) + fr * a.rframe : nullptr;
+    const T *rb = a.rb ? static_cast<const T *>(a.rb) + fr * a.rframe : nullptr;
+    const int64_t base = (int64_t)ai * a.sa + (int64_t)b0 * a.sb;
+    const bool line_fast = a.es == 1;          // contiguous lines: iterate along the line
+    for (int idx = threadIdx.x; idx < G * L; idx += blockDim.x) {
+        int g, e;
+        if (line_fast) { g = idx >> a.log2L; e = idx & (L - 1); }
+        else { e = idx / G; g = idx - e * G; }
+        C v = mkc<T>(T(0), T(0));
+        if (b0 + g < a.B) {
+            const int64_t o = base + (int64_t)g * a.sb + (int64_t)e * a.es;
+            if (ra) v = mkc<T>(ra[o], rb ? rb[o] : T(0));
+            else v = z[o];
+        }
+        s[g * ls + e] = v;
+    }
+    __syncthreads();
+    const C *twL = static_cast<const C *>(a.twL);
+    if (a.inv) fft_dit_inv_lines(s, a.log2L, G, ls, twL);
+    else fft_dif_lines(s, a.log2L, G, ls, twL);
+    // inter-pass twiddle W_N^{+-(digit * rev(pos))}, digit = line (FWD) or element (INV) index
+    const C *twN = static_cast<const C *>(a.twN);
+    const int N = a.N;
+    const C *filt = static_cast<const C *>(a.filt);
+    const T scale = T(a.scale);
+    for (int idx = threadIdx.x; idx < G * L; idx += blockDim.x) {
+        int g, e;
+        if (line_fast) { g = idx >> a.log2L; e = idx & (L - 1); }
+        else { e = idx / G; g = idx - e * G; }
+        if (b0 + g >= a.B) continue;
+        C v = s[g * ls + e];
+        if (a.tw_mode != TW_NONE) {
+            const int lb = a.tw_digit_is_a ? ai : b0 + g;                 // line digit
+            const int re = (int)(__brev((unsigned)e) >> (32 - a.log2L));   // rev(pos) in the line
+            const int rl = (int)(__brev((unsigned)lb) >> (32 - a.log2Lother));
+            // FWD (after F1): W_N^{line * rev(e)};  INV (after I2): conj W_N^{e * rev(line)}
+            const int k = a.tw_mode == TW_FWD ? (int)(((int64_t)lb * re) & (N - 1)) : (int)(((int64_t)e * rl) & (N - 1));
+            const C w = twN[k & (N / 2 - 1)];
+            const C ww = k < N / 2 ? w : mkc<T>(-w.x, -w.y);
+            v = a.tw_mode == TW_FWD ? cmul(v, ww) : cmulc(v, ww);
+        }
+        const int64_t o = base + (int64_t)g * a.sb + (int64_t)e * a.es;
+        if (filt) v = a.conj_filt ? cmulc(v, filt[o]) : cmul(v, filt[o]);
+        if (scale != T(1)) v = cscale(v, scale);
+        z[o] = v;
+    }
+}
+
+// u0 = max(Re z * scale, floor) (or unclamped), fpos = max(f, floor)
+template <typename T>
+__global__ void k_big_wiener_epilogue(const void *z_, const T *__restrict__ f, T *__restrict__ u, T *__restrict__ fpos,
+                                      int64_t n, T scale, T floor, int clamp) {
+    const cx_t<T> *z = static_cast<const cx_t<T> *>(z_);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        T v = z[i].x * scale;
+        if (clamp) v = v > floor ? v : floor;
+        u[i] = v;
+        if (fpos) {
+            const T fv = f[i];
+            fpos[i] = fv > floor ? fv : floor;
+        }
+    }
+}
+
+template <typename T>
+cudaError_t launch_subfft(const SubFftArgs &a0, int64_t batch, cudaStream_t st) {
+    SubFftArgs a = a0;
+    const int L = 1 << a.log2L;
+    a.G = std::max(1, std::min(16, 2048 / L));
+    const size_t smem = (size_t)a.G * (L + 1) * sizeof(cx_t<T>);
+    cudaError_t e = cudaFuncSetAttribute(k_subfft<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int blocks_b = (a.B + a.G - 1) / a.G;
+    for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
+        const int nb = (int)((batch - b0) < 65535 ? (batch - b0) : 65535);
+        SubFftArgs ab = a;
+        ab.z = static_cast<char *>(a.z) + b0 * a.frame * (int64_t)sizeof(cx_t<T>);
+        if (a.ra) ab.ra = static_cast<const char *>(a.ra) + b0 * a.rframe * (int64_t)sizeof(T);
+        if (a.rb) ab.rb = static_cast<const char *>(a.rb) + b0 * a.rframe * (int64_t)sizeof(T);
+        k_subfft<T><<<dim3((unsigned)(a.A * blocks_b), nb), 256, smem, st>>>(ab);
+    }
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_big_wiener_epilogue(const void *z, const void *f, void *u, void *fpos, int64_t n, double scale,
+                                       double floor, int clamp, cudaStream_t st) {
+    int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 32);
+    k_big_wiener_epilogue<T><<<blocks, 256, 0, st>>>(z, static_cast<const T *>(f), static_cast<T *>(u),
+                                                     static_cast<T *>(fpos), n, T(scale), T(floor), clamp);
+    return cudaGetLastError();
+}
+
+// ---- axis plans -------------------------------------------------------------------------
+
+// split N = N1 * N2 with both factors <= 256 (N <= 65536), N1 >= N2
+void split_axis(int N, int *N1, int *N2) {
+    int l = 0;
+    while ((1 << l) < N) ++l;
+    const int l2 = l / 2, l1 = l - l2;
+    *N1 = 1 << l1;
+    *N2 = 1 << l2;
+}
+
+// Forward (inv = 0) or inverse (inv = 1) two-pass transform along the rows (axis = 1,
+// length W) or columns (axis = 0, length H) of a [batch][H][W] complex field.
+template <typename T>
+cudaError_t big_axis(const BigAxis &ax, void *z, int H, int W, int axis, int inv, const void *ra, const void *rb,
+                     const void *filt, int conj_filt, double scale_last, int64_t batch, cudaStream_t st) {
+    const int N = axis == 1 ? W : H;
+    const int N1 = ax.N1, N2 = ax.N2;
+    SubFftArgs p1{}, p2{};
+    for (SubFftArgs *p : {&p1, &p2}) {
+        p->z = z; p->frame = (int64_t)H * W; p->rframe = (int64_t)H * W;
+        p->N = N; p->twN = ax.twN; p->inv = inv; p->scale = 1.0;
+    }
+    // pass "1" : sub-DFT over j2 (length N2, stride N1), lines j1 = 0..N1-1
+    // pass "2" : sub-DFT over j1 (length N1, stride 1),  lines p  = 0..N2-1
+    if (axis == 1) {
+        p1.A = H; p1.sa = W; p1.B = N1; p1.sb = 1; p1.es = N1;
+        p2.A = H; p2.sa = W; p2.B = N2; p2.sb = N1; p2.es = 1;
+    } else {
+        p1.A = N1; p1.sa = W; p1.B = W; p1.sb = 1; p1.es = (int64_t)N1 * W;
+        p2.A = N2; p2.sa = (int64_t)N1 * W; p2.B = W; p2.sb = 1; p2.es = W;
+    }
+    p1.log2L = ax.l2; p1.twL = ax.twN2; p1.log2Lother = ax.l1;
+    p2.log2L = ax.l1; p2.twL = ax.twN1; p2.log2Lother = ax.l2;
+    p1.tw_digit_is_a = axis == 0;          // the j1 digit: line index b (rows) or a (columns)
+    p2.tw_digit_is_a = axis == 0;          // the p digit likewise
+    cudaError_t e;
+    if (!inv) {
+        p1.tw_mode = TW_FWD; p1.ra = ra; p1.rb = rb;
+        p2.tw_mode = TW_NONE; p2.filt = filt; p2.conj_filt = conj_filt; p2.scale = scale_last;
+        if ((e = launch_subfft<T>(p1, batch, st)) != cudaSuccess) return e;
+        return launch_subfft<T>(p2, batch, st);
+    }
+    p2.tw_mode = TW_INV;                   // conj W_N^{j1 rev(p)} after the sub-IDFT over j1
+    p1.tw_mode = TW_NONE; p1.scale = scale_last;
+    if ((e = launch_subfft<T>(p2, batch, st)) != cudaSuccess) return e;
+    return launch_subfft<T>(p1, batch, st);
+}
+
+template cudaError_t launch_big_wiener_epilogue<double>(const void *, const void *, void *, void *, int64_t, double,
+                                                        double, int, cudaStream_t);
+template cudaError_t launch_big_wiener_epilogue<float>(const void *, const void *, void *, void *, int64_t, double,
+                                                       double, int, cudaStream_t);
+template cudaError_t big_axis<double>(const BigAxis &, void *, int, int, int, int, const void *, const void *,
+                                      const void *, int, double, int64_t, cudaStream_t);
+template cudaError_t big_axis<float>(const BigAxis &, void *, int, int, int, int, const void *, const void *,
+                                     const void *, int, double, int64_t, cudaStream_t);
+
+}  // namespace md

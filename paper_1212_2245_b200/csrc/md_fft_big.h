@@ -1,0 +1,41 @@
+// md_fft_big.h -- interface of the two-level FFT passes (md_fft_big.cu).
+#pragma once
+
+#include <algorithm>
+
+#include "md_internal.h"
+
+namespace md {
+
+enum { TW_NONE = 0, TW_FWD = 1, TW_INV = 2 };
+
+struct SubFftArgs {
+    void *z;                     // complex field, [batch] frames of `frame` elements
+    const void *ra, *rb;         // optional real inputs (first forward pass)
+    int64_t frame, rframe;
+    int A, B, G, log2L, log2Lother, N;
+    int64_t sa, sb, es;          // line (a, b) base = a*sa + b*sb, element stride es
+    const void *twL;             // W_L^k, k < L/2 (sub-transform)
+    const void *twN;             // W_N^k, k < N/2 (inter-pass twiddles)
+    int inv, tw_mode, tw_digit_is_a;
+    const void *filt;            // multiply by filt[address] after the pass (last forward pass)
+    int conj_filt;
+    double scale;
+};
+
+// one axis of a two-level transform: N = N1 * N2, twiddle tables in the plan dtype
+struct BigAxis {
+    int N, N1, N2, l1, l2;
+    const void *twN, *twN1, *twN2;
+};
+
+void split_axis(int N, int *N1, int *N2);
+template <typename T> cudaError_t launch_subfft(const SubFftArgs &, int64_t batch, cudaStream_t);
+template <typename T>
+cudaError_t big_axis(const BigAxis &ax, void *z, int H, int W, int axis, int inv, const void *ra, const void *rb,
+                     const void *filt, int conj_filt, double scale_last, int64_t batch, cudaStream_t st);
+template <typename T>
+cudaError_t launch_big_wiener_epilogue(const void *z, const void *f, void *u, void *fpos, int64_t n, double scale,
+                                       double floor, int clamp, cudaStream_t st);
+
+}  // namespace md

@@ -29,10 +29,11 @@ __device__ __forceinline__ int pf_resolve(int k, int n, int periodic) {
 
 template <typename T>
 __device__ void pf_load(T *s, int ss, const T *__restrict__ src, int H, int W, int y0, int x0, const PlaneHalo &h,
-                        int periodic) {
+                        int periodic, int slab) {
     const int rows = FY + h.ht + h.hb, cols = FX + h.hl + h.hr;
     for (int i = threadIdx.x / 32; i < rows; i += blockDim.x / 32) {
-        const int y = pf_resolve(y0 - h.ht + i, H, periodic);
+        // slab mode: the caller's buffer carries the neighbours' rows (halo), read them as is
+        const int y = slab ? y0 - h.ht + i : pf_resolve(y0 - h.ht + i, H, periodic);
         const T *srow = src + (int64_t)y * W;
         for (int j = threadIdx.x & 31; j < cols; j += 32) s[i * ss + j] = srow[pf_resolve(x0 - h.hl + j, W, periodic)];
     }
@@ -64,7 +65,7 @@ k_plane_a_fast(PlaneFastArgs<T, MAXT> a) {
     T *w = a.w + fr * fsz;
     const int y0 = blockIdx.y * FY, x0 = blockIdx.x * FX;
     const int ss = FX + a.hb.hl + a.hb.hr + 1;
-    pf_load<T>(su, ss, u, H, W, y0, x0, a.hb, a.periodic);
+    pf_load<T>(su, ss, u, H, W, y0, x0, a.hb, a.periodic, a.slab);
     __syncthreads();
     const int ty = threadIdx.x >> 3, cx = threadIdx.x & 7;
     const int y = y0 + ty;
@@ -108,13 +109,15 @@ k_plane_b_fast(PlaneFastArgs<T, MAXT> a) {
     const T *u = a.u + fr * fsz;
     T *uo = a.u_out + fr * fsz;
     const int y0 = blockIdx.y * FY, x0 = blockIdx.x * FX;
-    pf_load<T>(sp, ss, a.p + fr * fsz, H, W, y0, x0, a.ha, a.periodic);
-    if (ROBUST) pf_load<T>(sw, ss, a.w + fr * fsz, H, W, y0, x0, a.ha, a.periodic);
+    pf_load<T>(sp, ss, a.p + fr * fsz, H, W, y0, x0, a.ha, a.periodic, a.slab);
+    if (ROBUST) pf_load<T>(sw, ss, a.w + fr * fsz, H, W, y0, x0, a.ha, a.periodic, a.slab);
+    const int gy0 = a.gy0, Hg = a.Hg;
     for (int i = threadIdx.x / 32; i < FY + 4; i += 8) {
         const int yy = y0 - 2 + i;
+        const bool rok = gy0 + yy >= 0 && gy0 + yy < Hg && (a.slab || (yy >= 0 && yy < H));
         for (int j = threadIdx.x & 31; j < FX + 4; j += 32) {
             const int xx = x0 - 2 + j;
-            su[i * US + j] = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? u[(int64_t)yy * W + xx] : T(0);
+            su[i * US + j] = (rok && xx >= 0 && xx < W) ? u[(int64_t)yy * W + xx] : T(0);
         }
     }
     __syncthreads();
@@ -122,7 +125,8 @@ k_plane_b_fast(PlaneFastArgs<T, MAXT> a) {
     if (a.has_d) {
         for (int i = threadIdx.x / 32; i < FY + 2; i += 8) {
             const int yy = y0 - 1 + i;
-            if (yy < 0 || yy >= H) continue;
+            const int gyy = gy0 + yy;
+            if (gyy < 0 || gyy >= Hg) continue;
             for (int j = threadIdx.x & 31; j < FX + 2; j += 32) {
                 const int xx = x0 - 1 + j;
                 if (xx < 0 || xx >= W) continue;
@@ -131,8 +135,8 @@ k_plane_b_fast(PlaneFastArgs<T, MAXT> a) {
                 T q = T(0);
                 if (xx + 1 < W) { const T d = c[1] - c0; q += d * d; }
                 if (xx > 0) { const T d = c0 - c[-1]; q += d * d; }
-                if (yy + 1 < H) { const T d = c[US] - c0; q += d * d; }
-                if (yy > 0) { const T d = c0 - c[-US]; q += d * d; }
+                if (gyy + 1 < Hg) { const T d = c[US] - c0; q += d * d; }
+                if (gyy > 0) { const T d = c0 - c[-US]; q += d * d; }
                 sg[i * GS + j] = T(0.5) * frsqrt(T(0.5) * q + eps_r2);
             }
         }
@@ -158,8 +162,8 @@ k_plane_b_fast(PlaneFastArgs<T, MAXT> a) {
             const T gc = g[0];
             if (x + 1 < W) d += (gc + g[1]) * (c[1] - uv);
             if (x > 0) d -= (g[-1] + gc) * (uv - c[-1]);
-            if (y + 1 < H) d += (gc + g[GS]) * (c[US] - uv);
-            if (y > 0) d -= (g[-GS] + gc) * (uv - c[-US]);
+            if (gy0 + y + 1 < Hg) d += (gc + g[GS]) * (c[US] - uv);
+            if (gy0 + y > 0) d -= (g[-GS] + gc) * (uv - c[-US]);
         }
         T nm = num[r];
         T dn = ROBUST ? den[r] : T(1);
@@ -204,6 +208,7 @@ cudaError_t launch_plane_fast(const PlaneFastDesc &d, bool robust, int64_t batch
     a.w = static_cast<T *>(d.w);
     a.u_out = static_cast<T *>(d.u_out);
     a.H = d.H; a.W = d.W; a.periodic = d.periodic;
+    a.slab = d.slab; a.gy0 = d.slab ? d.gy0 : 0; a.Hg = d.slab ? d.Hg : d.H;
     a.hb = d.hb; a.ha = d.ha;
     fill_fast_taps<T, MAXT>(a.tb, *d.taps_blur, FX + d.hb.hl + d.hb.hr + 1);
     fill_fast_taps<T, MAXT>(a.ta, *d.taps_adj, FX + d.ha.hl + d.ha.hr + 1);
@@ -217,6 +222,16 @@ cudaError_t launch_plane_fast(const PlaneFastDesc &d, bool robust, int64_t batch
     cudaError_t e = cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sa);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
     if (e != cudaSuccess) return e;
+    if (d.slab) {
+        // stage A over the extended rows [row_a0, row_a0 + rows_a), stage B over the own rows
+        PlaneFastArgs<T, MAXT> aa = a;
+        const int64_t off = (int64_t)d.row_a0 * d.W;
+        aa.u += off; aa.f += off; aa.p += off; aa.w += off;
+        aa.H = d.rows_a; aa.gy0 = d.gy0 + d.row_a0;
+        ka<<<dim3((d.W + FX - 1) / FX, (d.rows_a + FY - 1) / FY, 1), 256, sa, st>>>(aa);
+        kb<<<dim3((d.W + FX - 1) / FX, (d.H + FY - 1) / FY, 1), 256, sb, st>>>(a);
+        return cudaGetLastError();
+    }
     const int64_t fsz = (int64_t)d.H * d.W;
     for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
         const int nb = (int)((batch - b0) < 65535 ? (batch - b0) : 65535);

@@ -19,6 +19,7 @@ template <typename T, int MAXT> struct PlaneFastArgs {
     const T *u, *f;     // iterate, floored observation
     T *p, *w, *u_out;
     int H, W, periodic;
+    int slab, gy0, Hg;  // slab mode: rows read directly (halo present); global row of row 0; global height
     PlaneHalo hb, ha;
     FastTaps<T, MAXT> tb, ta;
     T alpha, eps_d2, eps_r2;
@@ -30,6 +31,8 @@ struct PlaneFastDesc {
     const void *u, *f;
     void *p, *w, *u_out;
     int H, W, periodic;
+    int slab, gy0, Hg;         // see PlaneFastArgs
+    int rows_a, row_a0;        // slab: stage A computes rows [row_a0, row_a0 + rows_a) (relative to own row 0)
     PlaneHalo hb, ha;
     const std::vector<PlaneTap> *taps_blur, *taps_adj;   // host copies
     double alpha, eps_d2, eps_r2;

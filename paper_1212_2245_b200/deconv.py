@@ -355,7 +355,7 @@ class DeblurPipeline:
     def __init__(self, shape: tuple[int, int], psf: Psf, params: DeconvParams,
                  scenario: Scenario | None = None, workers: int = 1, lut: DivergenceLut | None = None,
                  dtype: str = "float64", fused: bool | None = None, force_fft2d: bool = False,
-                 generic_lines: bool = False):
+                 generic_lines: bool = False, big_fft: bool = False):
         if scenario is None:
             scenario = default_scenario(psf)
         if scenario in (Scenario.BOX_1D, Scenario.FOURIER_1D) and not psf.is_1d:
@@ -379,7 +379,8 @@ class DeblurPipeline:
                 raise ValueError("the blur axis must have power-of-two extent")
         self.psf = psf
         self._plan = GpuPlan(self.shape, psf, params, _SCENARIO_CONV[scenario], init="wiener", dtype=dtype,
-                             force_fft2d=force_fft2d, fused=fused, generic_lines=generic_lines)
+                             force_fft2d=force_fft2d, fused=fused, generic_lines=generic_lines,
+                             big_fft=big_fft)
         self._wiener_plan = None
 
     @property

@@ -38,7 +38,7 @@ class GpuPlan:
 
     def __init__(self, shape, psf: Psf, params: DeconvParams, conv: str, init: str = "wiener",
                  dtype: str = "float64", rl: bool = False, force_fft2d: bool = False,
-                 fused: bool | None = None, generic_lines: bool = False):
+                 fused: bool | None = None, generic_lines: bool = False, big_fft: bool = False):
         if dtype not in _DTYPES:
             raise ValueError(f"dtype must be one of {sorted(_DTYPES)}")
         if conv not in _CONV:
@@ -67,7 +67,7 @@ class GpuPlan:
         d.init = L.MD_INIT_WIENER if init == "wiener" else L.MD_INIT_CLAMPED
         d.iterations = int(params.iterations)
         d.flags = ((L.MD_FLAG_RL if rl else 0) | (L.MD_FLAG_FORCE_FFT2D if force_fft2d else 0)
-                   | (L.MD_FLAG_GENERIC_LINES if generic_lines else 0))
+                   | (L.MD_FLAG_GENERIC_LINES if generic_lines else 0) | (L.MD_FLAG_BIG_FFT if big_fft else 0))
         d.wiener_k, d.alpha = params.wiener_k, (0.0 if rl else params.alpha)
         d.eps_data, d.eps_reg, d.floor = params.eps_data, params.eps_reg, params.floor
         h = ctypes.c_void_p()

@@ -1,0 +1,249 @@
+"""One large image split into row slabs over ranks (BASELINE.json configs[4], "c5").
+
+SPMD driver: every rank owns ``S = H / world`` consecutive rows plus halo rows and runs
+
+  Wiener:  rows FFT (local) -> all-to-all (row slabs -> column blocks) -> column FFT,
+           x multiplier, inverse column FFT (local) -> all-to-all back -> inverse rows FFT
+           -> u0 = max(Wiener, floor), fpos = max(f, floor)                (deconv.py:660-672)
+  then ``iterations`` x:  halo exchange of u (periodic neighbours, matching the FOURIER_2D
+           convolver's wrap, deconv.py:359-376) -> one RRRL iteration on the slab
+           (direct taps, TV with Neumann boundary at the GLOBAL first/last row only)
+
+Communication is only the halo rows (NCCL send/recv to rank +-1 mod world) and the two
+spectrum transposes of the Wiener step (all-to-all). ``DistComm`` uses torch.distributed
+(NCCL on GPUs, gloo on CPU); ``LocalComm`` runs the same SPMD code with one thread per
+"rank" inside one process (host-side barriers and copies, no kernel waits on another), which
+is how the decomposition is exercised on a single GPU.
+
+Compute is delegated to a backend: ``CudaSlabBackend`` calls the C ABI (md_slab_*); tests may
+plug in a NumPy backend to check the decomposition logic on CPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+
+import numpy as np
+
+from . import _lib as L
+
+__all__ = ["SlabGeometry", "DistComm", "LocalComm", "CudaSlabBackend", "SlabWorker", "run_slabs"]
+
+
+class SlabGeometry:
+    def __init__(self, H: int, W: int, rank: int, world: int, top: int, bottom: int):
+        if H % world or W % world:
+            raise ValueError("image height and width must divide by the number of ranks")
+        self.H, self.W, self.rank, self.world = H, W, rank, world
+        self.S = H // world
+        self.Wb = W // world
+        self.top, self.bottom = top, bottom
+        if top > self.S or bottom > self.S:
+            raise ValueError("slabs thinner than the PSF halo")
+        self.row0 = rank * self.S
+
+    @property
+    def ext_rows(self) -> int:
+        return self.top + self.S + self.bottom
+
+
+# ---------------------------------------------------------------------------------- comms
+
+class DistComm:
+    """torch.distributed collectives (NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+
+    def exchange(self, rank, send_up, send_down, recv_up, recv_down):
+        """send_up -> rank-1 (its bottom halo); send_down -> rank+1 (its top halo); periodic."""
+        dist = self.dist
+        prev, nxt = (self.rank - 1) % self.world, (self.rank + 1) % self.world
+        if self.world == 1:
+            recv_up.copy_(send_down)
+            recv_down.copy_(send_up)
+            return
+        ops = [dist.P2POp(dist.isend, send_up.contiguous(), prev, self.group),
+               dist.P2POp(dist.irecv, recv_down, nxt, self.group),
+               dist.P2POp(dist.isend, send_down.contiguous(), nxt, self.group),
+               dist.P2POp(dist.irecv, recv_up, prev, self.group)]
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+
+    def all_to_all(self, rank, recv, send):
+        """send[q] goes to rank q, recv[q] comes from rank q (equal splits along dim 0)."""
+        if self.world == 1:
+            recv.copy_(send)
+            return
+        self.dist.all_to_all_single(recv, send, group=self.group)
+
+    def barrier(self, rank):
+        if self.world > 1:
+            self.dist.barrier(self.group)
+
+
+class LocalComm:
+    """All ranks as threads of one process; collectives = host barriers + tensor copies."""
+
+    def __init__(self, world: int):
+        self.world = world
+        self._bar = threading.Barrier(world)
+        self._box: dict = {}
+
+    def exchange(self, rank, send_up, send_down, recv_up, recv_down):
+        self._box[rank] = (send_up, send_down)
+        self._bar.wait()
+        prev, nxt = (rank - 1) % self.world, (rank + 1) % self.world
+        recv_up.copy_(self._box[prev][1])       # prev's bottom rows -> my top halo
+        recv_down.copy_(self._box[nxt][0])      # next's top rows -> my bottom halo
+        self._bar.wait()
+
+    def all_to_all(self, rank, recv, send):
+        self._box[rank] = send
+        self._bar.wait()
+        for q in range(self.world):
+            recv[q].copy_(self._box[q][rank])
+        self._bar.wait()
+
+    def barrier(self, rank):
+        self._bar.wait()
+
+
+# ---------------------------------------------------------------------------------- backend
+
+class CudaSlabBackend:
+    """Per-rank compute through the C ABI (md_slab_*)."""
+
+    def __init__(self, plan):
+        self.plan = plan
+        self.lib = plan.lib
+        top, bot = ctypes.c_int32(), ctypes.c_int32()
+        L.check(self.lib.md_slab_halo(plan._h, ctypes.byref(top), ctypes.byref(bot)))
+        self.halo = (top.value, bot.value)
+        self._mult = None
+
+    def halo_rows(self):
+        return self.halo
+
+    def prepare(self, geo: SlabGeometry):
+        ptr = ctypes.c_void_p()
+        L.check(self.lib.md_slab_prepare(self.plan._h, geo.rank * geo.Wb, geo.Wb, ctypes.byref(ptr)))
+        self._mult = ptr
+
+    def rows_fft(self, z, real_in, rows, inv, scale=1.0, stream=None):
+        L.check(self.lib.md_slab_rows_fft(self.plan._h, z.data_ptr(), None if real_in is None else real_in.data_ptr(),
+                                          rows, inv, scale, _sp(stream)))
+
+    def cols_filter(self, zc, cols, stream=None):
+        L.check(self.lib.md_slab_cols_filter(self.plan._h, zc.data_ptr(), cols, self._mult, _sp(stream)))
+
+    def epilogue(self, z, f, u0, fpos, rows, stream=None):
+        L.check(self.lib.md_slab_wiener_epilogue(self.plan._h, z.data_ptr(), f.data_ptr(), u0.data_ptr(),
+                                                 fpos.data_ptr(), rows, _sp(stream)))
+
+    def iterate(self, u_ext, fpos_ext, p_ext, w_ext, out_ext, geo: SlabGeometry, stream=None):
+        """One iteration on haloed [top + S + bottom, W] buffers (pointers at own row 0)."""
+        off = geo.top * geo.W * u_ext.element_size()
+        ptr = lambda t: t.data_ptr() + off
+        L.check(self.lib.md_slab_iterate(self.plan._h, ptr(u_ext), ptr(fpos_ext), ptr(p_ext), ptr(w_ext),
+                                         ptr(out_ext), geo.S, geo.row0, _sp(stream)))
+
+
+def _sp(stream):
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return s.cuda_stream or None
+
+
+# ---------------------------------------------------------------------------------- worker
+
+class SlabWorker:
+    """Buffers and SPMD program of one rank. ``f_own`` is this rank's [S, W] slab."""
+
+    def __init__(self, backend, geo: SlabGeometry, iterations: int, device, dtype):
+        import torch
+        if not geo.top or not geo.bottom:
+            raise ValueError("halo rows missing")
+        self.b, self.g, self.K = backend, geo, iterations
+        self.device, self.dtype = device, dtype
+        g = geo
+        ext = (g.ext_rows, g.W)
+        self.u = [torch.zeros(ext, dtype=dtype, device=device) for _ in range(2)]
+        self.fpos = torch.zeros(ext, dtype=dtype, device=device)
+        self.p = torch.zeros(ext, dtype=dtype, device=device)
+        self.w = torch.zeros(ext, dtype=dtype, device=device)
+        self.z = torch.zeros((g.S, g.W, 2), dtype=dtype, device=device)          # complex as (re, im)
+        self.zc = torch.zeros((g.H, g.Wb, 2), dtype=dtype, device=device)
+        self.send = torch.zeros((g.world, g.S, g.Wb, 2), dtype=dtype, device=device)
+        self.recv = torch.zeros_like(self.send)
+        backend.prepare(geo)
+
+    def own(self, t):
+        return t[self.g.top:self.g.top + self.g.S]
+
+    def _exchange(self, comm, t):
+        g = self.g
+        # my first `bottom` rows feed rank-1's bottom halo; my last `top` rows feed rank+1's top halo
+        comm.exchange(g.rank, self.own(t)[:g.bottom], self.own(t)[g.S - g.top:],
+                      t[:g.top], t[g.top + g.S:])
+
+    def run(self, comm, f_own):
+        g, b = self.g, self.b
+        # ---- Wiener: rows (local) -> transpose -> columns x M -> transpose back -> rows
+        b.rows_fft(self.z, f_own, g.S, 0)
+        self.send.copy_(self.z.view(g.S, g.world, g.Wb, 2).permute(1, 0, 2, 3))
+        comm.all_to_all(g.rank, self.recv, self.send)
+        self.zc.view(g.world, g.S, g.Wb, 2).copy_(self.recv)
+        b.cols_filter(self.zc, g.Wb)
+        self.send.copy_(self.zc.view(g.world, g.S, g.Wb, 2))
+        comm.all_to_all(g.rank, self.recv, self.send)
+        self.z.view(g.S, g.world, g.Wb, 2).copy_(self.recv.permute(1, 0, 2, 3))
+        b.rows_fft(self.z, None, g.S, 1)
+        cur = 0
+        b.epilogue(self.z, f_own, self.own(self.u[cur]), self.own(self.fpos), g.S)
+        self._exchange(comm, self.fpos)
+        # ---- iterations: halo exchange of u, then one fused-stage iteration on the slab
+        for k in range(self.K):
+            self._exchange(comm, self.u[cur])
+            nxt = 1 - cur
+            b.iterate(self.u[cur], self.fpos, self.p, self.w, self.u[nxt], g)
+            cur = nxt
+        return self.own(self.u[cur])
+
+
+def run_slabs(plan, f, world: int, backend_factory=CudaSlabBackend):
+    """Deblur one [H, W] device image as ``world`` row slabs inside this process (LocalComm,
+    one thread per slab). Returns the assembled [H, W] result."""
+    import torch
+    H, W = f.shape
+    comm = LocalComm(world)
+    out = torch.empty_like(f)
+    errors = []
+    backend = backend_factory(plan)
+    top, bottom = backend.halo_rows()
+    workers = [SlabWorker(backend_factory(plan) if r else backend, SlabGeometry(H, W, r, world, top, bottom),
+                          plan.params.iterations, f.device, f.dtype) for r in range(world)]
+    S = H // world
+
+    def body(r):
+        try:
+            torch.cuda.set_device(f.device)
+            res = workers[r].run(comm, f[r * S:(r + 1) * S].contiguous())
+            torch.cuda.synchronize()
+            out[r * S:(r + 1) * S].copy_(res)
+            torch.cuda.synchronize()
+        except BaseException as exc:            # surface worker failures, release the others
+            errors.append(exc)
+            comm._bar.abort()
+
+    threads = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:
+        raise errors[0]
+    return out

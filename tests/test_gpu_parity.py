@@ -351,3 +351,28 @@ def test_psf_bank_pipeline_matches_single_plans(md):
     for k, i in enumerate(idx):
         want = md.DeblurPipeline((64, 64), bank[i], params).run(md.Image(frames[k])).values
         np.testing.assert_array_equal(out[k], want)
+
+
+@pytest.mark.parametrize("name", ["pipe_f2d_line21_30_128", "pipe_f2d_3x5_64x128", "pipe_f2d_gauss31_128"])
+def test_two_level_fft_wiener_golden(md, name):
+    """The large-image Wiener (two-level FFT passes, md_fft_big.cu) forced at fixture size."""
+    d = load_golden(name)
+    if name == "pipe_f2d_gauss31_128":
+        with pytest.raises(ValueError):      # dense PSFs iterate through FFTs, not offered at that size
+            md.DeblurPipeline(d["f"].shape, product_psf(d), product_params(d), md.Scenario.FOURIER_2D, big_fft=True)
+        return
+    out = md.DeblurPipeline(d["f"].shape, product_psf(d), product_params(d), md.Scenario.FOURIER_2D,
+                            big_fft=True).run(md.Image(d["f"])).values
+    assert np.abs(out - d["out"]).max() <= FP64_TOL
+
+
+def test_two_level_fft_matches_single_pass_2048(md):
+    """c5-style line PSF on a 2048^2 frame: two-level FFT Wiener == single-pass Wiener."""
+    import torch
+    psf = md.Psf.line(21.0, 30.0)
+    g = md.make_test_image(2048, 2048)
+    f = torch.from_numpy(md.synth_blur(g, psf).values).cuda()
+    params = md.DeconvParams(iterations=2)
+    a = md.DeblurPipeline((2048, 2048), psf, params).run_batch(f)
+    b = md.DeblurPipeline((2048, 2048), psf, params, big_fft=True).run_batch(f)
+    assert float((a - b).abs().max()) <= FP64_TOL     # rounding only (~1e-8 after RRRL amplification)
