@@ -195,6 +195,80 @@ class C4:
 WORKLOADS = {"c1": C1, "c4": C4}
 
 
+def run_c5(args, rank: int, world: int, local: int) -> None:
+    """configs[4]: ONE size x size image (default 16384^2), line L=21 @30 deg, float64,
+    Wiener + 5 RRRL. N=1: the whole image through one plan (two-level FFT Wiener, direct-tap
+    iterations). N>1: row slabs over the ranks, NCCL halo exchange and all-to-all spectrum
+    transposes (paper_1212_2245_b200/slab.py). Metric: images/s (and Mpx/s); SURVEY 8(d)
+    algorithmic bytes per image = (7 + 5*8) field passes x 8 B x px."""
+    import torch
+    import torch.distributed as dist
+    import paper_1212_2245_b200 as md
+    from paper_1212_2245_b200.slab import CudaSlabBackend, DistComm, SlabGeometry, SlabWorker
+    n = args.size
+    psf = md.Psf.line(21.0, 30.0)
+    params = md.DeconvParams()
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    # synthetic scene on the device: smooth gradient + random blocks, blurred (clamped, GPU), 8-bit
+    yy = torch.linspace(0, 1, n, device="cuda", dtype=torch.float64)
+    g = 60.0 + 100.0 * yy[:, None] + 60.0 * yy[None, :]
+    blocks = torch.rand((n // 64, n // 64), generator=gen, device="cuda", dtype=torch.float64)
+    g = g + 40.0 * (blocks.repeat_interleave(64, 0).repeat_interleave(64, 1) - 0.5)
+    conv = md.make_convolver(psf, (n, n), "spatial")
+    f = torch.clamp(torch.floor(conv.blur(g.contiguous()) + 0.5), 0, 255)
+    del g
+    pipe = md.DeblurPipeline((n, n), psf, params, big_fft=True)
+    stream = torch.cuda.current_stream()
+    if world == 1:
+        u = torch.empty_like(f)
+        run = lambda: pipe.plan.run(f, out=u)
+    else:
+        be = CudaSlabBackend(pipe.plan)
+        geo = SlabGeometry(n, n, rank, world, *be.halo_rows())
+        worker = SlabWorker(be, geo, params.iterations, f.device, f.dtype)
+        comm = DistComm()
+        S = n // world
+        f_own = f[rank * S:(rank + 1) * S].contiguous()
+        del f
+        run = lambda: worker.run(comm, f_own)
+    for _ in range(args.warmup):
+        run()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            run()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    t = torch.tensor([ev0.elapsed_time(ev1)], device="cuda", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item()) / args.steps
+    if rank == 0:
+        pk = peaks()
+        bytes_img = (7 + 8 * params.iterations) * 8 * n * n
+        line = {
+            "metric": "c5: single-image deblur throughput (images/s)", "value": 1e3 / ms, "unit": "images/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (device-generated scene, GPU clamped line blur, 8-bit)",
+            "config": {"workload": f"c5: one {n}x{n} image, line L=21 @30deg, Wiener + 5 RRRL (BASELINE.json "
+                                   "configs[4])", "parallelism": f"row slabs x{world}" if world > 1 else "one plan",
+                       "plan": pipe.plan.describe},
+            "mpx_per_s": n * n / ms / 1e3,
+            "roofline": {"bound": "hbm", "kernel": "whole pipeline", "achieved": bytes_img / (ms / 1e3) / 1e9 / world,
+                         "peak": pk["hbm_gbs"], "unit": "GB/s per GPU",
+                         "frac": bytes_img / (ms / 1e3) / 1e9 / world / pk["hbm_gbs"], "traffic": None,
+                         "bytes_model": "SURVEY.md 8(d): (7 + 5x8) field passes x 8 B per pixel"},
+            "cpu_baseline": None,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+
+
 # ---------------------------------------------------------------------------------- clocks
 
 class ClockSampler:
@@ -332,7 +406,8 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c1", choices=sorted(WORKLOADS))
+    ap.add_argument("--config", default="c1", choices=sorted(WORKLOADS) + ["c5"])
+    ap.add_argument("--size", type=int, default=16384, help="c5 image side")
     ap.add_argument("--dtype", default="float32", choices=["float32", "float64"])
     ap.add_argument("--batch", type=int, default=None, help="frames per GPU per step")
     ap.add_argument("--e2e-batch", type=int, default=4096)
@@ -358,6 +433,12 @@ def main() -> None:
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.config == "c5":
+        run_c5(args, rank, world, local)
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
     import paper_1212_2245_b200 as md
 
     work = WORKLOADS[args.config](md, args)

@@ -505,7 +505,7 @@ int32_t md_plan_create(const md_plan_desc *desc, md_plan **out) {
             rc = make_filter(h64s, (int64_t)H * W, desc->wiener_k, desc->dtype, &P->d_mult);
             cudaFree(h64s);
             if (rc) return bail(rc);
-        } else if (pow2) {
+        } else if (pow2 && (P->periodic || wiener)) {
             if ((rc = build_twiddles(H, desc->dtype, &P->d_tw_H))) return bail(rc);
             if ((rc = build_twiddles(W, desc->dtype, &P->d_tw_W))) return bail(rc);
             std::vector<double> emb((size_t)H * W, 0.0);       // fft.py:204-221

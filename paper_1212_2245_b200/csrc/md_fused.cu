@@ -1,327 +1,8 @@
-// md_fused.cu -- all RRRL iterations of a frame in ONE launch, the iterate resident in the
-// distributed shared memory of a thread-block cluster (1D blur scenarios, small frames).
-//
-// Replaces the iteration loop of DeblurPipeline.run_timed (deconv.py:675-681) with
-// _iterate_rrrl and its callees (deconv.py:142-213, 415-446, 512-521) for box / 1D kernels.
-//
-// Geometry: one cluster of CL CTAs per frame; CTA `rank` owns RL = 8 * LPW consecutive
-// lines (line-major layout, lines along the blur axis). The blur and its adjoint act along
-// a line (warp-local, register windows, md_linefast.cuh); only the TV stencil couples
-// lines, so per iteration a CTA needs its neighbours' two boundary lines. Those are pushed
-// into the neighbours' shared memory (DSMEM stores, double-buffered by iteration parity)
-// and one cluster barrier per iteration publishes them. The observation is re-read from L2
-// (line-major, coalesced) each iteration; HBM sees u0/fpos in and u out only.
-//
-// Per iteration, per CTA:
-//   g on lines -1..RL (needs lines -2..RL+1)         | barrier
-//   per own line (warp): blur -> W, p (warp buffer) -> adjoint pair -> D -> u' in registers
-//   barrier; u' -> own smem lines; boundary lines -> neighbours' halo[parity^1]; cluster barrier
-#include <cooperative_groups.h>
-
-#include "md_fused.h"
-#include "md_lines_fast.h"
-#include "md_linefast.cuh"
-
-namespace cg = cooperative_groups;
+// md_fused.cu -- host dispatch of the cluster-resident iteration kernel
+// (md_fused_kernel.cuh): dense-tap instantiations here, symmetric-box ones in md_fused_box*.cu.
+#include "md_fused_kernel.cuh"
 
 namespace md {
-
-constexpr int FU_WARPS = 8;
-
-template <typename T, int R> struct FusedKArgs {
-    const T *u0;        // line-major clamped Wiener output [frames][m][n]
-    const T *fpos;      // line-major max(f, floor)
-    T *out;             // native layout result
-    int n, m, iterations, out_vert, periodic, cl;
-    DenseTaps<T, R> wb, wa;
-    T alpha, eps_d2, eps_r2;
-    int has_d;
-    LutView lut;
-};
-
-__device__ __forceinline__ int fu_wrap(int j, int n, int periodic) {
-    if (periodic) {
-        j %= n;
-        return j < 0 ? j + n : j;
-    }
-    return j < 0 ? 0 : (j >= n ? n - 1 : j);
-}
-
-template <typename T>
-__device__ __forceinline__ void fu_fill_halo(T *line, int n, int hw, int periodic, int lane) {
-    for (int q = lane; q < 2 * hw; q += 32) {
-        const int e = q < hw ? q : n + q;
-        line[xaddr(e)] = line[xaddr(hw + fu_wrap(e - hw, n, periodic))];
-    }
-}
-
-template <typename T, int R, int LPW, bool ROBUST>
-__global__ void __launch_bounds__(256)
-k_fused_lines(FusedKArgs<T, R> a) {
-    constexpr int HW = HaloOf<R>::value;
-    constexpr int WIN = SEG + 2 * R;
-    constexpr int RL = FU_WARPS * LPW;
-    cg::cluster_group cluster = cg::this_cluster();
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    T *sm = reinterpret_cast<T *>(smem_raw);
-    const int n = a.n, m = a.m;
-    const int ls = xline_len(n, HW);
-    const int rank = (int)cluster.block_rank();
-    const int CL = a.cl;
-    const int64_t frame = blockIdx.x / CL;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nseg = n / SEG;
-    const int base0 = xaddr(HW);
-    const int gl0 = rank * RL;                       // first global line owned
-    const int64_t fsz = (int64_t)n * m;
-    const T *fpos = a.fpos + frame * fsz;
-
-    // shared layout (in lines of `ls` elements)
-    T *own = sm;                                     // RL lines
-    auto halo_top = [&](int par) { return sm + (RL + 2 * par) * ls; };
-    auto halo_bot = [&](int par) { return sm + (RL + 4 + 2 * par) * ls; };
-    T *sg = sm + (RL + 8) * ls;                      // RL+2 lines: logical -1..RL
-    T *wp = sm + (2 * RL + 10 + 2 * warp) * ls;      // warp buffers: p, W
-    T *ww = wp + ls;
-    auto line_ptr = [&](int l, int par) -> T * {
-        if (l < 0) return halo_top(par) + (l + 2) * ls;
-        if (l >= RL) return halo_bot(par) + (l - RL) * ls;
-        return own + l * ls;
-    };
-
-    cluster.sync();                                  // all CTAs resident before DSMEM traffic
-    T *nb_top = rank > 0 ? cluster.map_shared_rank(sm, rank - 1) : nullptr;
-    T *nb_bot = rank < CL - 1 ? cluster.map_shared_rank(sm, rank + 1) : nullptr;
-
-    // ---- load u0 (own lines), fill x-halos, push boundary lines to the neighbours (parity 0)
-    {
-        const T *src = a.u0 + frame * fsz + (int64_t)gl0 * n;
-        for (int li = warp; li < RL; li += FU_WARPS) {
-            T *L = own + li * ls;
-            for (int j = lane; j < n; j += 32) L[xaddr(HW + j)] = src[(int64_t)li * n + j];
-            __syncwarp();
-            fu_fill_halo<T>(L, n, HW, a.periodic, lane);
-            __syncwarp();
-            if (li < 2 && nb_top)
-                for (int q = lane; q < ls; q += 32) (nb_top + (RL + 4 + li) * ls)[q] = L[q];
-            if (li >= RL - 2 && nb_bot)   // neighbour's top halo (parity 0), logical line li - RL
-                for (int q = lane; q < ls; q += 32) (nb_bot + (RL + (li - RL) + 2) * ls)[q] = L[q];
-        }
-    }
-    cluster.sync();
-
-    const T eps_r2 = a.eps_r2, eps_d2 = a.eps_d2, alpha = a.alpha;
-    for (int it = 0; it < a.iterations; ++it) {
-        const int par = it & 1;
-        const bool last = it == a.iterations - 1;
-        // ---- diffusivity g on logical lines -1..RL
-        if (a.has_d) {
-            for (int l = warp - 1; l <= RL; l += FU_WARPS) {
-                const int gl = gl0 + l;
-                if (gl < 0 || gl >= m) continue;
-                const bool up_ok = gl > 0, dn_ok = gl + 1 < m;
-                const T *row = line_ptr(l, par), *up = line_ptr(l - 1, par), *dn = line_ptr(l + 1, par);
-                for (int s = lane; s < nseg; s += 32) {
-                    const int off = base0 + 9 * s;
-                    T x[SEG + 2];
-#pragma unroll
-                    for (int k = -1; k <= SEG; ++k) x[k + 1] = row[off + koff(k)];
-                    T *G = sg + (l + 1) * ls + off;
-#pragma unroll
-                    for (int r = 0; r < SEG; ++r) {
-                        T dxr = x[r + 2] - x[r + 1];
-                        T dxl = x[r + 1] - x[r];
-                        if (r == SEG - 1 && s == nseg - 1) dxr = T(0);
-                        if (r == 0 && s == 0) dxl = T(0);
-                        const T yd = dn_ok ? dn[off + koff(r)] : x[r + 1];
-                        const T yu = up_ok ? up[off + koff(r)] : x[r + 1];
-                        const T dyd = yd - x[r + 1], dyu = x[r + 1] - yu;
-                        const T q = dxr * dxr + dxl * dxl + dyd * dyd + dyu * dyu;
-                        G[koff(r)] = T(0.5) * frsqrt(T(0.5) * q + eps_r2);
-                    }
-                }
-            }
-        }
-        __syncthreads();
-        // ---- per own line: blur -> W, p -> adjoint pair -> D -> update (registers)
-        T unew[LPW][SEG];
-#pragma unroll
-        for (int j = 0; j < LPW; ++j) {
-            const int li = warp + FU_WARPS * j;
-            const int gl = gl0 + li;
-            const bool up_ok = gl > 0, dn_ok = gl + 1 < m;
-            const T *U = own + li * ls;
-            const T *F = fpos + (int64_t)gl * n;
-            // nseg <= 32 (n <= 256): one segment per lane
-            const int s = lane;
-            const bool act = s < nseg;
-            const int off = base0 + 9 * s;
-            if (act) {
-                T fv[SEG];
-                if (sizeof(T) == 4) {
-                    const float4 *f4 = reinterpret_cast<const float4 *>(F + SEG * s);
-                    const float4 x0 = __ldg(f4), x1 = __ldg(f4 + 1);
-                    fv[0] = x0.x; fv[1] = x0.y; fv[2] = x0.z; fv[3] = x0.w;
-                    fv[4] = x1.x; fv[5] = x1.y; fv[6] = x1.z; fv[7] = x1.w;
-                } else {
-                    const double2 *f2 = reinterpret_cast<const double2 *>(F + SEG * s);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const double2 x = __ldg(f2 + i);
-                        fv[2 * i] = (T)x.x;
-                        fv[2 * i + 1] = (T)x.y;
-                    }
-                }
-                T v[WIN];
-#pragma unroll
-                for (int k = -R; k < SEG + R; ++k) v[k + R] = U[off + koff(k)];
-#pragma unroll
-                for (int r = 0; r < SEG; ++r) {
-                    T b = T(0);
-#pragma unroll
-                    for (int k = -R; k <= R; ++k) b += a.wb.w[k + R] * v[r + k + R];
-                    b = b > T(kGuard) ? b : T(kGuard);
-                    const T fp = fv[r];
-                    const T ratio = fp * frcp(b);
-                    if (ROBUST) {
-                        const T xr = b * frcp(fp);
-                        const T w = T(0.5) * frsqrt(r1_fast<T>(a.lut, xr) * fp + eps_d2);
-                        ww[off + koff(r)] = w;
-                        wp[off + koff(r)] = w * ratio;
-                    } else {
-                        wp[off + koff(r)] = ratio;
-                    }
-                }
-            }
-            __syncwarp();
-            fu_fill_halo<T>(wp, n, HW, a.periodic, lane);
-            if (ROBUST) fu_fill_halo<T>(ww, n, HW, a.periodic, lane);
-            __syncwarp();
-            if (act) {
-                T num[SEG], den[SEG];
-                {
-                    T v[WIN];
-#pragma unroll
-                    for (int k = -R; k < SEG + R; ++k) v[k + R] = wp[off + koff(k)];
-#pragma unroll
-                    for (int r = 0; r < SEG; ++r) {
-                        T acc = T(0);
-#pragma unroll
-                        for (int k = -R; k <= R; ++k) acc += a.wa.w[k + R] * v[r + k + R];
-                        num[r] = acc;
-                    }
-                }
-                if (ROBUST) {
-                    T v[WIN];
-#pragma unroll
-                    for (int k = -R; k < SEG + R; ++k) v[k + R] = ww[off + koff(k)];
-#pragma unroll
-                    for (int r = 0; r < SEG; ++r) {
-                        T acc = T(0);
-#pragma unroll
-                        for (int k = -R; k <= R; ++k) acc += a.wa.w[k + R] * v[r + k + R];
-                        den[r] = acc;
-                    }
-                }
-                T ux[SEG + 2];
-#pragma unroll
-                for (int k = -1; k <= SEG; ++k) ux[k + 1] = U[off + koff(k)];
-                if (a.has_d) {
-                    const T *G = sg + (li + 1) * ls + off;
-                    const T *Gu = G - ls, *Gd = G + ls;
-                    const T *Uu = line_ptr(li - 1, par) + off, *Ud = line_ptr(li + 1, par) + off;
-                    T gx[SEG + 2];
-#pragma unroll
-                    for (int k = -1; k <= SEG; ++k) gx[k + 1] = G[koff(k)];
-#pragma unroll
-                    for (int r = 0; r < SEG; ++r) {
-                        const T u = ux[r + 1], gc = gx[r + 1];
-                        T fr = (gc + gx[r + 2]) * (ux[r + 2] - u);
-                        T fl = (gx[r] + gc) * (u - ux[r]);
-                        if (r == SEG - 1 && s == nseg - 1) fr = T(0);
-                        if (r == 0 && s == 0) fl = T(0);
-                        T d = fr - fl;
-                        if (dn_ok) d += (gc + Gd[koff(r)]) * (Ud[koff(r)] - u);
-                        if (up_ok) d -= (Gu[koff(r)] + gc) * (u - Uu[koff(r)]);
-                        T nm = num[r] + alpha * (d > T(0) ? d : T(0));
-                        const T neg = alpha * (d < T(0) ? d : T(0));
-                        T dn = (ROBUST ? den[r] : T(1)) - neg;
-                        dn = dn > T(kGuard) ? dn : T(kGuard);
-                        unew[j][r] = (u * nm) * frcp(dn);
-                    }
-                } else {
-#pragma unroll
-                    for (int r = 0; r < SEG; ++r) {
-                        if (ROBUST) {
-                            const T dn = den[r] > T(kGuard) ? den[r] : T(kGuard);
-                            unew[j][r] = (ux[r + 1] * num[r]) * frcp(dn);
-                        } else {
-                            unew[j][r] = ux[r + 1] * num[r];
-                        }
-                    }
-                }
-            }
-            __syncwarp();
-        }
-        __syncthreads();
-        if (last) {
-            // ---- result to global, native orientation
-            T *dst = a.out + frame * fsz;
-#pragma unroll
-            for (int j = 0; j < LPW; ++j) {
-                const int li = warp + FU_WARPS * j;
-                const int gl = gl0 + li;
-                if (lane >= nseg) continue;
-                if (!a.out_vert) {
-                    T *o = dst + (int64_t)gl * n + SEG * lane;
-                    if (sizeof(T) == 4) {
-                        float4 *o4 = reinterpret_cast<float4 *>(o);
-                        o4[0] = make_float4(unew[j][0], unew[j][1], unew[j][2], unew[j][3]);
-                        o4[1] = make_float4(unew[j][4], unew[j][5], unew[j][6], unew[j][7]);
-                    } else {
-                        double2 *o2 = reinterpret_cast<double2 *>(o);
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) o2[i] = make_double2(unew[j][2 * i], unew[j][2 * i + 1]);
-                    }
-                } else {
-                    // lines are columns: stage through the (now free) own smem lines
-                    T *L = own + li * ls + base0 + 9 * lane;
-#pragma unroll
-                    for (int r = 0; r < SEG; ++r) L[koff(r)] = unew[j][r];
-                }
-            }
-            if (a.out_vert) {
-                __syncthreads();
-                // native frame [n rows][m cols]; own lines = columns gl0 .. gl0+RL-1
-                for (int idx = threadIdx.x; idx < RL * n; idx += blockDim.x) {
-                    const int row = idx / RL, li = idx - row * RL;
-                    dst[(int64_t)row * m + gl0 + li] = own[li * ls + xaddr(HW + row)];
-                }
-            }
-            break;
-        }
-        // ---- publish u': own lines + x-halos, boundary lines to the neighbours' halo[par^1]
-        const int npar = par ^ 1;
-#pragma unroll
-        for (int j = 0; j < LPW; ++j) {
-            const int li = warp + FU_WARPS * j;
-            T *L = own + li * ls;
-            if (lane < nseg) {
-                T *P = L + base0 + 9 * lane;
-#pragma unroll
-                for (int r = 0; r < SEG; ++r) P[koff(r)] = unew[j][r];
-            }
-            __syncwarp();
-            fu_fill_halo<T>(L, n, HW, a.periodic, lane);
-            __syncwarp();
-            if (li < 2 && nb_top)
-                for (int q = lane; q < ls; q += 32) (nb_top + (RL + 4 + 2 * npar + li) * ls)[q] = L[q];
-            if (li >= RL - 2 && nb_bot)
-                for (int q = lane; q < ls; q += 32) (nb_bot + (RL + 2 * npar + li - RL + 2) * ls)[q] = L[q];
-        }
-        cluster.sync();
-    }
-}
 
 // ---------------------------------------------------------------------------------- host
 
@@ -336,48 +17,14 @@ bool fused_lines_supported(int dtype, int n, int m, unsigned flags) {
     return cl >= 2 && cl <= 16;
 }
 
-template <typename T, int R, int LPW>
-cudaError_t launch_fused_t(const FusedKArgs<T, R> &a, bool robust, int64_t batch, cudaStream_t st) {
-    constexpr int HW = HaloOf<R>::value;
-    constexpr int RL = FU_WARPS * LPW;
-    const size_t smem = (size_t)(2 * RL + 10 + 2 * FU_WARPS) * xline_len(a.n, HW) * sizeof(T);
-    auto kern = robust ? k_fused_lines<T, R, LPW, true> : k_fused_lines<T, R, LPW, false>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    if (a.cl > 8) {
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return e;
-    }
-    const int64_t fsz = (int64_t)a.n * a.m;
-    const int64_t maxf = (int64_t)(0x7fffffff / a.cl);
-    for (int64_t b0 = 0; b0 < batch; b0 += maxf) {
-        const int64_t nb = std::min<int64_t>(maxf, batch - b0);
-        FusedKArgs<T, R> ab = a;
-        ab.u0 += b0 * fsz;
-        ab.fpos += b0 * fsz;
-        ab.out += b0 * fsz;
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3((unsigned)(nb * a.cl), 1, 1);
-        cfg.blockDim = dim3(256, 1, 1);
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = st;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = a.cl;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        e = cudaLaunchKernelEx(&cfg, kern, ab);
-        if (e != cudaSuccess) return e;
-    }
-    return cudaGetLastError();
-}
-
 template <typename T>
 cudaError_t launch_fused_lines(const FusedLinesArgs &d, int64_t batch, cudaStream_t st) {
     const int r = std::max(line_radius(d.blur), line_radius(d.adj));
     const int lpw = fused_lpw(sizeof(T) == 8 ? 0 : 1);
+    // symmetric integer box (odd length, default centre): O(1) sliding-sum specialisation
+    if (d.blur.kind == LINE_BOX && !d.blur.ends && d.blur.lo == -d.blur.hi && d.adj.lo == -d.adj.hi &&
+        d.blur.hi == d.adj.hi && d.blur.hi >= 1 && d.blur.hi <= 15 && d.robust)
+        return launch_fused_box<T>(d, d.blur.hi, batch, st);
     auto go = [&](auto rtag, auto ltag) -> cudaError_t {
         constexpr int RR = decltype(rtag)::value;
         constexpr int LP = decltype(ltag)::value;
@@ -392,7 +39,7 @@ cudaError_t launch_fused_lines(const FusedLinesArgs &d, int64_t batch, cudaStrea
         fill_dense<T, RR>(a.wa, d.adj, d.taps_adj_host);
         a.alpha = T(d.alpha); a.eps_d2 = T(d.eps_d2); a.eps_r2 = T(d.eps_r2); a.has_d = d.has_d;
         a.lut = d.lut;
-        return launch_fused_t<T, RR, LP>(a, d.robust != 0, batch, st);
+        return launch_fused_t<T, RR, LP, 0>(a, d.robust != 0, batch, st);
     };
     using I2 = std::integral_constant<int, 2>;
     using I4 = std::integral_constant<int, 4>;

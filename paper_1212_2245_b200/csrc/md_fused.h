@@ -18,6 +18,12 @@ struct FusedLinesArgs {
 };
 
 bool fused_lines_supported(int dtype, int n, int m, unsigned flags);
+template <typename T> cudaError_t launch_fused_box_parta(const FusedLinesArgs &, int radius, int64_t, cudaStream_t);
+template <typename T> cudaError_t launch_fused_box_partb(const FusedLinesArgs &, int radius, int64_t, cudaStream_t);
+template <typename T>
+inline cudaError_t launch_fused_box(const FusedLinesArgs &d, int radius, int64_t batch, cudaStream_t st) {
+    return radius <= 8 ? launch_fused_box_parta<T>(d, radius, batch, st) : launch_fused_box_partb<T>(d, radius, batch, st);
+}
 template <typename T> cudaError_t launch_fused_lines(const FusedLinesArgs &, int64_t batch, cudaStream_t);
 
 }  // namespace md
