@@ -33,43 +33,55 @@ template <int S> __host__ __device__ constexpr int bitrev(int x) {
     return r;
 }
 
-// in-register S-point DFT, natural order in and out; INV uses conjugate twiddles (unscaled)
-template <typename T, int S, bool INV>
-__device__ __forceinline__ void dft_reg(cx_t<T> (&v)[S]) {
-    using C = cx_t<T>;
-    C w[S];
+// in-register S-point transforms, in place, all indices compile-time:
+//   dif_reg : natural order in, bit-reversed order out, forward twiddles exp(-2 pi i k / 2h)
+//   dit_reg : bit-reversed order in, natural order out, inverse (conjugate) twiddles, unscaled
+template <typename T>
+__device__ __forceinline__ cx_t<T> twmul(cx_t<T> b, int k, int half, bool inv) {
+    if (k == 0) return b;
+    if (4 * k == 2 * half) return inv ? mkc<T>(-b.y, b.x) : mkc<T>(b.y, -b.x);   // -+ i
+    const int ti = k * (32 / (2 * half));
+    const T c = T(kC32[ti]);
+    const T sn = T(kC32[(ti + 24) & 31]);          // sin(2 pi ti / 32)
+    const T s = inv ? sn : -sn;
+    return mkc<T>(b.x * c - b.y * s, b.x * s + b.y * c);
+}
+
+template <typename T, int S>
+__device__ __forceinline__ void dif_reg(cx_t<T> (&v)[S]) {
 #pragma unroll
-    for (int i = 0; i < S; ++i) w[i] = v[bitrev<S>(i)];
+    for (int half = S / 2; half >= 1; half >>= 1) {
+#pragma unroll
+        for (int g = 0; g < S; g += 2 * half) {
+#pragma unroll
+            for (int k = 0; k < half; ++k) {
+                const cx_t<T> a = v[g + k], b = v[g + k + half];
+                v[g + k] = cadd(a, b);
+                v[g + k + half] = twmul<T>(csub(a, b), k, half, false);
+            }
+        }
+    }
+}
+
+template <typename T, int S>
+__device__ __forceinline__ void dit_inv_reg(cx_t<T> (&v)[S]) {
 #pragma unroll
     for (int half = 1; half < S; half <<= 1) {
 #pragma unroll
         for (int g = 0; g < S; g += 2 * half) {
 #pragma unroll
             for (int k = 0; k < half; ++k) {
-                // twiddle exp(-+ 2 pi i k / (2 half)) = index k * (32 / (2 half)) of the 32-table
-                const int ti = k * (32 / (2 * half));
-                const T c = T(kC32[ti]);
-                const T s = INV ? T(kC32[(ti + 24) & 31]) : -T(kC32[(ti + 24) & 31]);   // sin = cos(x - pi/2)
-                C a = w[g + k], b = w[g + k + half];
-                C t;
-                if (k == 0) {
-                    t = b;
-                } else if (4 * k == 2 * half) {          // quarter turn: -i (fwd) / +i (inv)
-                    t = INV ? mkc<T>(-b.y, b.x) : mkc<T>(b.y, -b.x);
-                } else {
-                    t = mkc<T>(b.x * c - b.y * s, b.x * s + b.y * c);
-                }
-                w[g + k] = cadd(a, t);
-                w[g + k + half] = csub(a, t);
+                const cx_t<T> t = twmul<T>(v[g + k + half], k, half, true);
+                const cx_t<T> a = v[g + k];
+                v[g + k + half] = csub(a, t);
+                v[g + k] = cadd(a, t);
             }
         }
     }
-#pragma unroll
-    for (int i = 0; i < S; ++i) v[i] = w[i];
 }
 
 template <typename T, int S>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, (sizeof(T) == 4 && S <= 16) ? 3 : 1)   // 3 blocks/SM (<= 85 regs)
 k_wiener_lines_reg(WienerLinesArgs a) {
     using C = cx_t<T>;
     constexpr int N = S * S;
@@ -120,27 +132,27 @@ k_wiener_lines_reg(WienerLinesArgs a) {
         }
     }
     __syncthreads();                            // twiddle table ready
-    // ---- forward: DFT over j2, twiddle W_n^{j1 k2}, transpose
-    dft_reg<T, S, false>(v);
+    // ---- forward: DFT over j2 (X[k2] lands at v[rev(k2)]), twiddle W_n^{j1 k2}, transpose
+    dif_reg<T, S>(v);
 #pragma unroll
-    for (int k2 = 0; k2 < S; ++k2) T2[k2 * TS + q] = cmul(v[k2], tw[(q * k2) & (N - 1)]);
+    for (int k2 = 0; k2 < S; ++k2) T2[k2 * TS + q] = cmul(v[bitrev<S>(k2)], tw[(q * k2) & (N - 1)]);
     __syncthreads();
-    // thread q = k2 now: DFT over j1
+    // thread q = k2 now: DFT over j1 (X[k2 + S k1] lands at v[rev(k1)])
 #pragma unroll
     for (int j1 = 0; j1 < S; ++j1) v[j1] = T2[q * TS + j1];
-    dft_reg<T, S, false>(v);
+    dif_reg<T, S>(v);
     // ---- filter X[k2 + S k1] *= M (M stored in natural order for this kernel)
     const C *mult = static_cast<const C *>(a.mult);
 #pragma unroll
-    for (int k1 = 0; k1 < S; ++k1) v[k1] = cmul(v[k1], __ldg(mult + q + S * k1));
-    // ---- inverse: DFT^-1 over k1, twiddle W_n^{-j1 k2}, transpose back
-    dft_reg<T, S, true>(v);
+    for (int k1 = 0; k1 < S; ++k1) v[bitrev<S>(k1)] = cmul(v[bitrev<S>(k1)], __ldg(mult + q + S * k1));
+    // ---- inverse: DFT^-1 over k1 (bit-reversed in, natural j1 out), twiddle W_n^{-j1 k2}
+    dit_inv_reg<T, S>(v);
 #pragma unroll
     for (int j1 = 0; j1 < S; ++j1) T2[q * TS + j1] = cmulc(v[j1], tw[(q * j1) & (N - 1)]);
     __syncthreads();
 #pragma unroll
-    for (int k2 = 0; k2 < S; ++k2) v[k2] = T2[k2 * TS + q];
-    dft_reg<T, S, true>(v);
+    for (int k2 = 0; k2 < S; ++k2) v[bitrev<S>(k2)] = T2[k2 * TS + q];
+    dit_inv_reg<T, S>(v);
     const T inv_n = T(1) / T(N);
     // ---- store x'[q + S j2]
     if (!a.in_vert && !a.out_vert) {
