@@ -124,6 +124,11 @@ int32_t md_run_profile(md_plan *plan, const void *f, void *u, int64_t batch, voi
  * chunk c-1); pinned host buffers make the copies asynchronous. Synchronises `stream`. */
 int32_t md_run_host_ex(md_plan *plan, const void *f, int32_t in_type, void *u, int32_t out_type,
                        int64_t batch, void *stream);
+/* md_run with one CUDA event per launch group: group_ms[i] / group_kind[i] (0 init, 1 iteration
+ * kernel(s), 2 layout) for i < *n_groups; the fused kernel is one group for all iterations */
+int32_t md_run_profile_groups(md_plan *plan, const void *f, void *u, int64_t batch, void *stream,
+                              double *group_ms, int32_t *group_kind, int32_t max_groups,
+                              int32_t *n_groups);
 /* number of kernel launches md_run issues for one call (for the bench's gpu_launches) */
 int32_t md_run_launch_count(const md_plan *plan, int64_t batch);
 
@@ -144,6 +149,10 @@ int32_t md_diffusion(int32_t dtype, const void *u, void *out, int64_t batch, int
 /* u' = u*num/den assembled from blurred b, optional weight w and diffusion d (_combine) */
 int32_t md_rrrl_step(md_plan *plan, const void *u, const void *f, const void *b, const void *w,
                      const void *d, void *out, int64_t batch, double alpha, void *stream);
+/* r1(x) = x - 1 - ln x through the device divergence table (DivergenceLut.r1, deconv.py:114-134) */
+int32_t md_lut_r1(int32_t dtype, const void *x, void *out, int64_t n, void *stream);
+/* copy the 133,057-entry float64 table to the host (DivergenceLut.table, deconv.py:101-112) */
+int32_t md_lut_table(double *host_out, int64_t count);
 /* x = max(x, 1e-12) in place (_blur_guarded, deconv.py:415-418) */
 int32_t md_guard(int32_t dtype, void *x, int64_t n, void *stream);
 /* min over n elements, written to *out_host (positivity contracts, deconv.py:410-412) */

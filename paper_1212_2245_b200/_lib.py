@@ -67,6 +67,8 @@ SIGNATURES = {
     "md_run_host_ex": (_I32, [_P, _P, _I32, _P, _I32, _I64, _P]),
     "md_run_launch_count": (_I32, [_P, _I64]),
     "md_run_profile": (_I32, [_P, _P, _P, _I64, _P, ctypes.POINTER(_D)]),
+    "md_run_profile_groups": (_I32, [_P, _P, _P, _I64, _P, ctypes.POINTER(_D), ctypes.POINTER(_I32), _I32,
+                                     ctypes.POINTER(_I32)]),
     "md_wiener": (_I32, [_P, _P, _P, _I64, _P]),
     "md_convolve": (_I32, [_P, _P, _P, _I64, _I32, _P]),
     "md_adjoint_pair": (_I32, [_P, _P, _P, _P, _P, _I64, _P]),
@@ -74,6 +76,8 @@ SIGNATURES = {
     "md_diffusion": (_I32, [_I32, _P, _P, _I64, _I32, _I32, _D, _P]),
     "md_rrrl_step": (_I32, [_P, _P, _P, _P, _P, _P, _P, _I64, _D, _P]),
     "md_guard": (_I32, [_I32, _P, _I64, _P]),
+    "md_lut_r1": (_I32, [_I32, _P, _P, _I64, _P]),
+    "md_lut_table": (_I32, [ctypes.POINTER(_D), _I64]),
     "md_min": (_I32, [_I32, _P, _I64, ctypes.POINTER(_D), _P]),
     "md_slab_halo": (_I32, [_P, ctypes.POINTER(_I32), ctypes.POINTER(_I32)]),
     "md_slab_prepare": (_I32, [_P, _I32, _I32, ctypes.POINTER(_P)]),

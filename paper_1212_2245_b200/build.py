@@ -67,6 +67,9 @@ def build(verbose: bool = False) -> str:
             if log:
                 sys.stderr.write(log)
     objs = [o for o, _ in results]
+    for stale in set(os.path.join(OBJ, f) for f in os.listdir(OBJ)) - set(objs):   # keep the cache small
+        if stale.endswith(".o"):
+            os.remove(stale)
     tmp = OUT + ".tmp"
     cmd = [nvcc, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"]
     res = subprocess.run(cmd, capture_output=True, text=True)

@@ -835,6 +835,29 @@ int32_t md_run_profile(md_plan *P, const void *f, void *u, int64_t batch, void *
     return rc;
 }
 
+int32_t md_run_profile_groups(md_plan *P, const void *f, void *u, int64_t batch, void *stream, double *group_ms,
+                              int32_t *group_kind, int32_t max_groups, int32_t *n_groups) {
+    if (!P || !group_ms || !group_kind || !n_groups || max_groups < 1) return fail(MD_EINVAL, "bad arguments");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Prof *pr = &g_prof_pool;
+    pr->n = 0;
+    cudaEventRecord(pr->get(0), st);
+    g_prof = pr;
+    int rc = md_run(P, f, u, batch, stream);
+    g_prof = nullptr;
+    if (rc) return rc;
+    cudaEventSynchronize(pr->ev[pr->n]);
+    const int n = std::min<int>(pr->n, max_groups);
+    for (int i = 1; i <= n; ++i) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, pr->ev[i - 1], pr->ev[i]);
+        group_ms[i - 1] = ms;
+        group_kind[i - 1] = pr->kind[i];
+    }
+    *n_groups = n;
+    return MD_OK;
+}
+
 int32_t md_run_launch_count(const md_plan *P, int64_t batch) {
     if (!P || batch <= 0) return 0;
     const int64_t chunk = auto_chunk(*P, batch);
@@ -1090,6 +1113,25 @@ int32_t md_robust_weight(int32_t dtype, const void *f, const void *b, void *out,
     const double e2 = eps_data * eps_data;
     CU(dtype == MD_F64 ? launch_robust_weight<double>(f, b, out, n, e2, floor, assume_floored, L, st)
                        : launch_robust_weight<float>(f, b, out, n, e2, floor, assume_floored, L, st));
+    return MD_OK;
+}
+
+int32_t md_lut_r1(int32_t dtype, const void *x, void *out, int64_t n, void *stream) {
+    if (!x || !out || n < 0) return fail(MD_EINVAL, "bad arguments");
+    LutView L;
+    int rc = lut_view(&L);
+    if (rc) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    CU(dtype == MD_F64 ? launch_lut_r1<double>(x, out, n, L, st) : launch_lut_r1<float>(x, out, n, L, st));
+    return MD_OK;
+}
+
+int32_t md_lut_table(double *host_out, int64_t count) {
+    if (!host_out || count < kLutCount) return fail(MD_EINVAL, "need room for the whole table");
+    LutView L;
+    int rc = lut_view(&L);
+    if (rc) return rc;
+    CU(cudaMemcpy(host_out, L.t64, kLutCount * sizeof(double), cudaMemcpyDeviceToHost));
     return MD_OK;
 }
 

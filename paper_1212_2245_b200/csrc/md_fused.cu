@@ -1,12 +1,22 @@
 // md_fused.cu -- host dispatch of the cluster-resident iteration kernel
 // (md_fused_kernel.cuh): dense-tap instantiations here, symmetric-box ones in md_fused_box*.cu.
+#include <cstdlib>
+
 #include "md_fused_kernel.cuh"
 
 namespace md {
 
 // ---------------------------------------------------------------------------------- host
 
-static int fused_lpw(int dtype) { return dtype == 0 ? 2 : 4; }
+// lines per warp: float64 uses 2 (16-line CTAs); float uses 4 unless MD_FUSED_LPW=2 (tuning knob)
+int fused_lpw(int dtype) {
+    if (dtype == 0) return 2;
+    static int v = [] {
+        const char *e = getenv("MD_FUSED_LPW");
+        return (e && atoi(e) == 2) ? 2 : 4;
+    }();
+    return v;
+}
 
 bool fused_lines_supported(int dtype, int n, int m, unsigned flags) {
     if (flags & 2u) return false;                  // MD_FLAG_NO_FUSED
@@ -43,7 +53,7 @@ cudaError_t launch_fused_lines(const FusedLinesArgs &d, int64_t batch, cudaStrea
     };
     using I2 = std::integral_constant<int, 2>;
     using I4 = std::integral_constant<int, 4>;
-    if (lpw == 2) {
+    if (lpw == 2 || sizeof(T) == 8) {
         if (r <= 4) return go(std::integral_constant<int, 4>{}, I2{});
         if (r <= 8) return go(std::integral_constant<int, 8>{}, I2{});
         return go(std::integral_constant<int, 16>{}, I2{});

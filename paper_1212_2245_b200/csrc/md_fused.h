@@ -18,6 +18,7 @@ struct FusedLinesArgs {
 };
 
 bool fused_lines_supported(int dtype, int n, int m, unsigned flags);
+int fused_lpw(int dtype);
 template <typename T> cudaError_t launch_fused_box_parta(const FusedLinesArgs &, int radius, int64_t, cudaStream_t);
 template <typename T> cudaError_t launch_fused_box_partb(const FusedLinesArgs &, int radius, int64_t, cudaStream_t);
 template <typename T>

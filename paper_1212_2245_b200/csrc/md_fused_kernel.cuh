@@ -85,7 +85,7 @@ __device__ __forceinline__ void fu_fill_halo(T *line, int n, int hw, int periodi
 }
 
 template <typename T, int R, int LPW, bool ROBUST, int BOXR>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, sizeof(T) == 4 ? (LPW == 2 ? 3 : 2) : 1)
 k_fused_lines(FusedKArgs<T, R> a) {
     constexpr int HW = HaloOf<R>::value;
     constexpr int WIN = SEG + 2 * R;
@@ -137,41 +137,53 @@ k_fused_lines(FusedKArgs<T, R> a) {
                 for (int q = lane; q < ls; q += 32) (nb_bot + (RL + (li - RL) + 2) * ls)[q] = L[q];
         }
     }
-    cluster.sync();
 
     const T eps_r2 = a.eps_r2, eps_d2 = a.eps_d2, alpha = a.alpha;
-    for (int it = 0; it < a.iterations; ++it) {
-        const int par = it & 1;
-        const bool last = it == a.iterations - 1;
-        // ---- diffusivity g on logical lines -1..RL
-        if (a.has_d) {
-            for (int l = warp - 1; l <= RL; l += FU_WARPS) {
-                const int gl = gl0 + l;
-                if (gl < 0 || gl >= m) continue;
-                const bool up_ok = gl > 0, dn_ok = gl + 1 < m;
-                const T *row = line_ptr(l, par), *up = line_ptr(l - 1, par), *dn = line_ptr(l + 1, par);
-                for (int s = lane; s < nseg; s += 32) {
-                    const int off = base0 + 9 * s;
-                    T x[SEG + 2];
+    // diffusivity g on logical lines l in [lb, le] (deconv.py:191-203); lines whose stencil
+    // touches a halo (l <= 0 or l >= RL-1) need the neighbours' rows of parity `par`
+    auto g_lines = [&](int lb, int le, int par) {
+        if (!a.has_d) return;
+        for (int l = lb + warp; l <= le; l += FU_WARPS) {
+            const int gl = gl0 + l;
+            if (gl < 0 || gl >= m) continue;
+            const bool up_ok = gl > 0, dn_ok = gl + 1 < m;
+            const T *row = line_ptr(l, par), *up = line_ptr(l - 1, par), *dn = line_ptr(l + 1, par);
+            for (int s = lane; s < nseg; s += 32) {
+                const int off = base0 + 9 * s;
+                T x[SEG + 2];
 #pragma unroll
-                    for (int k = -1; k <= SEG; ++k) x[k + 1] = row[off + koff(k)];
-                    T *G = sg + (l + 1) * ls + off;
+                for (int k = -1; k <= SEG; ++k) x[k + 1] = row[off + koff(k)];
+                T *G = sg + (l + 1) * ls + off;
 #pragma unroll
-                    for (int r = 0; r < SEG; ++r) {
-                        T dxr = x[r + 2] - x[r + 1];
-                        T dxl = x[r + 1] - x[r];
-                        if (r == SEG - 1 && s == nseg - 1) dxr = T(0);
-                        if (r == 0 && s == 0) dxl = T(0);
-                        const T yd = dn_ok ? dn[off + koff(r)] : x[r + 1];
-                        const T yu = up_ok ? up[off + koff(r)] : x[r + 1];
-                        const T dyd = yd - x[r + 1], dyu = x[r + 1] - yu;
-                        const T q = dxr * dxr + dxl * dxl + dyd * dyd + dyu * dyu;
-                        G[koff(r)] = T(0.5) * frsqrt(T(0.5) * q + eps_r2);
-                    }
+                for (int r = 0; r < SEG; ++r) {
+                    T dxr = x[r + 2] - x[r + 1];
+                    T dxl = x[r + 1] - x[r];
+                    if (r == SEG - 1 && s == nseg - 1) dxr = T(0);
+                    if (r == 0 && s == 0) dxl = T(0);
+                    const T yd = dn_ok ? dn[off + koff(r)] : x[r + 1];
+                    const T yu = up_ok ? up[off + koff(r)] : x[r + 1];
+                    const T dyd = yd - x[r + 1], dyu = x[r + 1] - yu;
+                    const T q = dxr * dxr + dxl * dxl + dyd * dyd + dyu * dyu;
+                    G[koff(r)] = T(0.5) * frsqrt(T(0.5) * q + eps_r2);
                 }
             }
         }
+    };
+    // split cluster barrier: release my DSMEM stores, compute the interior diffusivity (own
+    // lines only) while the neighbours catch up, then acquire and finish the boundary lines
+    auto publish_and_g = [&](int par) {
         __syncthreads();
+        asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+        g_lines(1, RL - 2, par);
+        asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+        g_lines(-1, 0, par);
+        g_lines(RL - 1, RL, par);
+        __syncthreads();
+    };
+    publish_and_g(0);
+    for (int it = 0; it < a.iterations; ++it) {
+        const int par = it & 1;
+        const bool last = it == a.iterations - 1;
         // ---- per own line: blur -> W, p -> adjoint pair -> D -> update (registers)
         T unew[LPW][SEG];
 #pragma unroll
@@ -335,7 +347,7 @@ k_fused_lines(FusedKArgs<T, R> a) {
             if (li >= RL - 2 && nb_bot)
                 for (int q = lane; q < ls; q += 32) (nb_bot + (RL + 2 * npar + li - RL + 2) * ls)[q] = L[q];
         }
-        cluster.sync();
+        publish_and_g(npar);
     }
 }
 

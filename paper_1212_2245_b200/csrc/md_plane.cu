@@ -231,6 +231,13 @@ __global__ void k_robust_weight(const T *__restrict__ f, const T *__restrict__ b
                          : robust_weight_general<T>(lut, f[i], b[i], eps2, floor);
 }
 
+// r1 through the device divergence table (DivergenceLut.r1, deconv.py:114-134)
+template <typename T>
+__global__ void k_lut_r1(const T *__restrict__ x, T *__restrict__ out, int64_t n, LutView lut) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = r1_lut<T>(lut, x[i]);
+}
+
 // ratio = f / b, optionally times w (first half of _combine)
 template <typename T>
 __global__ void k_ratio(const T *__restrict__ f, const T *__restrict__ b, const T *__restrict__ w,
@@ -384,6 +391,12 @@ cudaError_t launch_robust_weight(const void *f, const void *b, void *out, int64_
 }
 
 template <typename T>
+cudaError_t launch_lut_r1(const void *x, void *out, int64_t n, const LutView &lut, cudaStream_t st) {
+    k_lut_r1<T><<<ew_blocks(n), 256, 0, st>>>(static_cast<const T *>(x), static_cast<T *>(out), n, lut);
+    return cudaGetLastError();
+}
+
+template <typename T>
 cudaError_t launch_ratio(const void *f, const void *b, const void *w, void *out, int64_t n, cudaStream_t st) {
     k_ratio<T><<<ew_blocks(n), 256, 0, st>>>(static_cast<const T *>(f), static_cast<const T *>(b),
                                              static_cast<const T *>(w), static_cast<T *>(out), n);
@@ -440,6 +453,7 @@ cudaError_t launch_convert_out(const void *in, void *out, int out_type, int64_t 
     template cudaError_t launch_combine<T>(const void *, const void *, const void *, const void *,      \
                                            void *, int64_t, double, cudaStream_t);                      \
     template cudaError_t launch_guard<T>(void *, int64_t, cudaStream_t);                                \
+    template cudaError_t launch_lut_r1<T>(const void *, void *, int64_t, const LutView &, cudaStream_t); \
     template cudaError_t launch_min<T>(const void *, int64_t, double *, int, cudaStream_t);             \
     template cudaError_t launch_convert<T>(const void *, void *, int64_t, int, cudaStream_t);          \
     template cudaError_t launch_convert_in<T>(const void *, int, void *, int64_t, cudaStream_t);       \

@@ -50,6 +50,7 @@ template <typename T> cudaError_t launch_ratio(const void *f, const void *b, con
 template <typename T> cudaError_t launch_combine(const void *u, const void *num, const void *den, const void *d,
                                                  void *out, int64_t n, double alpha, cudaStream_t);
 template <typename T> cudaError_t launch_guard(void *x, int64_t n, cudaStream_t);
+template <typename T> cudaError_t launch_lut_r1(const void *x, void *out, int64_t n, const LutView &lut, cudaStream_t);
 template <typename T> cudaError_t launch_min(const void *x, int64_t n, double *partial, int nblocks, cudaStream_t);
 template <typename T> cudaError_t launch_convert(const void *in, void *out, int64_t n, int to_double, cudaStream_t);
 // host-frame type conversion: in_type / out_type are MD_IO_F64 (0), MD_IO_F32 (1), MD_IO_U8 (2)

@@ -112,6 +112,25 @@ class DivergenceLut:
         slope = 1.0 - 1.0 / upper
         return cls(delta, step, upper, direct_below, slope, (upper - 1.0 - math.log(upper)) - slope * upper)
 
+    @property
+    def table(self) -> np.ndarray:
+        """The 133,057 nodes x_i - 1 - ln x_i, built on the device (copied to the host)."""
+        import ctypes
+        from . import _lib as L
+        out = np.empty(133057)
+        L.check(L.lib().md_lut_table(out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), out.size))
+        out.setflags(write=False)
+        return out
+
+    def r1(self, x) -> np.ndarray:
+        """r1 by table interpolation with the linear / exact extensions, on the device."""
+        from . import _lib as L
+        from .plan import _stream_ptr
+        xd = _dev(np.asarray(x, dtype=np.float64))
+        out = xd.new_empty(xd.shape)
+        L.check(L.lib().md_lut_r1(L.MD_F64, xd.data_ptr(), out.data_ptr(), xd.numel(), _stream_ptr(None)))
+        return _host(out)
+
 
 @functools.lru_cache(maxsize=1)
 def default_divergence_lut() -> DivergenceLut:
@@ -404,28 +423,25 @@ class DeblurPipeline:
         return self._plan.run_host(a, out=out, stream=stream, out_dtype=out_dtype)
 
     def run_timed(self, f: Image) -> tuple[Image, StageTimes]:
-        """Deconvolve one image; stage times from CUDA events (the Wiener stage is timed by a
-        Wiener-only run of the same plan family; iterations share the remainder evenly)."""
+        """Deconvolve one image with per-stage times from CUDA events on the launch stream
+        (deconv.py:653-690). The per-iteration kernel path yields one time per iteration; the
+        fused cluster kernel runs all iterations in one launch, whose time is split evenly."""
         import torch
         self._check_shape(f.shape)
         fd = _dev(f, self.dtype)
-        if self._wiener_plan is None:
-            p0 = DeconvParams(self.params.wiener_k, self.params.alpha, 0, self.params.eps_data,
-                              self.params.eps_reg, self.params.floor)
-            self._wiener_plan = GpuPlan(self.shape, self.psf, p0, self._plan.conv, dtype=self.dtype)
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-        ev[0].record()
-        self._wiener_plan.run(fd)
-        ev[1].record()
-        ev[2].record()
-        out = self._plan.run(fd)
-        ev[3].record()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        out, groups = self._plan.run_groups(fd)
+        t1.record()
         torch.cuda.synchronize()
-        wiener_ms = ev[0].elapsed_time(ev[1])
-        total_ms = ev[2].elapsed_time(ev[3])
+        wiener_ms = sum(ms for kind, ms in groups if kind == "init")
+        iters = [ms for kind, ms in groups if kind == "iteration"]
         k = self.params.iterations
-        per = max(total_ms - wiener_ms, 0.0) / k if k else 0.0
-        return _image(out), StageTimes(wiener_ms=wiener_ms, iteration_ms=[per] * k, total_ms=total_ms)
+        if k and len(iters) != k:
+            iters = [sum(iters) / k] * k
+        total = max(t0.elapsed_time(t1), wiener_ms + sum(iters))
+        return _image(out), StageTimes(wiener_ms=wiener_ms, iteration_ms=iters if k else [], total_ms=total)
 
     def run(self, f: Image) -> Image:
         self._check_shape(f.shape)

@@ -139,6 +139,19 @@ class GpuPlan:
         L.check(self.lib.md_run_profile(self._h, f.data_ptr(), out.data_ptr(), n, _stream_ptr(stream), ms))
         return {"init_ms": ms[0], "iter_ms": ms[1], "layout_ms": ms[2], "groups": int(ms[3])}
 
+    def run_groups(self, f, out=None, stream=None):
+        """md_run with one CUDA event per launch group -> (out, [(kind, ms), ...])."""
+        n = self._check_frames(f)
+        out = self.empty_like(f) if out is None else out
+        cap = 4096
+        ms = (ctypes.c_double * cap)()
+        kinds = (ctypes.c_int32 * cap)()
+        cnt = ctypes.c_int32()
+        L.check(self.lib.md_run_profile_groups(self._h, f.data_ptr(), out.data_ptr(), n, _stream_ptr(stream), ms,
+                                               kinds, cap, ctypes.byref(cnt)))
+        names = {0: "init", 1: "iteration", 2: "layout"}
+        return out, [(names[kinds[i]], ms[i]) for i in range(cnt.value)]
+
     _IO = {np.dtype(np.float64): L.MD_IO_F64, np.dtype(np.float32): L.MD_IO_F32, np.dtype(np.uint8): L.MD_IO_U8}
 
     def run_host(self, f: np.ndarray, out: np.ndarray | None = None, stream=None,
