@@ -13,24 +13,46 @@
 namespace md {
 
 // `nl` lines of length n = 2^log2n at s[l * stride + j]; all threads of the block take part.
+// Pairs of radix-2 stages are fused into radix-4 units (4 elements in registers), halving the
+// shared-memory round trips and barriers; an odd stage count leaves one radix-2 stage.
+template <typename C>
+__device__ __forceinline__ C mul_mi(C a) {          // a * (-i)
+    C r; r.x = a.y; r.y = -a.x; return r;
+}
+
 template <typename C>
 __device__ void fft_dif_lines(C *s, int log2n, int nl, int stride, const C *__restrict__ tw) {
     const int n = 1 << log2n;
-    const int hb = log2n - 1;                  // log2(n/2)
-    const int nb = nl << hb;                   // butterflies per stage
-    int tstride = 1;
-    for (int lh = hb; lh >= 0; --lh, tstride <<= 1) {
-        const int half = 1 << lh;
-        for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-            const int l = b >> hb;
-            const int bb = b & ((n >> 1) - 1);
-            const int k = bb & (half - 1);
-            const int i0 = ((bb >> lh) << (lh + 1)) + k;
+    int lh = log2n - 1;
+    if (log2n & 1) {                               // lone radix-2 stage, half = n/2
+        const int half = n >> 1;
+        for (int b = threadIdx.x; b < (nl << lh); b += blockDim.x) {
+            const int l = b >> lh, k = b & (half - 1);
             C *row = s + l * stride;
-            C a = row[i0], c = row[i0 + half];
-            C w = tw[k * tstride];
-            row[i0] = cadd(a, c);
-            row[i0 + half] = cmul(csub(a, c), w);
+            const C a = row[k], c = row[k + half];
+            row[k] = cadd(a, c);
+            row[k + half] = cmul(csub(a, c), tw[k]);
+        }
+        __syncthreads();
+        --lh;
+    }
+    const int lu = log2n - 2;                      // log2(n/4) units per line
+    for (; lh >= 1; lh -= 2) {
+        const int h = 1 << lh, q = h >> 1;
+        for (int u = threadIdx.x; u < (nl << lu); u += blockDim.x) {
+            const int l = u >> lu, uu = u & ((n >> 2) - 1);
+            const int k = uu & (q - 1);
+            const int i0 = ((uu >> (lh - 1)) << (lh + 1)) + k;
+            C *row = s + l * stride;
+            const C x0 = row[i0], x1 = row[i0 + q], x2 = row[i0 + h], x3 = row[i0 + h + q];
+            const C w1 = tw[k << (log2n - 1 - lh)];    // W_{2h}^k
+            const C w2 = tw[k << (log2n - lh)];        // W_h^k
+            const C y0 = cadd(x0, x2), y2 = cmul(csub(x0, x2), w1);
+            const C y1 = cadd(x1, x3), y3 = cmul(csub(x1, x3), mul_mi(w1));
+            row[i0] = cadd(y0, y1);
+            row[i0 + q] = cmul(csub(y0, y1), w2);
+            row[i0 + h] = cadd(y2, y3);
+            row[i0 + h + q] = cmul(csub(y2, y3), w2);
         }
         __syncthreads();
     }
@@ -41,20 +63,40 @@ template <typename C>
 __device__ void fft_dit_inv_lines(C *s, int log2n, int nl, int stride, const C *__restrict__ tw) {
     const int n = 1 << log2n;
     const int hb = log2n - 1;
-    const int nb = nl << hb;
-    int tstride = n >> 1;
-    for (int lh = 0; lh <= hb; ++lh, tstride >>= 1) {
-        const int half = 1 << lh;
-        for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-            const int l = b >> hb;
-            const int bb = b & ((n >> 1) - 1);
-            const int k = bb & (half - 1);
-            const int i0 = ((bb >> lh) << (lh + 1)) + k;
+    const int lu = log2n - 2;
+    int lh = 0;
+    for (; lh + 1 <= hb; lh += 2) {                // stages half = 2^lh and 2^(lh+1)
+        const int q = 1 << lh, h = q << 1;
+        for (int u = threadIdx.x; u < (nl << lu); u += blockDim.x) {
+            const int l = u >> lu, uu = u & ((n >> 2) - 1);
+            const int k = uu & (q - 1);
+            const int i0 = ((uu >> lh) << (lh + 2)) + k;
             C *row = s + l * stride;
-            C t = cmulc(row[i0 + half], tw[k * tstride]);
-            C a = row[i0];
-            row[i0 + half] = csub(a, t);
-            row[i0] = cadd(a, t);
+            const C x0 = row[i0], x1 = row[i0 + q], x2 = row[i0 + h], x3 = row[i0 + h + q];
+            const C w2 = tw[k << (log2n - lh - 1)];    // W_h^k
+            const C w1 = tw[k << (log2n - lh - 2)];    // W_{2h}^k
+            C t = cmulc(x1, w2);
+            const C y0 = cadd(x0, t), y1 = csub(x0, t);
+            t = cmulc(x3, w2);
+            const C y2 = cadd(x2, t), y3 = csub(x2, t);
+            t = cmulc(y2, w1);
+            row[i0] = cadd(y0, t);
+            row[i0 + h] = csub(y0, t);
+            t = cmulc(y3, mul_mi(w1));
+            row[i0 + q] = cadd(y1, t);
+            row[i0 + h + q] = csub(y1, t);
+        }
+        __syncthreads();
+    }
+    if (lh == hb) {                                // lone radix-2 stage, half = n/2
+        const int half = n >> 1;
+        for (int b = threadIdx.x; b < (nl << hb); b += blockDim.x) {
+            const int l = b >> hb, k = b & (half - 1);
+            C *row = s + l * stride;
+            const C t = cmulc(row[k + half], tw[k]);
+            const C a = row[k];
+            row[k + half] = csub(a, t);
+            row[k] = cadd(a, t);
         }
         __syncthreads();
     }
