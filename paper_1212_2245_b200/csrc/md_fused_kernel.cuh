@@ -69,10 +69,8 @@ template <typename T, int R> struct FusedKArgs {
 };
 
 __device__ __forceinline__ int fu_wrap(int j, int n, int periodic) {
-    if (periodic) {
-        j %= n;
-        return j < 0 ? j + n : j;
-    }
+    // halos never exceed the extent, so one conditional wrap suffices (no integer modulo)
+    if (periodic) return j < 0 ? j + n : (j >= n ? j - n : j);
     return j < 0 ? 0 : (j >= n ? n - 1 : j);
 }
 

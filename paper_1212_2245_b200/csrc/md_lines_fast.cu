@@ -21,10 +21,8 @@ constexpr int FTL = 8;          // lines per block
 constexpr int FWARPS = 8;
 
 __device__ __forceinline__ int wrap_or_clamp(int j, int n, int periodic) {
-    if (periodic) {
-        j %= n;
-        return j < 0 ? j + n : j;
-    }
+    // halos never exceed the extent, so one conditional wrap suffices (no integer modulo)
+    if (periodic) return j < 0 ? j + n : (j >= n ? j - n : j);
     return j < 0 ? 0 : (j >= n ? n - 1 : j);
 }
 

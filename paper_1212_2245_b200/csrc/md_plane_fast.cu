@@ -20,10 +20,8 @@ constexpr int FX = 64, FY = 32;           // output tile
 constexpr int FR = 8;                     // outputs per thread (stride 8 along x)
 
 __device__ __forceinline__ int pf_resolve(int k, int n, int periodic) {
-    if (periodic) {
-        k %= n;
-        return k < 0 ? k + n : k;
-    }
+    // halos never exceed the extent, so one conditional wrap suffices (no integer modulo)
+    if (periodic) return k < 0 ? k + n : (k >= n ? k - n : k);
     return k < 0 ? 0 : (k >= n ? n - 1 : k);
 }
 
@@ -48,6 +46,23 @@ __device__ __forceinline__ void pf_taps(const T *s, const FastTaps<T, MAXT> &tp,
         const T w = tp.w[t];
 #pragma unroll
         for (int r = 0; r < FR; ++r) acc[r] += w * p[8 * r];
+    }
+}
+
+// num and den of the adjoint pair share the tap decode (deconv.py:425-430: adjoint_pair)
+template <typename T, int MAXT>
+__device__ __forceinline__ void pf_taps2(const T *s0, const T *s1, const FastTaps<T, MAXT> &tp, T a0[FR], T a1[FR]) {
+#pragma unroll
+    for (int r = 0; r < FR; ++r) a0[r] = a1[r] = T(0);
+    const int d = (int)(s1 - s0);
+    for (int t = 0; t < tp.nt; ++t) {
+        const T *p = s0 + tp.off[t];
+        const T w = tp.w[t];
+#pragma unroll
+        for (int r = 0; r < FR; ++r) {
+            a0[r] += w * p[8 * r];
+            a1[r] += w * p[d + 8 * r];
+        }
     }
 }
 
@@ -146,8 +161,12 @@ k_plane_b_fast(PlaneFastArgs<T, MAXT> a) {
     const int y = y0 + ty;
     if (y >= H) return;
     T num[FR], den[FR];
-    pf_taps<T, MAXT>(sp + (ty + a.ha.ht) * ss + a.ha.hl + cx, a.ta, num);
-    if (ROBUST) pf_taps<T, MAXT>(sw + (ty + a.ha.ht) * ss + a.ha.hl + cx, a.ta, den);
+    if (ROBUST) {
+        pf_taps2<T, MAXT>(sp + (ty + a.ha.ht) * ss + a.ha.hl + cx, sw + (ty + a.ha.ht) * ss + a.ha.hl + cx, a.ta,
+                          num, den);
+    } else {
+        pf_taps<T, MAXT>(sp + (ty + a.ha.ht) * ss + a.ha.hl + cx, a.ta, num);
+    }
     const T alpha = a.alpha;
 #pragma unroll
     for (int r = 0; r < FR; ++r) {
