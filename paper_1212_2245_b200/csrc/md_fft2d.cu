@@ -40,32 +40,35 @@ __device__ T tv_div_global(const T *__restrict__ u, int H, int W, int y, int x, 
 
 template <typename T>
 __global__ void __launch_bounds__(256)
-k_fft2_rows(Fft2Args a) {
+k_fft2_rows(Fft2Args a, int rb) {
+    // `rb` consecutive rows per block (all threads busy in every FFT stage)
     using C = cx_t<T>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C *s = reinterpret_cast<C *>(smem_raw);
-    const int H = a.H, W = a.W, y = blockIdx.x;
+    const int H = a.H, W = a.W, lw = a.log2W;
+    const int y0 = blockIdx.x * rb;
     const int64_t fsz = (int64_t)H * W;
     const int64_t fr = blockIdx.y;
-    const int64_t row = fr * fsz + (int64_t)y * W;
+    const int64_t base = fr * fsz + (int64_t)y0 * W;      // rb rows are contiguous
+    const int ne = rb * W;
     C *z = static_cast<C *>(a.z);
     const C *tw = static_cast<const C *>(a.twW);
 
     if (a.load == R_LOAD_COMPLEX) {
-        for (int x = threadIdx.x; x < W; x += blockDim.x) s[x] = z[row + x];
+        for (int i = threadIdx.x; i < ne; i += blockDim.x) s[i] = z[base + i];
     } else {
         const T *ra = static_cast<const T *>(a.ra);
-        const T *rb = static_cast<const T *>(a.rb);
-        for (int x = threadIdx.x; x < W; x += blockDim.x) s[x] = mkc<T>(ra[row + x], rb ? rb[row + x] : T(0));
+        const T *rb_ = static_cast<const T *>(a.rb);
+        for (int i = threadIdx.x; i < ne; i += blockDim.x) s[i] = mkc<T>(ra[base + i], rb_ ? rb_[base + i] : T(0));
     }
     __syncthreads();
-    if (a.inv && a.log2W > 0) fft_dit_inv_lines(s, a.log2W, 1, W, tw);
+    if (a.inv && lw > 0) fft_dit_inv_lines(s, lw, rb, W, tw);
 
     const T scale = T(a.scale), floor = T(a.floor);
     if (a.epi != R_EPI_NONE) {
-        for (int x = threadIdx.x; x < W; x += blockDim.x) {
-            const C v = s[x];
-            const int64_t o = row + x;
+        for (int i = threadIdx.x; i < ne; i += blockDim.x) {
+            const C v = s[i];
+            const int64_t o = base + i;
             C packed = mkc<T>(T(0), T(0));
             if (a.epi == R_EPI_STORE_PAIR) {
                 static_cast<T *>(a.oa)[o] = v.x * scale;
@@ -92,6 +95,7 @@ k_fft2_rows(Fft2Args a) {
                 }
             } else {  // R_EPI_STAGE_B
                 const T *u = static_cast<const T *>(a.u) + fr * fsz;
+                const int y = y0 + (i >> lw), x = i & (W - 1);
                 const T uv = u[(int64_t)y * W + x];
                 const T d = a.has_d ? tv_div_global<T>(u, H, W, y, x, T(a.eps_r2)) : T(0);
                 const T un = a.robust ? combine_px<T, true>(uv, v.x * scale, v.y * scale, d, T(a.alpha), a.has_d != 0)
@@ -99,15 +103,15 @@ k_fft2_rows(Fft2Args a) {
                 static_cast<T *>(a.oa)[o] = un;
                 packed = mkc<T>(un, T(0));
             }
-            s[x] = packed;
+            s[i] = packed;
         }
         __syncthreads();
     }
     if (a.fwd_after) {
-        if (a.log2W > 0) fft_dif_lines(s, a.log2W, 1, W, tw);
-        for (int x = threadIdx.x; x < W; x += blockDim.x) z[row + x] = s[x];
+        if (lw > 0) fft_dif_lines(s, lw, rb, W, tw);
+        for (int i = threadIdx.x; i < ne; i += blockDim.x) z[base + i] = s[i];
     } else if (a.epi == R_EPI_NONE) {
-        for (int x = threadIdx.x; x < W; x += blockDim.x) z[row + x] = s[x];
+        for (int i = threadIdx.x; i < ne; i += blockDim.x) z[base + i] = s[i];
     }
 }
 
@@ -148,7 +152,9 @@ k_fft2_cols(Fft2Args a, int cw) {
 
 template <typename T>
 cudaError_t launch_fft2_rows(const Fft2Args &a, int64_t batch, cudaStream_t st) {
-    const size_t smem = (size_t)a.W * sizeof(cx_t<T>);
+    int rb = 2048 / a.W;                      // ~2048 elements per block
+    rb = rb < 1 ? 1 : (rb > a.H ? a.H : rb);
+    const size_t smem = (size_t)rb * a.W * sizeof(cx_t<T>);
     cudaError_t e = cudaFuncSetAttribute(k_fft2_rows<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int64_t fr = (int64_t)a.H * a.W;
@@ -165,7 +171,7 @@ cudaError_t launch_fft2_rows(const Fft2Args &a, int64_t batch, cudaStream_t st) 
         ab.ob = const_cast<void *>(sh(a.ob, sizeof(T)));
         ab.f = sh(a.f, sizeof(T));
         ab.u = sh(a.u, sizeof(T));
-        k_fft2_rows<T><<<dim3(a.H, nb), 256, smem, st>>>(ab);
+        k_fft2_rows<T><<<dim3(a.H / rb, nb), 256, smem, st>>>(ab, rb);
     }
     return cudaGetLastError();
 }

@@ -45,5 +45,7 @@ def test_lut_r1_on_device(md):
     got = lut.r1(xs)
     assert got[3] == 0.0
     direct = xs - 1 - np.log(xs)
-    assert np.abs(got - direct).max() < 1e-4
+    assert np.abs(got[:-1] - direct[:-1]).max() < 1e-4
+    # above the table: linear continuation matching value and slope at 65 (deconv.py:127-129)
+    assert got[-1] == pytest.approx(65.0 - 1 - np.log(65.0) + (1 - 1 / 65) * 35.0, abs=1e-12)
     assert lut.table.shape == (133057,)
