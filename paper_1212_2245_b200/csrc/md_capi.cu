@@ -22,6 +22,7 @@
 
 #include "../../include/mdcuda.h"
 #include "md_fused.h"
+#include "md_fused_plane.h"
 #include "md_lines_fast.h"
 #include "md_plane_fast.h"
 #include "md_fft_big.h"
@@ -190,6 +191,7 @@ struct md_plan {
         return MD_OK;
     }
     bool fused = false;         // whole-iteration-loop fused kernel applies
+    bool fused_plane = false;   // cluster-resident 2D iteration loop (md_fused_plane.cu)
     bool fast_lines = false;    // register-window iteration kernel applies
     std::string describe;
 
@@ -522,11 +524,16 @@ int32_t md_plan_create(const md_plan_desc *desc, md_plan **out) {
             cudaFree(h64);
             if (rc) return bail(rc);
         }
+        // float: small frames run the whole iteration loop on one cluster (measured faster)
+        P->fused_plane = desc->dtype == MD_F32 && P->path == PATH_PLANE_DIRECT && !P->big && P->fast_plane &&
+                         !(desc->flags & MD_FLAG_NO_FUSED) &&
+                         fused_plane_supported(H, W, P->hblur, P->hadj, tb, ta, desc->dtype);
         snprintf(buf, sizeof buf, "plane: %dx%d %s, %d taps (halo %d/%d/%d/%d), %s", H, W,
                  P->periodic ? "periodic" : "clamped", P->hblur.nt, P->hblur.ht, P->hblur.hb, P->hblur.hl,
                  P->hblur.hr, use_fft ? "2D FFT convolver (4 launches/iteration)"
                                       : (P->big ? "two-level FFT Wiener, direct taps (2 launches/iteration)"
-                                                : "direct taps (2 launches/iteration)"));
+                                                : (P->fused_plane ? "direct taps, fused cluster iteration kernel"
+                                                                  : "direct taps (2 launches/iteration)")));
     }
     P->describe = buf;
     // divergence table (deconv.py:101-112, 137-139)
@@ -715,6 +722,17 @@ int run_plane(md_plan &P, const void *f, void *u, int64_t nb, char *scr, cudaStr
         }
         prof_mark(st, PK_INIT);
     }
+    if (P.fused_plane) {
+        FusedPlaneDesc fd{};
+        fd.u0 = A; fd.fpos = FP; fd.u_out = u;
+        fd.H = P.d.height; fd.W = P.d.width; fd.periodic = P.periodic; fd.iterations = K;
+        fd.hb = P.hblur; fd.ha = P.hadj; fd.taps_blur = &P.htaps_blur; fd.taps_adj = &P.htaps_adj;
+        fd.alpha = P.d.alpha; fd.eps_d2 = P.d.eps_data * P.d.eps_data; fd.eps_r2 = P.d.eps_reg * P.d.eps_reg;
+        fd.has_d = P.has_d; fd.robust = P.robust; fd.lut = P.lut;
+        CU(launch_fused_plane<T>(fd, nb, st));
+        prof_mark(st, PK_ITER);
+        return MD_OK;
+    }
     void *cur = A;
     for (int k = 0; k < K; ++k) {
         const bool last = k == K - 1;
@@ -797,13 +815,20 @@ int32_t md_plan_set_chunk(md_plan *P, int64_t frames) {
 
 int32_t md_plan_set_fused(md_plan *P, int32_t on) {
     if (!P) return fail(MD_EINVAL, "null plan");
+    if (P->path == PATH_PLANE_DIRECT) {
+        if (on && !(P->fast_plane && !P->big &&
+                    fused_plane_supported(P->d.height, P->d.width, P->hblur, P->hadj, P->htaps_blur, P->htaps_adj, P->d.dtype)))
+            return fail(MD_EINVAL, "fused kernel not available for this plan");
+        P->fused_plane = on != 0;
+        return MD_OK;
+    }
     if (on && !(P->path == PATH_LINES && P->fast_lines && fused_lines_supported(P->d.dtype, P->n, P->m, 0)))
         return fail(MD_EINVAL, "fused kernel not available for this plan");
     P->fused = on != 0;
     return MD_OK;
 }
 
-int32_t md_plan_is_fused(const md_plan *P) { return P && P->fused ? 1 : 0; }
+int32_t md_plan_is_fused(const md_plan *P) { return P && (P->fused || P->fused_plane) ? 1 : 0; }
 
 int32_t md_run(md_plan *P, const void *f, void *u, int64_t batch, void *stream) {
     if (!P || !f || !u || batch < 0) return fail(MD_EINVAL, "bad arguments");
@@ -873,7 +898,7 @@ int32_t md_run_launch_count(const md_plan *P, int64_t batch) {
         per = wiener ? 3 : 1;
         if (K > 0) {
             if (!wiener && P->path == PATH_PLANE_FFT) per += 1;
-            per += K * (P->path == PATH_PLANE_FFT ? 4 : 2);
+            per += P->fused_plane ? 1 : K * (P->path == PATH_PLANE_FFT ? 4 : 2);
         }
     }
     return (int32_t)(chunks * sub * per);

@@ -376,3 +376,72 @@ def test_two_level_fft_matches_single_pass_2048(md):
     a = md.DeblurPipeline((2048, 2048), psf, params).run_batch(f)
     b = md.DeblurPipeline((2048, 2048), psf, params, big_fft=True).run_batch(f)
     assert float((a - b).abs().max()) <= FP64_TOL     # rounding only (~1e-8 after RRRL amplification)
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+@pytest.mark.parametrize("name", ["pipe_f2d_3x5_64x128", "pipe_f2d_boxv9_64", "pipe_f2d_line21_30_128"])
+def test_fused_plane_kernel_matches_per_iteration_kernel(md, name, dtype):
+    """2D PSFs: the cluster-resident iteration loop (md_fused_plane.cu) reproduces the
+    two-kernel-per-iteration path and the reference."""
+    d = load_golden(name)
+    shape = d["f"].shape
+    on = md.DeblurPipeline(shape, product_psf(d), product_params(d), md.Scenario.FOURIER_2D, dtype=dtype, fused=True)
+    assert on.plan.fused
+    if dtype == "float32":                       # the float default picks it by itself
+        assert "fused" in md.DeblurPipeline(shape, product_psf(d), product_params(d),
+                                                    md.Scenario.FOURIER_2D, dtype=dtype).plan.describe
+    off = md.DeblurPipeline(shape, product_psf(d), product_params(d), md.Scenario.FOURIER_2D, dtype=dtype,
+                            fused=False)
+    assert not off.plan.fused
+    a = on.run(md.Image(d["f"])).values
+    b = off.run(md.Image(d["f"])).values
+    # float32: the fused kernel sums taps column by column, so rounding differs from the
+    # tap-order sum; on the noise-free line blur that is amplified, but stays inside TOL
+    np.testing.assert_allclose(a, b, rtol=0, atol=1e-9 if dtype == "float64" else TOL)
+    if dtype == "float64":
+        assert np.abs(a - d["out"]).max() <= FP64_TOL
+    elif name != "pipe_f2d_line21_30_128":       # noise-free line blur needs float64
+        assert np.abs(a - d["out"]).max() <= TOL
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+@pytest.mark.parametrize("rl", [False, True])
+@pytest.mark.parametrize("shape", [(64, 128), (128, 64), (256, 256)])
+def test_fused_plane_clamped_spatial(md, dtype, rl, shape):
+    """Clamped spatial convolver (edge-replicated halos at the cluster's first / last CTA)."""
+    import torch
+    from paper_1212_2245_b200.plan import GpuPlan
+    rng = np.random.default_rng(11)
+    psf = md.Psf.general_2d(rng.uniform(0.1, 1.0, (5, 4)))
+    params = md.DeconvParams(iterations=4)
+    g = md.make_test_image(shape[1], shape[0], seed=5).values
+    f = md.synth_blur(md.Image(g), psf).values + rng.normal(0, 2, shape)
+    tdt = torch.float64 if dtype == "float64" else torch.float32
+    fd = torch.from_numpy(np.stack([f, f[::-1].copy(), 255 - f])).cuda().to(tdt)
+    outs = []
+    for fused in (True, False):
+        plan = GpuPlan(shape, psf, params, "spatial", init="clamped", dtype=dtype, rl=rl, fused=fused)
+        assert plan.fused == fused
+        outs.append(plan.run(fd).double().cpu().numpy())
+    np.testing.assert_allclose(outs[0], outs[1], rtol=0, atol=1e-9 if dtype == "float64" else 2e-3)
+
+
+def test_fused_plane_c4_line_frames_independent(md):
+    """c4-style 256^2 frames under a line PSF: many frames per launch stay independent and the
+    float32 result stays within the north_star tolerance of float64."""
+    import torch
+    psf = md.Psf.line(17.0, 63.0)
+    g = md.make_test_image(256, 256, seed=9).values
+    rng = np.random.default_rng(4)
+    f = np.clip(md.synth_blur(md.Image(g), psf).values + rng.normal(0, 5, g.shape), 0, 255)
+    p32 = md.DeblurPipeline((256, 256), psf, md.DeconvParams(), md.Scenario.FOURIER_2D, dtype="float32")
+    assert p32.plan.fused
+    frames = torch.from_numpy(np.stack([f] * 45)).cuda().float()
+    frames[13] += 2.0
+    out = p32.run_batch(frames).double().cpu().numpy()
+    for i in (0, 12, 14, 44):
+        np.testing.assert_array_equal(out[i], out[0])
+    assert np.abs(out[13] - out[0]).max() > 0.1
+    ref = md.DeblurPipeline((256, 256), psf, md.DeconvParams(), md.Scenario.FOURIER_2D,
+                            dtype="float64").run(md.Image(f)).values
+    assert np.abs(out[0] - ref).max() <= TOL
