@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -78,12 +79,16 @@ inline void prof_mark(cudaStream_t st, int kind) {
 }
 
 // ---------------------------------------------------------------- plan-time kernels
-__global__ void k_build_lut(double *t64, float *t32) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kLutCount; i += gridDim.x * blockDim.x) {
+__global__ void k_build_lut(double *t64, float *t32, float2 *p32) {
+    auto val = [](int i) {
         const double x = kLutDelta + (1.0 / kLutInvStep) * (double)i;   // deconv.py:106-108
-        const double v = x - 1.0 - log(x);
+        return x - 1.0 - log(x);
+    };
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kLutCount; i += gridDim.x * blockDim.x) {
+        const double v = val(i);
         t64[i] = v;
         t32[i] = (float)v;
+        if (i + 1 < kLutCount) p32[i] = make_float2((float)v, (float)(val(i + 1) - v));
     }
 }
 
@@ -171,6 +176,7 @@ struct md_plan {
     // LUT
     double *d_lut64 = nullptr;
     float *d_lut32 = nullptr;
+    float2 *d_lutp32 = nullptr;
     LutView lut{};
     // scratch / staging
     DevBuf scratch, stage, partial;
@@ -198,7 +204,8 @@ struct md_plan {
     int64_t frame_elems() const { return (int64_t)d.height * d.width; }
     ~md_plan() {
         for (void *p : {(void *)d_taps_blur, (void *)d_taps_adj, (void *)d_ptaps_blur, (void *)d_ptaps_adj, d_tw_n,
-                        d_tw_H, d_tw_W, d_mult, d_mult_nat, d_hspec, (void *)d_lut64, (void *)d_lut32})
+                        d_tw_H, d_tw_W, d_mult, d_mult_nat, d_hspec, (void *)d_lut64, (void *)d_lut32,
+                        (void *)d_lutp32})
             if (p) cudaFree(p);
         for (void *p : owned) cudaFree(p);
         scratch.release();
@@ -214,6 +221,23 @@ struct md_plan {
 };
 
 namespace {
+
+// divergence table (deconv.py:101-112, 137-139): values in both precisions plus (value, step)
+// pairs for the float kernels' single-load interpolation
+int build_lut(md_plan *P) {
+    CU(cudaMalloc(&P->d_lut64, kLutCount * sizeof(double)));
+    CU(cudaMalloc(&P->d_lut32, kLutCount * sizeof(float)));
+    CU(cudaMalloc(&P->d_lutp32, (kLutCount - 1) * sizeof(float2)));
+    k_build_lut<<<(kLutCount + 255) / 256, 256>>>(P->d_lut64, P->d_lut32, P->d_lutp32);
+    CU(cudaGetLastError());
+    CU(cudaDeviceSynchronize());
+    P->lut.t64 = P->d_lut64;
+    P->lut.t32 = P->d_lut32;
+    P->lut.p32 = P->d_lutp32;
+    P->lut.slope = 1.0 - 1.0 / kLutUpper;
+    P->lut.intercept = (kLutUpper - 1.0 - std::log(kLutUpper)) - P->lut.slope * kLutUpper;
+    return MD_OK;
+}
 
 template <typename X>
 int upload(X **dst, const X *src, size_t count) {
@@ -537,15 +561,7 @@ int32_t md_plan_create(const md_plan_desc *desc, md_plan **out) {
     }
     P->describe = buf;
     // divergence table (deconv.py:101-112, 137-139)
-    CU(cudaMalloc(&P->d_lut64, kLutCount * sizeof(double)));
-    CU(cudaMalloc(&P->d_lut32, kLutCount * sizeof(float)));
-    k_build_lut<<<(kLutCount + 255) / 256, 256>>>(P->d_lut64, P->d_lut32);
-    CU(cudaGetLastError());
-    CU(cudaDeviceSynchronize());
-    P->lut.t64 = P->d_lut64;
-    P->lut.t32 = P->d_lut32;
-    P->lut.slope = 1.0 - 1.0 / kLutUpper;
-    P->lut.intercept = (kLutUpper - 1.0 - std::log(kLutUpper)) - P->lut.slope * kLutUpper;
+    if ((rc = build_lut(P))) return bail(rc);
     *out = P;
     return MD_OK;
 }
@@ -1106,22 +1122,18 @@ int32_t md_adjoint_pair(md_plan *P, const void *p, const void *q, void *op, void
                                 : adjoint_pair_typed<float>(*P, p, q, op, oq, batch, st);
 }
 
-// shared LUT for the plan-free step kernels
+// shared LUT for the plan-free step kernels (built once, never freed)
+static std::mutex g_lut_mu;
 static md_plan *g_lut_owner = nullptr;
 static int lut_view(LutView *out) {
+    std::lock_guard<std::mutex> lk(g_lut_mu);
     if (!g_lut_owner) {
         md_plan *P = new md_plan();
-        if (cudaMalloc(&P->d_lut64, kLutCount * sizeof(double)) != cudaSuccess ||
-            cudaMalloc(&P->d_lut32, kLutCount * sizeof(float)) != cudaSuccess) {
+        const int rc = build_lut(P);
+        if (rc) {
             delete P;
-            return fail(MD_ENOMEM, "LUT allocation failed");
+            return rc;
         }
-        k_build_lut<<<(kLutCount + 255) / 256, 256>>>(P->d_lut64, P->d_lut32);
-        CU(cudaDeviceSynchronize());
-        P->lut.t64 = P->d_lut64;
-        P->lut.t32 = P->d_lut32;
-        P->lut.slope = 1.0 - 1.0 / kLutUpper;
-        P->lut.intercept = (kLutUpper - 1.0 - std::log(kLutUpper)) - P->lut.slope * kLutUpper;
         g_lut_owner = P;
     }
     *out = g_lut_owner->lut;

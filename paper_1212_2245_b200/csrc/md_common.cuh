@@ -38,6 +38,7 @@ constexpr int kLutCount = 133057;                 // round((65 - 1/32) * 2048) +
 struct LutView {
     const double *t64;
     const float *t32;
+    const float2 *p32;                            // (t32[i], t[i+1] - t[i]), i < kLutCount - 1
     double slope, intercept;                      // linear continuation above `upper`
 };
 

@@ -34,13 +34,23 @@ __device__ __forceinline__ void conv_window(const T (&v)[SEG + 2 * R], const Den
                                             T out[SEG]) {
     if constexpr (BOXR > 0) {
         static_assert(BOXR == R, "box window radius must equal the register window radius");
-        T s = T(0);
+        // short dependency chains (few warps per scheduler): the first window by a pairwise
+        // tree, then the running sum over precomputed entering-minus-leaving differences
+        T t[2 * R + 1];
 #pragma unroll
-        for (int i = 0; i <= 2 * R; ++i) s += v[i];
+        for (int i = 0; i <= 2 * R; ++i) t[i] = v[i];
+#pragma unroll
+        for (int w = 1; w <= 2 * R; w *= 2)
+#pragma unroll
+            for (int i = 0; i + w <= 2 * R; i += 2 * w) t[i] += t[i + w];
+        T d[SEG];
+#pragma unroll
+        for (int r = 1; r < SEG; ++r) d[r] = v[r + 2 * R] - v[r - 1];
+        T s = t[0];
         out[0] = s * box_wi;
 #pragma unroll
         for (int r = 1; r < SEG; ++r) {
-            s += v[r + 2 * R] - v[r - 1];
+            s += d[r];
             out[r] = s * box_wi;
         }
     } else {

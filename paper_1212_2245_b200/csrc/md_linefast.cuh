@@ -48,7 +48,17 @@ __device__ __forceinline__ float flog(float x) {
 }
 __device__ __forceinline__ double flog(double x) { return log(x); }
 
-// r1 by table interpolation with both extensions evaluated branch-free (deconv.py:114-134)
+__device__ __forceinline__ float lut_interp(const LutView &L, int i, float t) {
+    const float2 p = __ldg(L.p32 + i);            // one 8-byte load: value and step
+    return p.x + p.y * t;
+}
+__device__ __forceinline__ double lut_interp(const LutView &L, int i, double t) {
+    const double lo = __ldg(L.t64 + i), hi = __ldg(L.t64 + i + 1);
+    return lo + (hi - lo) * t;
+}
+
+// r1 by table interpolation with both extensions evaluated branch-free (deconv.py:114-134);
+// a warp-vote skip of the rare direct-formula branch measured slower (reconvergence)
 template <typename T>
 __device__ __forceinline__ T r1_fast(const LutView &L, T x) {
     const T xc = x < T(kLutUpper) ? x : T(kLutUpper);
@@ -56,10 +66,7 @@ __device__ __forceinline__ T r1_fast(const LutView &L, T x) {
     pos = pos > T(0) ? pos : T(0);
     int i = (int)pos;
     i = i < kLutCount - 2 ? i : kLutCount - 2;
-    const T t = pos - T(i);
-    const T lo = lut_fetch(L, i, T(0));
-    const T hi = lut_fetch(L, i + 1, T(0));
-    T r = lo + (hi - lo) * t;
+    T r = lut_interp(L, i, pos - T(i));
     if (x > T(kLutUpper)) r = T(L.slope) * x + T(L.intercept);
     if (x < T(kLutDirectBelow)) r = x - T(1) - flog(x);
     return r;
