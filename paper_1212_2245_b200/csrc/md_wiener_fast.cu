@@ -126,9 +126,15 @@ k_wiener_lines_reg(WienerLinesArgs a) {
             if (v1) x1 = in[(int64_t)l1 * N + j];
         }
         v[j2] = mkc<T>(x0, x1);
-        if (fpos && !a.in_vert) {
-            if (v0) fpos[(int64_t)l0 * N + j] = x0 > floor ? x0 : floor;
-            if (v1) fpos[(int64_t)l1 * N + j] = x1 > floor ? x1 : floor;
+    }
+    // fpos after ALL loads: a store between them (possible alias of `in`) would serialise the
+    // loads behind each other's latency
+    if (fpos && !a.in_vert) {
+#pragma unroll
+        for (int j2 = 0; j2 < S; ++j2) {
+            const int j = q + S * j2;
+            if (v0) fpos[(int64_t)l0 * N + j] = v[j2].x > floor ? v[j2].x : floor;
+            if (v1) fpos[(int64_t)l1 * N + j] = v[j2].y > floor ? v[j2].y : floor;
         }
     }
     __syncthreads();                            // twiddle table ready
