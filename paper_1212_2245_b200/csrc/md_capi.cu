@@ -705,14 +705,18 @@ int wiener_plane(md_plan &P, const void *f, void *out, void *fpos, void *z, bool
                                          clamp ? 1 : 0, st));
         return MD_OK;
     }
+    // two frames per complex field unless the FFT-path iteration needs z afterwards
     Fft2Args a = fft2_base<T>(P);
+    a.pairs = fwd_after ? 0 : 1;
+    a.nreal = nb;
+    const int64_t nz = a.pairs ? (nb + 1) / 2 : nb;
     a.load = R_LOAD_REAL; a.ra = f; a.rb = nullptr; a.z = z; a.epi = R_EPI_NONE; a.fwd_after = 1;
-    CU(launch_fft2_rows<T>(a, nb, st));
+    CU(launch_fft2_rows<T>(a, nz, st));
     a.filt = P.d_mult; a.conj_filt = 0; a.col_inv = 1;
-    CU(launch_fft2_cols<T>(a, nb, st));
+    CU(launch_fft2_cols<T>(a, nz, st));
     a.load = R_LOAD_COMPLEX; a.inv = 1; a.epi = R_EPI_WIENER; a.fwd_after = fwd_after;
     a.oa = out; a.ob = fpos; a.f = f; a.floor = clamp ? P.d.floor : 0.0;
-    CU(launch_fft2_rows<T>(a, nb, st));
+    CU(launch_fft2_rows<T>(a, nz, st));
     return MD_OK;
 }
 

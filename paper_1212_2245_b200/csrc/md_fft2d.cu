@@ -43,6 +43,7 @@ __global__ void __launch_bounds__(256)
 k_fft2_rows(Fft2Args a, int rb) {
     // `rb` consecutive rows per block (all threads busy in every FFT stage)
     using C = cx_t<T>;
+    constexpr int U = 4;                              // global loads in flight per thread
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C *s = reinterpret_cast<C *>(smem_raw);
     const int H = a.H, W = a.W, lw = a.log2W;
@@ -50,60 +51,109 @@ k_fft2_rows(Fft2Args a, int rb) {
     const int64_t fsz = (int64_t)H * W;
     const int64_t fr = blockIdx.y;
     const int64_t base = fr * fsz + (int64_t)y0 * W;      // rb rows are contiguous
+    // real frames: with pairing, frames 2 fr (real part) and 2 fr + 1 (imaginary part)
+    const int64_t fa = a.pairs ? 2 * fr : fr;
+    const bool has_b = a.pairs && fa + 1 < a.nreal;
+    const int64_t rbase_a = fa * fsz + (int64_t)y0 * W, rbase_b = rbase_a + fsz;
     const int ne = rb * W;
+    const int bd = blockDim.x;
     C *z = static_cast<C *>(a.z);
     const C *tw = static_cast<const C *>(a.twW);
 
     if (a.load == R_LOAD_COMPLEX) {
-        for (int i = threadIdx.x; i < ne; i += blockDim.x) s[i] = z[base + i];
+        for (int i0 = threadIdx.x; i0 < ne; i0 += U * bd) {
+            C v[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) if (i0 + k * bd < ne) v[k] = z[base + i0 + k * bd];
+#pragma unroll
+            for (int k = 0; k < U; ++k) if (i0 + k * bd < ne) s[i0 + k * bd] = v[k];
+        }
     } else {
         const T *ra = static_cast<const T *>(a.ra);
-        const T *rb_ = static_cast<const T *>(a.rb);
-        for (int i = threadIdx.x; i < ne; i += blockDim.x) s[i] = mkc<T>(ra[base + i], rb_ ? rb_[base + i] : T(0));
+        // R_LOAD_PAIR: second real field at rb (same frame); pairing: the next frame of ra
+        const T *rbp = a.pairs ? (has_b ? ra + rbase_b : nullptr)
+                               : (a.rb ? static_cast<const T *>(a.rb) + rbase_a : nullptr);
+        for (int i0 = threadIdx.x; i0 < ne; i0 += U * bd) {
+            T xa[U], xb[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const int i = i0 + k * bd;
+                xa[k] = i < ne ? ra[rbase_a + i] : T(0);
+                xb[k] = (i < ne && rbp) ? rbp[i] : T(0);
+            }
+#pragma unroll
+            for (int k = 0; k < U; ++k) if (i0 + k * bd < ne) s[i0 + k * bd] = mkc<T>(xa[k], xb[k]);
+        }
     }
     __syncthreads();
     if (a.inv && lw > 0) fft_dit_inv_lines(s, lw, rb, W, tw);
 
     const T scale = T(a.scale), floor = T(a.floor);
     if (a.epi != R_EPI_NONE) {
-        for (int i = threadIdx.x; i < ne; i += blockDim.x) {
-            const C v = s[i];
-            const int64_t o = base + i;
-            C packed = mkc<T>(T(0), T(0));
-            if (a.epi == R_EPI_STORE_PAIR) {
-                static_cast<T *>(a.oa)[o] = v.x * scale;
-                if (a.ob) static_cast<T *>(a.ob)[o] = v.y * scale;
-            } else if (a.epi == R_EPI_WIENER) {
-                T w = v.x * scale;
-                if (floor > T(0)) w = w > floor ? w : floor;     // u0 = max(Wiener, floor)
-                static_cast<T *>(a.oa)[o] = w;
-                if (a.ob) {
-                    const T fv = static_cast<const T *>(a.f)[o];
-                    static_cast<T *>(a.ob)[o] = fv > floor ? fv : floor;
+        for (int i0 = threadIdx.x; i0 < ne; i0 += U * bd) {
+            // global operands of U elements first: the stores below could alias them, so a
+            // load issued after a store would wait for it
+            T g0[U], g1[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const int i = i0 + k * bd;
+                g0[k] = g1[k] = T(0);
+                if (i >= ne) continue;
+                if (a.epi == R_EPI_WIENER && a.ob) {
+                    g0[k] = static_cast<const T *>(a.f)[rbase_a + i];
+                    if (has_b) g1[k] = static_cast<const T *>(a.f)[rbase_b + i];
+                } else if (a.epi == R_EPI_STAGE_A) {
+                    g0[k] = static_cast<const T *>(a.f)[base + i];
+                } else if (a.epi == R_EPI_STAGE_B) {
+                    g0[k] = static_cast<const T *>(a.u)[base + i];
                 }
-                packed = mkc<T>(w, T(0));
-            } else if (a.epi == R_EPI_STAGE_A) {
-                T b = v.x * scale;
-                b = b > T(kGuard) ? b : T(kGuard);
-                const T fp = static_cast<const T *>(a.f)[o];
-                const T ratio = fp / b;
-                if (a.robust) {
-                    const T wv = robust_weight_floored<T>(a.lut, fp, b, T(a.eps_d2));
-                    packed = mkc<T>(wv * ratio, wv);
-                } else {
-                    packed = mkc<T>(ratio, T(0));
-                }
-            } else {  // R_EPI_STAGE_B
-                const T *u = static_cast<const T *>(a.u) + fr * fsz;
-                const int y = y0 + (i >> lw), x = i & (W - 1);
-                const T uv = u[(int64_t)y * W + x];
-                const T d = a.has_d ? tv_div_global<T>(u, H, W, y, x, T(a.eps_r2)) : T(0);
-                const T un = a.robust ? combine_px<T, true>(uv, v.x * scale, v.y * scale, d, T(a.alpha), a.has_d != 0)
-                                      : combine_px<T, false>(uv, v.x * scale, T(0), d, T(a.alpha), a.has_d != 0);
-                static_cast<T *>(a.oa)[o] = un;
-                packed = mkc<T>(un, T(0));
             }
-            s[i] = packed;
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const int i = i0 + k * bd;
+                if (i >= ne) continue;
+                const C v = s[i];
+                const int64_t o = base + i;
+                C packed = mkc<T>(T(0), T(0));
+                if (a.epi == R_EPI_STORE_PAIR) {
+                    static_cast<T *>(a.oa)[o] = v.x * scale;
+                    if (a.ob) static_cast<T *>(a.ob)[o] = v.y * scale;
+                } else if (a.epi == R_EPI_WIENER) {
+                    T w = v.x * scale, w1 = v.y * scale;
+                    if (floor > T(0)) {                  // u0 = max(Wiener, floor)
+                        w = w > floor ? w : floor;
+                        w1 = w1 > floor ? w1 : floor;
+                    }
+                    static_cast<T *>(a.oa)[rbase_a + i] = w;
+                    if (has_b) static_cast<T *>(a.oa)[rbase_b + i] = w1;
+                    if (a.ob) {
+                        static_cast<T *>(a.ob)[rbase_a + i] = g0[k] > floor ? g0[k] : floor;
+                        if (has_b) static_cast<T *>(a.ob)[rbase_b + i] = g1[k] > floor ? g1[k] : floor;
+                    }
+                    packed = mkc<T>(w, T(0));
+                } else if (a.epi == R_EPI_STAGE_A) {
+                    T b = v.x * scale;
+                    b = b > T(kGuard) ? b : T(kGuard);
+                    const T fp = g0[k];
+                    const T ratio = fp / b;
+                    if (a.robust) {
+                        const T wv = robust_weight_floored<T>(a.lut, fp, b, T(a.eps_d2));
+                        packed = mkc<T>(wv * ratio, wv);
+                    } else {
+                        packed = mkc<T>(ratio, T(0));
+                    }
+                } else {  // R_EPI_STAGE_B
+                    const T *u = static_cast<const T *>(a.u) + fr * fsz;
+                    const int y = y0 + (i >> lw), x = i & (W - 1);
+                    const T uv = g0[k];
+                    const T d = a.has_d ? tv_div_global<T>(u, H, W, y, x, T(a.eps_r2)) : T(0);
+                    const T un = a.robust ? combine_px<T, true>(uv, v.x * scale, v.y * scale, d, T(a.alpha), a.has_d != 0)
+                                          : combine_px<T, false>(uv, v.x * scale, T(0), d, T(a.alpha), a.has_d != 0);
+                    static_cast<T *>(a.oa)[o] = un;
+                    packed = mkc<T>(un, T(0));
+                }
+                s[i] = packed;
+            }
         }
         __syncthreads();
     }
@@ -157,20 +207,23 @@ cudaError_t launch_fft2_rows(const Fft2Args &a, int64_t batch, cudaStream_t st) 
     const size_t smem = (size_t)rb * a.W * sizeof(cx_t<T>);
     cudaError_t e = cudaFuncSetAttribute(k_fft2_rows<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    // `batch` counts complex fields; with pairing the real pointers advance two frames per field
     const int64_t fr = (int64_t)a.H * a.W;
+    const int64_t rstep = a.pairs ? 2 : 1;
     for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
         const int nb = (int)((batch - b0) < 65535 ? (batch - b0) : 65535);
         Fft2Args ab = a;
-        auto sh = [&](const void *p, size_t es) -> const void * {
-            return p ? static_cast<const char *>(p) + b0 * fr * es : nullptr;
+        auto sh = [&](const void *p, size_t es, int64_t step) -> const void * {
+            return p ? static_cast<const char *>(p) + step * b0 * fr * es : nullptr;
         };
-        ab.ra = sh(a.ra, sizeof(T));
-        ab.rb = sh(a.rb, sizeof(T));
-        ab.z = const_cast<void *>(sh(a.z, sizeof(cx_t<T>)));
-        ab.oa = const_cast<void *>(sh(a.oa, sizeof(T)));
-        ab.ob = const_cast<void *>(sh(a.ob, sizeof(T)));
-        ab.f = sh(a.f, sizeof(T));
-        ab.u = sh(a.u, sizeof(T));
+        ab.ra = sh(a.ra, sizeof(T), rstep);
+        ab.rb = sh(a.rb, sizeof(T), rstep);
+        ab.z = const_cast<void *>(sh(a.z, sizeof(cx_t<T>), 1));
+        ab.oa = const_cast<void *>(sh(a.oa, sizeof(T), rstep));
+        ab.ob = const_cast<void *>(sh(a.ob, sizeof(T), rstep));
+        ab.f = sh(a.f, sizeof(T), rstep);
+        ab.u = sh(a.u, sizeof(T), 1);
+        ab.nreal = a.nreal - rstep * b0;
         k_fft2_rows<T><<<dim3(a.H / rb, nb), 256, smem, st>>>(ab, rb);
     }
     return cudaGetLastError();

@@ -78,6 +78,10 @@ struct Fft2Args {
     double floor, alpha, eps_d2, eps_r2, scale;
     int has_d, robust;
     LutView lut;
+    // frame pairing (Wiener init): real frames 2z and 2z+1 ride in the real / imaginary part of
+    // complex field z (h is real, so the filter maps each part to itself); nreal = real frames
+    int pairs;
+    int64_t nreal;
     // column pass
     const void *filt;           // cx_t<T>[H][W] in storage (bit-reversed) coordinates, or null
     int conj_filt, col_inv;     // multiply by conj(filt); run the inverse DIT after the multiply
