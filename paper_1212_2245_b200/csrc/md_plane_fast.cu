@@ -85,6 +85,13 @@ k_plane_a_fast(PlaneFastArgs<T, MAXT> a) {
     const int ty = threadIdx.x >> 3, cx = threadIdx.x & 7;
     const int y = y0 + ty;
     if (y >= H) return;
+    // observation first: loads issued after the p / W stores below would wait for them
+    T fr8[FR];
+#pragma unroll
+    for (int r = 0; r < FR; ++r) {
+        const int x = x0 + cx + 8 * r;
+        fr8[r] = x < W ? f[(int64_t)y * W + x] : T(1);
+    }
     T b[FR];
     pf_taps<T, MAXT>(su + (ty + a.hb.ht) * ss + a.hb.hl + cx, a.tb, b);
     const T eps_d2 = a.eps_d2;
@@ -94,7 +101,7 @@ k_plane_a_fast(PlaneFastArgs<T, MAXT> a) {
         if (x >= W) continue;
         const int64_t o = (int64_t)y * W + x;
         const T bb = b[r] > T(kGuard) ? b[r] : T(kGuard);
-        const T fv = f[o];
+        const T fv = fr8[r];
         const T ratio = fv * frcp(bb);
         if (ROBUST) {
             const T wv = T(0.5) * frsqrt(r1_fast<T>(a.lut, bb * frcp(fv)) * fv + eps_d2);
