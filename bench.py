@@ -51,6 +51,17 @@ def peaks() -> dict:
         return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
 
 
+def measured_traffic(key: str, frames: int):
+    """DRAM bytes of the dominant kernel for `frames` frames per launch, scaled from the
+    committed ncu capture (profiles/ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            d = json.load(fh)[key]
+        return (d["dram_bytes_read"] + d["dram_bytes_write"]) / d["frames"] * frames
+    except Exception:
+        return None
+
+
 def host_cores() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -86,6 +97,10 @@ class C1:
         self.host = np.tile(base, (-(-args.batch // k), 1, 1))[:args.batch]
         self.cpu_items = [("box", self.psf, base[i]) for i in range(k)]
         self.latency_plan = self.pipe.plan
+
+    def iter_launches(self, n) -> int:
+        """Launches of the fused iteration kernel for n frames (one per internal chunk)."""
+        return max(1, self.pipe.plan.launch_count(n) // 2)
 
     def run(self, f, u):
         self.pipe.plan.run(f, out=u)
@@ -540,7 +555,11 @@ def main() -> None:
             "roofline": {"bound": "hbm",
                          "kernel": "RRRL iteration" + (" (fused cluster kernel)" if work.fused else ""),
                          "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                         "frac": (achieved / pk["hbm_gbs"]) if achieved else None, "traffic": None,
+                         "frac": (achieved / pk["hbm_gbs"]) if achieved else None,
+                         "traffic": (measured_traffic(f"{args.config}_{args.dtype}", args.batch / work.iter_launches(args.batch))
+                                     if work.fused else None),
+                         "traffic_note": "DRAM bytes per launch of the fused kernel (ncu, scaled to this batch); "
+                                         "iterate, p, W stay on chip, so traffic is the compulsory stream only",
                          "peak_source": pk["source"],
                          "bytes_model": "SURVEY.md 8(d): 8 field passes per RRRL iteration x 65536 px x "
                                         f"{esz} B per frame; time = CUDA events around the iteration launches"},
