@@ -508,7 +508,7 @@ int32_t md_plan_create(const md_plan_desc *desc, md_plan **out) {
         if ((rc = upload(&P->d_ptaps_adj, ta.data(), ta.size()))) return bail(rc);
         P->htaps_blur = tb;
         P->htaps_adj = ta;
-        P->fast_plane = !(desc->flags & MD_FLAG_GENERIC_LINES) && plane_fast_supported(P->hblur, P->hadj, desc->dtype);
+        P->fast_plane = !(desc->flags & MD_FLAG_GENERIC_LINES) && plane_fast_supported(P->hblur, P->hadj, tb, ta, desc->dtype);
         if (pow2 && P->big) {
             BigAxis h64{}, w64{};
             std::vector<void *> tmp;

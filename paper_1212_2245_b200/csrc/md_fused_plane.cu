@@ -28,8 +28,8 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
-#include <map>
 
+#include "md_coltaps.cuh"
 #include "md_fused_plane.h"
 #include "md_linefast.cuh"
 
@@ -44,21 +44,6 @@ constexpr int FP_WARPS = 16 * FP_SPLIT;
 constexpr int FP_THREADS = FP_WARPS * 32;
 constexpr int FP_MAXRL = 2 * FP_WARPS / FP_SPLIT;   // one row pair per FP_SPLIT warps
 constexpr int FP_MAXHX = 32;                    // x-halo sources lie in the first / last 32 columns
-constexpr int FP_MAXC = 64;                     // tap columns
-constexpr int FP_MAXW = 192;                    // column weights (runs incl. interior zeros)
-
-template <typename T> struct Vec2;
-template <> struct Vec2<float> { using type = float2; };
-template <> struct Vec2<double> { using type = double2; };
-
-// taps grouped by column: c[k].x = dy0 * rs + dx (offset of the column's first tap),
-// c[k].y = len | (first weight index << 16); weights w[...] top to bottom
-template <typename T> struct ColTaps {
-    int ncol;
-    int2 c[FP_MAXC];
-    T w[FP_MAXW];
-};
-
 template <typename T> struct FusedPlaneKArgs {
     const T *u0, *fpos;
     T *out;
@@ -124,78 +109,6 @@ __device__ __forceinline__ void fp_copy(void *dst, const void *src, int bytes) {
     int4 *d = static_cast<int4 *>(dst);
     const int4 *s = static_cast<const int4 *>(src);
     for (int i = threadIdx.x; i < bytes / 16; i += blockDim.x) d[i] = s[i];
-}
-
-// blur of a row pair: a0 = row 0, a1 = row 1 (s points at row 0, column `lane`)
-template <typename T, int J>
-__device__ __forceinline__ void fp_cols(const T *s, int rs, const ColTaps<T> &tp, T a0[J], T a1[J]) {
-#pragma unroll
-    for (int j = 0; j < J; ++j) a0[j] = a1[j] = T(0);
-    for (int c = 0; c < tp.ncol; ++c) {
-        const int2 ci = tp.c[c];
-        const T *p = s + ci.x;
-        const int len = ci.y & 0xffff;
-        const T *wc = tp.w + (ci.y >> 16);
-        T wp = wc[0];
-#pragma unroll
-        for (int j = 0; j < J; ++j) a0[j] += wp * p[32 * j];
-        for (int i = 1; i < len; ++i) {
-            p += rs;
-            const T wi = wc[i];
-#pragma unroll
-            for (int j = 0; j < J; ++j) {
-                const T v = p[32 * j];
-                a0[j] += wi * v;
-                a1[j] += wp * v;
-            }
-            wp = wi;
-        }
-        p += rs;
-#pragma unroll
-        for (int j = 0; j < J; ++j) a1[j] += wp * p[32 * j];
-    }
-}
-
-// adjoint pair of a row pair over interleaved (p, W): n = sum w p, d = sum w W
-template <typename T, int J>
-__device__ __forceinline__ void fp_cols2(const typename Vec2<T>::type *s, int rs, const ColTaps<T> &tp, T n0[J],
-                                         T n1[J], T d0[J], T d1[J]) {
-    using T2 = typename Vec2<T>::type;
-#pragma unroll
-    for (int j = 0; j < J; ++j) n0[j] = n1[j] = d0[j] = d1[j] = T(0);
-    for (int c = 0; c < tp.ncol; ++c) {
-        const int2 ci = tp.c[c];
-        const T2 *p = s + ci.x;
-        const int len = ci.y & 0xffff;
-        const T *wc = tp.w + (ci.y >> 16);
-        T wp = wc[0];
-#pragma unroll
-        for (int j = 0; j < J; ++j) {
-            const T2 v = p[32 * j];
-            n0[j] += wp * v.x;
-            d0[j] += wp * v.y;
-        }
-        for (int i = 1; i < len; ++i) {
-            p += rs;
-            const T wi = wc[i];
-#pragma unroll
-            for (int j = 0; j < J; ++j) {
-                const T2 v = p[32 * j];
-                n0[j] += wi * v.x;
-                d0[j] += wi * v.y;
-                n1[j] += wp * v.x;
-                d1[j] += wp * v.y;
-            }
-            wp = wi;
-        }
-        p += rs;
-#pragma unroll
-        for (int j = 0; j < J; ++j) {
-            const T2 v = p[32 * j];
-            n1[j] += wp * v.x;
-            d1[j] += wp * v.y;
-        }
-    }
 }
 
 __device__ __forceinline__ void fp_cluster_sync() {
@@ -267,7 +180,7 @@ k_fused_plane(FusedPlaneKArgs<T> a) {
         // ---- stage A: blur -> (p, W) on own rows
         if (pair) {
             T b[2][JW];
-            fp_cols<T, JW>(urow(sm, r0) + hx + xl, rs, a.tb, b[0], b[1]);
+            col_taps_pair<T, JW, 32>(urow(sm, r0) + hx + xl, rs, a.tb, b[0], b[1]);
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
                 const T *F = fpos + (int64_t)(gy0 + r0 + k) * W + xl;
@@ -325,7 +238,7 @@ k_fused_plane(FusedPlaneKArgs<T> a) {
         T unew[2][JW];
         if (pair) {
             T num[2][JW], den[2][JW];
-            fp_cols2<T, JW>(pwrow(sm, r0) + hx + xl, rs, a.ta, num[0], num[1], den[0], den[1]);
+            col_taps_pair2<T, JW, 32>(pwrow(sm, r0) + hx + xl, rs, a.ta, num[0], num[1], den[0], den[1]);
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
                 const int r = r0 + k;
@@ -390,30 +303,6 @@ struct FpGeom {
     size_t smem;
 };
 
-// taps -> columns (fixed dx, consecutive dy; gaps inside a run get zero weights)
-template <typename T> bool build_cols(const std::vector<PlaneTap> &taps, int rs, ColTaps<T> *ct) {
-    std::map<int, std::map<int, double>> by_dx;
-    for (const PlaneTap &t : taps) by_dx[t.dx][t.dy] += t.w;
-    if (by_dx.size() > (size_t)FP_MAXC) return false;
-    int nw = 0, nc = 0;
-    for (const auto &col : by_dx) {
-        const int dy0 = col.second.begin()->first, dy1 = col.second.rbegin()->first;
-        const int len = dy1 - dy0 + 1;
-        if (nw + len > FP_MAXW) return false;
-        if (ct) {
-            ct->c[nc] = make_int2(dy0 * rs + col.first, len | (nw << 16));
-            for (int i = 0; i < len; ++i) {
-                const auto it = col.second.find(dy0 + i);
-                ct->w[nw + i] = it == col.second.end() ? T(0) : T(it->second);
-            }
-        }
-        nw += len;
-        ++nc;
-    }
-    if (ct) ct->ncol = nc;
-    return true;
-}
-
 bool fp_geometry(int H, int W, const PlaneHalo &hb, const PlaneHalo &ha, int dtype, FpGeom *g) {
     if (W != 64 && W != 128 && W != 256) return false;
     const int es = dtype == 0 ? 8 : 4;
@@ -444,7 +333,7 @@ cudaError_t launch_j(const FusedPlaneDesc &d, const FpGeom &g, int64_t batch, cu
     a.out = static_cast<T *>(d.u_out);
     a.H = d.H; a.W = d.W; a.rl = g.rl; a.cl = g.cl; a.periodic = d.periodic; a.iterations = d.iterations;
     a.hx = g.hx; a.rs = g.rs; a.ut = g.ut; a.ub = g.ub; a.pt = g.pt; a.pb = g.pb;
-    if (!build_cols<T>(*d.taps_blur, g.rs, &a.tb) || !build_cols<T>(*d.taps_adj, g.rs, &a.ta))
+    if (!build_col_taps<T>(*d.taps_blur, g.rs, &a.tb) || !build_col_taps<T>(*d.taps_adj, g.rs, &a.ta))
         return cudaErrorNotSupported;
     a.alpha = T(d.alpha); a.eps_d2 = T(d.eps_d2); a.eps_r2 = T(d.eps_r2); a.has_d = d.has_d;
     a.lut = d.lut;
@@ -484,8 +373,8 @@ bool fused_plane_supported(int H, int W, const PlaneHalo &hb, const PlaneHalo &h
                            const std::vector<PlaneTap> &taps_blur, const std::vector<PlaneTap> &taps_adj, int dtype) {
     FpGeom g;
     if (!fp_geometry(H, W, hb, ha, dtype, &g)) return false;
-    return dtype == 0 ? build_cols<double>(taps_blur, g.rs, nullptr) && build_cols<double>(taps_adj, g.rs, nullptr)
-                      : build_cols<float>(taps_blur, g.rs, nullptr) && build_cols<float>(taps_adj, g.rs, nullptr);
+    return dtype == 0 ? build_col_taps<double>(taps_blur, g.rs, nullptr) && build_col_taps<double>(taps_adj, g.rs, nullptr)
+                      : build_col_taps<float>(taps_blur, g.rs, nullptr) && build_col_taps<float>(taps_adj, g.rs, nullptr);
 }
 
 template <typename T>

@@ -5,11 +5,11 @@
 // 359-376, 512-521) together with _weight_arrays (142-162), _diffusion_arrays (187-213) and
 // _combine (421-446).
 //
-// Tile 64 x 32 outputs per block, 256 threads; thread (row ty, column group cx) owns the 8
-// outputs x = cx + 8 r (r = 0..7) of row ty, so a warp's lanes read consecutive shared-memory
-// words for every tap. The tap list lives in the kernel parameters as (smem offset, weight)
-// pairs precomputed on the host for the tile stride, so a tap costs one offset add, eight
-// shared loads with immediate offsets and eight FMAs, shared by the eight outputs.
+// Tile 64 x 32 outputs per block, 256 threads; thread (pair tp, column cx) owns the outputs
+// of rows 2tp, 2tp+1 at x = cx + 16 r (r = 0..3), so a half-warp reads 16 consecutive
+// shared-memory words per tap. Taps are regrouped on the host into columns (md_coltaps.cuh):
+// each loaded value feeds both rows of the pair. Stage B stages p and W interleaved, so one
+// load feeds both halves of the adjoint pair.
 #include "md_plane.h"
 #include "md_plane_fast.h"
 #include "md_linefast.cuh"
@@ -17,7 +17,8 @@
 namespace md {
 
 constexpr int FX = 64, FY = 32;           // output tile
-constexpr int FR = 8;                     // outputs per thread (stride 8 along x)
+constexpr int PJ = 4;                     // outputs per row per thread (column stride 16)
+constexpr int PS = 72;                    // u / g tile stride: 2 * PS = 16 (mod 32) -> half-warps on disjoint banks
 
 __device__ __forceinline__ int pf_resolve(int k, int n, int periodic) {
     // halos never exceed the extent, so one conditional wrap suffices (no integer modulo)
@@ -25,50 +26,28 @@ __device__ __forceinline__ int pf_resolve(int k, int n, int periodic) {
     return k < 0 ? 0 : (k >= n ? n - 1 : k);
 }
 
-template <typename T>
-__device__ void pf_load(T *s, int ss, const T *__restrict__ src, int H, int W, int y0, int x0, const PlaneHalo &h,
-                        int periodic, int slab) {
+// tile rows [y0 - ht, y0 + FY + hb) x cols [x0 - hl, x0 + FX + hr) of one or two fields
+template <typename T, typename E, typename Get>
+__device__ void pf_load(E *s, int ss, int H, int W, int y0, int x0, const PlaneHalo &h, int periodic, int slab,
+                        Get get) {
     const int rows = FY + h.ht + h.hb, cols = FX + h.hl + h.hr;
     for (int i = threadIdx.x / 32; i < rows; i += blockDim.x / 32) {
         // slab mode: the caller's buffer carries the neighbours' rows (halo), read them as is
         const int y = slab ? y0 - h.ht + i : pf_resolve(y0 - h.ht + i, H, periodic);
-        const T *srow = src + (int64_t)y * W;
-        for (int j = threadIdx.x & 31; j < cols; j += 32) s[i * ss + j] = srow[pf_resolve(x0 - h.hl + j, W, periodic)];
+        for (int j = threadIdx.x & 31; j < cols; j += 32) s[i * ss + j] = get((int64_t)y * W + pf_resolve(x0 - h.hl + j, W, periodic));
     }
 }
 
-template <typename T, int MAXT>
-__device__ __forceinline__ void pf_taps(const T *s, const FastTaps<T, MAXT> &tp, T acc[FR]) {
-#pragma unroll
-    for (int r = 0; r < FR; ++r) acc[r] = T(0);
-    for (int t = 0; t < tp.nt; ++t) {
-        const T *p = s + tp.off[t];
-        const T w = tp.w[t];
-#pragma unroll
-        for (int r = 0; r < FR; ++r) acc[r] += w * p[8 * r];
-    }
+// f32 u-tile stride for stage A: 8 (mod 16) so the two half-warps (rows 2 apart) use disjoint banks
+template <typename T> __host__ __device__ inline int pf_stride_a(const PlaneHalo &h) {
+    const int base = FX + h.hl + h.hr;
+    return sizeof(T) == 4 ? base + ((8 - base) % 16 + 16) % 16 : base;
 }
+template <typename T> __host__ __device__ inline int pf_stride_b(const PlaneHalo &h) { return FX + h.hl + h.hr; }
 
-// num and den of the adjoint pair share the tap decode (deconv.py:425-430: adjoint_pair)
-template <typename T, int MAXT>
-__device__ __forceinline__ void pf_taps2(const T *s0, const T *s1, const FastTaps<T, MAXT> &tp, T a0[FR], T a1[FR]) {
-#pragma unroll
-    for (int r = 0; r < FR; ++r) a0[r] = a1[r] = T(0);
-    const int d = (int)(s1 - s0);
-    for (int t = 0; t < tp.nt; ++t) {
-        const T *p = s0 + tp.off[t];
-        const T w = tp.w[t];
-#pragma unroll
-        for (int r = 0; r < FR; ++r) {
-            a0[r] += w * p[8 * r];
-            a1[r] += w * p[d + 8 * r];
-        }
-    }
-}
-
-template <typename T, int MAXT, bool ROBUST>
+template <typename T, bool ROBUST>
 __global__ void __launch_bounds__(256)
-k_plane_a_fast(PlaneFastArgs<T, MAXT> a) {
+k_plane_a_fast(PlaneFastArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T *su = reinterpret_cast<T *>(smem_raw);
     const int H = a.H, W = a.W;
@@ -79,67 +58,78 @@ k_plane_a_fast(PlaneFastArgs<T, MAXT> a) {
     T *p = a.p + fr * fsz;
     T *w = a.w + fr * fsz;
     const int y0 = blockIdx.y * FY, x0 = blockIdx.x * FX;
-    const int ss = FX + a.hb.hl + a.hb.hr + 1;
-    pf_load<T>(su, ss, u, H, W, y0, x0, a.hb, a.periodic, a.slab);
+    const int ss = a.ssa;
+    pf_load<T>(su, ss, H, W, y0, x0, a.hb, a.periodic, a.slab, [&](int64_t o) { return u[o]; });
     __syncthreads();
-    const int ty = threadIdx.x >> 3, cx = threadIdx.x & 7;
-    const int y = y0 + ty;
-    if (y >= H) return;
+    const int tp = threadIdx.x >> 4, cx = threadIdx.x & 15;
+    const int yp = y0 + 2 * tp;
+    if (yp >= H) return;
     // observation first: loads issued after the p / W stores below would wait for them
-    T fr8[FR];
+    T fv[2][PJ];
 #pragma unroll
-    for (int r = 0; r < FR; ++r) {
-        const int x = x0 + cx + 8 * r;
-        fr8[r] = x < W ? f[(int64_t)y * W + x] : T(1);
-    }
-    T b[FR];
-    pf_taps<T, MAXT>(su + (ty + a.hb.ht) * ss + a.hb.hl + cx, a.tb, b);
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int r = 0; r < PJ; ++r) {
+            const int x = x0 + cx + 16 * r;
+            fv[k][r] = (x < W && yp + k < H) ? f[(int64_t)(yp + k) * W + x] : T(1);
+        }
+    T b[2][PJ];
+    col_taps_pair<T, PJ, 16>(su + (2 * tp + a.hb.ht) * ss + a.hb.hl + cx, ss, a.tb, b[0], b[1]);
     const T eps_d2 = a.eps_d2;
 #pragma unroll
-    for (int r = 0; r < FR; ++r) {
-        const int x = x0 + cx + 8 * r;
-        if (x >= W) continue;
-        const int64_t o = (int64_t)y * W + x;
-        const T bb = b[r] > T(kGuard) ? b[r] : T(kGuard);
-        const T fv = fr8[r];
-        const T ratio = fv * frcp(bb);
-        if (ROBUST) {
-            const T wv = T(0.5) * frsqrt(r1_fast<T>(a.lut, bb * frcp(fv)) * fv + eps_d2);
-            w[o] = wv;
-            p[o] = wv * ratio;
-        } else {
-            p[o] = ratio;
+    for (int k = 0; k < 2; ++k) {
+        const int y = yp + k;
+        if (y >= H) break;
+#pragma unroll
+        for (int r = 0; r < PJ; ++r) {
+            const int x = x0 + cx + 16 * r;
+            if (x >= W) continue;
+            const int64_t o = (int64_t)y * W + x;
+            const T bb = b[k][r] > T(kGuard) ? b[k][r] : T(kGuard);
+            const T ratio = fv[k][r] * frcp(bb);
+            if (ROBUST) {
+                const T wv = T(0.5) * frsqrt(r1_fast<T>(a.lut, bb * frcp(fv[k][r])) * fv[k][r] + eps_d2);
+                w[o] = wv;
+                p[o] = wv * ratio;
+            } else {
+                p[o] = ratio;
+            }
         }
     }
 }
 
-template <typename T, int MAXT, bool ROBUST>
+template <typename T, bool ROBUST>
 __global__ void __launch_bounds__(256)
-k_plane_b_fast(PlaneFastArgs<T, MAXT> a) {
+k_plane_b_fast(PlaneFastArgs<T> a) {
+    using T2 = typename Vec2<T>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int H = a.H, W = a.W;
-    const int ss = FX + a.ha.hl + a.ha.hr + 1;
+    const int ss = a.ssb;
     const int rows = FY + a.ha.ht + a.ha.hb;
-    T *sp = reinterpret_cast<T *>(smem_raw);
-    T *sw = sp + rows * ss;
-    T *su = ROBUST ? sw + rows * ss : sw;          // (FY+4) x (FX+5): u with a 2-pixel halo
-    constexpr int US = FX + 5;
-    T *sg = su + (FY + 4) * US;                     // (FY+2) x (FX+3): diffusivity
-    constexpr int GS = FX + 3;
+    T2 *spw = reinterpret_cast<T2 *>(smem_raw);
+    T *su = reinterpret_cast<T *>(spw + rows * ss);  // (FY+4) x PS: u with a 2-pixel halo
+    T *sg = su + (FY + 4) * PS;                      // (FY+2) x PS: diffusivity
     const int64_t fsz = (int64_t)H * W;
     const int64_t fr = blockIdx.z;
     const T *u = a.u + fr * fsz;
     T *uo = a.u_out + fr * fsz;
     const int y0 = blockIdx.y * FY, x0 = blockIdx.x * FX;
-    pf_load<T>(sp, ss, a.p + fr * fsz, H, W, y0, x0, a.ha, a.periodic, a.slab);
-    if (ROBUST) pf_load<T>(sw, ss, a.w + fr * fsz, H, W, y0, x0, a.ha, a.periodic, a.slab);
+    {
+        const T *pp = a.p + fr * fsz, *ww = a.w + fr * fsz;
+        pf_load<T>(spw, ss, H, W, y0, x0, a.ha, a.periodic, a.slab, [&](int64_t o) {
+            T2 v;
+            v.x = pp[o];
+            v.y = ROBUST ? ww[o] : T(0);
+            return v;
+        });
+    }
     const int gy0 = a.gy0, Hg = a.Hg;
     for (int i = threadIdx.x / 32; i < FY + 4; i += 8) {
         const int yy = y0 - 2 + i;
         const bool rok = gy0 + yy >= 0 && gy0 + yy < Hg && (a.slab || (yy >= 0 && yy < H));
         for (int j = threadIdx.x & 31; j < FX + 4; j += 32) {
             const int xx = x0 - 2 + j;
-            su[i * US + j] = (rok && xx >= 0 && xx < W) ? u[(int64_t)yy * W + xx] : T(0);
+            su[i * PS + j] = (rok && xx >= 0 && xx < W) ? u[(int64_t)yy * W + xx] : T(0);
         }
     }
     __syncthreads();
@@ -152,82 +142,81 @@ k_plane_b_fast(PlaneFastArgs<T, MAXT> a) {
             for (int j = threadIdx.x & 31; j < FX + 2; j += 32) {
                 const int xx = x0 - 1 + j;
                 if (xx < 0 || xx >= W) continue;
-                const T *c = su + (i + 1) * US + (j + 1);
+                const T *c = su + (i + 1) * PS + (j + 1);
                 const T c0 = c[0];
                 T q = T(0);
                 if (xx + 1 < W) { const T d = c[1] - c0; q += d * d; }
                 if (xx > 0) { const T d = c0 - c[-1]; q += d * d; }
-                if (gyy + 1 < Hg) { const T d = c[US] - c0; q += d * d; }
-                if (gyy > 0) { const T d = c0 - c[-US]; q += d * d; }
-                sg[i * GS + j] = T(0.5) * frsqrt(T(0.5) * q + eps_r2);
+                if (gyy + 1 < Hg) { const T d = c[PS] - c0; q += d * d; }
+                if (gyy > 0) { const T d = c0 - c[-PS]; q += d * d; }
+                sg[i * PS + j] = T(0.5) * frsqrt(T(0.5) * q + eps_r2);
             }
         }
         __syncthreads();
     }
-    const int ty = threadIdx.x >> 3, cx = threadIdx.x & 7;
-    const int y = y0 + ty;
-    if (y >= H) return;
-    T num[FR], den[FR];
-    if (ROBUST) {
-        pf_taps2<T, MAXT>(sp + (ty + a.ha.ht) * ss + a.ha.hl + cx, sw + (ty + a.ha.ht) * ss + a.ha.hl + cx, a.ta,
-                          num, den);
-    } else {
-        pf_taps<T, MAXT>(sp + (ty + a.ha.ht) * ss + a.ha.hl + cx, a.ta, num);
-    }
+    const int tp = threadIdx.x >> 4, cx = threadIdx.x & 15;
+    const int ty0 = 2 * tp;
+    if (y0 + ty0 >= H) return;
+    T num[2][PJ], den[2][PJ];
+    col_taps_pair2<T, PJ, 16>(spw + (ty0 + a.ha.ht) * ss + a.ha.hl + cx, ss, a.ta, num[0], num[1], den[0], den[1]);
     const T alpha = a.alpha;
 #pragma unroll
-    for (int r = 0; r < FR; ++r) {
-        const int tx = cx + 8 * r;
-        const int x = x0 + tx;
-        if (x >= W) continue;
-        const T *c = su + (ty + 2) * US + (tx + 2);
-        const T uv = c[0];
-        T d = T(0);
-        if (a.has_d) {
-            const T *g = sg + (ty + 1) * GS + (tx + 1);
-            const T gc = g[0];
-            if (x + 1 < W) d += (gc + g[1]) * (c[1] - uv);
-            if (x > 0) d -= (g[-1] + gc) * (uv - c[-1]);
-            if (gy0 + y + 1 < Hg) d += (gc + g[GS]) * (c[US] - uv);
-            if (gy0 + y > 0) d -= (g[-GS] + gc) * (uv - c[-US]);
+    for (int k = 0; k < 2; ++k) {
+        const int ty = ty0 + k;
+        const int y = y0 + ty;
+        if (y >= H) break;
+#pragma unroll
+        for (int r = 0; r < PJ; ++r) {
+            const int tx = cx + 16 * r;
+            const int x = x0 + tx;
+            if (x >= W) continue;
+            const T *c = su + (ty + 2) * PS + (tx + 2);
+            const T uv = c[0];
+            T d = T(0);
+            if (a.has_d) {
+                const T *g = sg + (ty + 1) * PS + (tx + 1);
+                const T gc = g[0];
+                if (x + 1 < W) d += (gc + g[1]) * (c[1] - uv);
+                if (x > 0) d -= (g[-1] + gc) * (uv - c[-1]);
+                if (gy0 + y + 1 < Hg) d += (gc + g[PS]) * (c[PS] - uv);
+                if (gy0 + y > 0) d -= (g[-PS] + gc) * (uv - c[-PS]);
+            }
+            T nm = num[k][r];
+            T dn = ROBUST ? den[k][r] : T(1);
+            if (a.has_d) {
+                nm += alpha * (d > T(0) ? d : T(0));
+                dn -= alpha * (d < T(0) ? d : T(0));
+            } else if (!ROBUST) {
+                uo[(int64_t)y * W + x] = uv * nm;
+                continue;
+            }
+            dn = dn > T(kGuard) ? dn : T(kGuard);
+            uo[(int64_t)y * W + x] = (uv * nm) * frcp(dn);
         }
-        T nm = num[r];
-        T dn = ROBUST ? den[r] : T(1);
-        if (a.has_d) {
-            nm += alpha * (d > T(0) ? d : T(0));
-            dn -= alpha * (d < T(0) ? d : T(0));
-        } else if (!ROBUST) {
-            uo[(int64_t)y * W + x] = uv * nm;
-            continue;
-        }
-        dn = dn > T(kGuard) ? dn : T(kGuard);
-        uo[(int64_t)y * W + x] = (uv * nm) * frcp(dn);
     }
 }
 
 // ---------------------------------------------------------------------------------- host
 
-bool plane_fast_supported(const PlaneHalo &hb, const PlaneHalo &ha, int dtype) {
-    if (hb.nt > kPlaneMaxTaps || ha.nt > kPlaneMaxTaps) return false;
-    const size_t es = dtype == 0 ? 8 : 4;
-    const size_t sa = (size_t)(FY + ha.ht + ha.hb) * (FX + ha.hl + ha.hr + 1);
-    const size_t need = (2 * sa + (FY + 4) * (FX + 5) + (FY + 2) * (FX + 3)) * es;
-    return need <= 200 * 1024;
+static size_t smem_a(const PlaneHalo &hb, size_t es, int ssa) { return (size_t)(FY + hb.ht + hb.hb) * ssa * es; }
+static size_t smem_b(const PlaneHalo &ha, size_t es, int ssb) {
+    return (size_t)(FY + ha.ht + ha.hb) * ssb * 2 * es + (size_t)(2 * FY + 6) * PS * es;
 }
 
-template <typename T, int MAXT>
-static void fill_fast_taps(FastTaps<T, MAXT> &ft, const std::vector<PlaneTap> &taps, int ss) {
-    ft.nt = (int)taps.size();
-    for (int t = 0; t < ft.nt; ++t) {
-        ft.off[t] = taps[t].dy * ss + taps[t].dx;
-        ft.w[t] = T(taps[t].w);
-    }
+bool plane_fast_supported(const PlaneHalo &hb, const PlaneHalo &ha, const std::vector<PlaneTap> &taps_blur,
+                          const std::vector<PlaneTap> &taps_adj, int dtype) {
+    if (hb.nt > kPlaneMaxTaps || ha.nt > kPlaneMaxTaps) return false;
+    const size_t es = dtype == 0 ? 8 : 4;
+    const int ssa = dtype == 0 ? pf_stride_a<double>(hb) : pf_stride_a<float>(hb);
+    const int ssb = dtype == 0 ? pf_stride_b<double>(ha) : pf_stride_b<float>(ha);
+    if (smem_a(hb, es, ssa) > 200 * 1024 || smem_b(ha, es, ssb) > 200 * 1024) return false;
+    return dtype == 0 ? build_col_taps<double>(taps_blur, ssa, nullptr) && build_col_taps<double>(taps_adj, ssb, nullptr)
+                      : build_col_taps<float>(taps_blur, ssa, nullptr) && build_col_taps<float>(taps_adj, ssb, nullptr);
 }
 
 template <typename T>
 cudaError_t launch_plane_fast(const PlaneFastDesc &d, bool robust, int64_t batch, cudaStream_t st) {
-    constexpr int MAXT = kPlaneMaxTaps;
-    PlaneFastArgs<T, MAXT> a{};
+    PlaneFastArgs<T> a{};
     a.u = static_cast<const T *>(d.u);
     a.f = static_cast<const T *>(d.f);
     a.p = static_cast<T *>(d.p);
@@ -236,21 +225,21 @@ cudaError_t launch_plane_fast(const PlaneFastDesc &d, bool robust, int64_t batch
     a.H = d.H; a.W = d.W; a.periodic = d.periodic;
     a.slab = d.slab; a.gy0 = d.slab ? d.gy0 : 0; a.Hg = d.slab ? d.Hg : d.H;
     a.hb = d.hb; a.ha = d.ha;
-    fill_fast_taps<T, MAXT>(a.tb, *d.taps_blur, FX + d.hb.hl + d.hb.hr + 1);
-    fill_fast_taps<T, MAXT>(a.ta, *d.taps_adj, FX + d.ha.hl + d.ha.hr + 1);
+    a.ssa = pf_stride_a<T>(d.hb);
+    a.ssb = pf_stride_b<T>(d.ha);
+    if (!build_col_taps<T>(*d.taps_blur, a.ssa, &a.tb) || !build_col_taps<T>(*d.taps_adj, a.ssb, &a.ta))
+        return cudaErrorNotSupported;
     a.alpha = T(d.alpha); a.eps_d2 = T(d.eps_d2); a.eps_r2 = T(d.eps_r2); a.has_d = d.has_d;
     a.lut = d.lut;
-    const size_t sa = (size_t)(FY + d.hb.ht + d.hb.hb) * (FX + d.hb.hl + d.hb.hr + 1) * sizeof(T);
-    const size_t tb = (size_t)(FY + d.ha.ht + d.ha.hb) * (FX + d.ha.hl + d.ha.hr + 1);
-    const size_t sb = ((robust ? 2 : 1) * tb + (FY + 4) * (FX + 5) + (FY + 2) * (FX + 3)) * sizeof(T);
-    auto ka = robust ? k_plane_a_fast<T, MAXT, true> : k_plane_a_fast<T, MAXT, false>;
-    auto kb = robust ? k_plane_b_fast<T, MAXT, true> : k_plane_b_fast<T, MAXT, false>;
+    const size_t sa = smem_a(d.hb, sizeof(T), a.ssa), sb = smem_b(d.ha, sizeof(T), a.ssb);
+    auto ka = robust ? k_plane_a_fast<T, true> : k_plane_a_fast<T, false>;
+    auto kb = robust ? k_plane_b_fast<T, true> : k_plane_b_fast<T, false>;
     cudaError_t e = cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sa);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
     if (e != cudaSuccess) return e;
     if (d.slab) {
         // stage A over the extended rows [row_a0, row_a0 + rows_a), stage B over the own rows
-        PlaneFastArgs<T, MAXT> aa = a;
+        PlaneFastArgs<T> aa = a;
         const int64_t off = (int64_t)d.row_a0 * d.W;
         aa.u += off; aa.f += off; aa.p += off; aa.w += off;
         aa.H = d.rows_a; aa.gy0 = d.gy0 + d.row_a0;
@@ -261,7 +250,7 @@ cudaError_t launch_plane_fast(const PlaneFastDesc &d, bool robust, int64_t batch
     const int64_t fsz = (int64_t)d.H * d.W;
     for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
         const int nb = (int)((batch - b0) < 65535 ? (batch - b0) : 65535);
-        PlaneFastArgs<T, MAXT> ab = a;
+        PlaneFastArgs<T> ab = a;
         ab.u += b0 * fsz; ab.f += b0 * fsz; ab.p += b0 * fsz; ab.w += b0 * fsz; ab.u_out += b0 * fsz;
         const dim3 grid((d.W + FX - 1) / FX, (d.H + FY - 1) / FY, nb);
         ka<<<grid, 256, sa, st>>>(ab);

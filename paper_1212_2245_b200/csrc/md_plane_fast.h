@@ -3,25 +3,20 @@
 
 #include <vector>
 
-#include "md_plane.h"
+#include "md_coltaps.cuh"
 
 namespace md {
 
 constexpr int kPlaneMaxTaps = 128;
 
-template <typename T, int MAXT> struct FastTaps {
-    int nt;
-    int off[MAXT];      // dy * tile_stride + dx
-    T w[MAXT];
-};
-
-template <typename T, int MAXT> struct PlaneFastArgs {
+template <typename T> struct PlaneFastArgs {
     const T *u, *f;     // iterate, floored observation
     T *p, *w, *u_out;
     int H, W, periodic;
     int slab, gy0, Hg;  // slab mode: rows read directly (halo present); global row of row 0; global height
     PlaneHalo hb, ha;
-    FastTaps<T, MAXT> tb, ta;
+    int ssa, ssb;       // shared row strides of the stage-A u tile and the stage-B (p, W) tile
+    ColTaps<T> tb, ta;  // column-grouped taps for those strides
     T alpha, eps_d2, eps_r2;
     int has_d;
     LutView lut;
@@ -40,7 +35,8 @@ struct PlaneFastDesc {
     LutView lut;
 };
 
-bool plane_fast_supported(const PlaneHalo &hb, const PlaneHalo &ha, int dtype);
+bool plane_fast_supported(const PlaneHalo &hb, const PlaneHalo &ha, const std::vector<PlaneTap> &taps_blur,
+                          const std::vector<PlaneTap> &taps_adj, int dtype);
 template <typename T> cudaError_t launch_plane_fast(const PlaneFastDesc &, bool robust, int64_t, cudaStream_t);
 
 }  // namespace md
