@@ -33,17 +33,35 @@ k_subfft(SubFftArgs a) {
     const T *rb = a.rb ? static_cast<const T *>(a.rb) + fr * a.rframe : nullptr;
     const int64_t base = (int64_t)ai * a.sa + (int64_t)b0 * a.sb;
     const bool line_fast = a.es == 1;          // contiguous lines: iterate along the line
-    for (int idx = threadIdx.x; idx < G * L; idx += blockDim.x) {
-        int g, e;
+    constexpr int U = 4;                       // global loads in flight per thread
+    const int n = G * L, bd = blockDim.x;
+    const int lg = 31 - __clz(G);              // G is a power of two
+    auto coords = [&](int idx, int &g, int &e) {
         if (line_fast) { g = idx >> a.log2L; e = idx & (L - 1); }
-        else { e = idx / G; g = idx - e * G; }
-        C v = mkc<T>(T(0), T(0));
-        if (b0 + g < a.B) {
-            const int64_t o = base + (int64_t)g * a.sb + (int64_t)e * a.es;
-            if (ra) v = mkc<T>(ra[o], rb ? rb[o] : T(0));
-            else v = z[o];
+        else { e = idx >> lg; g = idx & (G - 1); }
+    };
+    for (int i0 = threadIdx.x; i0 < n; i0 += U * bd) {
+        C v[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const int idx = i0 + k * bd;
+            int g, e;
+            coords(idx, g, e);
+            v[k] = mkc<T>(T(0), T(0));
+            if (idx < n && b0 + g < a.B) {
+                const int64_t o = base + (int64_t)g * a.sb + (int64_t)e * a.es;
+                if (ra) v[k] = mkc<T>(ra[o], rb ? rb[o] : T(0));
+                else v[k] = z[o];
+            }
         }
-        s[g * ls + e] = v;
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const int idx = i0 + k * bd;
+            if (idx >= n) break;
+            int g, e;
+            coords(idx, g, e);
+            s[g * ls + e] = v[k];
+        }
     }
     __syncthreads();
     const C *twL = static_cast<const C *>(a.twL);
@@ -54,26 +72,39 @@ k_subfft(SubFftArgs a) {
     const int N = a.N;
     const C *filt = static_cast<const C *>(a.filt);
     const T scale = T(a.scale);
-    for (int idx = threadIdx.x; idx < G * L; idx += blockDim.x) {
-        int g, e;
-        if (line_fast) { g = idx >> a.log2L; e = idx & (L - 1); }
-        else { e = idx / G; g = idx - e * G; }
-        if (b0 + g >= a.B) continue;
-        C v = s[g * ls + e];
-        if (a.tw_mode != TW_NONE) {
-            const int lb = a.tw_digit_is_a ? ai : b0 + g;                 // line digit
-            const int re = (int)(__brev((unsigned)e) >> (32 - a.log2L));   // rev(pos) in the line
-            const int rl = (int)(__brev((unsigned)lb) >> (32 - a.log2Lother));
-            // FWD (after F1): W_N^{line * rev(e)};  INV (after I2): conj W_N^{e * rev(line)}
-            const int k = a.tw_mode == TW_FWD ? (int)(((int64_t)lb * re) & (N - 1)) : (int)(((int64_t)e * rl) & (N - 1));
-            const C w = twN[k & (N / 2 - 1)];
-            const C ww = k < N / 2 ? w : mkc<T>(-w.x, -w.y);
-            v = a.tw_mode == TW_FWD ? cmul(v, ww) : cmulc(v, ww);
+    for (int i0 = threadIdx.x; i0 < n; i0 += U * bd) {
+        // table and filter operands first: loads after the z stores below would wait on them
+        C tw[U], fl[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const int idx = i0 + k * bd;
+            int g, e;
+            coords(idx, g, e);
+            tw[k] = fl[k] = mkc<T>(T(1), T(0));
+            if (idx >= n || b0 + g >= a.B) continue;
+            if (a.tw_mode != TW_NONE) {
+                const int lb = a.tw_digit_is_a ? ai : b0 + g;                 // line digit
+                const int re = (int)(__brev((unsigned)e) >> (32 - a.log2L));   // rev(pos) in the line
+                const int rl = (int)(__brev((unsigned)lb) >> (32 - a.log2Lother));
+                // FWD (after F1): W_N^{line * rev(e)};  INV (after I2): conj W_N^{e * rev(line)}
+                const int kk = a.tw_mode == TW_FWD ? (int)(((int64_t)lb * re) & (N - 1)) : (int)(((int64_t)e * rl) & (N - 1));
+                const C w = twN[kk & (N / 2 - 1)];
+                tw[k] = kk < N / 2 ? w : mkc<T>(-w.x, -w.y);
+            }
+            if (filt) fl[k] = filt[base + (int64_t)g * a.sb + (int64_t)e * a.es];
         }
-        const int64_t o = base + (int64_t)g * a.sb + (int64_t)e * a.es;
-        if (filt) v = a.conj_filt ? cmulc(v, filt[o]) : cmul(v, filt[o]);
-        if (scale != T(1)) v = cscale(v, scale);
-        z[o] = v;
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const int idx = i0 + k * bd;
+            int g, e;
+            coords(idx, g, e);
+            if (idx >= n || b0 + g >= a.B) continue;
+            C v = s[g * ls + e];
+            if (a.tw_mode != TW_NONE) v = a.tw_mode == TW_FWD ? cmul(v, tw[k]) : cmulc(v, tw[k]);
+            if (filt) v = a.conj_filt ? cmulc(v, fl[k]) : cmul(v, fl[k]);
+            if (scale != T(1)) v = cscale(v, scale);
+            z[base + (int64_t)g * a.sb + (int64_t)e * a.es] = v;
+        }
     }
 }
 
@@ -97,7 +128,7 @@ template <typename T>
 cudaError_t launch_subfft(const SubFftArgs &a0, int64_t batch, cudaStream_t st) {
     SubFftArgs a = a0;
     const int L = 1 << a.log2L;
-    a.G = std::max(1, std::min(16, 2048 / L));
+    a.G = std::max(1, std::min(16, 2048 / L));   // power of two (L is)
     const size_t smem = (size_t)a.G * (L + 1) * sizeof(cx_t<T>);
     cudaError_t e = cudaFuncSetAttribute(k_subfft<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
