@@ -58,7 +58,12 @@ k_fft2_rows(Fft2Args a, int rb) {
     const int ne = rb * W;
     const int bd = blockDim.x;
     C *z = static_cast<C *>(a.z);
-    const C *tw = static_cast<const C *>(a.twW);
+    // twiddles staged in shared memory behind the rows: the butterflies read them every stage
+    C *tw = s + ne;
+    {
+        const C *twg = static_cast<const C *>(a.twW);
+        for (int k = threadIdx.x; k < (W >> 1); k += blockDim.x) tw[k] = twg[k];
+    }
 
     if (a.load == R_LOAD_COMPLEX) {
         for (int i0 = threadIdx.x; i0 < ne; i0 += U * bd) {
@@ -175,7 +180,11 @@ k_fft2_cols(Fft2Args a, int cw) {
     const int x0 = blockIdx.x * cw;
     const int64_t base = blockIdx.y * (int64_t)H * W;
     C *z = static_cast<C *>(a.z);
-    const C *tw = static_cast<const C *>(a.twH);
+    C *tw = s + cw * cs;                              // staged twiddles (see k_fft2_rows)
+    {
+        const C *twg = static_cast<const C *>(a.twH);
+        for (int k = threadIdx.x; k < (H >> 1); k += blockDim.x) tw[k] = twg[k];
+    }
     for (int idx = threadIdx.x; idx < cw * H; idx += blockDim.x) {
         const int y = idx / cw, c = idx - y * cw;
         if (x0 + c < W) s[c * cs + y] = z[base + (int64_t)y * W + x0 + c];
@@ -204,7 +213,7 @@ template <typename T>
 cudaError_t launch_fft2_rows(const Fft2Args &a, int64_t batch, cudaStream_t st) {
     int rb = 2048 / a.W;                      // ~2048 elements per block
     rb = rb < 1 ? 1 : (rb > a.H ? a.H : rb);
-    const size_t smem = (size_t)rb * a.W * sizeof(cx_t<T>);
+    const size_t smem = ((size_t)rb * a.W + a.W / 2 + 1) * sizeof(cx_t<T>);
     cudaError_t e = cudaFuncSetAttribute(k_fft2_rows<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     // `batch` counts complex fields; with pairing the real pointers advance two frames per field
@@ -233,7 +242,7 @@ template <typename T>
 cudaError_t launch_fft2_cols(const Fft2Args &a, int64_t batch, cudaStream_t st) {
     int cw = 4096 / a.H;
     cw = cw > 16 ? 16 : (cw < 1 ? 1 : cw);
-    const size_t smem = (size_t)cw * (a.H + 1) * sizeof(cx_t<T>);
+    const size_t smem = ((size_t)cw * (a.H + 1) + a.H / 2 + 1) * sizeof(cx_t<T>);
     cudaError_t e = cudaFuncSetAttribute(k_fft2_cols<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int64_t fr = (int64_t)a.H * a.W;

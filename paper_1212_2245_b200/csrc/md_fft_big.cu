@@ -63,8 +63,9 @@ k_subfft(SubFftArgs a) {
             s[g * ls + e] = v[k];
         }
     }
+    C *twL = s + G * ls;                       // sub-transform twiddles staged in shared memory
+    for (int k = threadIdx.x; k < (L >> 1); k += bd) twL[k] = static_cast<const C *>(a.twL)[k];
     __syncthreads();
-    const C *twL = static_cast<const C *>(a.twL);
     if (a.inv) fft_dit_inv_lines(s, a.log2L, G, ls, twL);
     else fft_dif_lines(s, a.log2L, G, ls, twL);
     // inter-pass twiddle W_N^{+-(digit * rev(pos))}, digit = line (FWD) or element (INV) index
@@ -129,7 +130,7 @@ cudaError_t launch_subfft(const SubFftArgs &a0, int64_t batch, cudaStream_t st) 
     SubFftArgs a = a0;
     const int L = 1 << a.log2L;
     a.G = std::max(1, std::min(16, 2048 / L));   // power of two (L is)
-    const size_t smem = (size_t)a.G * (L + 1) * sizeof(cx_t<T>);
+    const size_t smem = ((size_t)a.G * (L + 1) + L / 2 + 1) * sizeof(cx_t<T>);
     cudaError_t e = cudaFuncSetAttribute(k_subfft<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int blocks_b = (a.B + a.G - 1) / a.G;
