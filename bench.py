@@ -105,6 +105,10 @@ class C1:
     def run(self, f, u):
         self.pipe.plan.run(f, out=u)
 
+    @staticmethod
+    def e2e_entry(src, dst) -> str:
+        return f"DeblurPipeline.run_batch({src}) -> {dst} (md_run_host_ex, copies pipelined over 3 streams)"
+
     def run_profile(self, f, u) -> dict:
         return self.pipe.plan.run_profile(f, out=u)
 
@@ -196,8 +200,12 @@ class C4:
         return self.host[sel], self.index[sel]
 
     def run_host(self, hin, hout, ctx):
-        for b, s, e in self.pipe.groups(ctx):
-            self.pipe.pipes[b].run_batch(hin[s:e], out=hout[s:e])
+        self.pipe.run_host(hin, ctx, out=hout)
+
+    @staticmethod
+    def e2e_entry(src, dst) -> str:
+        return (f"PsfBankPipeline.run_host({src}) -> {dst} (copies of PSF group g+1 / g-1 overlap the "
+                "deconvolution of group g: 3 streams, md_convert + md_run per group)")
 
     def launches(self, n) -> int:
         return self.pipe.launch_count(self.index[:n])
@@ -566,11 +574,10 @@ def main() -> None:
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": e2e_in,
                     "d2h_bytes_per_step": e2e_out, "frames_per_step": nb,
-                    "entry": "DeblurPipeline.run_batch(pinned uint8 frames) -> float32 results "
-                             "(md_run_host_ex, copies pipelined over 3 streams)"},
+                    "entry": work.e2e_entry("pinned uint8 frames", "float32 results")},
             "e2e_f64": {"value": e2e64_value, "unit": "frames/s", "h2d_bytes_per_step": e2e64_in,
                         "d2h_bytes_per_step": e2e64_out, "frames_per_step": nb64,
-                        "entry": "DeblurPipeline.run_batch(pinned float64) -> float64 (drop-in Image semantics)"},
+                        "entry": work.e2e_entry("pinned float64 frames", "float64 (drop-in Image semantics)")},
             "gpu_launches": work.launches(args.batch) * args.steps,
             "clocks": clk.summary(),
         }

@@ -124,6 +124,10 @@ int32_t md_run_profile(md_plan *plan, const void *f, void *u, int64_t batch, voi
  * chunk c-1); pinned host buffers make the copies asynchronous. Synchronises `stream`. */
 int32_t md_run_host_ex(md_plan *plan, const void *f, int32_t in_type, void *u, int32_t out_type,
                        int64_t batch, void *stream);
+/* element type conversion of n DEVICE values on `stream` (no sync): in_type any MD_IO_*,
+ * out_type MD_IO_F32 or MD_IO_F64 -- the device half of the host entries, exported for callers
+ * that stage their own copies (e.g. a PSF bank pipelining several plans) */
+int32_t md_convert(const void *in, int32_t in_type, void *out, int32_t out_type, int64_t n, void *stream);
 /* md_run with one CUDA event per launch group: group_ms[i] / group_kind[i] (0 init, 1 iteration
  * kernel(s), 2 layout) for i < *n_groups; the fused kernel is one group for all iterations */
 int32_t md_run_profile_groups(md_plan *plan, const void *f, void *u, int64_t batch, void *stream,

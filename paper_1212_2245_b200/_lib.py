@@ -65,6 +65,7 @@ SIGNATURES = {
     "md_run": (_I32, [_P, _P, _P, _I64, _P]),
     "md_run_host": (_I32, [_P, _P, _P, _I64, _P]),
     "md_run_host_ex": (_I32, [_P, _P, _I32, _P, _I32, _I64, _P]),
+    "md_convert": (_I32, [_P, _I32, _P, _I32, _I64, _P]),
     "md_run_launch_count": (_I32, [_P, _I64]),
     "md_run_profile": (_I32, [_P, _P, _P, _I64, _P, ctypes.POINTER(_D)]),
     "md_run_profile_groups": (_I32, [_P, _P, _P, _I64, _P, ctypes.POINTER(_D), ctypes.POINTER(_I32), _I32,

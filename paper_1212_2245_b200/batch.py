@@ -65,6 +65,78 @@ class PsfBankPipeline:
         res[torch.from_numpy(order).to(frames.device)] = dst
         return res
 
+    def run_host(self, frames, psf_index, out=None, out_dtype=np.float32, max_piece: int = 512):
+        """Host frames (uint8 / float32 / float64 ``[N, H, W]``) -> host results, pipelined across
+        PSF groups: the host->device copy of group g+1 and the device->host copy of group g-1
+        overlap the deconvolution of group g (three CUDA streams, events between them). Pinned
+        (page-locked) host arrays make the copies asynchronous."""
+        import torch
+        from .plan import convert_dev, torch_dtype
+        a = np.asarray(frames)
+        idx = np.asarray(psf_index, dtype=np.int64)
+        if a.ndim != 3 or a.shape[1:] != self.shape or a.shape[0] != idx.size:
+            raise ValueError(f"frames must be [N, {self.shape[0]}, {self.shape[1]}] with one PSF index each")
+        if a.dtype not in (np.uint8, np.float32, np.float64):
+            a = a.astype(np.float64)
+        if idx.size and (idx.min() < 0 or idx.max() >= len(self.pipes)):
+            raise ValueError("PSF index out of range")
+        order = np.argsort(idx, kind="stable")
+        sorted_already = bool(np.all(order == np.arange(idx.size)))
+        if not sorted_already:
+            a, idx = a[order], idx[order]
+        a = np.ascontiguousarray(a)
+        n = a.shape[0]
+        res = np.empty(a.shape, dtype=out_dtype) if (out is None or not sorted_already) else out
+        if res.dtype not in (np.float32, np.float64) or res.shape != a.shape or not res.flags.c_contiguous:
+            raise ValueError("out must be a C-contiguous float32/float64 array of the frames' shape")
+        pdt = torch_dtype(self.pipes[0].dtype)
+        odt = torch.from_numpy(np.zeros(1, res.dtype)).dtype
+        key = (n, a.dtype.str, res.dtype.str)
+        if getattr(self, "_host_key", None) != key:         # device staging, reused across calls
+            hin_t = torch.from_numpy(a[:1]).dtype
+            dev = torch.device("cuda")
+            self._dbuf = {"in": torch.empty(a.shape, dtype=hin_t, device=dev),
+                          "f": torch.empty(a.shape, dtype=pdt, device=dev),
+                          "u": torch.empty(a.shape, dtype=pdt, device=dev),
+                          "o": torch.empty(a.shape, dtype=odt, device=dev) if odt != pdt else None}
+            self._streams = [torch.cuda.Stream() for _ in range(3)]
+            self._host_key = key
+        d = self._dbuf
+        h2d, cmp, d2h = self._streams
+        hin, hout = torch.from_numpy(a), torch.from_numpy(res)
+        din = d["in"]
+        dfin = din if din.dtype == pdt else d["f"]
+        dres = d["o"] if d["o"] is not None else d["u"]
+        pieces = []
+        for b, s, e in self.groups(idx):
+            for p0 in range(s, e, max_piece):
+                pieces.append((b, p0, min(e, p0 + max_piece)))
+        cur = torch.cuda.current_stream()
+        for st in (h2d, cmp, d2h):
+            st.wait_stream(cur)
+        for b, s, e in pieces:
+            with torch.cuda.stream(h2d):
+                din[s:e].copy_(hin[s:e], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(h2d)
+            cmp.wait_event(ev)
+            if dfin is not din:
+                convert_dev(din[s:e], dfin[s:e], stream=cmp)
+            self.pipes[b].plan.run(dfin[s:e], out=d["u"][s:e], stream=cmp)
+            if dres is not d["u"]:
+                convert_dev(d["u"][s:e], dres[s:e], stream=cmp)
+            ev = torch.cuda.Event()
+            ev.record(cmp)
+            d2h.wait_event(ev)
+            with torch.cuda.stream(d2h):
+                hout[s:e].copy_(dres[s:e], non_blocking=True)
+        d2h.synchronize()
+        if sorted_already:
+            return res
+        dst = np.empty(res.shape, dtype=res.dtype) if out is None else out
+        dst[order] = res
+        return dst
+
     def launch_count(self, psf_index) -> int:
         idx = np.sort(np.asarray(psf_index))
         return sum(self.pipes[b].plan.launch_count(e - s) for b, s, e in self.groups(idx))

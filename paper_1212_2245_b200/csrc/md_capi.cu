@@ -981,6 +981,17 @@ int32_t md_run_host_ex(md_plan *P, const void *f, int32_t in_type, void *u, int3
     return MD_OK;
 }
 
+int32_t md_convert(const void *in, int32_t in_type, void *out, int32_t out_type, int64_t n, void *stream) {
+    if (!in || !out || n < 0) return fail(MD_EINVAL, "bad arguments");
+    if (in_type != MD_IO_F64 && in_type != MD_IO_F32 && in_type != MD_IO_U8) return fail(MD_EINVAL, "bad input type");
+    if (out_type != MD_IO_F64 && out_type != MD_IO_F32) return fail(MD_EINVAL, "bad output type");
+    if (n == 0) return MD_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    CU(out_type == MD_IO_F64 ? launch_convert_in<double>(in, in_type, out, n, st)
+                             : launch_convert_in<float>(in, in_type, out, n, st));
+    return MD_OK;
+}
+
 int32_t md_run_host(md_plan *P, const double *f, double *u, int64_t batch, void *stream) {
     return md_run_host_ex(P, f, MD_IO_F64, u, MD_IO_F64, batch, stream);
 }

@@ -218,6 +218,20 @@ def device_min(t, stream=None) -> float:
     return out.value
 
 
+def convert_dev(src, dst, stream=None):
+    """Element type conversion of device tensors (uint8 / float32 / float64 -> float32 / float64)
+    by the library's conversion kernel (md_convert), on `stream`, without synchronising."""
+    import torch
+    io = {torch.float64: L.MD_IO_F64, torch.float32: L.MD_IO_F32, torch.uint8: L.MD_IO_U8}
+    if src.numel() != dst.numel() or not src.is_contiguous() or not dst.is_contiguous():
+        raise ValueError("convert_dev needs contiguous tensors of equal size")
+    if src.dtype not in io or dst.dtype not in (torch.float32, torch.float64):
+        raise TypeError(f"unsupported conversion {src.dtype} -> {dst.dtype}")
+    L.check(L.lib().md_convert(src.data_ptr(), io[src.dtype], dst.data_ptr(), io[dst.dtype], src.numel(),
+                               _stream_ptr(stream)))
+    return dst
+
+
 def guard_(t, stream=None):
     L.check(L.lib().md_guard(dtype_code(t), t.data_ptr(), t.numel(), _stream_ptr(stream)))
     return t

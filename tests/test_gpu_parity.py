@@ -463,3 +463,22 @@ def test_fused_plane_c4_line_frames_independent(md):
     ref = md.DeblurPipeline((256, 256), psf, md.DeconvParams(), md.Scenario.FOURIER_2D,
                             dtype="float64").run(md.Image(f)).values
     assert np.abs(out[0] - ref).max() <= TOL
+
+
+def test_psf_bank_host_entry_matches_device_run(md):
+    """PsfBankPipeline.run_host: unsorted uint8 / float64 host frames, pipelined per group,
+    equal to the device path."""
+    import torch
+    from paper_1212_2245_b200.batch import PsfBankPipeline
+    bank = [md.Psf.uniform_box(md.BlurAxis.VERTICAL, 7), md.Psf.general_1d([1, 2, 4, 2], md.BlurAxis.HORIZONTAL),
+            md.Psf.line(9.0, 75.0)]
+    pipe = PsfBankPipeline((64, 64), bank, md.DeconvParams(), dtype="float32")
+    rng = np.random.default_rng(2)
+    idx = rng.integers(0, 3, 23)
+    frames = rng.integers(20, 230, (23, 64, 64)).astype(np.uint8)
+    want = pipe.run(torch.from_numpy(frames.astype(np.float32)).cuda(), idx).cpu().numpy()
+    got = pipe.run_host(frames, idx, max_piece=4)
+    assert got.dtype == np.float32
+    np.testing.assert_array_equal(got, want)
+    got64 = pipe.run_host(frames.astype(np.float64), idx, out_dtype=np.float64)
+    np.testing.assert_array_equal(got64, want.astype(np.float64))
