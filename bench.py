@@ -533,6 +533,7 @@ def main() -> None:
     e2e_value, e2e_in, e2e_out = e2e_rate(np.uint8, np.float32, nb)
     nb64 = min(nb, 1024)
     e2e64_value, e2e64_in, e2e64_out = e2e_rate(np.float64, np.float64, nb64)
+    e2e8_value, e2e8_in, e2e8_out = e2e_rate(np.uint8, np.uint8, nb)
 
     if rank == 0:
         pk = peaks()
@@ -578,6 +579,10 @@ def main() -> None:
             "e2e_f64": {"value": e2e64_value, "unit": "frames/s", "h2d_bytes_per_step": e2e64_in,
                         "d2h_bytes_per_step": e2e64_out, "frames_per_step": nb64,
                         "entry": work.e2e_entry("pinned float64 frames", "float64 (drop-in Image semantics)")},
+            "e2e_u8": {"value": e2e8_value, "unit": "frames/s", "h2d_bytes_per_step": e2e8_in,
+                       "d2h_bytes_per_step": e2e8_out, "frames_per_step": nb,
+                       "entry": work.e2e_entry("pinned uint8 frames", "uint8 frames quantised like the "
+                                               "reference's write_pgm (pgm.py:56-58), the CLI's output")},
             "gpu_launches": work.launches(args.batch) * args.steps,
             "clocks": clk.summary(),
         }

@@ -118,15 +118,18 @@ int32_t md_run_profile(md_plan *plan, const void *f, void *u, int64_t batch, voi
 /* host frame types for md_run_host_ex */
 #define MD_IO_F64 0
 #define MD_IO_F32 1
-#define MD_IO_U8 2    /* 8-bit grey frames (camera / PGM capture), input only */
+#define MD_IO_U8 2    /* 8-bit grey frames (camera / PGM capture); as an OUTPUT type of
+                         md_run_host_ex: the reference's write_pgm quantisation
+                         clip(floor(u + 0.5), 0, 255) (pgm.py:56-58) */
 /* md_run from HOST frames of type in_type to HOST results of type out_type. Chunks are
  * pipelined over internal streams (H2D of chunk c+1 overlaps compute of chunk c and D2H of
  * chunk c-1); pinned host buffers make the copies asynchronous. Synchronises `stream`. */
 int32_t md_run_host_ex(md_plan *plan, const void *f, int32_t in_type, void *u, int32_t out_type,
                        int64_t batch, void *stream);
-/* element type conversion of n DEVICE values on `stream` (no sync): in_type any MD_IO_*,
- * out_type MD_IO_F32 or MD_IO_F64 -- the device half of the host entries, exported for callers
- * that stage their own copies (e.g. a PSF bank pipelining several plans) */
+/* element type conversion of n DEVICE values on `stream` (no sync): any MD_IO_* to float32 /
+ * float64, or float32 / float64 to MD_IO_U8 (write_pgm quantisation) -- the device half of the
+ * host entries, exported for callers that stage their own copies (e.g. a PSF bank pipelining
+ * several plans) */
 int32_t md_convert(const void *in, int32_t in_type, void *out, int32_t out_type, int64_t n, void *stream);
 /* md_run with one CUDA event per launch group: group_ms[i] / group_kind[i] (0 init, 1 iteration
  * kernel(s), 2 layout) for i < *n_groups; the fused kernel is one group for all iterations */

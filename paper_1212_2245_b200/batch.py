@@ -66,7 +66,8 @@ class PsfBankPipeline:
         return res
 
     def run_host(self, frames, psf_index, out=None, out_dtype=np.float32, max_piece: int = 512):
-        """Host frames (uint8 / float32 / float64 ``[N, H, W]``) -> host results, pipelined across
+        """Host frames (uint8 / float32 / float64 ``[N, H, W]``) -> host results (float32 / float64,
+        or uint8 with the reference's write_pgm quantisation), pipelined across
         PSF groups: the host->device copy of group g+1 and the device->host copy of group g-1
         overlap the deconvolution of group g (three CUDA streams, events between them). Pinned
         (page-locked) host arrays make the copies asynchronous."""
@@ -87,8 +88,8 @@ class PsfBankPipeline:
         a = np.ascontiguousarray(a)
         n = a.shape[0]
         res = np.empty(a.shape, dtype=out_dtype) if (out is None or not sorted_already) else out
-        if res.dtype not in (np.float32, np.float64) or res.shape != a.shape or not res.flags.c_contiguous:
-            raise ValueError("out must be a C-contiguous float32/float64 array of the frames' shape")
+        if res.dtype not in (np.float32, np.float64, np.uint8) or res.shape != a.shape or not res.flags.c_contiguous:
+            raise ValueError("out must be a C-contiguous float32/float64/uint8 array of the frames' shape")
         pdt = torch_dtype(self.pipes[0].dtype)
         odt = torch.from_numpy(np.zeros(1, res.dtype)).dtype
         key = (n, a.dtype.str, res.dtype.str)

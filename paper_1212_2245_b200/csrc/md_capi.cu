@@ -928,7 +928,8 @@ int32_t md_run_host_ex(md_plan *P, const void *f, int32_t in_type, void *u, int3
                        void *stream) {
     if (!P || !f || !u || batch < 0) return fail(MD_EINVAL, "bad arguments");
     if (in_type != MD_IO_F64 && in_type != MD_IO_F32 && in_type != MD_IO_U8) return fail(MD_EINVAL, "bad input type");
-    if (out_type != MD_IO_F64 && out_type != MD_IO_F32) return fail(MD_EINVAL, "bad output type");
+    if (out_type != MD_IO_F64 && out_type != MD_IO_F32 && out_type != MD_IO_U8)
+        return fail(MD_EINVAL, "bad output type");
     if (batch == 0) return MD_OK;
     cudaStream_t user = static_cast<cudaStream_t>(stream);
     const int64_t fe = P->frame_elems();
@@ -984,9 +985,16 @@ int32_t md_run_host_ex(md_plan *P, const void *f, int32_t in_type, void *u, int3
 int32_t md_convert(const void *in, int32_t in_type, void *out, int32_t out_type, int64_t n, void *stream) {
     if (!in || !out || n < 0) return fail(MD_EINVAL, "bad arguments");
     if (in_type != MD_IO_F64 && in_type != MD_IO_F32 && in_type != MD_IO_U8) return fail(MD_EINVAL, "bad input type");
-    if (out_type != MD_IO_F64 && out_type != MD_IO_F32) return fail(MD_EINVAL, "bad output type");
+    if (out_type != MD_IO_F64 && out_type != MD_IO_F32 && out_type != MD_IO_U8)
+        return fail(MD_EINVAL, "bad output type");
+    if (out_type == MD_IO_U8 && in_type == MD_IO_U8) return fail(MD_EINVAL, "uint8 -> uint8 is not a conversion");
     if (n == 0) return MD_OK;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (out_type == MD_IO_U8) {            // write_pgm quantisation of float results
+        CU(in_type == MD_IO_F64 ? launch_convert_out<double>(in, out, MD_IO_U8, n, st)
+                                : launch_convert_out<float>(in, out, MD_IO_U8, n, st));
+        return MD_OK;
+    }
     CU(out_type == MD_IO_F64 ? launch_convert_in<double>(in, in_type, out, n, st)
                              : launch_convert_in<float>(in, in_type, out, n, st));
     return MD_OK;

@@ -303,8 +303,16 @@ __global__ void k_convert_in(const void *__restrict__ in, int in_type, T *__rest
 template <typename T>
 __global__ void k_convert_out(const T *__restrict__ in, void *__restrict__ out, int out_type, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        if (out_type == 1) static_cast<float *>(out)[i] = (float)in[i];
-        else static_cast<double *>(out)[i] = (double)in[i];
+        if (out_type == 1) {
+            static_cast<float *>(out)[i] = (float)in[i];
+        } else if (out_type == 2) {
+            // 8-bit grey, the reference's write_pgm rule: clip(floor(v + 0.5), 0, 255) (pgm.py:56-58)
+            T v = floor(in[i] + T(0.5));
+            v = v < T(0) ? T(0) : (v > T(255) ? T(255) : v);
+            static_cast<unsigned char *>(out)[i] = (unsigned char)v;
+        } else {
+            static_cast<double *>(out)[i] = (double)in[i];
+        }
     }
 }
 

@@ -167,8 +167,9 @@ class GpuPlan:
             raise ValueError(f"plan prepared for shape {self.shape}, got {f.shape[-2:]}")
         n = 1 if f.ndim == 2 else int(np.prod(f.shape[:-2]))
         out = np.empty(f.shape, dtype=out_dtype) if out is None else out
-        if out.dtype not in (np.float32, np.float64) or out.shape != f.shape or not out.flags.c_contiguous:
-            raise ValueError("out must be a C-contiguous float32/float64 array of the input's shape")
+        if out.dtype not in (np.float32, np.float64, np.uint8) or out.shape != f.shape or not out.flags.c_contiguous:
+            raise ValueError("out must be a C-contiguous float32/float64/uint8 array of the input's shape "
+                             "(uint8: write_pgm quantisation)")
         L.check(self.lib.md_run_host_ex(self._h, f.ctypes.data, self._IO[f.dtype], out.ctypes.data,
                                         self._IO[out.dtype], n, _stream_ptr(stream)))
         return out
@@ -219,13 +220,14 @@ def device_min(t, stream=None) -> float:
 
 
 def convert_dev(src, dst, stream=None):
-    """Element type conversion of device tensors (uint8 / float32 / float64 -> float32 / float64)
-    by the library's conversion kernel (md_convert), on `stream`, without synchronising."""
+    """Element type conversion of device tensors (uint8 / float32 / float64 -> float32 / float64,
+    float -> uint8 with write_pgm quantisation) by the library's conversion kernel (md_convert),
+    on `stream`, without synchronising."""
     import torch
     io = {torch.float64: L.MD_IO_F64, torch.float32: L.MD_IO_F32, torch.uint8: L.MD_IO_U8}
     if src.numel() != dst.numel() or not src.is_contiguous() or not dst.is_contiguous():
         raise ValueError("convert_dev needs contiguous tensors of equal size")
-    if src.dtype not in io or dst.dtype not in (torch.float32, torch.float64):
+    if src.dtype not in io or dst.dtype not in io or (dst.dtype == torch.uint8 and src.dtype == torch.uint8):
         raise TypeError(f"unsupported conversion {src.dtype} -> {dst.dtype}")
     L.check(L.lib().md_convert(src.data_ptr(), io[src.dtype], dst.data_ptr(), io[dst.dtype], src.numel(),
                                _stream_ptr(stream)))

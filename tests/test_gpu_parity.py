@@ -482,3 +482,19 @@ def test_psf_bank_host_entry_matches_device_run(md):
     np.testing.assert_array_equal(got, want)
     got64 = pipe.run_host(frames.astype(np.float64), idx, out_dtype=np.float64)
     np.testing.assert_array_equal(got64, want.astype(np.float64))
+
+
+def test_host_entry_uint8_out_is_write_pgm_quantisation(md):
+    """uint8 results from the host entries follow the reference's write_pgm rounding."""
+    from paper_1212_2245_b200.batch import PsfBankPipeline
+    d = load_golden("pipe_c1_box_h15_256")
+    pipe = md.DeblurPipeline((256, 256), product_psf(d), product_params(d), dtype="float32")
+    rng = np.random.default_rng(8)
+    frames = np.stack([np.clip(d["f"] + rng.normal(0, 3, d["f"].shape), 0, 255).round() for _ in range(9)])
+    f32 = pipe.run_batch(frames.astype(np.uint8), out_dtype=np.float32)
+    u8 = pipe.run_batch(frames.astype(np.uint8), out_dtype=np.uint8)
+    # rounding evaluated in the plan's precision (float32), as the conversion kernel does
+    np.testing.assert_array_equal(u8, np.clip(np.floor(f32 + np.float32(0.5)), 0, 255).astype(np.uint8))
+    bank = PsfBankPipeline((256, 256), [product_psf(d)], product_params(d), dtype="float32")
+    b8 = bank.run_host(frames.astype(np.uint8), np.zeros(9, np.int64), out_dtype=np.uint8)
+    np.testing.assert_array_equal(b8, u8)
