@@ -26,15 +26,32 @@ __device__ __forceinline__ int pf_resolve(int k, int n, int periodic) {
     return k < 0 ? 0 : (k >= n ? n - 1 : k);
 }
 
-// tile rows [y0 - ht, y0 + FY + hb) x cols [x0 - hl, x0 + FX + hr) of one or two fields
+// tile rows [y0 - ht, y0 + FY + hb) x cols [x0 - hl, x0 + FX + hr) of one or two fields; U
+// global loads in flight per thread (a load-then-store loop would wait out each latency)
 template <typename T, typename E, typename Get>
 __device__ void pf_load(E *s, int ss, int H, int W, int y0, int x0, const PlaneHalo &h, int periodic, int slab,
                         Get get) {
+    constexpr int U = 4;
     const int rows = FY + h.ht + h.hb, cols = FX + h.hl + h.hr;
-    for (int i = threadIdx.x / 32; i < rows; i += blockDim.x / 32) {
-        // slab mode: the caller's buffer carries the neighbours' rows (halo), read them as is
-        const int y = slab ? y0 - h.ht + i : pf_resolve(y0 - h.ht + i, H, periodic);
-        for (int j = threadIdx.x & 31; j < cols; j += 32) s[i * ss + j] = get((int64_t)y * W + pf_resolve(x0 - h.hl + j, W, periodic));
+    const int n = rows * cols, bd = blockDim.x;
+    for (int i0 = threadIdx.x; i0 < n; i0 += U * bd) {
+        E v[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const int idx = i0 + k * bd;
+            if (idx >= n) break;
+            const int i = idx / cols, j = idx - i * cols;
+            // slab mode: the caller's buffer carries the neighbours' rows (halo), read them as is
+            const int y = slab ? y0 - h.ht + i : pf_resolve(y0 - h.ht + i, H, periodic);
+            v[k] = get((int64_t)y * W + pf_resolve(x0 - h.hl + j, W, periodic));
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const int idx = i0 + k * bd;
+            if (idx >= n) break;
+            const int i = idx / cols, j = idx - i * cols;
+            s[i * ss + j] = v[k];
+        }
     }
 }
 
@@ -124,12 +141,28 @@ k_plane_b_fast(PlaneFastArgs<T> a) {
         });
     }
     const int gy0 = a.gy0, Hg = a.Hg;
-    for (int i = threadIdx.x / 32; i < FY + 4; i += 8) {
-        const int yy = y0 - 2 + i;
-        const bool rok = gy0 + yy >= 0 && gy0 + yy < Hg && (a.slab || (yy >= 0 && yy < H));
-        for (int j = threadIdx.x & 31; j < FX + 4; j += 32) {
-            const int xx = x0 - 2 + j;
-            su[i * PS + j] = (rok && xx >= 0 && xx < W) ? u[(int64_t)yy * W + xx] : T(0);
+    {
+        constexpr int U = 4, UC = FX + 4;
+        const int n = (FY + 4) * UC, bd = blockDim.x;
+        for (int i0 = threadIdx.x; i0 < n; i0 += U * bd) {
+            T v[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const int idx = i0 + k * bd;
+                v[k] = T(0);
+                if (idx >= n) continue;
+                const int i = idx / UC, j = idx - i * UC;
+                const int yy = y0 - 2 + i, xx = x0 - 2 + j;
+                const bool rok = gy0 + yy >= 0 && gy0 + yy < Hg && (a.slab || (yy >= 0 && yy < H));
+                if (rok && xx >= 0 && xx < W) v[k] = u[(int64_t)yy * W + xx];
+            }
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const int idx = i0 + k * bd;
+                if (idx >= n) break;
+                const int i = idx / UC, j = idx - i * UC;
+                su[i * PS + j] = v[k];
+            }
         }
     }
     __syncthreads();
