@@ -206,6 +206,10 @@ k_fused_lines(FusedKArgs<T, R> a) {
             const bool act = s < nseg;
             const int off = base0 + 9 * s;
             if (act) {
+                // the observation of this warp's next line (next iteration's first line after the
+                // last) into L1 now, so its load below hits L1 instead of waiting on L2
+                const int ln = j + 1 < LPW ? li + FU_WARPS : warp;
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(fpos + (int64_t)(gl0 + ln) * n + SEG * s));
                 T fv[SEG];
                 if (sizeof(T) == 4) {
                     const float4 *f4 = reinterpret_cast<const float4 *>(F + SEG * s);

@@ -1,0 +1,4 @@
+timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -p no:cacheprovider -k "fused or golden" > gpurun_out/pytest_p.log 2>&1; echo "pytest rc=$?"
+tail -1 gpurun_out/pytest_p.log
+for i in 1 2; do timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value']), d['stage_ms_per_step'])"; done
+FP_FRAMES=1024 timeout 120 python scripts/fp_probe.py
