@@ -18,7 +18,9 @@
 
 namespace md {
 
-template <typename T>
+// LINE_FAST: contiguous lines (es == 1); TW: the inter-pass twiddle mode (TW_NONE / FWD / INV),
+// compile-time so that each pass carries only its own epilogue
+template <typename T, bool LINE_FAST, int TW>
 __global__ void __launch_bounds__(256)
 k_subfft(SubFftArgs a) {
     using C = cx_t<T>;
@@ -32,7 +34,7 @@ k_subfft(SubFftArgs a) {
     const T *ra = a.ra ? static_cast<const T *>(a.ra) + fr * a.rframe : nullptr;
     const T *rb = a.rb ? static_cast<const T *>(a.rb) + fr * a.rframe : nullptr;
     const int64_t base = (int64_t)ai * a.sa + (int64_t)b0 * a.sb;
-    const bool line_fast = a.es == 1;          // contiguous lines: iterate along the line
+    constexpr bool line_fast = LINE_FAST;      // contiguous lines: iterate along the line
     constexpr int U = 4;                       // global loads in flight per thread
     const int n = G * L, bd = blockDim.x;
     const int lg = 31 - __clz(G);              // G is a power of two
@@ -83,12 +85,12 @@ k_subfft(SubFftArgs a) {
             coords(idx, g, e);
             tw[k] = fl[k] = mkc<T>(T(1), T(0));
             if (idx >= n || b0 + g >= a.B) continue;
-            if (a.tw_mode != TW_NONE) {
+            if (TW != TW_NONE) {
                 const int lb = a.tw_digit_is_a ? ai : b0 + g;                 // line digit
                 const int re = (int)(__brev((unsigned)e) >> (32 - a.log2L));   // rev(pos) in the line
                 const int rl = (int)(__brev((unsigned)lb) >> (32 - a.log2Lother));
                 // FWD (after F1): W_N^{line * rev(e)};  INV (after I2): conj W_N^{e * rev(line)}
-                const int kk = a.tw_mode == TW_FWD ? (int)(((int64_t)lb * re) & (N - 1)) : (int)(((int64_t)e * rl) & (N - 1));
+                const int kk = TW == TW_FWD ? (int)(((int64_t)lb * re) & (N - 1)) : (int)(((int64_t)e * rl) & (N - 1));
                 const C w = twN[kk & (N / 2 - 1)];
                 tw[k] = kk < N / 2 ? w : mkc<T>(-w.x, -w.y);
             }
@@ -101,7 +103,7 @@ k_subfft(SubFftArgs a) {
             coords(idx, g, e);
             if (idx >= n || b0 + g >= a.B) continue;
             C v = s[g * ls + e];
-            if (a.tw_mode != TW_NONE) v = a.tw_mode == TW_FWD ? cmul(v, tw[k]) : cmulc(v, tw[k]);
+            if (TW != TW_NONE) v = TW == TW_FWD ? cmul(v, tw[k]) : cmulc(v, tw[k]);
             if (filt) v = a.conj_filt ? cmulc(v, fl[k]) : cmul(v, fl[k]);
             if (scale != T(1)) v = cscale(v, scale);
             z[base + (int64_t)g * a.sb + (int64_t)e * a.es] = v;
@@ -131,7 +133,13 @@ cudaError_t launch_subfft(const SubFftArgs &a0, int64_t batch, cudaStream_t st) 
     const int L = 1 << a.log2L;
     a.G = std::max(1, std::min(16, 2048 / L));   // power of two (L is)
     const size_t smem = ((size_t)a.G * (L + 1) + L / 2 + 1) * sizeof(cx_t<T>);
-    cudaError_t e = cudaFuncSetAttribute(k_subfft<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    auto pick = [&](auto lf) {
+        constexpr bool LF = decltype(lf)::value;
+        return a.tw_mode == TW_FWD ? k_subfft<T, LF, TW_FWD> : (a.tw_mode == TW_INV ? k_subfft<T, LF, TW_INV>
+                                                                                     : k_subfft<T, LF, TW_NONE>);
+    };
+    auto kern = a.es == 1 ? pick(std::true_type{}) : pick(std::false_type{});
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int blocks_b = (a.B + a.G - 1) / a.G;
     for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
@@ -140,7 +148,7 @@ cudaError_t launch_subfft(const SubFftArgs &a0, int64_t batch, cudaStream_t st) 
         ab.z = static_cast<char *>(a.z) + b0 * a.frame * (int64_t)sizeof(cx_t<T>);
         if (a.ra) ab.ra = static_cast<const char *>(a.ra) + b0 * a.rframe * (int64_t)sizeof(T);
         if (a.rb) ab.rb = static_cast<const char *>(a.rb) + b0 * a.rframe * (int64_t)sizeof(T);
-        k_subfft<T><<<dim3((unsigned)(a.A * blocks_b), nb), 256, smem, st>>>(ab);
+        kern<<<dim3((unsigned)(a.A * blocks_b), nb), 256, smem, st>>>(ab);
     }
     return cudaGetLastError();
 }
