@@ -58,8 +58,10 @@ k_fft2_rows(Fft2Args a, int rb) {
     const int ne = rb * W;
     const int bd = blockDim.x;
     C *z = static_cast<C *>(a.z);
+    const int LS = fpad_len(W);                       // padded row stride (md_fft.cuh)
+    auto sp = [&](int i) { return (i >> lw) * LS + fpad(i & (W - 1)); };
     // twiddles staged in shared memory behind the rows: the butterflies read them every stage
-    C *tw = s + ne;
+    C *tw = s + rb * LS;
     {
         const C *twg = static_cast<const C *>(a.twW);
         for (int k = threadIdx.x; k < (W >> 1); k += blockDim.x) tw[k] = twg[k];
@@ -71,7 +73,7 @@ k_fft2_rows(Fft2Args a, int rb) {
 #pragma unroll
             for (int k = 0; k < U; ++k) if (i0 + k * bd < ne) v[k] = z[base + i0 + k * bd];
 #pragma unroll
-            for (int k = 0; k < U; ++k) if (i0 + k * bd < ne) s[i0 + k * bd] = v[k];
+            for (int k = 0; k < U; ++k) if (i0 + k * bd < ne) s[sp(i0 + k * bd)] = v[k];
         }
     } else {
         const T *ra = static_cast<const T *>(a.ra);
@@ -87,11 +89,11 @@ k_fft2_rows(Fft2Args a, int rb) {
                 xb[k] = (i < ne && rbp) ? rbp[i] : T(0);
             }
 #pragma unroll
-            for (int k = 0; k < U; ++k) if (i0 + k * bd < ne) s[i0 + k * bd] = mkc<T>(xa[k], xb[k]);
+            for (int k = 0; k < U; ++k) if (i0 + k * bd < ne) s[sp(i0 + k * bd)] = mkc<T>(xa[k], xb[k]);
         }
     }
     __syncthreads();
-    if (a.inv && lw > 0) fft_dit_inv_lines(s, lw, rb, W, tw);
+    if (a.inv && lw > 0) fft_dit_inv_lines(s, lw, rb, LS, tw);
 
     const T scale = T(a.scale), floor = T(a.floor);
     if (a.epi != R_EPI_NONE) {
@@ -117,7 +119,7 @@ k_fft2_rows(Fft2Args a, int rb) {
             for (int k = 0; k < U; ++k) {
                 const int i = i0 + k * bd;
                 if (i >= ne) continue;
-                const C v = s[i];
+                const C v = s[sp(i)];
                 const int64_t o = base + i;
                 C packed = mkc<T>(T(0), T(0));
                 if (a.epi == R_EPI_STORE_PAIR) {
@@ -157,16 +159,16 @@ k_fft2_rows(Fft2Args a, int rb) {
                     static_cast<T *>(a.oa)[o] = un;
                     packed = mkc<T>(un, T(0));
                 }
-                s[i] = packed;
+                s[sp(i)] = packed;
             }
         }
         __syncthreads();
     }
     if (a.fwd_after) {
-        if (lw > 0) fft_dif_lines(s, lw, rb, W, tw);
-        for (int i = threadIdx.x; i < ne; i += blockDim.x) z[base + i] = s[i];
+        if (lw > 0) fft_dif_lines(s, lw, rb, LS, tw);
+        for (int i = threadIdx.x; i < ne; i += blockDim.x) z[base + i] = s[sp(i)];
     } else if (a.epi == R_EPI_NONE) {
-        for (int i = threadIdx.x; i < ne; i += blockDim.x) z[base + i] = s[i];
+        for (int i = threadIdx.x; i < ne; i += blockDim.x) z[base + i] = s[sp(i)];
     }
 }
 
@@ -176,7 +178,7 @@ k_fft2_cols(Fft2Args a, int cw) {
     using C = cx_t<T>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C *s = reinterpret_cast<C *>(smem_raw);
-    const int H = a.H, W = a.W, cs = H + 1;
+    const int H = a.H, W = a.W, cs = fline_stride(H);      // padded column stride (md_fft.cuh)
     const int x0 = blockIdx.x * cw;
     const int64_t base = blockIdx.y * (int64_t)H * W;
     C *z = static_cast<C *>(a.z);
@@ -187,8 +189,8 @@ k_fft2_cols(Fft2Args a, int cw) {
     }
     for (int idx = threadIdx.x; idx < cw * H; idx += blockDim.x) {
         const int y = idx / cw, c = idx - y * cw;
-        if (x0 + c < W) s[c * cs + y] = z[base + (int64_t)y * W + x0 + c];
-        else s[c * cs + y] = mkc<T>(T(0), T(0));
+        if (x0 + c < W) s[c * cs + fpad(y)] = z[base + (int64_t)y * W + x0 + c];
+        else s[c * cs + fpad(y)] = mkc<T>(T(0), T(0));
     }
     __syncthreads();
     if (a.log2H > 0) fft_dif_lines(s, a.log2H, cw, cs, tw);
@@ -198,14 +200,14 @@ k_fft2_cols(Fft2Args a, int cw) {
             const int c = idx / H, y = idx - c * H;
             if (x0 + c >= W) continue;
             const C f = __ldg(filt + (int64_t)y * W + x0 + c);
-            s[c * cs + y] = a.conj_filt ? cmulc(s[c * cs + y], f) : cmul(s[c * cs + y], f);
+            s[c * cs + fpad(y)] = a.conj_filt ? cmulc(s[c * cs + fpad(y)], f) : cmul(s[c * cs + fpad(y)], f);
         }
         __syncthreads();
     }
     if (a.col_inv && a.log2H > 0) fft_dit_inv_lines(s, a.log2H, cw, cs, tw);
     for (int idx = threadIdx.x; idx < cw * H; idx += blockDim.x) {
         const int y = idx / cw, c = idx - y * cw;
-        if (x0 + c < W) z[base + (int64_t)y * W + x0 + c] = s[c * cs + y];
+        if (x0 + c < W) z[base + (int64_t)y * W + x0 + c] = s[c * cs + fpad(y)];
     }
 }
 
@@ -213,7 +215,7 @@ template <typename T>
 cudaError_t launch_fft2_rows(const Fft2Args &a, int64_t batch, cudaStream_t st) {
     int rb = 2048 / a.W;                      // ~2048 elements per block
     rb = rb < 1 ? 1 : (rb > a.H ? a.H : rb);
-    const size_t smem = ((size_t)rb * a.W + a.W / 2 + 1) * sizeof(cx_t<T>);
+    const size_t smem = ((size_t)rb * fpad_len(a.W) + a.W / 2 + 1) * sizeof(cx_t<T>);
     cudaError_t e = cudaFuncSetAttribute(k_fft2_rows<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     // `batch` counts complex fields; with pairing the real pointers advance two frames per field
@@ -242,7 +244,7 @@ template <typename T>
 cudaError_t launch_fft2_cols(const Fft2Args &a, int64_t batch, cudaStream_t st) {
     int cw = 4096 / a.H;
     cw = cw > 16 ? 16 : (cw < 1 ? 1 : cw);
-    const size_t smem = ((size_t)cw * (a.H + 1) + a.H / 2 + 1) * sizeof(cx_t<T>);
+    const size_t smem = ((size_t)cw * fline_stride(a.H) + a.H / 2 + 1) * sizeof(cx_t<T>);
     cudaError_t e = cudaFuncSetAttribute(k_fft2_cols<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int64_t fr = (int64_t)a.H * a.W;
