@@ -1,42 +1,19 @@
-// md_fused_box_b -- symmetric-box specialisations of the fused kernel, radius 9..15.
+// md_fused_box_b -- box specialisations of the fused kernel, radius 9..15 (split over two
+// translation units to keep compile times short).
 #include "md_fused_kernel.cuh"
 
 namespace md {
 
-template <typename T, int RR, int LP>
-static cudaError_t go_lp(const FusedLinesArgs &d, int64_t batch, cudaStream_t st) {
-    FusedKArgs<T, RR> a{};
-    a.u0 = static_cast<const T *>(d.u_in);
-    a.fpos = static_cast<const T *>(d.fpos);
-    a.out = static_cast<T *>(d.u_out);
-    a.n = d.n; a.m = d.m; a.iterations = d.iterations; a.out_vert = d.out_vert;
-    a.periodic = d.blur.periodic;
-    a.cl = d.m / (8 * LP);
-    a.alpha = T(d.alpha); a.eps_d2 = T(d.eps_d2); a.eps_r2 = T(d.eps_r2); a.has_d = d.has_d;
-    a.lut = d.lut;
-    a.box_wi = T(d.blur.wi);
-    return launch_fused_t<T, RR, LP, RR>(a, true, batch, st);
-}
-
 template <typename T>
 cudaError_t launch_fused_box_partb(const FusedLinesArgs &d, int radius, int64_t batch, cudaStream_t st) {
-    const int lpw = fused_lpw(sizeof(T) == 8 ? 0 : 1);
-    auto go = [&](auto rtag) -> cudaError_t {
-        constexpr int RR = decltype(rtag)::value;
-        if constexpr (sizeof(T) == 8) {
-            return go_lp<T, RR, 2>(d, batch, st);
-        } else {
-            return lpw == 2 ? go_lp<T, RR, 2>(d, batch, st) : go_lp<T, RR, 4>(d, batch, st);
-        }
-    };
     switch (radius) {
-        case 9: return go(std::integral_constant<int, 9>{});
-        case 10: return go(std::integral_constant<int, 10>{});
-        case 11: return go(std::integral_constant<int, 11>{});
-        case 12: return go(std::integral_constant<int, 12>{});
-        case 13: return go(std::integral_constant<int, 13>{});
-        case 14: return go(std::integral_constant<int, 14>{});
-        case 15: return go(std::integral_constant<int, 15>{});
+        case 9: return launch_fused_box_lpw<T, 9>(d, batch, st);
+        case 10: return launch_fused_box_lpw<T, 10>(d, batch, st);
+        case 11: return launch_fused_box_lpw<T, 11>(d, batch, st);
+        case 12: return launch_fused_box_lpw<T, 12>(d, batch, st);
+        case 13: return launch_fused_box_lpw<T, 13>(d, batch, st);
+        case 14: return launch_fused_box_lpw<T, 14>(d, batch, st);
+        case 15: return launch_fused_box_lpw<T, 15>(d, batch, st);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -28,10 +28,12 @@ namespace cg = cooperative_groups;
 namespace md {
 
 // window convolution of 8 outputs: dense taps over [-R, R] (constant-bank FMAs), or, for a
-// symmetric integer box of radius BOXR (= R), an O(1)-per-output sliding sum
-template <typename T, int R, int BOXR>
+// box (equal interior weights) of radius BOXR (= R), an O(1)-per-output sliding sum over
+// [-R, R] plus weight corrections at k = -R, -R+1, R-1, R (even-length and fractional boxes:
+// deconv.py box convolver, conv.py:141-173)
+template <typename T, int R, int BOXR, bool BOXC>
 __device__ __forceinline__ void conv_window(const T (&v)[SEG + 2 * R], const DenseTaps<T, R> &taps, T box_wi,
-                                            T out[SEG]) {
+                                            const T (&corr)[4], T out[SEG]) {
     if constexpr (BOXR > 0) {
         static_assert(BOXR == R, "box window radius must equal the register window radius");
         // short dependency chains (few warps per scheduler): the first window by a pairwise
@@ -52,6 +54,11 @@ __device__ __forceinline__ void conv_window(const T (&v)[SEG + 2 * R], const Den
         for (int r = 1; r < SEG; ++r) {
             s += d[r];
             out[r] = s * box_wi;
+        }
+        if constexpr (BOXC) {
+#pragma unroll
+            for (int r = 0; r < SEG; ++r)
+                out[r] += corr[0] * v[r] + corr[1] * v[r + 1] + corr[2] * v[r + 2 * R - 1] + corr[3] * v[r + 2 * R];
         }
     } else {
 #pragma unroll
@@ -75,8 +82,27 @@ template <typename T, int R> struct FusedKArgs {
     T alpha, eps_d2, eps_r2;
     int has_d;
     LutView lut;
-    T box_wi;           // 1/L for the symmetric-box specialisation
+    T box_wi;           // box specialisation: interior weight
+    T box_cb[4], box_ca[4];   // weight corrections at k = -R, -R+1, R-1, R (blur, adjoint)
 };
+
+// host: a box line convolution as interior weight wi over [-R, R] plus corrections at
+// k = -R, -R+1, R-1, R; false when it has no such form (then the dense path runs)
+template <typename T, int R>
+bool box_corrections(const LineConv &c, double wi, T corr[4]) {
+    DenseTaps<T, R> d;
+    fill_dense<T, R>(d, c, nullptr);
+    for (int k = -R + 2; k <= R - 2; ++k)
+        if (d.w[k + R] != T(wi)) return false;
+    if (R == 1) {                                    // k = -R+1 = R-1 = 0: must be interior
+        if (d.w[1] != T(wi)) return false;
+        corr[0] = d.w[0] - T(wi); corr[1] = corr[2] = T(0); corr[3] = d.w[2] - T(wi);
+        return true;
+    }
+    const int ks[4] = {-R, -R + 1, R - 1, R};
+    for (int i = 0; i < 4; ++i) corr[i] = d.w[ks[i] + R] - T(wi);
+    return true;
+}
 
 __device__ __forceinline__ int fu_wrap(int j, int n, int periodic) {
     // halos never exceed the extent, so one conditional wrap suffices (no integer modulo)
@@ -92,7 +118,7 @@ __device__ __forceinline__ void fu_fill_halo(T *line, int n, int hw, int periodi
     }
 }
 
-template <typename T, int R, int LPW, bool ROBUST, int BOXR>
+template <typename T, int R, int LPW, bool ROBUST, int BOXR, bool BOXC>
 __global__ void __launch_bounds__(256, sizeof(T) == 4 ? (LPW == 2 ? 3 : 2) : 1)
 k_fused_lines(FusedKArgs<T, R> a) {
     constexpr int HW = HaloOf<R>::value;
@@ -229,7 +255,7 @@ k_fused_lines(FusedKArgs<T, R> a) {
 #pragma unroll
                 for (int k = -R; k < SEG + R; ++k) v[k + R] = U[off + koff(k)];
                 T bl[SEG];
-                conv_window<T, R, BOXR>(v, a.wb, a.box_wi, bl);
+                conv_window<T, R, BOXR, BOXC>(v, a.wb, a.box_wi, a.box_cb, bl);
 #pragma unroll
                 for (int r = 0; r < SEG; ++r) {
                     const T b = bl[r] > T(kGuard) ? bl[r] : T(kGuard);
@@ -255,13 +281,13 @@ k_fused_lines(FusedKArgs<T, R> a) {
                     T v[WIN];
 #pragma unroll
                     for (int k = -R; k < SEG + R; ++k) v[k + R] = wp[off + koff(k)];
-                    conv_window<T, R, BOXR>(v, a.wa, a.box_wi, num);
+                    conv_window<T, R, BOXR, BOXC>(v, a.wa, a.box_wi, a.box_ca, num);
                 }
                 if (ROBUST) {
                     T v[WIN];
 #pragma unroll
                     for (int k = -R; k < SEG + R; ++k) v[k + R] = ww[off + koff(k)];
-                    conv_window<T, R, BOXR>(v, a.wa, a.box_wi, den);
+                    conv_window<T, R, BOXR, BOXC>(v, a.wa, a.box_wi, a.box_ca, den);
                 }
                 T ux[SEG + 2];
 #pragma unroll
@@ -363,12 +389,13 @@ k_fused_lines(FusedKArgs<T, R> a) {
     }
 }
 
-template <typename T, int R, int LPW, int BOXR>
-cudaError_t launch_fused_t(const FusedKArgs<T, R> &a, bool robust, int64_t batch, cudaStream_t st) {
+// launch one instantiation of k_fused_lines (cluster of a.cl CTAs per frame)
+template <typename T, int R, int LPW>
+cudaError_t launch_fused_t(void (*kern)(FusedKArgs<T, R>), const FusedKArgs<T, R> &a, int64_t batch,
+                           cudaStream_t st) {
     constexpr int HW = HaloOf<R>::value;
     constexpr int RL = FU_WARPS * LPW;
     const size_t smem = (size_t)(2 * RL + 10 + 2 * FU_WARPS) * xline_len(a.n, HW) * sizeof(T);
-    auto kern = robust ? k_fused_lines<T, R, LPW, true, BOXR> : k_fused_lines<T, R, LPW, false, BOXR>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     if (a.cl > 8) {
@@ -399,6 +426,32 @@ cudaError_t launch_fused_t(const FusedKArgs<T, R> &a, bool robust, int64_t batch
         if (e != cudaSuccess) return e;
     }
     return cudaGetLastError();
+}
+
+// box specialisation of radius RR (md_fused_box_a.cu / md_fused_box_b.cu instantiate it)
+template <typename T, int RR, int LP>
+cudaError_t launch_fused_box_r(const FusedLinesArgs &d, int64_t batch, cudaStream_t st) {
+    FusedKArgs<T, RR> a{};
+    a.u0 = static_cast<const T *>(d.u_in);
+    a.fpos = static_cast<const T *>(d.fpos);
+    a.out = static_cast<T *>(d.u_out);
+    a.n = d.n; a.m = d.m; a.iterations = d.iterations; a.out_vert = d.out_vert;
+    a.periodic = d.blur.periodic;
+    a.cl = d.m / (FU_WARPS * LP);
+    a.alpha = T(d.alpha); a.eps_d2 = T(d.eps_d2); a.eps_r2 = T(d.eps_r2); a.has_d = d.has_d;
+    a.lut = d.lut;
+    a.box_wi = T(d.blur.wi);
+    if (!box_corrections<T, RR>(d.blur, d.blur.wi, a.box_cb) || !box_corrections<T, RR>(d.adj, d.blur.wi, a.box_ca))
+        return cudaErrorNotSupported;
+    bool corr = false;           // odd integer boxes: the plain sliding sum (no correction code)
+    for (int i = 0; i < 4; ++i) corr = corr || a.box_cb[i] != T(0) || a.box_ca[i] != T(0);
+    return launch_fused_t<T, RR, LP>(corr ? k_fused_lines<T, RR, LP, true, RR, true> : k_fused_lines<T, RR, LP, true, RR, false>,
+                                     a, batch, st);
+}
+
+template <typename T, int RR>
+cudaError_t launch_fused_box_lpw(const FusedLinesArgs &d, int64_t batch, cudaStream_t st) {
+    return launch_fused_box_r<T, RR, sizeof(T) == 8 ? 2 : 4>(d, batch, st);
 }
 
 }  // namespace md
