@@ -943,7 +943,8 @@ int32_t md_run_host_ex(md_plan *P, const void *f, int32_t in_type, void *u, int3
                  out_b = (size_t)fe * ob * chunk;
     const size_t scr_b = (size_t)scratch_fields(*P) * fe * P->es * chunk;
     const size_t per = align_up(in_b) + align_up(tin_b) + align_up(tout_b) + align_up(out_b) + align_up(scr_b);
-    rc = P->stage.ensure(per * kHostStreams);
+    const int nstreams = (int)std::min<int64_t>(kHostStreams, (batch + chunk - 1) / chunk);
+    rc = P->stage.ensure(per * nstreams);      // one staging slot per stream actually used
     if (rc) return rc;
     CU(cudaEventRecord(P->ev_start, user));
     for (int s = 0; s < kHostStreams; ++s) CU(cudaStreamWaitEvent(P->hstream[s], P->ev_start, 0));
