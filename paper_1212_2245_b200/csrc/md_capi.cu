@@ -234,8 +234,6 @@ int build_lut(md_plan *P) {
     P->lut.t64 = P->d_lut64;
     P->lut.t32 = P->d_lut32;
     P->lut.p32 = P->d_lutp32;
-    P->lut.slope = 1.0 - 1.0 / kLutUpper;
-    P->lut.intercept = (kLutUpper - 1.0 - std::log(kLutUpper)) - P->lut.slope * kLutUpper;
     return MD_OK;
 }
 

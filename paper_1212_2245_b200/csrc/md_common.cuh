@@ -34,12 +34,15 @@ constexpr double kLutInvStep = 2048.0;
 constexpr double kLutUpper = 65.0;
 constexpr double kLutDirectBelow = 0.5;
 constexpr int kLutCount = 133057;                 // round((65 - 1/32) * 2048) + 1
+// linear continuation above `upper`, matching value and slope of x - 1 - ln x at 65
+// (deconv.py:108-112, 127-129): slope 1 - 1/65, intercept (65 - 1 - ln 65) - slope * 65
+constexpr double kLutSlope = 64.0 / 65.0;
+constexpr double kLutIntercept = -4.1743872698956395;   // as the reference rounds it
 
 struct LutView {
     const double *t64;
     const float *t32;
     const float2 *p32;                            // (t32[i], t[i+1] - t[i]), i < kLutCount - 1
-    double slope, intercept;                      // linear continuation above `upper`
 };
 
 __device__ __forceinline__ double lut_fetch(const LutView &L, int i, double) { return __ldg(L.t64 + i); }
@@ -52,7 +55,7 @@ __device__ __forceinline__ float drsqrt(float x) { return rsqrtf(x); }
 template <typename T>
 __device__ __forceinline__ T r1_lut(const LutView &L, T x) {
     if (x < T(kLutDirectBelow)) return x - T(1) - dlog(x);
-    if (x > T(kLutUpper)) return T(L.slope) * x + T(L.intercept);
+    if (x > T(kLutUpper)) return T(kLutSlope) * x + T(kLutIntercept);
     T pos = (x - T(kLutDelta)) * T(kLutInvStep);
     int i = (int)pos;                              // pos >= (0.5 - 1/32) * 2048 > 0 here
     i = i > kLutCount - 2 ? kLutCount - 2 : i;

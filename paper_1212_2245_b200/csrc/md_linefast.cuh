@@ -67,7 +67,7 @@ __device__ __forceinline__ T r1_fast(const LutView &L, T x) {
     int i = (int)pos;
     i = i < kLutCount - 2 ? i : kLutCount - 2;
     T r = lut_interp(L, i, pos - T(i));
-    if (x > T(kLutUpper)) r = T(L.slope) * x + T(L.intercept);
+    if (x > T(kLutUpper)) r = T(kLutSlope) * x + T(kLutIntercept);
     if (x < T(kLutDirectBelow)) r = x - T(1) - flog(x);
     return r;
 }
