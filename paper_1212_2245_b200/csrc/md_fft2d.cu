@@ -96,6 +96,7 @@ k_fft2_rows(Fft2Args a, int rb) {
     if (a.inv && lw > 0) fft_dit_inv_lines(s, lw, rb, LS, tw);
 
     const T scale = T(a.scale), floor = T(a.floor);
+    const T eps_d2 = T(a.eps_d2), eps_r2 = T(a.eps_r2), alpha = T(a.alpha);   // converted once
     if (a.epi != R_EPI_NONE) {
         for (int i0 = threadIdx.x; i0 < ne; i0 += U * bd) {
             // global operands of U elements first: the stores below could alias them, so a
@@ -144,7 +145,7 @@ k_fft2_rows(Fft2Args a, int rb) {
                     const T fp = g0[k];
                     const T ratio = fp / b;
                     if (a.robust) {
-                        const T wv = robust_weight_floored<T>(a.lut, fp, b, T(a.eps_d2));
+                        const T wv = robust_weight_floored<T>(a.lut, fp, b, eps_d2);
                         packed = mkc<T>(wv * ratio, wv);
                     } else {
                         packed = mkc<T>(ratio, T(0));
@@ -153,9 +154,9 @@ k_fft2_rows(Fft2Args a, int rb) {
                     const T *u = static_cast<const T *>(a.u) + fr * fsz;
                     const int y = y0 + (i >> lw), x = i & (W - 1);
                     const T uv = g0[k];
-                    const T d = a.has_d ? tv_div_global<T>(u, H, W, y, x, T(a.eps_r2)) : T(0);
-                    const T un = a.robust ? combine_px<T, true>(uv, v.x * scale, v.y * scale, d, T(a.alpha), a.has_d != 0)
-                                          : combine_px<T, false>(uv, v.x * scale, T(0), d, T(a.alpha), a.has_d != 0);
+                    const T d = a.has_d ? tv_div_global<T>(u, H, W, y, x, eps_r2) : T(0);
+                    const T un = a.robust ? combine_px<T, true>(uv, v.x * scale, v.y * scale, d, alpha, a.has_d != 0)
+                                          : combine_px<T, false>(uv, v.x * scale, T(0), d, alpha, a.has_d != 0);
                     static_cast<T *>(a.oa)[o] = un;
                     packed = mkc<T>(un, T(0));
                 }
