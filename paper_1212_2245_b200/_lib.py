@@ -13,7 +13,8 @@ import os
 from .core import ContractError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmdcuda.so")
+# MD_LIB: an alternative build of the same library (kernel experiments, scripts/build_variant.py)
+LIB_PATH = os.environ.get("MD_LIB") or os.path.join(_HERE, "libmdcuda.so")
 
 MD_OK, MD_EINVAL, MD_ECONTRACT, MD_ECUDA, MD_ENOMEM = 0, -1, -2, -3, -4
 MD_F64, MD_F32 = 0, 1

@@ -175,9 +175,9 @@ k_fused_lines(FusedKArgs<T, R> a) {
     const T eps_r2 = a.eps_r2, eps_d2 = a.eps_d2, alpha = a.alpha;
     // diffusivity g on logical lines l in [lb, le] (deconv.py:191-203); lines whose stencil
     // touches a halo (l <= 0 or l >= RL-1) need the neighbours' rows of parity `par`
-    auto g_lines = [&](int lb, int le, int par) {
+    auto g_lines = [&](int lb, int le, int par, int wl) {
         if (!a.has_d) return;
-        for (int l = lb + warp; l <= le; l += FU_WARPS) {
+        for (int l = lb + wl; l <= le; l += FU_WARPS) {
             const int gl = gl0 + l;
             if (gl < 0 || gl >= m) continue;
             const bool up_ok = gl > 0, dn_ok = gl + 1 < m;
@@ -198,7 +198,8 @@ k_fused_lines(FusedKArgs<T, R> a) {
                     const T yu = up_ok ? up[off + koff(r)] : x[r + 1];
                     const T dyd = yd - x[r + 1], dyu = x[r + 1] - yu;
                     const T q = dxr * dxr + dxl * dxl + dyd * dyd + dyu * dyu;
-                    G[koff(r)] = T(0.5) * frsqrt(T(0.5) * q + eps_r2);
+                    // float: 0.5 / sqrt(q/2 + eps^2) as 1 / sqrt(2 q + 4 eps^2) (no scaling multiply)
+                    G[koff(r)] = sizeof(T) == 4 ? frsqrt(T(2) * q + T(4) * eps_r2) : T(0.5) * frsqrt(T(0.5) * q + eps_r2);
                 }
             }
         }
@@ -208,10 +209,19 @@ k_fused_lines(FusedKArgs<T, R> a) {
     auto publish_and_g = [&](int par) {
         __syncthreads();
         asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
-        g_lines(1, RL - 2, par);
+        // interior lines dealt from warp 2 on (warps 0 and 1 get one line fewer when RL - 2 is
+        // not a multiple of 8); the four halo-dependent lines go one each to warps 0..3, so
+        // the critical path after the wait is a single line
+#ifndef MD_FU_GOLDBAL
+        g_lines(1, RL - 2, par, (warp + FU_WARPS - 2) % FU_WARPS);
         asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-        g_lines(-1, 0, par);
-        g_lines(RL - 1, RL, par);
+        if (warp < 4) g_lines(warp < 2 ? -1 : RL - 1, warp < 2 ? 0 : RL, par, warp & 1);
+#else
+        g_lines(1, RL - 2, par, warp);
+        asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+        g_lines(-1, 0, par, warp);
+        g_lines(RL - 1, RL, par, warp);
+#endif
         __syncthreads();
     };
     publish_and_g(0);
