@@ -35,6 +35,7 @@ cudaError_t launch_fused_lines(const FusedLinesArgs &d, int64_t batch, cudaStrea
         a.u0 = static_cast<const T *>(d.u_in);
         a.fpos = static_cast<const T *>(d.fpos);
         a.out = static_cast<T *>(d.u_out);
+        a.query = d.query;
         a.n = d.n; a.m = d.m; a.iterations = d.iterations; a.out_vert = d.out_vert;
         a.periodic = d.blur.periodic;
         a.cl = d.m / (FU_WARPS * LP);

@@ -15,6 +15,7 @@ struct FusedLinesArgs {
     double alpha, eps_d2, eps_r2;
     int has_d, robust;
     LutView lut;
+    int *query;            // non-null: store the resident cluster count, launch nothing
 };
 
 bool fused_lines_supported(int dtype, int n, int m, unsigned flags);

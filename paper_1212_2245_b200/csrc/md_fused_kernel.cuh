@@ -77,6 +77,7 @@ template <typename T, int R> struct FusedKArgs {
     const T *u0;        // line-major clamped Wiener output [frames][m][n]
     const T *fpos;      // line-major max(f, floor)
     T *out;             // native layout result
+    int *query;         // host: non-null = report the resident cluster count instead of launching
     int n, m, iterations, out_vert, periodic, cl;
     DenseTaps<T, R> wb, wa;
     T alpha, eps_d2, eps_r2;
@@ -152,6 +153,10 @@ k_fused_lines(FusedKArgs<T, R> a) {
         return own + l * ls;
     };
 
+    // the next chunk's Wiener step is a programmatic dependent launch (md_capi.cu,
+    // run_lines_pipelined): it starts once every CTA of this grid has started, i.e. during the
+    // last wave, on the SMs the wave leaves free
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     cluster.sync();                                  // all CTAs resident before DSMEM traffic
     T *nb_top = rank > 0 ? cluster.map_shared_rank(sm, rank - 1) : nullptr;
     T *nb_bot = rank < CL - 1 ? cluster.map_shared_rank(sm, rank + 1) : nullptr;
@@ -412,6 +417,20 @@ cudaError_t launch_fused_t(void (*kern)(FusedKArgs<T, R>), const FusedKArgs<T, R
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
     }
+    if (a.query) {
+        cudaLaunchConfig_t q = {};
+        q.gridDim = dim3((unsigned)a.cl, 1, 1);
+        q.blockDim = dim3(256, 1, 1);
+        q.dynamicSmemBytes = smem;
+        cudaLaunchAttribute qa[1];
+        qa[0].id = cudaLaunchAttributeClusterDimension;
+        qa[0].val.clusterDim.x = a.cl;
+        qa[0].val.clusterDim.y = 1;
+        qa[0].val.clusterDim.z = 1;
+        q.attrs = qa;
+        q.numAttrs = 1;
+        return cudaOccupancyMaxActiveClusters(a.query, kern, &q);
+    }
     const int64_t fsz = (int64_t)a.n * a.m;
     const int64_t maxf = (int64_t)(0x7fffffff / a.cl);
     for (int64_t b0 = 0; b0 < batch; b0 += maxf) {
@@ -445,6 +464,7 @@ cudaError_t launch_fused_box_r(const FusedLinesArgs &d, int64_t batch, cudaStrea
     a.u0 = static_cast<const T *>(d.u_in);
     a.fpos = static_cast<const T *>(d.fpos);
     a.out = static_cast<T *>(d.u_out);
+    a.query = d.query;
     a.n = d.n; a.m = d.m; a.iterations = d.iterations; a.out_vert = d.out_vert;
     a.periodic = d.blur.periodic;
     a.cl = d.m / (FU_WARPS * LP);

@@ -31,6 +31,7 @@ struct WienerLinesArgs {
     const void *mult;     // Wiener multiplier, bit-reversed order, cx_t<T>[n]
     const void *tw;       // cx_t<T>[n/2]
     double floor;
+    int pdl;              // launched as a programmatic dependent of the preceding kernel
 };
 
 struct IterLinesArgs {

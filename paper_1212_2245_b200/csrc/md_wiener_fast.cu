@@ -83,6 +83,11 @@ __device__ __forceinline__ void dit_inv_reg(cx_t<T> (&v)[S]) {
 template <typename T, int S>
 __global__ void __launch_bounds__(256, (sizeof(T) == 4 && S <= 16) ? 3 : 1)   // 3 blocks/SM (<= 85 regs)
 k_wiener_lines_reg(WienerLinesArgs a) {
+    // programmatic dependent launch (md_capi.cu, run_lines_pipelined): this grid may start while
+    // the preceding cluster iteration kernel still runs; its last block waits for that kernel
+    // to finish, so this grid's completion implies the predecessor's
+    if (a.pdl && blockIdx.x == gridDim.x - 1 && blockIdx.y == gridDim.y - 1)
+        asm volatile("griddepcontrol.wait;\n" ::: "memory");
     using C = cx_t<T>;
     constexpr int N = S * S;
     constexpr int PB = 256 / S;                 // line pairs per block
@@ -231,7 +236,19 @@ cudaError_t launch_wiener_reg_t(const WienerLinesArgs &a, int64_t batch, cudaStr
         ab.in = static_cast<const char *>(a.in) + b0 * fb;
         ab.out = static_cast<char *>(a.out) + b0 * fb;
         if (a.fpos) ab.fpos = static_cast<char *>(a.fpos) + b0 * fb;
-        k_wiener_lines_reg<T, S><<<dim3(groups, nb), 256, smem, st>>>(ab);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(groups, nb);
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = (a.pdl && b0 == 0) ? 1 : 0;
+        ab.pdl = a.pdl && b0 == 0;
+        e = cudaLaunchKernelEx(&cfg, k_wiener_lines_reg<T, S>, ab);
+        if (e != cudaSuccess) return e;
     }
     return cudaGetLastError();
 }

@@ -328,6 +328,29 @@ def test_fused_batch_many_frames(md):
     assert np.abs(out[7] - ref).max() > 0.1
 
 
+@pytest.mark.parametrize("chunk", [40, 64, 300])
+def test_fused_chunk_pipeline_bitwise(md, chunk):
+    """Batches over several chunks run the Wiener step of chunk c+1 as a programmatic dependent
+    launch beside chunk c's iteration kernel (md_capi.cu run_lines_pipelined): same bits as one
+    chunk, every frame, including a ragged last chunk."""
+    import torch
+    d = load_golden("pipe_c1_box_h15_256")
+    pipe = md.DeblurPipeline((256, 256), product_psf(d), product_params(d), dtype="float32")
+    assert pipe.plan.fused
+    g = torch.Generator().manual_seed(5)
+    frames = (torch.from_numpy(np.stack([d["f"]] * 301)).float()
+              + torch.randn((301, 256, 256), generator=g)).cuda()
+    whole = pipe.run_batch(frames).cpu().numpy()
+    pipe.plan.set_chunk(chunk)
+    try:
+        parts = pipe.run_batch(frames).cpu().numpy()
+    finally:
+        pipe.plan.set_chunk(0)
+    np.testing.assert_array_equal(parts, whole)
+    one = pipe.run_batch(frames[250:251]).cpu().numpy()
+    np.testing.assert_array_equal(parts[250], one[0])
+
+
 def test_plan_reports_launches(md):
     pipe = md.DeblurPipeline((256, 256), md.Psf.uniform_box(md.BlurAxis.HORIZONTAL, 15), md.DeconvParams())
     assert pipe.plan.launch_count(16) >= 2
