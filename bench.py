@@ -557,7 +557,7 @@ def main() -> None:
         iter_bytes = work.iter_bytes(args.batch, esz) * args.steps
         achieved = iter_bytes / (prof["iter_ms"] / 1e3) / 1e9 if prof["iter_ms"] > 0 else None
         cpu = None
-        if not args.no_cpu:
+        if not args.no_cpu and world == 1:            # the CPU baseline: rank 0 at N=1 only
             cores = host_cores()
             jobs = cpu_jobs(work, args.cpu_frames_per_core, cores)
             pool = mp.get_context("fork").Pool(cores)
