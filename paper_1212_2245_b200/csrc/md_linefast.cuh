@@ -28,19 +28,37 @@ __host__ __device__ constexpr int koff(int k) { return k + (k >= 0 ? k / 8 : -((
 template <typename T, int R> struct DenseTaps { T w[2 * R + 1]; };
 
 // fast reciprocal / reciprocal square root / log: one MUFU op for float (operands here are
-// positive normal numbers: b >= 1e-12, fpos >= floor, q + eps^2 > 0), IEEE-accurate for double
+// positive normal numbers: b >= 1e-12, fpos >= floor, q + eps^2 > 0), Newton-refined for double
 __device__ __forceinline__ float frcp(float x) {
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
-__device__ __forceinline__ double frcp(double x) { return 1.0 / x; }
+// double: the MUFU estimate (about 2^-22 relative) refined by two Newton steps -- within an ulp
+// or two of the IEEE quotient at a fraction of its cost (no special-case path: operands are
+// positive normal numbers here)
+__device__ __forceinline__ double frcp(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-x, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-x, y, 1.0);
+    return fma(y, e, y);
+}
 __device__ __forceinline__ float frsqrt(float x) {
     float r;
     asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
-__device__ __forceinline__ double frsqrt(double x) { return 1.0 / sqrt(x); }
+__device__ __forceinline__ double frsqrt(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double h = 0.5 * x;
+    double t = fma(-h * y, y, 0.5);           // y <- y (1.5 - x y^2 / 2), twice
+    y = fma(y, t, y);
+    t = fma(-h * y, y, 0.5);
+    return fma(y, t, y);
+}
 __device__ __forceinline__ float flog(float x) {
     float r;
     asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
