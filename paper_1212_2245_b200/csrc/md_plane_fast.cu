@@ -26,31 +26,43 @@ __device__ __forceinline__ int pf_resolve(int k, int n, int periodic) {
     return k < 0 ? 0 : (k >= n ? n - 1 : k);
 }
 
-// tile rows [y0 - ht, y0 + FY + hb) x cols [x0 - hl, x0 + FX + hr) of one or two fields; U
-// global loads in flight per thread (a load-then-store loop would wait out each latency)
+// tile rows [y0 - ht, y0 + FY + hb) x cols [x0 - hl, x0 + FX + hr) of one or two fields. A warp
+// walks rows, its lanes the columns (CJ column slots per lane, resolved once per block, so
+// no per-element division or wrap); two rows per step keep 2 CJ global loads in flight.
+constexpr int PF_CJ = 4;                  // cols <= 32 * PF_CJ (FX + x-halos <= 128)
 template <typename T, typename E, typename Get>
 __device__ void pf_load(E *s, int ss, int H, int W, int y0, int x0, const PlaneHalo &h, int periodic, int slab,
                         Get get) {
-    constexpr int U = 4;
     const int rows = FY + h.ht + h.hb, cols = FX + h.hl + h.hr;
-    const int n = rows * cols, bd = blockDim.x;
-    for (int i0 = threadIdx.x; i0 < n; i0 += U * bd) {
-        E v[U];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    int xr[PF_CJ];
 #pragma unroll
-        for (int k = 0; k < U; ++k) {
-            const int idx = i0 + k * bd;
-            if (idx >= n) break;
-            const int i = idx / cols, j = idx - i * cols;
-            // slab mode: the caller's buffer carries the neighbours' rows (halo), read them as is
-            const int y = slab ? y0 - h.ht + i : pf_resolve(y0 - h.ht + i, H, periodic);
-            v[k] = get((int64_t)y * W + pf_resolve(x0 - h.hl + j, W, periodic));
+    for (int c = 0; c < PF_CJ; ++c) {
+        const int j = lane + 32 * c;
+        xr[c] = j < cols ? pf_resolve(x0 - h.hl + j, W, periodic) : -1;
+    }
+    auto yres = [&](int i) {
+        // slab mode: the caller's buffer carries the neighbours' rows (halo), read them as is
+        return slab ? y0 - h.ht + i : pf_resolve(y0 - h.ht + i, H, periodic);
+    };
+    for (int i = warp; i < rows; i += 2 * nw) {
+        const int i2 = i + nw;
+        const bool two = i2 < rows;
+        const int64_t b0 = (int64_t)yres(i) * W, b1 = two ? (int64_t)yres(i2) * W : b0;
+        E v0[PF_CJ], v1[PF_CJ];
+#pragma unroll
+        for (int c = 0; c < PF_CJ; ++c) {
+            if (xr[c] >= 0) {
+                v0[c] = get(b0 + xr[c]);
+                if (two) v1[c] = get(b1 + xr[c]);
+            }
         }
 #pragma unroll
-        for (int k = 0; k < U; ++k) {
-            const int idx = i0 + k * bd;
-            if (idx >= n) break;
-            const int i = idx / cols, j = idx - i * cols;
-            s[i * ss + j] = v[k];
+        for (int c = 0; c < PF_CJ; ++c) {
+            if (xr[c] >= 0) {
+                s[i * ss + lane + 32 * c] = v0[c];
+                if (two) s[i2 * ss + lane + 32 * c] = v1[c];
+            }
         }
     }
 }
@@ -239,6 +251,7 @@ static size_t smem_b(const PlaneHalo &ha, size_t es, int ssb) {
 bool plane_fast_supported(const PlaneHalo &hb, const PlaneHalo &ha, const std::vector<PlaneTap> &taps_blur,
                           const std::vector<PlaneTap> &taps_adj, int dtype) {
     if (hb.nt > kPlaneMaxTaps || ha.nt > kPlaneMaxTaps) return false;
+    if (FX + hb.hl + hb.hr > 32 * PF_CJ || FX + ha.hl + ha.hr > 32 * PF_CJ) return false;   // pf_load column slots
     const size_t es = dtype == 0 ? 8 : 4;
     const int ssa = dtype == 0 ? pf_stride_a<double>(hb) : pf_stride_a<float>(hb);
     const int ssb = dtype == 0 ? pf_stride_b<double>(ha) : pf_stride_b<float>(ha);
