@@ -780,12 +780,12 @@ int wiener_plane(md_plan &P, const void *f, void *out, void *fpos, void *z, bool
                  int64_t nb, cudaStream_t st) {
     if (P.big) {
         const int H = P.d.height, W = P.d.width;
+        // rows forward (real input) | columns: forward, x M and inverse of the inner digit fused
+        // | rows inverse whose last pass writes u0 and fpos: 6 passes over the complex field
         CU(big_axis<T>(P.bigW, z, H, W, 1, 0, f, nullptr, nullptr, 0, 1.0, nb, st));
-        CU(big_axis<T>(P.bigH, z, H, W, 0, 0, nullptr, nullptr, P.d_mult, 0, 1.0, nb, st));
-        CU(big_axis<T>(P.bigH, z, H, W, 0, 1, nullptr, nullptr, nullptr, 0, 1.0, nb, st));
-        CU(big_axis<T>(P.bigW, z, H, W, 1, 1, nullptr, nullptr, nullptr, 0, 1.0, nb, st));
-        CU(launch_big_wiener_epilogue<T>(z, f, out, fpos, (int64_t)H * W * nb, 1.0 / ((double)H * W), P.d.floor,
-                                         clamp ? 1 : 0, st));
+        CU(big_axis_filter<T>(P.bigH, z, H, W, 0, P.d_mult, 0, nb, st));
+        CU(big_axis_inv_wiener<T>(P.bigW, z, H, W, 1, 1.0 / ((double)H * W), f, out, fpos, P.d.floor, clamp ? 1 : 0,
+                                  nb, st));
         return MD_OK;
     }
     // two frames per complex field unless the FFT-path iteration needs z afterwards
@@ -1000,7 +1000,7 @@ int32_t md_run_launch_count(const md_plan *P, int64_t batch) {
         per = 1;
         if (K > 0) per += P->fused ? 1 : K + (P->vert ? 1 : 0);
     } else {
-        per = wiener ? 3 : 1;
+        per = wiener ? (P->big ? 6 : 3) : 1;      // two-level Wiener: 6 sub-transform passes
         if (K > 0) {
             if (!wiener && P->path == PATH_PLANE_FFT) per += 1;
             per += P->fused_plane ? 1 : K * (P->path == PATH_PLANE_FFT ? 4 : 2);
@@ -1403,13 +1403,8 @@ int32_t md_slab_cols_filter(md_plan *P, void *zc, int32_t cols, const void *mult
     if (rc) return rc;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int H = P->d.height;
-    if (P->d.dtype == MD_F64) {
-        CU(big_axis<double>(P->bigH, zc, H, cols, 0, 0, nullptr, nullptr, mult_block, 0, 1.0, 1, st));
-        CU(big_axis<double>(P->bigH, zc, H, cols, 0, 1, nullptr, nullptr, nullptr, 0, 1.0, 1, st));
-    } else {
-        CU(big_axis<float>(P->bigH, zc, H, cols, 0, 0, nullptr, nullptr, mult_block, 0, 1.0, 1, st));
-        CU(big_axis<float>(P->bigH, zc, H, cols, 0, 1, nullptr, nullptr, nullptr, 0, 1.0, 1, st));
-    }
+    CU(P->d.dtype == MD_F64 ? big_axis_filter<double>(P->bigH, zc, H, cols, 0, mult_block, 0, 1, st)
+                            : big_axis_filter<float>(P->bigH, zc, H, cols, 0, mult_block, 0, 1, st));
     return MD_OK;
 }
 

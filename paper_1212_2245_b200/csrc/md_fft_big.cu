@@ -68,13 +68,33 @@ k_subfft(SubFftArgs a) {
     C *twL = s + G * ls;                       // sub-transform twiddles staged in shared memory
     for (int k = threadIdx.x; k < (L >> 1); k += bd) twL[k] = static_cast<const C *>(a.twL)[k];
     __syncthreads();
-    if (a.inv) fft_dit_inv_lines(s, a.log2L, G, ls, twL);
-    else fft_dif_lines(s, a.log2L, G, ls, twL);
+    const C *filt = static_cast<const C *>(a.filt);
+    if (TW == TW_FILT_INV) {
+        fft_dif_lines(s, a.log2L, G, ls, twL);
+        for (int idx = threadIdx.x; idx < n; idx += bd) {
+            int g, e;
+            coords(idx, g, e);
+            if (b0 + g >= a.B) continue;
+            const C fl = filt[base + (int64_t)g * a.sb + (int64_t)e * a.es];
+            C &v = s[g * ls + fpad(e)];
+            v = a.conj_filt ? cmulc(v, fl) : cmul(v, fl);
+        }
+        __syncthreads();
+        fft_dit_inv_lines(s, a.log2L, G, ls, twL);
+    } else if (a.inv) {
+        fft_dit_inv_lines(s, a.log2L, G, ls, twL);
+    } else {
+        fft_dif_lines(s, a.log2L, G, ls, twL);
+    }
     // inter-pass twiddle W_N^{+-(digit * rev(pos))}, digit = line (FWD) or element (INV) index
     const C *twN = static_cast<const C *>(a.twN);
     const int N = a.N;
-    const C *filt = static_cast<const C *>(a.filt);
     const T scale = T(a.scale);
+    constexpr bool FILT_EPI = TW != TW_FILT_INV;        // the fused mode filtered in shared memory
+    constexpr int TWM = TW == TW_FILT_INV ? TW_INV : TW;
+    T *wu = static_cast<T *>(a.wu), *wfp = static_cast<T *>(a.wfpos);
+    const T *wf = static_cast<const T *>(a.wf);
+    const T wfloor = T(a.floor);
     for (int i0 = threadIdx.x; i0 < n; i0 += U * bd) {
         // table and filter operands first: loads after the z stores below would wait on them
         C tw[U], fl[U];
@@ -85,16 +105,16 @@ k_subfft(SubFftArgs a) {
             coords(idx, g, e);
             tw[k] = fl[k] = mkc<T>(T(1), T(0));
             if (idx >= n || b0 + g >= a.B) continue;
-            if (TW != TW_NONE) {
+            if (TWM != TW_NONE) {
                 const int lb = a.tw_digit_is_a ? ai : b0 + g;                 // line digit
                 const int re = (int)(__brev((unsigned)e) >> (32 - a.log2L));   // rev(pos) in the line
                 const int rl = (int)(__brev((unsigned)lb) >> (32 - a.log2Lother));
                 // FWD (after F1): W_N^{line * rev(e)};  INV (after I2): conj W_N^{e * rev(line)}
-                const int kk = TW == TW_FWD ? (int)(((int64_t)lb * re) & (N - 1)) : (int)(((int64_t)e * rl) & (N - 1));
+                const int kk = TWM == TW_FWD ? (int)(((int64_t)lb * re) & (N - 1)) : (int)(((int64_t)e * rl) & (N - 1));
                 const C w = twN[kk & (N / 2 - 1)];
                 tw[k] = kk < N / 2 ? w : mkc<T>(-w.x, -w.y);
             }
-            if (filt) fl[k] = filt[base + (int64_t)g * a.sb + (int64_t)e * a.es];
+            if (FILT_EPI && filt) fl[k] = filt[base + (int64_t)g * a.sb + (int64_t)e * a.es];
         }
 #pragma unroll
         for (int k = 0; k < U; ++k) {
@@ -103,10 +123,21 @@ k_subfft(SubFftArgs a) {
             coords(idx, g, e);
             if (idx >= n || b0 + g >= a.B) continue;
             C v = s[g * ls + fpad(e)];
-            if (TW != TW_NONE) v = TW == TW_FWD ? cmul(v, tw[k]) : cmulc(v, tw[k]);
-            if (filt) v = a.conj_filt ? cmulc(v, fl[k]) : cmul(v, fl[k]);
+            if (TWM != TW_NONE) v = TWM == TW_FWD ? cmul(v, tw[k]) : cmulc(v, tw[k]);
+            if (FILT_EPI && filt) v = a.conj_filt ? cmulc(v, fl[k]) : cmul(v, fl[k]);
             if (scale != T(1)) v = cscale(v, scale);
-            z[base + (int64_t)g * a.sb + (int64_t)e * a.es] = v;
+            const int64_t o = base + (int64_t)g * a.sb + (int64_t)e * a.es;
+            if (TW == TW_NONE && wu) {
+                // Wiener epilogue (deconv.py:666-672): real part, clamp, floored observation
+                const T x = v.x;
+                wu[fr * a.rframe + o] = a.clamp ? (x > wfloor ? x : wfloor) : x;
+                if (wfp) {
+                    const T fv = wf[fr * a.rframe + o];
+                    wfp[fr * a.rframe + o] = fv > wfloor ? fv : wfloor;
+                }
+            } else {
+                z[o] = v;
+            }
         }
     }
 }
@@ -135,8 +166,9 @@ cudaError_t launch_subfft(const SubFftArgs &a0, int64_t batch, cudaStream_t st) 
     const size_t smem = ((size_t)a.G * fline_stride(L) + L / 2 + 1) * sizeof(cx_t<T>);
     auto pick = [&](auto lf) {
         constexpr bool LF = decltype(lf)::value;
-        return a.tw_mode == TW_FWD ? k_subfft<T, LF, TW_FWD> : (a.tw_mode == TW_INV ? k_subfft<T, LF, TW_INV>
-                                                                                     : k_subfft<T, LF, TW_NONE>);
+        return a.tw_mode == TW_FWD ? k_subfft<T, LF, TW_FWD>
+               : (a.tw_mode == TW_INV ? k_subfft<T, LF, TW_INV>
+                                      : (a.tw_mode == TW_FILT_INV ? k_subfft<T, LF, TW_FILT_INV> : k_subfft<T, LF, TW_NONE>));
     };
     auto kern = a.es == 1 ? pick(std::true_type{}) : pick(std::false_type{});
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -148,6 +180,9 @@ cudaError_t launch_subfft(const SubFftArgs &a0, int64_t batch, cudaStream_t st) 
         ab.z = static_cast<char *>(a.z) + b0 * a.frame * (int64_t)sizeof(cx_t<T>);
         if (a.ra) ab.ra = static_cast<const char *>(a.ra) + b0 * a.rframe * (int64_t)sizeof(T);
         if (a.rb) ab.rb = static_cast<const char *>(a.rb) + b0 * a.rframe * (int64_t)sizeof(T);
+        if (a.wu) ab.wu = static_cast<char *>(a.wu) + b0 * a.rframe * (int64_t)sizeof(T);
+        if (a.wfpos) ab.wfpos = static_cast<char *>(a.wfpos) + b0 * a.rframe * (int64_t)sizeof(T);
+        if (a.wf) ab.wf = static_cast<const char *>(a.wf) + b0 * a.rframe * (int64_t)sizeof(T);
         kern<<<dim3((unsigned)(a.A * blocks_b), nb), 256, smem, st>>>(ab);
     }
     return cudaGetLastError();
@@ -175,6 +210,57 @@ void split_axis(int N, int *N1, int *N2) {
 
 // Forward (inv = 0) or inverse (inv = 1) two-pass transform along the rows (axis = 1,
 // length W) or columns (axis = 0, length H) of a [batch][H][W] complex field.
+// the two passes of one axis: "1" = sub-DFT over j2 (length N2, stride N1), lines j1;
+// "2" = sub-DFT over j1 (length N1, stride 1), lines p
+static void axis_passes(const BigAxis &ax, void *z, int H, int W, int axis, SubFftArgs &p1, SubFftArgs &p2) {
+    const int N = axis == 1 ? W : H;
+    const int N1 = ax.N1, N2 = ax.N2;
+    p1 = SubFftArgs{};
+    p2 = SubFftArgs{};
+    for (SubFftArgs *p : {&p1, &p2}) {
+        p->z = z; p->frame = (int64_t)H * W; p->rframe = (int64_t)H * W;
+        p->N = N; p->twN = ax.twN; p->scale = 1.0;
+    }
+    if (axis == 1) {
+        p1.A = H; p1.sa = W; p1.B = N1; p1.sb = 1; p1.es = N1;
+        p2.A = H; p2.sa = W; p2.B = N2; p2.sb = N1; p2.es = 1;
+    } else {
+        p1.A = N1; p1.sa = W; p1.B = W; p1.sb = 1; p1.es = (int64_t)N1 * W;
+        p2.A = N2; p2.sa = (int64_t)N1 * W; p2.B = W; p2.sb = 1; p2.es = W;
+    }
+    p1.log2L = ax.l2; p1.twL = ax.twN2; p1.log2Lother = ax.l1;
+    p2.log2L = ax.l1; p2.twL = ax.twN1; p2.log2Lother = ax.l2;
+    p1.tw_digit_is_a = axis == 0;
+    p2.tw_digit_is_a = axis == 0;
+}
+
+template <typename T>
+cudaError_t big_axis_filter(const BigAxis &ax, void *z, int H, int W, int axis, const void *filt, int conj_filt,
+                            int64_t batch, cudaStream_t st) {
+    SubFftArgs p1, p2;
+    axis_passes(ax, z, H, W, axis, p1, p2);
+    cudaError_t e;
+    p1.tw_mode = TW_FWD;
+    if ((e = launch_subfft<T>(p1, batch, st)) != cudaSuccess) return e;
+    p2.tw_mode = TW_FILT_INV; p2.filt = filt; p2.conj_filt = conj_filt;
+    if ((e = launch_subfft<T>(p2, batch, st)) != cudaSuccess) return e;
+    p1.tw_mode = TW_NONE; p1.inv = 1;
+    return launch_subfft<T>(p1, batch, st);
+}
+
+template <typename T>
+cudaError_t big_axis_inv_wiener(const BigAxis &ax, void *z, int H, int W, int axis, double scale, const void *f,
+                                void *u, void *fpos, double floor, int clamp, int64_t batch, cudaStream_t st) {
+    SubFftArgs p1, p2;
+    axis_passes(ax, z, H, W, axis, p1, p2);
+    cudaError_t e;
+    p2.tw_mode = TW_INV; p2.inv = 1;
+    if ((e = launch_subfft<T>(p2, batch, st)) != cudaSuccess) return e;
+    p1.tw_mode = TW_NONE; p1.inv = 1; p1.scale = scale;
+    p1.wu = u; p1.wfpos = fpos; p1.wf = f; p1.floor = floor; p1.clamp = clamp;
+    return launch_subfft<T>(p1, batch, st);
+}
+
 template <typename T>
 cudaError_t big_axis(const BigAxis &ax, void *z, int H, int W, int axis, int inv, const void *ra, const void *rb,
                      const void *filt, int conj_filt, double scale_last, int64_t batch, cudaStream_t st) {
@@ -215,6 +301,14 @@ template cudaError_t launch_big_wiener_epilogue<double>(const void *, const void
                                                         double, int, cudaStream_t);
 template cudaError_t launch_big_wiener_epilogue<float>(const void *, const void *, void *, void *, int64_t, double,
                                                        double, int, cudaStream_t);
+template cudaError_t big_axis_filter<double>(const BigAxis &, void *, int, int, int, const void *, int, int64_t,
+                                             cudaStream_t);
+template cudaError_t big_axis_filter<float>(const BigAxis &, void *, int, int, int, const void *, int, int64_t,
+                                            cudaStream_t);
+template cudaError_t big_axis_inv_wiener<double>(const BigAxis &, void *, int, int, int, double, const void *, void *,
+                                                 void *, double, int, int64_t, cudaStream_t);
+template cudaError_t big_axis_inv_wiener<float>(const BigAxis &, void *, int, int, int, double, const void *, void *,
+                                                void *, double, int, int64_t, cudaStream_t);
 template cudaError_t big_axis<double>(const BigAxis &, void *, int, int, int, int, const void *, const void *,
                                       const void *, int, double, int64_t, cudaStream_t);
 template cudaError_t big_axis<float>(const BigAxis &, void *, int, int, int, int, const void *, const void *,

@@ -7,7 +7,9 @@
 
 namespace md {
 
-enum { TW_NONE = 0, TW_FWD = 1, TW_INV = 2 };
+// TW_FILT_INV: forward sub-DFT, x filter, inverse sub-DFT, then the TW_INV twiddle -- the
+// middle of a filtered axis (F2, filter, I2) in one pass
+enum { TW_NONE = 0, TW_FWD = 1, TW_INV = 2, TW_FILT_INV = 3 };
 
 struct SubFftArgs {
     void *z;                     // complex field, [batch] frames of `frame` elements
@@ -21,6 +23,12 @@ struct SubFftArgs {
     const void *filt;            // multiply by filt[address] after the pass (last forward pass)
     int conj_filt;
     double scale;
+    // optional Wiener epilogue instead of storing z (last inverse pass): u = max(Re z * scale,
+    // floor) (or unclamped), fpos = max(f, floor), real fields indexed like z
+    void *wu, *wfpos;
+    const void *wf;
+    double floor;
+    int clamp;
 };
 
 // one axis of a two-level transform: N = N1 * N2, twiddle tables in the plan dtype
@@ -34,6 +42,15 @@ template <typename T> cudaError_t launch_subfft(const SubFftArgs &, int64_t batc
 template <typename T>
 cudaError_t big_axis(const BigAxis &ax, void *z, int H, int W, int axis, int inv, const void *ra, const void *rb,
                      const void *filt, int conj_filt, double scale_last, int64_t batch, cudaStream_t st);
+// filtered transform along one axis: forward (F1, then F2 + filter + I2 fused), inverse I1;
+// with wu set, the last pass writes the Wiener result instead of z (see SubFftArgs)
+template <typename T>
+cudaError_t big_axis_filter(const BigAxis &ax, void *z, int H, int W, int axis, const void *filt, int conj_filt,
+                            int64_t batch, cudaStream_t st);
+// inverse transform along one axis whose last pass writes u / fpos (Wiener epilogue)
+template <typename T>
+cudaError_t big_axis_inv_wiener(const BigAxis &ax, void *z, int H, int W, int axis, double scale, const void *f,
+                                void *u, void *fpos, double floor, int clamp, int64_t batch, cudaStream_t st);
 template <typename T>
 cudaError_t launch_big_wiener_epilogue(const void *z, const void *f, void *u, void *fpos, int64_t n, double scale,
                                        double floor, int clamp, cudaStream_t st);
