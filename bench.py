@@ -286,6 +286,30 @@ def run_c5(args, rank: int, world: int, local: int) -> None:
         e2e = {"value": 1.0 / el, "unit": "images/s", "h2d_bytes_per_step": hin_np.nbytes,
                "d2h_bytes_per_step": hout_np.nbytes,
                "entry": "DeblurPipeline.run_batch(pinned float64 image) -> float64 (md_run_host_ex)"}
+    fp64 = None
+    if world == 1:
+        # the direct-tap iterations are FP64-ALU work: their flops against a measured FP64 peak
+        # (cuBLAS DGEMM here, the same data path as the FP64 FMA units on B200)
+        prof = pipe.plan.run_profile(f, out=u)
+        taps = int(np.count_nonzero(psf.weights))
+        flops = 2.0 * 3 * taps * n * n * params.iterations
+        a = torch.randn((8192, 8192), device="cuda", dtype=torch.float64)
+        for _ in range(2):
+            a @ a
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(3):
+            a @ a
+        e1.record()
+        e1.synchronize()
+        peak_tf = 3 * 2 * 8192.0 ** 3 / (e0.elapsed_time(e1) / 1e3) / 1e12
+        del a
+        ach = flops / (prof["iter_ms"] / 1e3) / 1e12
+        fp64 = {"bound": "fp64", "kernel": "direct-tap RRRL iteration stages (k_plane_a_fast / k_plane_b_fast)",
+                "achieved": ach, "peak": peak_tf, "unit": "TFLOP/s", "frac": ach / peak_tf,
+                "peak_source": "measured in this run: cuBLAS DGEMM 8192^3 (torch.matmul float64)",
+                "flop_model": f"2 flop x (blur + adjoint pair = 3) x {taps} taps per pixel per iteration",
+                "stage_ms": {k: prof[k] for k in ("init_ms", "iter_ms")}}
     if rank == 0:
         pk = peaks()
         bytes_img = (7 + 8 * params.iterations) * 8 * n * n
@@ -302,6 +326,8 @@ def run_c5(args, rank: int, world: int, local: int) -> None:
                          "peak": pk["hbm_gbs"], "unit": "GB/s per GPU",
                          "frac": bytes_img / (ms / 1e3) / 1e9 / world / pk["hbm_gbs"], "traffic": None,
                          "bytes_model": "SURVEY.md 8(d): (7 + 5x8) field passes x 8 B per pixel"},
+            "roofline_fp64": fp64,
+            "gpu_launches": pipe.plan.launch_count(1) * args.steps if world == 1 else None,
             "cpu_baseline": None,
             "e2e": e2e,
             "clocks": clk.summary(),

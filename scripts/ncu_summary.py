@@ -2,7 +2,7 @@
 """Summarise an ncu --set full report (.ncu-rep) or a launch-list CSV into markdown.
 
     python scripts/ncu_summary.py gpurun_out/prof.ncu-rep            # per-kernel key metrics
-    python scripts/ncu_summary.py --launches gpurun_out/launches.csv # time share per kernel
+    python scripts/ncu_summary.py --launches gpurun_out/launches.csv [MIN_CTAS] # time share per kernel
 """
 
 from __future__ import annotations
@@ -49,13 +49,20 @@ def rep(path: str) -> str:
     return "\n".join(out)
 
 
-def launches(path: str) -> str:
+def launches(path: str, min_ctas: int = 0) -> str:
+    """Time share per kernel; min_ctas > 0 keeps only launches with at least that many CTAs
+    (drops plan-time and single-frame latency launches from a bench command's list)."""
     rows = [r for r in csv.reader(open(path)) if len(r) > 10]
     hdr = rows[0]
     ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    gi = hdr.index("Grid Size") if "Grid Size" in hdr else None
     agg = collections.OrderedDict()
     scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
     for r in rows[1:]:
+        if min_ctas and gi is not None:
+            g = [int(x) for x in r[gi].strip("()").split(",")]
+            if g[0] * g[1] * g[2] < min_ctas:
+                continue
         k = r[ki].split("(")[0]
         agg.setdefault(k, []).append(float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0))
     tot = sum(sum(v) for v in agg.values())
@@ -67,6 +74,6 @@ def launches(path: str) -> str:
 
 if __name__ == "__main__":
     if sys.argv[1] == "--launches":
-        print(launches(sys.argv[2]))
+        print(launches(sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 0))
     else:
         print(rep(sys.argv[1]))
