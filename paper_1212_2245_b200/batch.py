@@ -46,7 +46,10 @@ class PsfBankPipeline:
                 start = i
         return out
 
-    def run(self, frames, psf_index, out=None, stream=None):
+    def run(self, frames, psf_index, out=None, stream=None, streams: int = 1):
+        """``streams`` > 1 deals the PSF groups round-robin over that many internal CUDA streams
+        (ordered after, and joined back into, the caller's stream), so one group's last
+        partial wave of clusters overlaps the next group's launches."""
         import torch
         idx = np.asarray(psf_index, dtype=np.int64)
         if frames.shape[0] != idx.size:
@@ -57,8 +60,20 @@ class PsfBankPipeline:
         sorted_already = bool(np.all(order == np.arange(idx.size)))
         src = frames if sorted_already else frames[torch.from_numpy(order).to(frames.device)]
         dst = (out if (out is not None and sorted_already) else torch.empty_like(src))
-        for b, s, e in self.groups(idx[order]):
-            self.pipes[b].plan.run(src[s:e], out=dst[s:e], stream=stream)
+        groups = self.groups(idx[order])
+        if streams > 1 and len(groups) > 1:
+            base = stream if stream is not None else torch.cuda.current_stream()
+            if len(getattr(self, "_run_streams", ())) != streams:
+                self._run_streams = [torch.cuda.Stream() for _ in range(streams)]
+            for st in self._run_streams:
+                st.wait_stream(base)
+            for k, (b, s, e) in enumerate(groups):
+                self.pipes[b].plan.run(src[s:e], out=dst[s:e], stream=self._run_streams[k % streams])
+            for st in self._run_streams:
+                base.wait_stream(st)
+        else:
+            for b, s, e in groups:
+                self.pipes[b].plan.run(src[s:e], out=dst[s:e], stream=stream)
         if sorted_already:
             return dst
         res = torch.empty_like(dst) if out is None else out

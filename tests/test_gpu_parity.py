@@ -376,6 +376,9 @@ def test_psf_bank_pipeline_matches_single_plans(md):
         # 2D-PSF groups run their Wiener FFTs two frames per complex field (real / imaginary
         # part), which only changes rounding
         np.testing.assert_allclose(out[k], want, rtol=0, atol=0 if bank[i].kind.value != "2d" else 1e-9)
+    # the PSF groups dealt over internal streams: the same bits
+    for ns in (2, 3):
+        np.testing.assert_array_equal(pipe.run(torch.from_numpy(frames).cuda(), idx, streams=ns).cpu().numpy(), out)
 
 
 def test_paired_2d_wiener_matches_single_frames(md):
