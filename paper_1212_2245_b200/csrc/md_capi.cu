@@ -47,6 +47,11 @@ int fail(int code, const std::string &msg) {
     } while (0)
 
 bool is_pow2(int n) { return n >= 1 && (n & (n - 1)) == 0; }
+
+// a non-sticky error left by a call whose failure was handled (e.g. a kernel variant whose
+// shared-memory attribute is refused, then another path taken) must not be reported by the
+// next entry point's launch check
+inline void clear_stale_error() { (void)cudaGetLastError(); }
 int ilog2(int n) { int l = 0; while ((1 << l) < n) ++l; return l; }
 
 enum Path { PATH_LINES = 0, PATH_PLANE_DIRECT = 1, PATH_PLANE_FFT = 2 };
@@ -406,6 +411,7 @@ int32_t md_plan_create(const md_plan_desc *desc, md_plan **out) {
     *out = nullptr;
     int rc = validate(desc);
     if (rc) return rc;
+    clear_stale_error();
     md_plan *P = new md_plan();
     P->d = *desc;
     P->w.assign(desc->psf_weights, desc->psf_weights + (size_t)desc->psf_rows * desc->psf_cols);
@@ -444,8 +450,12 @@ int32_t md_plan_create(const md_plan_desc *desc, md_plan **out) {
         }
         P->fast_lines = !(desc->flags & MD_FLAG_GENERIC_LINES) &&
                         iter_fast_supported(desc->dtype, P->n, P->lblur, P->ladj);
-        if (is_pow2(P->n)) {
-            P->log2n = ilog2(P->n);
+        const size_t lim = desc->dtype == MD_F64 ? 4096 : 8192;
+        if (wiener && (size_t)P->n > lim) return bail(fail(MD_EINVAL, "blur-axis length above the on-chip FFT limit"));
+        if (desc->iterations > 0 && !P->fast_lines && !iter_lines_fits(desc->dtype, P->n, 2 * T))
+            return bail(fail(MD_EINVAL, "blur-axis length above the on-chip line-iteration limit"));
+        if (is_pow2(P->n)) P->log2n = ilog2(P->n);
+        if (is_pow2(P->n) && (size_t)P->n <= lim) {      // line FFT tables (Wiener step)
             if ((rc = build_twiddles(P->n, desc->dtype, &P->d_tw_n))) return bail(rc);
             std::vector<double> emb(P->n, 0.0);       // fft.py:192-201
             for (int j = 0; j < T; ++j) emb[((j - desc->center_row) % P->n + P->n) % P->n] = P->w[j];
@@ -466,8 +476,6 @@ int32_t md_plan_create(const md_plan_desc *desc, md_plan **out) {
             CU(cudaDeviceSynchronize());
             P->wiener_reg = !(desc->flags & MD_FLAG_GENERIC_LINES) && wiener_reg_supported(desc->dtype, P->n);
         }
-        const size_t lim = desc->dtype == MD_F64 ? 4096 : 8192;
-        if (wiener && (size_t)P->n > lim) return bail(fail(MD_EINVAL, "blur-axis length above the on-chip FFT limit"));
         // default: the cluster kernel for float (measured faster); float64 keeps the
         // per-iteration kernel (16-CTA clusters at one CTA per SM lose to it), opt-in via
         // md_plan_set_fused
@@ -936,8 +944,10 @@ int32_t md_plan_set_fused(md_plan *P, int32_t on) {
 int32_t md_plan_is_fused(const md_plan *P) { return P && (P->fused || P->fused_plane) ? 1 : 0; }
 
 int32_t md_run(md_plan *P, const void *f, void *u, int64_t batch, void *stream) {
-    if (!P || !f || !u || batch < 0) return fail(MD_EINVAL, "bad arguments");
-    if (batch == 0) return MD_OK;
+    if (!P || batch < 0) return fail(MD_EINVAL, "bad arguments");
+    if (batch == 0) return MD_OK;                   // empty batch: nothing to read (pointers may be null)
+    if (!f || !u) return fail(MD_EINVAL, "bad arguments");
+    clear_stale_error();
     if (f == u) return fail(MD_EINVAL, "input and output must not alias");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     return P->d.dtype == MD_F64 ? run_typed<double>(*P, f, u, batch, st) : run_typed<float>(*P, f, u, batch, st);
@@ -1011,11 +1021,13 @@ int32_t md_run_launch_count(const md_plan *P, int64_t batch) {
 
 int32_t md_run_host_ex(md_plan *P, const void *f, int32_t in_type, void *u, int32_t out_type, int64_t batch,
                        void *stream) {
-    if (!P || !f || !u || batch < 0) return fail(MD_EINVAL, "bad arguments");
+    if (!P || batch < 0) return fail(MD_EINVAL, "bad arguments");
     if (in_type != MD_IO_F64 && in_type != MD_IO_F32 && in_type != MD_IO_U8) return fail(MD_EINVAL, "bad input type");
     if (out_type != MD_IO_F64 && out_type != MD_IO_F32 && out_type != MD_IO_U8)
         return fail(MD_EINVAL, "bad output type");
     if (batch == 0) return MD_OK;
+    if (!f || !u) return fail(MD_EINVAL, "bad arguments");
+    clear_stale_error();
     cudaStream_t user = static_cast<cudaStream_t>(stream);
     const int64_t fe = P->frame_elems();
     const int ib = io_bytes(in_type), ob = io_bytes(out_type);
@@ -1096,6 +1108,7 @@ int32_t md_wiener(md_plan *P, const void *f, void *out, int64_t batch, void *str
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (P->path == PATH_LINES) {
         if (P->log2n < 0) return fail(MD_EINVAL, "the blur axis must have power-of-two extent");
+        if (!P->d_mult) return fail(MD_EINVAL, "blur-axis length above the on-chip FFT limit");
         WienerLinesArgs a{};
         a.in = f; a.out = out; a.fpos = nullptr; a.n = P->n; a.log2n = P->log2n; a.m = P->m;
         a.in_vert = P->vert; a.out_vert = P->vert; a.clamp = 0; a.mult = P->d_mult; a.tw = P->d_tw_n;

@@ -453,6 +453,13 @@ cudaError_t launch_clamp2(const void *in, void *o1, void *o2, int64_t n, double 
     return cudaGetLastError();
 }
 
+// the generic per-iteration line kernel keeps 5 tl + 6 padded lines on chip: it fits while one
+// line tile (tl = 1) stays within the opt-in shared memory of a block
+bool iter_lines_fits(int dtype, int n, int ntaps) {
+    const size_t smem = dtype == 0 ? iter_lines_smem<double>(n, 1, ntaps) : iter_lines_smem<float>(n, 1, ntaps);
+    return smem <= 227 * 1024;
+}
+
 #define MD_INST(T)                                                                                 \
     template cudaError_t launch_wiener_lines<T>(const WienerLinesArgs &, int64_t, cudaStream_t);    \
     template cudaError_t launch_iter_lines<T>(const IterLinesArgs &, bool, int64_t, cudaStream_t);  \

@@ -1,0 +1,109 @@
+"""Edge cases of the CUDA path against the CPU oracle: empty and ragged
+batches, extreme observations (all zero, saturated, impulse noise), the longest supported blur
+axis and the limits just past it. Oracle-checked at sizes the NumPy restatement finishes in
+seconds; bar max|d| <= 1e-4 * 255 (north_star)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4 * 255.0
+
+
+@pytest.fixture(scope="module")
+def md():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_1212_2245_b200 as md
+    return md
+
+
+def _oracle(md, f, psf, params, scenario):
+    from oracle import wr3l_oracle as O
+    if psf.kind.value == "box":
+        op = O.make_psf("box", axis="h" if psf.axis == md.BlurAxis.HORIZONTAL else "v", length=psf.length)
+    elif psf.kind.value == "1d":
+        op = O.make_psf("1d", weights=psf.weights, center=psf.center,
+                        axis="h" if psf.axis == md.BlurAxis.HORIZONTAL else "v")
+    else:
+        op = O.OPsf("2d", psf.weights, psf.center)
+    p = O.OParams(wiener_k=params.wiener_k, alpha=params.alpha, iterations=params.iterations,
+                  eps_data=params.eps_data, eps_reg=params.eps_reg, floor=params.floor)
+    return O.pipeline(np.asarray(f, dtype=np.float64), op, p, scenario)
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_empty_batch(md, dtype):
+    import torch
+    pipe = md.DeblurPipeline((64, 64), md.Psf.uniform_box(md.BlurAxis.HORIZONTAL, 7), md.DeconvParams(), dtype=dtype)
+    tdt = torch.float64 if dtype == "float64" else torch.float32
+    out = pipe.run_batch(torch.empty((0, 64, 64), device="cuda", dtype=tdt))
+    assert tuple(out.shape) == (0, 64, 64)
+    host = pipe.run_batch(np.empty((0, 64, 64), dtype=np.uint8), out_dtype=np.float32)
+    assert host.shape == (0, 64, 64)
+
+
+@pytest.mark.parametrize("n", [1, 3, 33, 35])
+def test_ragged_batch_sizes_fused(md, n):
+    """Batch sizes around the resident-cluster count of the fused kernel: each frame as alone."""
+    import torch
+    psf = md.Psf.uniform_box(md.BlurAxis.HORIZONTAL, 15)
+    pipe = md.DeblurPipeline((256, 256), psf, md.DeconvParams(), dtype="float32")
+    assert pipe.plan.fused
+    g = md.make_test_image(256, 256)
+    base = md.quantize(md.add_gaussian_noise(md.synth_blur(g, psf), 5.0, seed=1)).values
+    frames = np.stack([np.roll(base, 7 * i, axis=0) for i in range(n)])
+    out = pipe.run_batch(torch.from_numpy(frames).cuda().float()).cpu().numpy()
+    for i in (0, n - 1):
+        one = pipe.run_batch(torch.from_numpy(frames[i:i + 1]).cuda().float()).cpu().numpy()[0]
+        np.testing.assert_array_equal(out[i], one)
+
+
+@pytest.mark.parametrize("kind", ["zeros", "saturated", "impulse"])
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_extreme_observations_vs_oracle(md, kind, dtype):
+    """All-zero frames (every pixel on the floor), saturated frames and salt-and-pepper impulse
+    noise (the robust data term's case, deconv.py:142-180) match the oracle."""
+    psf = md.Psf.uniform_box(md.BlurAxis.HORIZONTAL, 9)
+    params = md.DeconvParams()
+    g = md.make_test_image(64, 128)
+    if kind == "zeros":
+        f = np.zeros((64, 128))
+    elif kind == "saturated":
+        f = np.full((64, 128), 255.0)
+    else:
+        f = md.synth_blur(g, psf).values.copy()
+        rng = np.random.default_rng(4)
+        hit = rng.random(f.shape) < 0.05
+        f[hit] = np.where(rng.random(hit.sum()) < 0.5, 0.0, 255.0)
+    out = md.DeblurPipeline(f.shape, psf, params, md.Scenario.BOX_1D, dtype=dtype).run(md.Image(f)).values
+    ref = _oracle(md, f, psf, params, "box")
+    assert np.isfinite(out).all()
+    assert np.abs(out - ref).max() <= TOL
+
+
+def test_longest_lines_vs_oracle(md):
+    """The longest float32 blur axes: 4096-sample lines through Wiener + RRRL (the line-iteration
+    kernel's on-chip limit) and 8192-sample lines through the Wiener step alone (the line FFT's)."""
+    psf = md.Psf.uniform_box(md.BlurAxis.HORIZONTAL, 15)
+    for n, iters in ((4096, 2), (8192, 0)):
+        params = md.DeconvParams(iterations=iters)
+        g = md.make_test_image(n, 16)
+        f = md.quantize(md.add_gaussian_noise(md.synth_blur(g, psf), 5.0, seed=2)).values
+        out = md.DeblurPipeline(f.shape, psf, params, dtype="float32").run(md.Image(f)).values
+        ref = _oracle(md, f, psf, params, "box")
+        assert np.abs(out - ref).max() <= TOL, n
+
+
+def test_limits_raise(md):
+    """Past the on-chip limits -- line FFT (Wiener), line iteration -- and non-power-of-two blur
+    axes, plan creation raises ValueError (the reference's own ValueError cases, fft.py:63-66)."""
+    psf = md.Psf.uniform_box(md.BlurAxis.HORIZONTAL, 15)
+    for shape, dtype, iters in (((16, 16384), "float32", 0), ((16, 8192), "float64", 0),
+                                ((16, 8192), "float32", 5), ((16, 4096), "float64", 5), ((16, 100), "float64", 5)):
+        with pytest.raises(ValueError):
+            md.DeblurPipeline(shape, psf, md.DeconvParams(iterations=iters), dtype=dtype)
