@@ -484,7 +484,7 @@ int32_t md_plan_create(const md_plan_desc *desc, md_plan **out) {
         if (P->fused) P->fused_clusters = lines_fused_clusters<float>(*P);
         snprintf(buf, sizeof buf, "lines: n=%d m=%d %s %s %s, %s", P->n, P->m, P->vert ? "vertical" : "horizontal",
                  use_box ? "box" : "taps", periodic ? "periodic" : "clamped",
-                 P->fused ? "fused persistent iteration kernel"
+                 P->fused ? "fused cluster iteration kernel"
                           : (P->fast_lines ? "k_wiener_lines + k_iter_lines_fast per iteration"
                                            : "k_wiener_lines + k_iter_lines per iteration"));
     } else {
