@@ -27,50 +27,6 @@ namespace cg = cooperative_groups;
 
 namespace md {
 
-// window convolution of 8 outputs: dense taps over [-R, R] (constant-bank FMAs), or, for a
-// box (equal interior weights) of radius BOXR (= R), an O(1)-per-output sliding sum over
-// [-R, R] plus weight corrections at k = -R, -R+1, R-1, R (even-length and fractional boxes:
-// deconv.py box convolver, conv.py:141-173)
-template <typename T, int R, int BOXR, bool BOXC>
-__device__ __forceinline__ void conv_window(const T (&v)[SEG + 2 * R], const DenseTaps<T, R> &taps, T box_wi,
-                                            const T (&corr)[4], T out[SEG]) {
-    if constexpr (BOXR > 0) {
-        static_assert(BOXR == R, "box window radius must equal the register window radius");
-        // short dependency chains (few warps per scheduler): the first window by a pairwise
-        // tree, then the running sum over precomputed entering-minus-leaving differences
-        T t[2 * R + 1];
-#pragma unroll
-        for (int i = 0; i <= 2 * R; ++i) t[i] = v[i];
-#pragma unroll
-        for (int w = 1; w <= 2 * R; w *= 2)
-#pragma unroll
-            for (int i = 0; i + w <= 2 * R; i += 2 * w) t[i] += t[i + w];
-        T d[SEG];
-#pragma unroll
-        for (int r = 1; r < SEG; ++r) d[r] = v[r + 2 * R] - v[r - 1];
-        T s = t[0];
-        out[0] = s * box_wi;
-#pragma unroll
-        for (int r = 1; r < SEG; ++r) {
-            s += d[r];
-            out[r] = s * box_wi;
-        }
-        if constexpr (BOXC) {
-#pragma unroll
-            for (int r = 0; r < SEG; ++r)
-                out[r] += corr[0] * v[r] + corr[1] * v[r + 1] + corr[2] * v[r + 2 * R - 1] + corr[3] * v[r + 2 * R];
-        }
-    } else {
-#pragma unroll
-        for (int r = 0; r < SEG; ++r) {
-            T acc = T(0);
-#pragma unroll
-            for (int k = -R; k <= R; ++k) acc += taps.w[k + R] * v[r + k + R];
-            out[r] = acc;
-        }
-    }
-}
-
 constexpr int FU_WARPS = 8;
 
 template <typename T, int R> struct FusedKArgs {
@@ -86,24 +42,6 @@ template <typename T, int R> struct FusedKArgs {
     T box_wi;           // box specialisation: interior weight
     T box_cb[4], box_ca[4];   // weight corrections at k = -R, -R+1, R-1, R (blur, adjoint)
 };
-
-// host: a box line convolution as interior weight wi over [-R, R] plus corrections at
-// k = -R, -R+1, R-1, R; false when it has no such form (then the dense path runs)
-template <typename T, int R>
-bool box_corrections(const LineConv &c, double wi, T corr[4]) {
-    DenseTaps<T, R> d;
-    fill_dense<T, R>(d, c, nullptr);
-    for (int k = -R + 2; k <= R - 2; ++k)
-        if (d.w[k + R] != T(wi)) return false;
-    if (R == 1) {                                    // k = -R+1 = R-1 = 0: must be interior
-        if (d.w[1] != T(wi)) return false;
-        corr[0] = d.w[0] - T(wi); corr[1] = corr[2] = T(0); corr[3] = d.w[2] - T(wi);
-        return true;
-    }
-    const int ks[4] = {-R, -R + 1, R - 1, R};
-    for (int i = 0; i < 4; ++i) corr[i] = d.w[ks[i] + R] - T(wi);
-    return true;
-}
 
 __device__ __forceinline__ int fu_wrap(int j, int n, int periodic) {
     // halos never exceed the extent, so one conditional wrap suffices (no integer modulo)

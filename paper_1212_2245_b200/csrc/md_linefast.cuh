@@ -27,6 +27,51 @@ __host__ __device__ constexpr int koff(int k) { return k + (k >= 0 ? k / 8 : -((
 
 template <typename T, int R> struct DenseTaps { T w[2 * R + 1]; };
 
+// window convolution of 8 outputs: dense taps over [-R, R] (constant-bank FMAs), or, for a
+// box (equal interior weights) of radius BOXR (= R), an O(1)-per-output sliding sum over
+// [-R, R] plus weight corrections at k = -R, -R+1, R-1, R (even-length and fractional boxes:
+// deconv.py box convolver, conv.py:141-173)
+template <typename T, int R, int BOXR, bool BOXC>
+__device__ __forceinline__ void conv_window(const T (&v)[SEG + 2 * R], const DenseTaps<T, R> &taps, T box_wi,
+                                            const T (&corr)[4], T out[SEG]) {
+    if constexpr (BOXR > 0) {
+        static_assert(BOXR == R, "box window radius must equal the register window radius");
+        // short dependency chains (few warps per scheduler): the first window by a pairwise
+        // tree, then the running sum over precomputed entering-minus-leaving differences
+        T t[2 * R + 1];
+#pragma unroll
+        for (int i = 0; i <= 2 * R; ++i) t[i] = v[i];
+#pragma unroll
+        for (int w = 1; w <= 2 * R; w *= 2)
+#pragma unroll
+            for (int i = 0; i + w <= 2 * R; i += 2 * w) t[i] += t[i + w];
+        T d[SEG];
+#pragma unroll
+        for (int r = 1; r < SEG; ++r) d[r] = v[r + 2 * R] - v[r - 1];
+        T s = t[0];
+        out[0] = s * box_wi;
+#pragma unroll
+        for (int r = 1; r < SEG; ++r) {
+            s += d[r];
+            out[r] = s * box_wi;
+        }
+        if constexpr (BOXC) {
+#pragma unroll
+            for (int r = 0; r < SEG; ++r)
+                out[r] += corr[0] * v[r] + corr[1] * v[r + 1] + corr[2] * v[r + 2 * R - 1] + corr[3] * v[r + 2 * R];
+        }
+    } else {
+#pragma unroll
+        for (int r = 0; r < SEG; ++r) {
+            T acc = T(0);
+#pragma unroll
+            for (int k = -R; k <= R; ++k) acc += taps.w[k + R] * v[r + k + R];
+            out[r] = acc;
+        }
+    }
+}
+
+
 // fast reciprocal / reciprocal square root / log: one MUFU op for float (operands here are
 // positive normal numbers: b >= 1e-12, fpos >= floor, q + eps^2 > 0), Newton-refined for double
 __device__ __forceinline__ float frcp(float x) {
