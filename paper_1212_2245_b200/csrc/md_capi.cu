@@ -202,6 +202,13 @@ struct md_plan {
         return MD_OK;
     }
     int fused_clusters = 0;     // resident clusters of the fused-lines kernel (0 = unknown)
+    // concurrent use: host-side enqueue under a per-plan lock; a call on another stream than the
+    // previous one waits (device side) for it, since both would use the plan's scratch
+    std::recursive_mutex mu;
+    int use_depth = 0;
+    cudaEvent_t use_done = nullptr;
+    cudaStream_t use_stream = nullptr;
+    bool use_any = false;
     bool fused = false;         // whole-iteration-loop fused kernel applies
     bool fused_plane = false;   // cluster-resident 2D iteration loop (md_fused_plane.cu)
     bool fast_lines = false;    // register-window iteration kernel applies
@@ -223,6 +230,7 @@ struct md_plan {
             if (ev_done[s]) cudaEventDestroy(ev_done[s]);
         }
         if (ev_start) cudaEventDestroy(ev_start);
+        if (use_done) cudaEventDestroy(use_done);
     }
 };
 
@@ -392,6 +400,33 @@ int validate(const md_plan_desc *d) {
 template <typename T> int lines_fused_clusters(md_plan &P);
 
 }  // namespace
+
+// RAII guard of an entry point that uses a plan's scratch (see md_plan::mu)
+class PlanUse {
+  public:
+    PlanUse(md_plan *P, cudaStream_t st) : P_(P), st_(st), lk_(P->mu) {
+        outer_ = P_->use_depth++ == 0;
+        if (outer_ && P_->use_any && P_->use_stream != st_) cudaStreamWaitEvent(st_, P_->use_done, 0);
+    }
+    ~PlanUse() {
+        if (outer_) {
+            if (P_->use_done || cudaEventCreateWithFlags(&P_->use_done, cudaEventDisableTiming) == cudaSuccess) {
+                cudaEventRecord(P_->use_done, st_);
+                P_->use_stream = st_;
+                P_->use_any = true;
+            }
+        }
+        --P_->use_depth;
+    }
+    PlanUse(const PlanUse &) = delete;
+    PlanUse &operator=(const PlanUse &) = delete;
+
+  private:
+    md_plan *P_;
+    cudaStream_t st_;
+    std::unique_lock<std::recursive_mutex> lk_;
+    bool outer_ = false;
+};
 
 // ======================================================================== C ABI
 extern "C" {
@@ -921,12 +956,14 @@ int64_t md_plan_scratch_bytes(const md_plan *P, int64_t batch) {
 
 int32_t md_plan_set_chunk(md_plan *P, int64_t frames) {
     if (!P || frames < 0) return fail(MD_EINVAL, "bad chunk");
+    std::lock_guard<std::recursive_mutex> lock(P->mu);
     P->chunk = frames;
     return MD_OK;
 }
 
 int32_t md_plan_set_fused(md_plan *P, int32_t on) {
     if (!P) return fail(MD_EINVAL, "null plan");
+    std::lock_guard<std::recursive_mutex> lock(P->mu);
     if (P->path == PATH_PLANE_DIRECT) {
         if (on && !(P->fast_plane && !P->big &&
                     fused_plane_supported(P->d.height, P->d.width, P->hblur, P->hadj, P->htaps_blur, P->htaps_adj, P->d.dtype)))
@@ -950,12 +987,14 @@ int32_t md_run(md_plan *P, const void *f, void *u, int64_t batch, void *stream) 
     clear_stale_error();
     if (f == u) return fail(MD_EINVAL, "input and output must not alias");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    PlanUse use(P, st);
     return P->d.dtype == MD_F64 ? run_typed<double>(*P, f, u, batch, st) : run_typed<float>(*P, f, u, batch, st);
 }
 
 int32_t md_run_profile(md_plan *P, const void *f, void *u, int64_t batch, void *stream, double *ms_out) {
     if (!P || !ms_out) return fail(MD_EINVAL, "bad arguments");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    PlanUse use(P, st);
     Prof *pr = &g_prof_pool;
     pr->n = 0;
     cudaEventRecord(pr->get(0), st);
@@ -979,6 +1018,7 @@ int32_t md_run_profile_groups(md_plan *P, const void *f, void *u, int64_t batch,
                               int32_t *group_kind, int32_t max_groups, int32_t *n_groups) {
     if (!P || !group_ms || !group_kind || !n_groups || max_groups < 1) return fail(MD_EINVAL, "bad arguments");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    PlanUse use(P, st);
     Prof *pr = &g_prof_pool;
     pr->n = 0;
     cudaEventRecord(pr->get(0), st);
@@ -1029,6 +1069,7 @@ int32_t md_run_host_ex(md_plan *P, const void *f, int32_t in_type, void *u, int3
     if (!f || !u) return fail(MD_EINVAL, "bad arguments");
     clear_stale_error();
     cudaStream_t user = static_cast<cudaStream_t>(stream);
+    PlanUse use(P, user);
     const int64_t fe = P->frame_elems();
     const int ib = io_bytes(in_type), ob = io_bytes(out_type);
     // pipeline: chunk c runs H2D -> convert -> pipeline -> convert -> D2H on internal stream
@@ -1106,6 +1147,7 @@ int32_t md_wiener(md_plan *P, const void *f, void *out, int64_t batch, void *str
     if (!P || !f || !out || batch < 0) return fail(MD_EINVAL, "bad arguments");
     if (batch == 0) return MD_OK;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    PlanUse use(P, st);
     if (P->path == PATH_LINES) {
         if (P->log2n < 0) return fail(MD_EINVAL, "the blur axis must have power-of-two extent");
         if (!P->d_mult) return fail(MD_EINVAL, "blur-axis length above the on-chip FFT limit");
@@ -1232,6 +1274,7 @@ int32_t md_convolve(md_plan *P, const void *in, void *out, int64_t batch, int32_
     if (batch == 0) return MD_OK;
     if (in == out) return fail(MD_EINVAL, "input and output must not alias");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    PlanUse use(P, st);
     return P->d.dtype == MD_F64 ? convolve_typed<double>(*P, in, out, batch, which, st)
                                 : convolve_typed<float>(*P, in, out, batch, which, st);
 }
@@ -1240,6 +1283,7 @@ int32_t md_adjoint_pair(md_plan *P, const void *p, const void *q, void *op, void
     if (!P || !p || !q || !op || !oq || batch < 0) return fail(MD_EINVAL, "bad arguments");
     if (batch == 0) return MD_OK;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    PlanUse use(P, st);
     return P->d.dtype == MD_F64 ? adjoint_pair_typed<double>(*P, p, q, op, oq, batch, st)
                                 : adjoint_pair_typed<float>(*P, p, q, op, oq, batch, st);
 }
@@ -1309,6 +1353,7 @@ int32_t md_rrrl_step(md_plan *P, const void *u, const void *f, const void *b, co
     if (!P || !u || !f || !b || !out || batch < 0) return fail(MD_EINVAL, "bad arguments");
     if (batch == 0) return MD_OK;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    PlanUse use(P, st);
     const int64_t n = P->frame_elems() * batch;
     const size_t fb = (size_t)n * P->es;
     int rc = P->stage.ensure(4 * fb);
@@ -1405,6 +1450,7 @@ int32_t md_slab_rows_fft(md_plan *P, void *z, const void *real_in, int32_t rows,
     int rc = slab_check(P);
     if (rc) return rc;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    PlanUse use(P, st);
     const int W = P->d.width;
     CU(P->d.dtype == MD_F64 ? big_axis<double>(P->bigW, z, rows, W, 1, inv, real_in, nullptr, nullptr, 0, scale, 1, st)
                             : big_axis<float>(P->bigW, z, rows, W, 1, inv, real_in, nullptr, nullptr, 0, scale, 1, st));
@@ -1415,6 +1461,7 @@ int32_t md_slab_cols_filter(md_plan *P, void *zc, int32_t cols, const void *mult
     int rc = slab_check(P);
     if (rc) return rc;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    PlanUse use(P, st);
     const int H = P->d.height;
     CU(P->d.dtype == MD_F64 ? big_axis_filter<double>(P->bigH, zc, H, cols, 0, mult_block, 0, 1, st)
                             : big_axis_filter<float>(P->bigH, zc, H, cols, 0, mult_block, 0, 1, st));
@@ -1426,6 +1473,7 @@ int32_t md_slab_wiener_epilogue(md_plan *P, const void *z, const void *f, void *
     int rc = slab_check(P);
     if (rc) return rc;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    PlanUse use(P, st);
     const int64_t n = (int64_t)rows * P->d.width;
     const double scale = 1.0 / ((double)P->d.height * P->d.width);
     CU(P->d.dtype == MD_F64 ? launch_big_wiener_epilogue<double>(z, f, u0, fpos, n, scale, P->d.floor, 1, st)
@@ -1438,6 +1486,7 @@ int32_t md_slab_iterate(md_plan *P, const void *u, const void *fpos, void *p, vo
     int rc = slab_check(P);
     if (rc) return rc;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    PlanUse use(P, st);
     PlaneFastDesc s{};
     s.u = u; s.f = fpos; s.p = p; s.w = w; s.u_out = u_out;     // all point at own row 0 of haloed buffers
     s.H = rows; s.W = P->d.width; s.periodic = P->periodic;
