@@ -175,11 +175,12 @@ k_fft2_rows(Fft2Args a, int rb) {
 
 template <typename T>
 __global__ void __launch_bounds__(256)
-k_fft2_cols(Fft2Args a, int cw) {
+k_fft2_cols(Fft2Args a, int lcw) {
     using C = cx_t<T>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C *s = reinterpret_cast<C *>(smem_raw);
     const int H = a.H, W = a.W, cs = fline_stride(H);      // padded column stride (md_fft.cuh)
+    const int cw = 1 << lcw, lh = a.log2H;                  // powers of two: shifts, no division
     const int x0 = blockIdx.x * cw;
     const int64_t base = blockIdx.y * (int64_t)H * W;
     C *z = static_cast<C *>(a.z);
@@ -189,7 +190,7 @@ k_fft2_cols(Fft2Args a, int cw) {
         for (int k = threadIdx.x; k < (H >> 1); k += blockDim.x) tw[k] = twg[k];
     }
     for (int idx = threadIdx.x; idx < cw * H; idx += blockDim.x) {
-        const int y = idx / cw, c = idx - y * cw;
+        const int y = idx >> lcw, c = idx & (cw - 1);
         if (x0 + c < W) s[c * cs + fpad(y)] = z[base + (int64_t)y * W + x0 + c];
         else s[c * cs + fpad(y)] = mkc<T>(T(0), T(0));
     }
@@ -198,7 +199,7 @@ k_fft2_cols(Fft2Args a, int cw) {
     if (a.filt) {
         const C *filt = static_cast<const C *>(a.filt);
         for (int idx = threadIdx.x; idx < cw * H; idx += blockDim.x) {
-            const int c = idx / H, y = idx - c * H;
+            const int c = idx >> lh, y = idx & (H - 1);
             if (x0 + c >= W) continue;
             const C f = __ldg(filt + (int64_t)y * W + x0 + c);
             s[c * cs + fpad(y)] = a.conj_filt ? cmulc(s[c * cs + fpad(y)], f) : cmul(s[c * cs + fpad(y)], f);
@@ -207,7 +208,7 @@ k_fft2_cols(Fft2Args a, int cw) {
     }
     if (a.col_inv && a.log2H > 0) fft_dit_inv_lines(s, a.log2H, cw, cs, tw);
     for (int idx = threadIdx.x; idx < cw * H; idx += blockDim.x) {
-        const int y = idx / cw, c = idx - y * cw;
+        const int y = idx >> lcw, c = idx & (cw - 1);
         if (x0 + c < W) z[base + (int64_t)y * W + x0 + c] = s[c * cs + fpad(y)];
     }
 }
@@ -244,7 +245,9 @@ cudaError_t launch_fft2_rows(const Fft2Args &a, int64_t batch, cudaStream_t st) 
 template <typename T>
 cudaError_t launch_fft2_cols(const Fft2Args &a, int64_t batch, cudaStream_t st) {
     int cw = 4096 / a.H;
-    cw = cw > 16 ? 16 : (cw < 1 ? 1 : cw);
+    cw = cw > 16 ? 16 : (cw < 1 ? 1 : cw);          // a power of two (H is)
+    int lcw = 0;
+    while ((1 << lcw) < cw) ++lcw;
     const size_t smem = ((size_t)cw * fline_stride(a.H) + a.H / 2 + 1) * sizeof(cx_t<T>);
     cudaError_t e = cudaFuncSetAttribute(k_fft2_cols<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -253,7 +256,7 @@ cudaError_t launch_fft2_cols(const Fft2Args &a, int64_t batch, cudaStream_t st) 
         const int nb = (int)((batch - b0) < 65535 ? (batch - b0) : 65535);
         Fft2Args ab = a;
         ab.z = static_cast<char *>(a.z) + b0 * fr * sizeof(cx_t<T>);
-        k_fft2_cols<T><<<dim3((a.W + cw - 1) / cw, nb), 256, smem, st>>>(ab, cw);
+        k_fft2_cols<T><<<dim3((a.W + cw - 1) / cw, nb), 256, smem, st>>>(ab, lcw);
     }
     return cudaGetLastError();
 }
