@@ -46,9 +46,10 @@ def peaks() -> dict:
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
             d = json.load(fh)
-        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+        return {"hbm_gbs": float(d["hbm_gbs"]), "sm_max_mhz": float(d.get("sm_max_mhz", 1965.0)),
+                "source": "measured (MEASURED_PEAKS.json)"}
     except Exception:
-        return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "source": "fallback (B200_PROFILING.md)"}
 
 
 def measured_traffic(key: str, frames: int):
@@ -58,6 +59,17 @@ def measured_traffic(key: str, frames: int):
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
             d = json.load(fh)[key]
         return (d["dram_bytes_read"] + d["dram_bytes_write"]) / d["frames"] * frames
+    except Exception:
+        return None
+
+
+def measured_smem(key: str, frames: int):
+    """Shared-memory wavefronts (128 B) of the dominant kernel for `frames` frames, from the
+    committed ncu capture, or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            d = json.load(fh)[key]
+        return d["smem_wavefronts"] / d["frames"] * frames
     except Exception:
         return None
 
@@ -610,6 +622,20 @@ def main() -> None:
             cpu = {"value": r, "unit": "frames/s", "cores": cores, "kind": "port",
                    "sample": f"{sum(len(j) for j in jobs)} frames of this workload ({wall:.1f} s wall) through "
                              "oracle/wr3l_oracle.pipeline (NumPy float64), one process per host core"}
+        # the fused kernel keeps the iterate on chip, so its other roofline is the shared-memory
+        # pipe (north_star: "HBM (or SMEM for fused in-cluster)"): ncu wavefronts per frame over
+        # this run's iteration time, against SMs x 128 B/clk x the max SM clock
+        smem_roof = None
+        wf = measured_smem(f"{args.config}_{args.dtype}", args.batch) if work.fused else None
+        if wf and prof["iter_ms"] > 0:
+            sms = torch.cuda.get_device_properties(local).multi_processor_count
+            ach = wf * 128 * args.steps / (prof["iter_ms"] / 1e3) / 1e12
+            pk_s = sms * 128 * pk["sm_max_mhz"] * 1e6 / 1e12
+            smem_roof = {"bound": "smem", "kernel": "RRRL iteration (fused cluster kernel)", "achieved": ach,
+                         "peak": pk_s, "unit": "TB/s", "frac": ach / pk_s,
+                         "wavefronts_per_frame": wf / args.batch,
+                         "source": "ncu l1tex__data_pipe_lsu_wavefronts_mem_shared.sum (profiles/ncu_traffic.json) "
+                                   "over this run's iteration time; peak = SMs x 128 B/clk x max SM clock"}
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
@@ -635,6 +661,7 @@ def main() -> None:
                          "peak_source": pk["source"],
                          "bytes_model": "SURVEY.md 8(d): 8 field passes per RRRL iteration x 65536 px x "
                                         f"{esz} B per frame; time = CUDA events around the iteration launches"},
+            "roofline_smem": smem_roof,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": e2e_in,
                     "d2h_bytes_per_step": e2e_out, "frames_per_step": nb,
