@@ -33,7 +33,9 @@ k_subfft(SubFftArgs a) {
     C *z = static_cast<C *>(a.z) + fr * a.frame;
     const T *ra = a.ra ? static_cast<const T *>(a.ra) + fr * a.rframe : nullptr;
     const T *rb = a.rb ? static_cast<const T *>(a.rb) + fr * a.rframe : nullptr;
-    const int64_t base = (int64_t)ai * a.sa + (int64_t)b0 * a.sb;
+    // offsets within a frame fit 32 bits (launch_subfft checks frame < 2^31): cheaper address math
+    const int sb = (int)a.sb, es = (int)a.es;
+    const int base = ai * (int)a.sa + b0 * sb;
     constexpr bool line_fast = LINE_FAST;      // contiguous lines: iterate along the line
     constexpr int U = 4;                       // global loads in flight per thread
     const int n = G * L, bd = blockDim.x;
@@ -51,7 +53,7 @@ k_subfft(SubFftArgs a) {
             coords(idx, g, e);
             v[k] = mkc<T>(T(0), T(0));
             if (idx < n && b0 + g < a.B) {
-                const int64_t o = base + (int64_t)g * a.sb + (int64_t)e * a.es;
+                const int o = base + g * sb + e * es;
                 if (ra) v[k] = mkc<T>(ra[o], rb ? rb[o] : T(0));
                 else v[k] = z[o];
             }
@@ -75,7 +77,7 @@ k_subfft(SubFftArgs a) {
             int g, e;
             coords(idx, g, e);
             if (b0 + g >= a.B) continue;
-            const C fl = filt[base + (int64_t)g * a.sb + (int64_t)e * a.es];
+            const C fl = filt[base + g * sb + e * es];
             C &v = s[g * ls + fpad(e)];
             v = a.conj_filt ? cmulc(v, fl) : cmul(v, fl);
         }
@@ -114,7 +116,7 @@ k_subfft(SubFftArgs a) {
                 const C w = twN[kk & (N / 2 - 1)];
                 tw[k] = kk < N / 2 ? w : mkc<T>(-w.x, -w.y);
             }
-            if (FILT_EPI && filt) fl[k] = filt[base + (int64_t)g * a.sb + (int64_t)e * a.es];
+            if (FILT_EPI && filt) fl[k] = filt[base + g * sb + e * es];
         }
 #pragma unroll
         for (int k = 0; k < U; ++k) {
@@ -126,7 +128,7 @@ k_subfft(SubFftArgs a) {
             if (TWM != TW_NONE) v = TWM == TW_FWD ? cmul(v, tw[k]) : cmulc(v, tw[k]);
             if (FILT_EPI && filt) v = a.conj_filt ? cmulc(v, fl[k]) : cmul(v, fl[k]);
             if (scale != T(1)) v = cscale(v, scale);
-            const int64_t o = base + (int64_t)g * a.sb + (int64_t)e * a.es;
+            const int o = base + g * sb + e * es;
             if (TW == TW_NONE && wu) {
                 // Wiener epilogue (deconv.py:666-672): real part, clamp, floored observation
                 const T x = v.x;
@@ -160,6 +162,7 @@ __global__ void k_big_wiener_epilogue(const void *z_, const T *__restrict__ f, T
 
 template <typename T>
 cudaError_t launch_subfft(const SubFftArgs &a0, int64_t batch, cudaStream_t st) {
+    if (a0.frame >= (1ll << 31)) return cudaErrorNotSupported;     // 32-bit in-frame offsets
     SubFftArgs a = a0;
     const int L = 1 << a.log2L;
     a.G = std::max(1, std::min(16, 2048 / L));   // power of two (L is)
