@@ -81,6 +81,7 @@ SIGNATURES = {
     "md_lut_r1": (_I32, [_I32, _P, _P, _I64, _P]),
     "md_lut_table": (_I32, [ctypes.POINTER(_D), _I64]),
     "md_min": (_I32, [_I32, _P, _I64, ctypes.POINTER(_D), _P]),
+    "md_fft": (_I32, [_I32, _P, _I32, _I64, _I32, _P]),
     "md_slab_halo": (_I32, [_P, ctypes.POINTER(_I32), ctypes.POINTER(_I32)]),
     "md_slab_prepare": (_I32, [_P, _I32, _I32, ctypes.POINTER(_P)]),
     "md_slab_rows_fft": (_I32, [_P, _P, _P, _I32, _I32, _D, _P]),

@@ -17,7 +17,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -1366,6 +1368,63 @@ int32_t md_rrrl_step(md_plan *P, const void *u, const void *f, const void *b, co
     if (!d) alpha = 0.0;
     CU(f64 ? launch_combine<double>(u, NUM, w ? DEN : nullptr, d, out, n, alpha, st)
            : launch_combine<float>(u, NUM, w ? DEN : nullptr, d, out, n, alpha, st));
+    return MD_OK;
+}
+
+// natural-order complex transforms of `lines` contiguous lines of length n, in place
+// (FourierPlan.forward / inverse, fft.py:52-117): tables per (n, dtype) built once
+int32_t md_fft(int32_t dtype, void *z, int32_t n, int64_t lines, int32_t inverse, void *stream) {
+    if ((dtype != MD_F64 && dtype != MD_F32) || lines < 0 || n < 1 || n > 65536 || !is_pow2(n))
+        return fail(MD_EINVAL, "transform length must be a power of two in [1, 65536]");
+    if (lines == 0 || n == 1) return MD_OK;               // length 1: the identity both ways
+    if (!z) return fail(MD_EINVAL, "bad arguments");
+    clear_stale_error();
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    struct Tables { void *tw = nullptr; BigAxis ax{}; std::vector<void *> owned; };
+    static std::mutex mu;
+    static std::map<std::tuple<int, int, int>, Tables> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const bool single = n <= (dtype == MD_F64 ? fft_lines_max_single<double>() : fft_lines_max_single<float>());
+    Tables *tb;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        auto key = std::make_tuple(n, dtype, dev);
+        auto it = cache.find(key);
+        if (it == cache.end()) {
+            Tables t;
+            int rc = single ? build_twiddles(n, dtype, &t.tw) : build_big_axis(n, dtype, &t.ax, t.owned);
+            if (rc) return rc;
+            it = cache.emplace(key, std::move(t)).first;
+        }
+        tb = &it->second;
+    }
+    if (single) {
+        CU(dtype == MD_F64 ? launch_fft_lines_nat<double>(z, n, lines, tb->tw, inverse ? 1 : 0, st)
+                           : launch_fft_lines_nat<float>(z, n, lines, tb->tw, inverse ? 1 : 0, st));
+        return MD_OK;
+    }
+    if (lines * (int64_t)n >= (1ll << 31)) return fail(MD_EINVAL, "too many elements for one two-level transform");
+    const size_t bytes = (size_t)lines * n * (dtype == MD_F64 ? 16 : 8);
+    void *tmp = nullptr;
+    CU(cudaMallocAsync(&tmp, bytes, st));
+    cudaError_t e;
+    if (!inverse) {
+        e = dtype == MD_F64 ? big_axis<double>(tb->ax, z, (int)lines, n, 1, 0, nullptr, nullptr, nullptr, 0, 1.0, 1, st)
+                            : big_axis<float>(tb->ax, z, (int)lines, n, 1, 0, nullptr, nullptr, nullptr, 0, 1.0, 1, st);
+        if (e == cudaSuccess)
+            e = dtype == MD_F64 ? launch_fft_perm<double>(z, tmp, tb->ax, lines, 1, st)
+                                : launch_fft_perm<float>(z, tmp, tb->ax, lines, 1, st);
+    } else {
+        e = dtype == MD_F64 ? launch_fft_perm<double>(z, tmp, tb->ax, lines, 0, st)
+                            : launch_fft_perm<float>(z, tmp, tb->ax, lines, 0, st);
+        if (e == cudaSuccess)
+            e = dtype == MD_F64 ? big_axis<double>(tb->ax, tmp, (int)lines, n, 1, 1, nullptr, nullptr, nullptr, 0, 1.0 / n, 1, st)
+                                : big_axis<float>(tb->ax, tmp, (int)lines, n, 1, 1, nullptr, nullptr, nullptr, 0, 1.0 / n, 1, st);
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(z, tmp, bytes, cudaMemcpyDeviceToDevice, st);
+    cudaFreeAsync(tmp, st);
+    CU(e);
     return MD_OK;
 }
 

@@ -51,6 +51,13 @@ cudaError_t big_axis_filter(const BigAxis &ax, void *z, int H, int W, int axis, 
 template <typename T>
 cudaError_t big_axis_inv_wiener(const BigAxis &ax, void *z, int H, int W, int axis, double scale, const void *f,
                                 void *u, void *fpos, double floor, int clamp, int64_t batch, cudaStream_t st);
+// natural-order transforms of contiguous lines (md_fft_api.cu)
+template <typename T> int fft_lines_max_single();
+template <typename T>
+cudaError_t launch_fft_lines_nat(void *z, int n, int64_t lines, const void *tw, int inverse, cudaStream_t st);
+template <typename T>
+cudaError_t launch_fft_perm(const void *in, void *out, const BigAxis &ax, int64_t lines, int to_natural,
+                            cudaStream_t st);
 template <typename T>
 cudaError_t launch_big_wiener_epilogue(const void *z, const void *f, void *u, void *fpos, int64_t n, double scale,
                                        double floor, int clamp, cudaStream_t st);

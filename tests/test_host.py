@@ -175,3 +175,24 @@ class TestPsfBankGrouping:
         assert PsfBankPipeline.groups(None, np.array([], dtype=np.int64)) == []
         with pytest.raises(ValueError):
             PsfBankPipeline.groups(None, np.array([1, 0]))
+
+
+def test_fft_api_host_side():
+    """Host-side pieces of the transform API (paper_1212_2245_b200/fft.py): PSF embedding equals
+    the oracle's (fft.py:192-221), plan validation as the reference (fft.py:62-66), and no CPU
+    fallback for the transform itself."""
+    import paper_1212_2245_b200 as md
+    from oracle import wr3l_oracle as O
+    box = md.Psf.uniform_box(md.BlurAxis.VERTICAL, 7.5)
+    np.testing.assert_array_equal(md.embed_psf_1d(box, 32), O.embed_1d(O.make_psf("box", axis="v", length=7.5), 32))
+    line = md.Psf.line(9.0, 30.0)
+    np.testing.assert_array_equal(md.embed_psf_2d(line, (32, 64)), O.embed_2d(O.OPsf("2d", line.weights, line.center), (32, 64)))
+    for n in (0, 3, 1 << 17):
+        with pytest.raises(ValueError):
+            md.FourierPlan(n)
+    with pytest.raises(ValueError):
+        md.embed_psf_1d(md.Psf.uniform_box(md.BlurAxis.VERTICAL, 31), 16)
+    import torch
+    if not torch.cuda.is_available():
+        with pytest.raises((md._lib.CudaUnavailable, RuntimeError)):
+            md.plan_fft(8).forward(np.ones(8))
