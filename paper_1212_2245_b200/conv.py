@@ -8,10 +8,12 @@ convolution (fft.py:283-307), realised by direct wrap-around taps or 2D FFTs.
 
 from __future__ import annotations
 
-from .core import Image, Psf, PsfKind
+import numpy as np
+
+from .core import BlurAxis, Image, Psf, PsfKind, materialize_box_kernel
 from .deconv import _dev, _image, make_convolver
 
-__all__ = ["spatial_convolve", "box_convolve", "fourier_convolve"]
+__all__ = ["spatial_convolve", "box_convolve", "fourier_convolve", "convolve_array", "box_filter_array"]
 
 
 def _check_support(psf: Psf, shape) -> None:
@@ -40,3 +42,17 @@ def fourier_convolve(image: Image, psf: Psf, plans=None) -> Image:
     """Circular convolution (fft.py:283-307); transformed axes must be powers of two."""
     c = make_convolver(psf, image.shape, "fourier2d" if psf.kind is PsfKind.GENERAL_2D else "fourier")
     return _image(c._plan.convolve(_dev(image), 0))
+
+
+def convolve_array(a: np.ndarray, psf: Psf) -> np.ndarray:
+    """Array-level direct-summation convolution (conv.py:85-116; see spatial_convolve)."""
+    return spatial_convolve(Image(np.asarray(a, dtype=np.float64)), psf).values
+
+
+def box_filter_array(a: np.ndarray, length: float, center: int, axis: int = 0) -> np.ndarray:
+    """Array-level box filter of ``length`` with the given tap ``center`` along ``axis``
+    (conv.py:131-138): the clamped sliding-window convolver."""
+    w = materialize_box_kernel(length)
+    psf = Psf(PsfKind.UNIFORM_BOX_1D, w, int(center), axis=BlurAxis.VERTICAL if axis == 0 else BlurAxis.HORIZONTAL,
+              length=float(length))
+    return box_convolve(Image(np.asarray(a, dtype=np.float64)), psf).values

@@ -122,3 +122,17 @@ def test_rrrl_deblur_parallel_equals_serial(md, workers):
         md.rrrl_deblur_parallel(g, md.Psf.line(5.0, 20.0), md.DeconvParams())
     with pytest.raises(ValueError):
         md.rrrl_deblur_parallel(g, md.Psf.uniform_box(md.BlurAxis.HORIZONTAL, 5), md.DeconvParams(), 0)
+
+
+def test_array_level_convolutions_vs_oracle(md):
+    """convolve_array / box_filter_array (conv.py:85-138) against the oracle's clamped direct
+    summation and box filter, including a non-default box centre."""
+    from oracle import wr3l_oracle as O
+    rng = np.random.default_rng(5)
+    a = rng.uniform(0, 255, (48, 64))
+    line = md.Psf.line(7.0, 60.0)
+    np.testing.assert_allclose(md.convolve_array(a, line), O.clamped_convolve(a, O.OPsf("2d", line.weights, line.center)),
+                               rtol=0, atol=1e-9)
+    for length, center, axis in ((9.0, 4, 0), (7.5, 2, 1), (12.0, 9, 0)):
+        want = O.box_filter(a, length, center, axis=axis)
+        np.testing.assert_allclose(md.box_filter_array(a, length, center, axis), want, rtol=0, atol=1e-9)
