@@ -8,10 +8,46 @@ construction (the argument is validated, as in the reference, and otherwise unus
 
 from __future__ import annotations
 
-from .core import DeconvParams, Image, Psf, PsfKind
-from .deconv import rrrl_deblur
+import time
 
-__all__ = ["rrrl_deblur_parallel"]
+import numpy as np
+
+from .core import DeconvParams, Image, Psf, PsfKind
+from .deconv import GpuConvolver, prepare_state, rrrl_deblur, rrrl_step
+
+__all__ = ["rrrl_deblur_parallel", "ColumnSharpeningEngine"]
+
+
+class ColumnSharpeningEngine:
+    """The reference's threaded RRRL iteration engine (parallel.py:43-114) with the same
+    interface, iterating on the device: ``run(u0, fpos, convolver, iterations, iteration_ms)``
+    applies ``iterations`` RRRL updates to ``u0`` against the floored observation ``fpos`` with a
+    device convolver (``GpuConvolver`` from ``make_convolver``); ``workers`` is validated as in
+    the reference and otherwise unused (the GPU is the parallel engine)."""
+
+    def __init__(self, params: DeconvParams, lut, workers: int):
+        if workers < 1:
+            raise ValueError("worker count must be at least 1")
+        self.params = params
+        self.lut = lut
+        self.workers = int(workers)
+
+    def run(self, u0: np.ndarray, fpos: np.ndarray, convolver, iterations: int,
+            iteration_ms: list[float] | None = None) -> np.ndarray:
+        if iterations <= 0:
+            return u0
+        if not isinstance(convolver, GpuConvolver):
+            raise TypeError("ColumnSharpeningEngine.run needs a device convolver (make_convolver)")
+        import torch
+        u, f = Image(u0), Image(fpos)
+        for _ in range(iterations):
+            t0 = time.perf_counter()
+            st = prepare_state(u, f, convolver.psf, self.params, convolver=convolver, lut=self.lut)
+            u = rrrl_step(st, f, convolver.psf, self.params, convolver=convolver)
+            if iteration_ms is not None:
+                torch.cuda.synchronize()
+                iteration_ms.append(1e3 * (time.perf_counter() - t0))
+        return np.array(u.values)
 
 
 def rrrl_deblur_parallel(f: Image, h: Psf, params: DeconvParams, worker_count: int = 1, *, convolver=None,

@@ -136,3 +136,21 @@ def test_array_level_convolutions_vs_oracle(md):
     for length, center, axis in ((9.0, 4, 0), (7.5, 2, 1), (12.0, 9, 0)):
         want = O.box_filter(a, length, center, axis=axis)
         np.testing.assert_allclose(md.box_filter_array(a, length, center, axis), want, rtol=0, atol=1e-9)
+
+
+def test_column_sharpening_engine(md):
+    """ColumnSharpeningEngine (parallel.py:43-114) through the step API equals rrrl_deblur."""
+    from paper_1212_2245_b200.parallel import ColumnSharpeningEngine
+    g = md.make_test_image(96, 64)
+    psf = md.Psf.uniform_box(md.BlurAxis.VERTICAL, 9)
+    f = md.synth_blur(g, psf)
+    params = md.DeconvParams()
+    fpos = np.maximum(f.values, params.floor)
+    times = []
+    eng = ColumnSharpeningEngine(params, None, 4)
+    u = eng.run(fpos.copy(), fpos, md.make_convolver(psf, f.shape, "box"), params.iterations, times)
+    want = md.rrrl_deblur(f, psf, params, convolver="box").values
+    np.testing.assert_allclose(u, want, rtol=0, atol=1e-9)
+    assert len(times) == params.iterations
+    with pytest.raises(ValueError):
+        ColumnSharpeningEngine(params, None, 0)
