@@ -628,6 +628,17 @@ namespace {
 // scratch fields per frame (in elements of the plan dtype)
 constexpr int64_t kChunkScratch = 4ll << 30;
 
+// per-plan scratch bound: 4 GiB, or a sixteenth of the device memory on smaller GPUs (plans are
+// cached by the Python layer, several may hold scratch at once)
+int64_t chunk_scratch_cap() {
+    static int64_t cap = [] {
+        size_t fr = 0, total = 0;
+        if (cudaMemGetInfo(&fr, &total) != cudaSuccess) { cudaGetLastError(); return kChunkScratch; }
+        return std::max<int64_t>(256ll << 20, std::min<int64_t>(kChunkScratch, (int64_t)(total / 16)));
+    }();
+    return cap;
+}
+
 bool lines_pipelined(const md_plan &P) {
     return P.path == PATH_LINES && P.fused && P.wiener_reg && P.d.init == MD_INIT_WIENER && P.d.iterations > 0;
 }
@@ -642,11 +653,11 @@ int scratch_fields(const md_plan &P) {
 
 int64_t auto_chunk(const md_plan &P, int64_t batch) {
     if (P.chunk > 0) return std::min(P.chunk, batch);
-    // keep one chunk's scratch within kChunkScratch: large chunks, because every launch ends on a
+    // keep one chunk's scratch within chunk_scratch_cap(): large chunks, because every launch ends on a
     // partial wave of clusters (measured: 4096 c1 frames as one chunk 8.21 ms, as four pipelined
     // chunks 8.30 ms)
     const int64_t per = (int64_t)scratch_fields(P) * P.frame_elems() * P.es;
-    int64_t c = std::max<int64_t>(1, kChunkScratch / std::max<int64_t>(per, 1));
+    int64_t c = std::max<int64_t>(1, chunk_scratch_cap() / std::max<int64_t>(per, 1));
     if (lines_pipelined(P) && P.fused_clusters > 0 && batch > c) {
         // whole rounds of the resident clusters per chunk, the rounds spread evenly over the
         // chunks: no chunk ends on a nearly empty round
