@@ -138,3 +138,19 @@ def test_one_plan_from_two_threads_and_streams(md):
     torch.cuda.synchronize()
     for o, w in zip(outs, want):
         assert torch.equal(o, w)
+
+
+def test_bench_pipeline_stage_samples(md):
+    """bench_pipeline (bench.py:80-115) on CUDA-event stage times: stage names, pooled iteration
+    samples (runs x iterations), first / later split, positive times; report renders them."""
+    psf = md.Psf.uniform_box(md.BlurAxis.HORIZONTAL, 9)
+    f = md.synth_blur(md.make_test_image(64, 64), psf)
+    for dtype in ("float64", "float32"):
+        st = md.bench_pipeline(f, psf, md.DeconvParams(), runs=3, warmup=True, split_first_iteration=True, dtype=dtype)
+        assert st.runs == 3
+        assert list(st.per_stage) == ["wiener", "rrrl_iteration", "rrrl_total", "total", "rrrl_first_iteration",
+                                      "rrrl_later_iterations"]
+        assert st.per_stage["rrrl_iteration"].samples == 15
+        assert st.per_stage["rrrl_later_iterations"].samples == 12
+        assert st.mean_ms > 0 and st.per_stage["wiener"].mean_ms > 0
+        assert md.report(st, "csv").startswith("scenario,stage,runs,mean_ms,std_ms,min_ms,max_ms\n")

@@ -196,3 +196,26 @@ def test_fft_api_host_side():
     if not torch.cuda.is_available():
         with pytest.raises((md._lib.CudaUnavailable, RuntimeError)):
             md.plan_fft(8).forward(np.ones(8))
+
+
+def test_benchmark_report_formats_match_reference():
+    """report() renders the reference's human table and CSV byte for byte (bench.py:118-138);
+    the expected strings were produced by the reference's own report() on these samples."""
+    from paper_1212_2245_b200.benchmark import StageStats, TimingStats, report
+    st = {k: StageStats.from_samples(v) for k, v in {"wiener": [1.0, 1.5, 2.0], "rrrl_iteration": [0.25, 0.5, 0.75, 1.25],
+          "rrrl_total": [3.0], "total": [4.0, 4.5]}.items()}
+    ts = TimingStats("box", 3, st)
+    assert report(ts, "human") == (
+        "scenario box, 3 runs\n  wiener             1.500 +-  0.500 ms  (1.000 .. 2.000, n=3)\n"
+        "  rrrl_iteration     0.688 +-  0.427 ms  (0.250 .. 1.250, n=4)\n"
+        "  rrrl_total         3.000 +-  0.000 ms  (3.000 .. 3.000, n=1)\n"
+        "  total              4.250 +-  0.354 ms  (4.000 .. 4.500, n=2)\n")
+    assert report(ts, "csv") == (
+        "scenario,stage,runs,mean_ms,std_ms,min_ms,max_ms\nbox,wiener,3,1.500,0.500,1.000,2.000\n"
+        "box,rrrl_iteration,4,0.688,0.427,0.250,1.250\nbox,rrrl_total,1,3.000,0.000,3.000,3.000\n"
+        "box,total,2,4.250,0.354,4.000,4.500\n")
+    assert StageStats.from_samples([]) == StageStats(0, 0.0, 0.0, 0.0, 0.0)
+    assert StageStats.from_samples([2.0]) == StageStats(1, 2.0, 0.0, 2.0, 2.0)
+    assert ts.mean_ms == st["total"].mean_ms and ts.max_ms == 4.5
+    with pytest.raises(ValueError):
+        report(ts, "xml")
