@@ -517,7 +517,8 @@ int32_t md_plan_create(const md_plan_desc *desc, md_plan **out) {
         // per-iteration kernel (16-CTA clusters at one CTA per SM lose to it), opt-in via
         // md_plan_set_fused
         P->fused = desc->dtype == MD_F32 && P->fast_lines &&
-                   fused_lines_supported(desc->dtype, P->n, P->m, desc->flags);
+                   fused_lines_supported(desc->dtype, P->n, P->m, desc->flags,
+                                         std::max(line_radius(P->lblur), line_radius(P->ladj)));
         if (P->fused) P->fused_clusters = lines_fused_clusters<float>(*P);
         snprintf(buf, sizeof buf, "lines: n=%d m=%d %s %s %s, %s", P->n, P->m, P->vert ? "vertical" : "horizontal",
                  use_box ? "box" : "taps", periodic ? "periodic" : "clamped",
@@ -984,7 +985,8 @@ int32_t md_plan_set_fused(md_plan *P, int32_t on) {
         P->fused_plane = on != 0;
         return MD_OK;
     }
-    if (on && !(P->path == PATH_LINES && P->fast_lines && fused_lines_supported(P->d.dtype, P->n, P->m, 0)))
+    if (on && !(P->path == PATH_LINES && P->fast_lines && fused_lines_supported(P->d.dtype, P->n, P->m, 0,
+                                                                         std::max(line_radius(P->lblur), line_radius(P->ladj)))))
         return fail(MD_EINVAL, "fused kernel not available for this plan");
     P->fused = on != 0;
     P->fused_clusters = !on ? 0 : (P->d.dtype == MD_F64 ? lines_fused_clusters<double>(*P) : lines_fused_clusters<float>(*P));

@@ -7,14 +7,13 @@ namespace md {
 
 // ---------------------------------------------------------------------------------- host
 
-// lines per warp: float64 uses 2 (16-line CTAs, one per SM); float 4 (32-line CTAs, two per SM;
-// 2 lines per warp measured 10 % slower)
-int fused_lpw(int dtype) { return dtype == 0 ? 2 : 4; }
+// lines per warp (fused_lp in md_fused_kernel.cuh): float64 2; float 4, or 2 for radii above 8
+int fused_lpw(int dtype, int radius) { return dtype == 0 ? 2 : (radius > 8 ? 2 : 4); }
 
-bool fused_lines_supported(int dtype, int n, int m, unsigned flags) {
+bool fused_lines_supported(int dtype, int n, int m, unsigned flags, int radius) {
     if (flags & 2u) return false;                  // MD_FLAG_NO_FUSED
     if (n % SEG != 0 || n / SEG > 32 || n < 64) return false;
-    const int rl = FU_WARPS * fused_lpw(dtype);
+    const int rl = FU_WARPS * fused_lpw(dtype, radius);
     if (m % rl != 0) return false;
     const int cl = m / rl;
     return cl >= 2 && cl <= 16;
@@ -30,7 +29,7 @@ cudaError_t launch_fused_lines(const FusedLinesArgs &d, int64_t batch, cudaStrea
     }
     auto go = [&](auto rtag) -> cudaError_t {
         constexpr int RR = decltype(rtag)::value;
-        constexpr int LP = sizeof(T) == 8 ? 2 : 4;
+        constexpr int LP = fused_lp<T, RR>();
         FusedKArgs<T, RR> a{};
         a.u0 = static_cast<const T *>(d.u_in);
         a.fpos = static_cast<const T *>(d.fpos);

@@ -18,8 +18,9 @@ struct FusedLinesArgs {
     int *query;            // non-null: store the resident cluster count, launch nothing
 };
 
-bool fused_lines_supported(int dtype, int n, int m, unsigned flags);
-int fused_lpw(int dtype);
+// radius: max(blur, adjoint) line radius (line_radius, md_lines_fast.h)
+bool fused_lines_supported(int dtype, int n, int m, unsigned flags, int radius);
+int fused_lpw(int dtype, int radius);
 template <typename T> cudaError_t launch_fused_box_parta(const FusedLinesArgs &, int radius, int64_t, cudaStream_t);
 template <typename T> cudaError_t launch_fused_box_partb(const FusedLinesArgs &, int radius, int64_t, cudaStream_t);
 template <typename T>

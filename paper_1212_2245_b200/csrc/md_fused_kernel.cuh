@@ -58,7 +58,7 @@ __device__ __forceinline__ void fu_fill_halo(T *line, int n, int hw, int periodi
 }
 
 template <typename T, int R, int LPW, bool ROBUST, int BOXR, bool BOXC>
-__global__ void __launch_bounds__(256, sizeof(T) == 4 ? (LPW == 2 ? 3 : 2) : 1)
+__global__ void __launch_bounds__(256, sizeof(T) == 4 ? (LPW == 2 && R <= 8 ? 3 : 2) : 1)
 k_fused_lines(FusedKArgs<T, R> a) {
     constexpr int HW = HaloOf<R>::value;
     constexpr int WIN = SEG + 2 * R;
@@ -417,9 +417,14 @@ cudaError_t launch_fused_box_r(const FusedLinesArgs &d, int64_t batch, cudaStrea
                                      a, batch, st);
 }
 
+// lines per warp: 4 in float (32-line CTAs, 8-CTA clusters, two CTAs per SM); for radii above 8
+// the lines carry a 16-sample halo and a 32-line CTA no longer fits twice into an SM's shared
+// memory (117 KB), so those run 16-line CTAs in 16-CTA clusters, again two per SM; float64: 2
+template <typename T, int RR> constexpr int fused_lp() { return sizeof(T) == 8 ? 2 : (RR > 8 ? 2 : 4); }
+
 template <typename T, int RR>
 cudaError_t launch_fused_box_lpw(const FusedLinesArgs &d, int64_t batch, cudaStream_t st) {
-    return launch_fused_box_r<T, RR, sizeof(T) == 8 ? 2 : 4>(d, batch, st);
+    return launch_fused_box_r<T, RR, fused_lp<T, RR>()>(d, batch, st);
 }
 
 }  // namespace md
