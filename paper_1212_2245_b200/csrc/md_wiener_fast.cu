@@ -189,37 +189,42 @@ k_wiener_lines_reg(WienerLinesArgs a) {
         return;
     }
     // vertical input -> line-major output (and fpos): stage the pair through shared memory so
-    // that consecutive threads write consecutive samples of a line
+    // that consecutive threads write consecutive samples of a line. Staged lines are NP = N + 1
+    // apart: the column-order writes (consecutive threads = consecutive lines) then hit distinct
+    // banks instead of one (a stride of N words is a multiple of 32)
+    constexpr int NP = N + 1;
     __syncthreads();
-    T *st = reinterpret_cast<T *>(tr);          // PB pairs x 2 lines x N reals (fits: PB*S*TS complex)
+    T *st = reinterpret_cast<T *>(tr);          // 2 PB lines x NP reals (fits: PB (S TS + 1) complex)
 #pragma unroll
     for (int j2 = 0; j2 < S; ++j2) {
         const int j = q + S * j2;
         T y0 = v[j2].x * inv_n, y1 = v[j2].y * inv_n;
         if (a.clamp) { y0 = y0 > floor ? y0 : floor; y1 = y1 > floor ? y1 : floor; }
-        st[(2 * p) * N + j] = y0;
-        st[(2 * p + 1) * N + j] = y1;
+        st[(2 * p) * NP + j] = y0;
+        st[(2 * p + 1) * NP + j] = y1;
     }
     __syncthreads();
     const int lbase = 2 * blockIdx.x * PB;
     for (int idx = threadIdx.x; idx < 2 * PB * N; idx += blockDim.x) {
         const int li = idx / N, j = idx - li * N;
-        if (lbase + li < m) out[(int64_t)(lbase + li) * N + j] = st[idx];
+        if (lbase + li < m) out[(int64_t)(lbase + li) * N + j] = st[li * NP + j];
     }
     if (fpos) {
         __syncthreads();
         for (int idx = threadIdx.x; idx < 2 * PB * N; idx += blockDim.x) {
             const int j = idx / (2 * PB), li = idx - j * (2 * PB);
-            if (lbase + li < m) st[li * N + j] = in[(int64_t)j * m + lbase + li];
+            if (lbase + li < m) st[li * NP + j] = in[(int64_t)j * m + lbase + li];
         }
         __syncthreads();
         for (int idx = threadIdx.x; idx < 2 * PB * N; idx += blockDim.x) {
             const int li = idx / N, j = idx - li * N;
-            const T x = st[idx];
+            const T x = st[li * NP + j];
             if (lbase + li < m) fpos[(int64_t)(lbase + li) * N + j] = x > floor ? x : floor;
         }
     }
 }
+
+static_assert(2 * 16 * (256 + 1) <= 2 * 16 * (16 * 17 + 1), "staging fits the transpose buffer (S = 16)");
 
 template <typename T, int S>
 cudaError_t launch_wiener_reg_t(const WienerLinesArgs &a, int64_t batch, cudaStream_t st) {
