@@ -93,7 +93,7 @@ k_wiener_lines_reg(WienerLinesArgs a) {
     constexpr int PB = 256 / S;                 // line pairs per block
     constexpr int TS = S + 1;                   // transpose row stride (padding)
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    C *tw = reinterpret_cast<C *>(smem_raw);    // W_n^k, k < N
+    C *tw = reinterpret_cast<C *>(smem_raw);    // W_n^(q k) at [k][q], q, k < S
     C *tr = tw + N;                             // PB transposes of S x TS
     const int m = a.m;
     const int64_t fr = blockIdx.y;
@@ -103,10 +103,12 @@ k_wiener_lines_reg(WienerLinesArgs a) {
     T *fpos = a.fpos ? static_cast<T *>(a.fpos) + fr * fsz : nullptr;
     const T floor = T(a.floor);
     const C *twg = static_cast<const C *>(a.tw);
-    for (int k = threadIdx.x; k < N; k += blockDim.x) {
-        // the plan table holds W_n^k for k < n/2; the rest is its negation
-        const C t = twg[k & (N / 2 - 1)];
-        tw[k] = k < N / 2 ? t : mkc<T>(-t.x, -t.y);
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        // inter-step twiddles arranged [k][q] = W_n^(q k) (q, k < S, q k < n): the lanes of a
+        // step read consecutive entries (a W_n^(q k) lookup by q k strides the banks for even k)
+        const int k = (i / S) * (i % S);
+        const C t = twg[k & (N / 2 - 1)];         // the plan table holds W_n^k for k < n/2
+        tw[i] = k < N / 2 ? t : mkc<T>(-t.x, -t.y);
     }
     const int t = threadIdx.x;
     // thread -> (pair p, lane-in-pair q); vertical input: p fastest for coalescing
@@ -146,7 +148,7 @@ k_wiener_lines_reg(WienerLinesArgs a) {
     // ---- forward: DFT over j2 (X[k2] lands at v[rev(k2)]), twiddle W_n^{j1 k2}, transpose
     dif_reg<T, S>(v);
 #pragma unroll
-    for (int k2 = 0; k2 < S; ++k2) T2[k2 * TS + q] = cmul(v[bitrev<S>(k2)], tw[(q * k2) & (N - 1)]);
+    for (int k2 = 0; k2 < S; ++k2) T2[k2 * TS + q] = cmul(v[bitrev<S>(k2)], tw[k2 * S + q]);
     __syncthreads();
     // thread q = k2 now: DFT over j1 (X[k2 + S k1] lands at v[rev(k1)])
 #pragma unroll
@@ -159,7 +161,7 @@ k_wiener_lines_reg(WienerLinesArgs a) {
     // ---- inverse: DFT^-1 over k1 (bit-reversed in, natural j1 out), twiddle W_n^{-j1 k2}
     dit_inv_reg<T, S>(v);
 #pragma unroll
-    for (int j1 = 0; j1 < S; ++j1) T2[q * TS + j1] = cmulc(v[j1], tw[(q * j1) & (N - 1)]);
+    for (int j1 = 0; j1 < S; ++j1) T2[q * TS + j1] = cmulc(v[j1], tw[j1 * S + q]);
     __syncthreads();
 #pragma unroll
     for (int k2 = 0; k2 < S; ++k2) v[bitrev<S>(k2)] = T2[k2 * TS + q];
