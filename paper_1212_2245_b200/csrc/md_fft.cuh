@@ -32,7 +32,20 @@ __device__ __forceinline__ C mul_mi(C a) {          // a * (-i)
     C r; r.x = a.y; r.y = -a.x; return r;
 }
 
+// Stage-major twiddle table for the STAGED variants: the stage with butterfly half-size h reads
+// W_{2h}^k, k < h, at tws[h - 1 + k] (n - 1 entries in all), so consecutive lanes of a stage
+// read consecutive entries -- the natural table read at tw[k << shift] strides the banks. Filled
+// by a block from the plan's natural table twg[k] = W_n^k, k < n/2.
 template <typename C>
+__device__ __forceinline__ void stage_twiddles(C *tws, const C *__restrict__ twg, int log2n) {
+    const int n = 1 << log2n;
+    for (int i = threadIdx.x; i < n - 1; i += blockDim.x) {
+        const int lh = 31 - __clz(i + 1), h = 1 << lh;     // stage of entry i
+        tws[i] = twg[(i - (h - 1)) << (log2n - 1 - lh)];   // W_{2h}^k = W_n^{k n / 2h}
+    }
+}
+
+template <bool STAGED = false, typename C>
 __device__ void fft_dif_lines(C *s, int log2n, int nl, int stride, const C *__restrict__ tw) {
     const int n = 1 << log2n;
     int lh = log2n - 1;
@@ -43,7 +56,7 @@ __device__ void fft_dif_lines(C *s, int log2n, int nl, int stride, const C *__re
             C *row = s + l * stride;
             const C a = row[fpad(k)], c = row[fpad(k + half)];
             row[fpad(k)] = cadd(a, c);
-            row[fpad(k + half)] = cmul(csub(a, c), tw[k]);
+            row[fpad(k + half)] = cmul(csub(a, c), tw[STAGED ? half - 1 + k : k]);
         }
         __syncthreads();
         --lh;
@@ -57,8 +70,8 @@ __device__ void fft_dif_lines(C *s, int log2n, int nl, int stride, const C *__re
             const int i0 = ((uu >> (lh - 1)) << (lh + 1)) + k;
             C *row = s + l * stride;
             const C x0 = row[fpad(i0)], x1 = row[fpad(i0 + q)], x2 = row[fpad(i0 + h)], x3 = row[fpad(i0 + h + q)];
-            const C w1 = tw[k << (log2n - 1 - lh)];    // W_{2h}^k
-            const C w2 = tw[k << (log2n - lh)];        // W_h^k
+            const C w1 = STAGED ? tw[h - 1 + k] : tw[k << (log2n - 1 - lh)];      // W_{2h}^k
+            const C w2 = STAGED ? tw[q - 1 + k] : tw[k << (log2n - lh)];          // W_h^k
             const C y0 = cadd(x0, x2), y2 = cmul(csub(x0, x2), w1);
             const C y1 = cadd(x1, x3), y3 = cmul(csub(x1, x3), mul_mi(w1));
             row[fpad(i0)] = cadd(y0, y1);
@@ -71,7 +84,7 @@ __device__ void fft_dif_lines(C *s, int log2n, int nl, int stride, const C *__re
 }
 
 // inverse (conjugate twiddles), bit-reversed in -> natural out, unscaled
-template <typename C>
+template <bool STAGED = false, typename C>
 __device__ void fft_dit_inv_lines(C *s, int log2n, int nl, int stride, const C *__restrict__ tw) {
     const int n = 1 << log2n;
     const int hb = log2n - 1;
@@ -85,8 +98,8 @@ __device__ void fft_dit_inv_lines(C *s, int log2n, int nl, int stride, const C *
             const int i0 = ((uu >> lh) << (lh + 2)) + k;
             C *row = s + l * stride;
             const C x0 = row[fpad(i0)], x1 = row[fpad(i0 + q)], x2 = row[fpad(i0 + h)], x3 = row[fpad(i0 + h + q)];
-            const C w2 = tw[k << (log2n - lh - 1)];    // W_h^k
-            const C w1 = tw[k << (log2n - lh - 2)];    // W_{2h}^k
+            const C w2 = STAGED ? tw[q - 1 + k] : tw[k << (log2n - lh - 1)];      // W_h^k
+            const C w1 = STAGED ? tw[h - 1 + k] : tw[k << (log2n - lh - 2)];      // W_{2h}^k
             C t = cmulc(x1, w2);
             const C y0 = cadd(x0, t), y1 = csub(x0, t);
             t = cmulc(x3, w2);
@@ -105,7 +118,7 @@ __device__ void fft_dit_inv_lines(C *s, int log2n, int nl, int stride, const C *
         for (int b = threadIdx.x; b < (nl << hb); b += blockDim.x) {
             const int l = b >> hb, k = b & (half - 1);
             C *row = s + l * stride;
-            const C t = cmulc(row[fpad(k + half)], tw[k]);
+            const C t = cmulc(row[fpad(k + half)], tw[STAGED ? half - 1 + k : k]);
             const C a = row[fpad(k)];
             row[fpad(k + half)] = csub(a, t);
             row[fpad(k)] = cadd(a, t);

@@ -40,7 +40,7 @@ __device__ T tv_div_global(const T *__restrict__ u, int H, int W, int y, int x, 
 
 template <typename T>
 __global__ void __launch_bounds__(256)
-k_fft2_rows(Fft2Args a, int rb) {
+k_fft2_rows(Fft2Args a, int rb, int staged) {
     // `rb` consecutive rows per block (all threads busy in every FFT stage)
     using C = cx_t<T>;
     constexpr int U = 4;                              // global loads in flight per thread
@@ -64,7 +64,8 @@ k_fft2_rows(Fft2Args a, int rb) {
     C *tw = s + rb * LS;
     {
         const C *twg = static_cast<const C *>(a.twW);
-        for (int k = threadIdx.x; k < (W >> 1); k += blockDim.x) tw[k] = twg[k];
+        if (staged) stage_twiddles(tw, twg, lw);      // stage-major: conflict-free per-stage reads
+        else for (int k = threadIdx.x; k < (W >> 1); k += blockDim.x) tw[k] = twg[k];
     }
 
     if (a.load == R_LOAD_COMPLEX) {
@@ -93,7 +94,10 @@ k_fft2_rows(Fft2Args a, int rb) {
         }
     }
     __syncthreads();
-    if (a.inv && lw > 0) fft_dit_inv_lines(s, lw, rb, LS, tw);
+    if (a.inv && lw > 0) {
+        if (staged) fft_dit_inv_lines<true>(s, lw, rb, LS, tw);
+        else fft_dit_inv_lines<false>(s, lw, rb, LS, tw);
+    }
 
     const T scale = T(a.scale), floor = T(a.floor);
     const T eps_d2 = T(a.eps_d2), eps_r2 = T(a.eps_r2), alpha = T(a.alpha);   // converted once
@@ -166,7 +170,10 @@ k_fft2_rows(Fft2Args a, int rb) {
         __syncthreads();
     }
     if (a.fwd_after) {
-        if (lw > 0) fft_dif_lines(s, lw, rb, LS, tw);
+        if (lw > 0) {
+            if (staged) fft_dif_lines<true>(s, lw, rb, LS, tw);
+            else fft_dif_lines<false>(s, lw, rb, LS, tw);
+        }
         for (int i = threadIdx.x; i < ne; i += blockDim.x) z[base + i] = s[sp(i)];
     } else if (a.epi == R_EPI_NONE) {
         for (int i = threadIdx.x; i < ne; i += blockDim.x) z[base + i] = s[sp(i)];
@@ -187,7 +194,7 @@ k_fft2_cols(Fft2Args a, int lcw) {
     C *tw = s + cw * cs;                              // staged twiddles (see k_fft2_rows)
     {
         const C *twg = static_cast<const C *>(a.twH);
-        for (int k = threadIdx.x; k < (H >> 1); k += blockDim.x) tw[k] = twg[k];
+        stage_twiddles(tw, twg, a.log2H);
     }
     for (int idx = threadIdx.x; idx < cw * H; idx += blockDim.x) {
         const int y = idx >> lcw, c = idx & (cw - 1);
@@ -195,7 +202,7 @@ k_fft2_cols(Fft2Args a, int lcw) {
         else s[c * cs + fpad(y)] = mkc<T>(T(0), T(0));
     }
     __syncthreads();
-    if (a.log2H > 0) fft_dif_lines(s, a.log2H, cw, cs, tw);
+    if (a.log2H > 0) fft_dif_lines<true>(s, a.log2H, cw, cs, tw);
     if (a.filt) {
         const C *filt = static_cast<const C *>(a.filt);
         for (int idx = threadIdx.x; idx < cw * H; idx += blockDim.x) {
@@ -206,7 +213,7 @@ k_fft2_cols(Fft2Args a, int lcw) {
         }
         __syncthreads();
     }
-    if (a.col_inv && a.log2H > 0) fft_dit_inv_lines(s, a.log2H, cw, cs, tw);
+    if (a.col_inv && a.log2H > 0) fft_dit_inv_lines<true>(s, a.log2H, cw, cs, tw);
     for (int idx = threadIdx.x; idx < cw * H; idx += blockDim.x) {
         const int y = idx >> lcw, c = idx & (cw - 1);
         if (x0 + c < W) z[base + (int64_t)y * W + x0 + c] = s[c * cs + fpad(y)];
@@ -217,7 +224,14 @@ template <typename T>
 cudaError_t launch_fft2_rows(const Fft2Args &a, int64_t batch, cudaStream_t st) {
     int rb = 2048 / a.W;                      // ~2048 elements per block
     rb = rb < 1 ? 1 : (rb > a.H ? a.H : rb);
-    const size_t smem = ((size_t)rb * fpad_len(a.W) + a.W / 2 + 1) * sizeof(cx_t<T>);
+    // stage-major twiddles (W - 1 entries) unless they would not fit (the plan-time float64
+    // spectrum of an 8192-sample line): then the natural table (W / 2)
+    size_t smem = ((size_t)rb * fpad_len(a.W) + a.W + 1) * sizeof(cx_t<T>);
+    int staged = 1;
+    if (smem > 227 * 1024) {
+        smem = ((size_t)rb * fpad_len(a.W) + a.W / 2 + 1) * sizeof(cx_t<T>);
+        staged = 0;
+    }
     cudaError_t e = cudaFuncSetAttribute(k_fft2_rows<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     // `batch` counts complex fields; with pairing the real pointers advance two frames per field
@@ -237,7 +251,7 @@ cudaError_t launch_fft2_rows(const Fft2Args &a, int64_t batch, cudaStream_t st) 
         ab.f = sh(a.f, sizeof(T), rstep);
         ab.u = sh(a.u, sizeof(T), 1);
         ab.nreal = a.nreal - rstep * b0;
-        k_fft2_rows<T><<<dim3(a.H / rb, nb), 256, smem, st>>>(ab, rb);
+        k_fft2_rows<T><<<dim3(a.H / rb, nb), 256, smem, st>>>(ab, rb, staged);
     }
     return cudaGetLastError();
 }
@@ -248,7 +262,7 @@ cudaError_t launch_fft2_cols(const Fft2Args &a, int64_t batch, cudaStream_t st) 
     cw = cw > 16 ? 16 : (cw < 1 ? 1 : cw);          // a power of two (H is)
     int lcw = 0;
     while ((1 << lcw) < cw) ++lcw;
-    const size_t smem = ((size_t)cw * fline_stride(a.H) + a.H / 2 + 1) * sizeof(cx_t<T>);
+    const size_t smem = ((size_t)cw * fline_stride(a.H) + a.H + 1) * sizeof(cx_t<T>);
     cudaError_t e = cudaFuncSetAttribute(k_fft2_cols<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int64_t fr = (int64_t)a.H * a.W;

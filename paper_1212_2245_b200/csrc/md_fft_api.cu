@@ -29,7 +29,7 @@ __global__ void __launch_bounds__(256) k_fft_lines_nat(cx_t<T> *z, int log2n, in
     C *s = reinterpret_cast<C *>(smem_raw);
     const int n = 1 << log2n, ls = fline_stride(n);
     C *tw = s + G * ls;
-    for (int k = threadIdx.x; k < (n >> 1); k += blockDim.x) tw[k] = twg[k];
+    stage_twiddles(tw, twg, log2n);
     const int64_t l0 = (int64_t)blockIdx.x * G;
     const int gl = (int)(lines - l0 < G ? lines - l0 : G);
     C *zb = z + l0 * n;
@@ -44,8 +44,8 @@ __global__ void __launch_bounds__(256) k_fft_lines_nat(cx_t<T> *z, int log2n, in
     }
     __syncthreads();
     if (log2n > 0) {
-        if (inverse) fft_dit_inv_lines(s, log2n, G, ls, tw);
-        else fft_dif_lines(s, log2n, G, ls, tw);
+        if (inverse) fft_dit_inv_lines<true>(s, log2n, G, ls, tw);
+        else fft_dif_lines<true>(s, log2n, G, ls, tw);
     }
     const T scale = inverse ? T(1) / T(n) : T(1);
     for (int i = threadIdx.x; i < gl * n; i += blockDim.x) {
@@ -82,7 +82,7 @@ cudaError_t launch_fft_lines_nat(void *z, int n, int64_t lines, const void *tw, 
     int log2n = 0;
     while ((1 << log2n) < n) ++log2n;
     const int G = std::max(1, std::min(16, 2048 / n));
-    const size_t smem = ((size_t)G * fline_stride(n) + n / 2 + 1) * sizeof(C);
+    const size_t smem = ((size_t)G * fline_stride(n) + n + 1) * sizeof(C);
     cudaError_t e = cudaFuncSetAttribute(k_fft_lines_nat<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int64_t blocks = (lines + G - 1) / G;

@@ -68,11 +68,11 @@ k_subfft(SubFftArgs a) {
         }
     }
     C *twL = s + G * ls;                       // sub-transform twiddles staged in shared memory
-    for (int k = threadIdx.x; k < (L >> 1); k += bd) twL[k] = static_cast<const C *>(a.twL)[k];
+    stage_twiddles(twL, static_cast<const C *>(a.twL), a.log2L);   // stage-major (md_fft.cuh)
     __syncthreads();
     const C *filt = static_cast<const C *>(a.filt);
     if (TW == TW_FILT_INV) {
-        fft_dif_lines(s, a.log2L, G, ls, twL);
+        fft_dif_lines<true>(s, a.log2L, G, ls, twL);
         for (int idx = threadIdx.x; idx < n; idx += bd) {
             int g, e;
             coords(idx, g, e);
@@ -82,11 +82,11 @@ k_subfft(SubFftArgs a) {
             v = a.conj_filt ? cmulc(v, fl) : cmul(v, fl);
         }
         __syncthreads();
-        fft_dit_inv_lines(s, a.log2L, G, ls, twL);
+        fft_dit_inv_lines<true>(s, a.log2L, G, ls, twL);
     } else if (a.inv) {
-        fft_dit_inv_lines(s, a.log2L, G, ls, twL);
+        fft_dit_inv_lines<true>(s, a.log2L, G, ls, twL);
     } else {
-        fft_dif_lines(s, a.log2L, G, ls, twL);
+        fft_dif_lines<true>(s, a.log2L, G, ls, twL);
     }
     // inter-pass twiddle W_N^{+-(digit * rev(pos))}, digit = line (FWD) or element (INV) index
     const C *twN = static_cast<const C *>(a.twN);
@@ -166,7 +166,7 @@ cudaError_t launch_subfft(const SubFftArgs &a0, int64_t batch, cudaStream_t st) 
     SubFftArgs a = a0;
     const int L = 1 << a.log2L;
     a.G = std::max(1, std::min(16, 2048 / L));   // power of two (L is)
-    const size_t smem = ((size_t)a.G * fline_stride(L) + L / 2 + 1) * sizeof(cx_t<T>);
+    const size_t smem = ((size_t)a.G * fline_stride(L) + L + 1) * sizeof(cx_t<T>);
     auto pick = [&](auto lf) {
         constexpr bool LF = decltype(lf)::value;
         return a.tw_mode == TW_FWD ? k_subfft<T, LF, TW_FWD>
