@@ -81,7 +81,7 @@ __device__ __forceinline__ void dit_inv_reg(cx_t<T> (&v)[S]) {
 }
 
 template <typename T, int S>
-__global__ void __launch_bounds__(256, (sizeof(T) == 4 && S <= 16) ? 3 : 1)   // 3 blocks/SM (<= 85 regs)
+__global__ void __launch_bounds__(256, S <= 16 ? (sizeof(T) == 4 ? 3 : 2) : 1)   // float 3 blocks/SM (<= 85 regs), double 2
 k_wiener_lines_reg(WienerLinesArgs a) {
     // programmatic dependent launch (md_capi.cu, run_lines_pipelined): this grid may start while
     // the preceding cluster iteration kernel still runs; its last block waits for that kernel
