@@ -16,13 +16,16 @@ namespace md {
 // radix-4 stages with small spans access elements 8, 32, ... apart; unpadded, 16-byte (f64
 // complex) elements at stride 8 all fall into one bank group (16-way conflicts, measured
 // 2.8e8 conflicts per two-level pass at 16384^2); padded, they spread over all banks.
-__host__ __device__ constexpr int fpad(int j) { return j + (j >> 3); }
+// ES = element bytes: 16-byte (complex double) lines pad once per 8 elements, 8-byte (complex
+// float) ones once per 16 -- then a half-warp's 8-byte accesses at strides 1, 2, 4, 8, 16 hit
+// distinct banks (one pad per 8 left the small-span radix-4 stages 2-4-way conflicted)
+template <int ES = 16> __host__ __device__ constexpr int fpad(int j) { return j + (j >> (ES <= 8 ? 4 : 3)); }
 // storage length of a padded line of n elements
-__host__ __device__ constexpr int fpad_len(int n) { return fpad(n - 1) + 1; }
+template <int ES = 16> __host__ __device__ constexpr int fpad_len(int n) { return fpad<ES>(n - 1) + 1; }
 // stride between padded lines that are accessed across lines (transposed loads / stores):
 // = 1 (mod 8), so 8 consecutive lines fall into 8 different bank groups for 16-byte complex
 // elements (and 16 into different bank pairs for 8-byte ones)
-__host__ __device__ constexpr int fline_stride(int n) { return ((fpad_len(n) + 6) & ~7) + 1; }
+template <int ES = 16> __host__ __device__ constexpr int fline_stride(int n) { return ((fpad_len<ES>(n) + 6) & ~7) + 1; }
 
 // `nl` lines of length n = 2^log2n at s[l * stride + fpad(j)]; all threads of the block take part.
 // Pairs of radix-2 stages are fused into radix-4 units (4 elements in registers), halving the
@@ -54,9 +57,9 @@ __device__ void fft_dif_lines(C *s, int log2n, int nl, int stride, const C *__re
         for (int b = threadIdx.x; b < (nl << lh); b += blockDim.x) {
             const int l = b >> lh, k = b & (half - 1);
             C *row = s + l * stride;
-            const C a = row[fpad(k)], c = row[fpad(k + half)];
-            row[fpad(k)] = cadd(a, c);
-            row[fpad(k + half)] = cmul(csub(a, c), tw[STAGED ? half - 1 + k : k]);
+            const C a = row[fpad<sizeof(C)>(k)], c = row[fpad<sizeof(C)>(k + half)];
+            row[fpad<sizeof(C)>(k)] = cadd(a, c);
+            row[fpad<sizeof(C)>(k + half)] = cmul(csub(a, c), tw[STAGED ? half - 1 + k : k]);
         }
         __syncthreads();
         --lh;
@@ -69,15 +72,15 @@ __device__ void fft_dif_lines(C *s, int log2n, int nl, int stride, const C *__re
             const int k = uu & (q - 1);
             const int i0 = ((uu >> (lh - 1)) << (lh + 1)) + k;
             C *row = s + l * stride;
-            const C x0 = row[fpad(i0)], x1 = row[fpad(i0 + q)], x2 = row[fpad(i0 + h)], x3 = row[fpad(i0 + h + q)];
+            const C x0 = row[fpad<sizeof(C)>(i0)], x1 = row[fpad<sizeof(C)>(i0 + q)], x2 = row[fpad<sizeof(C)>(i0 + h)], x3 = row[fpad<sizeof(C)>(i0 + h + q)];
             const C w1 = STAGED ? tw[h - 1 + k] : tw[k << (log2n - 1 - lh)];      // W_{2h}^k
             const C w2 = STAGED ? tw[q - 1 + k] : tw[k << (log2n - lh)];          // W_h^k
             const C y0 = cadd(x0, x2), y2 = cmul(csub(x0, x2), w1);
             const C y1 = cadd(x1, x3), y3 = cmul(csub(x1, x3), mul_mi(w1));
-            row[fpad(i0)] = cadd(y0, y1);
-            row[fpad(i0 + q)] = cmul(csub(y0, y1), w2);
-            row[fpad(i0 + h)] = cadd(y2, y3);
-            row[fpad(i0 + h + q)] = cmul(csub(y2, y3), w2);
+            row[fpad<sizeof(C)>(i0)] = cadd(y0, y1);
+            row[fpad<sizeof(C)>(i0 + q)] = cmul(csub(y0, y1), w2);
+            row[fpad<sizeof(C)>(i0 + h)] = cadd(y2, y3);
+            row[fpad<sizeof(C)>(i0 + h + q)] = cmul(csub(y2, y3), w2);
         }
         __syncthreads();
     }
@@ -97,7 +100,7 @@ __device__ void fft_dit_inv_lines(C *s, int log2n, int nl, int stride, const C *
             const int k = uu & (q - 1);
             const int i0 = ((uu >> lh) << (lh + 2)) + k;
             C *row = s + l * stride;
-            const C x0 = row[fpad(i0)], x1 = row[fpad(i0 + q)], x2 = row[fpad(i0 + h)], x3 = row[fpad(i0 + h + q)];
+            const C x0 = row[fpad<sizeof(C)>(i0)], x1 = row[fpad<sizeof(C)>(i0 + q)], x2 = row[fpad<sizeof(C)>(i0 + h)], x3 = row[fpad<sizeof(C)>(i0 + h + q)];
             const C w2 = STAGED ? tw[q - 1 + k] : tw[k << (log2n - lh - 1)];      // W_h^k
             const C w1 = STAGED ? tw[h - 1 + k] : tw[k << (log2n - lh - 2)];      // W_{2h}^k
             C t = cmulc(x1, w2);
@@ -105,11 +108,11 @@ __device__ void fft_dit_inv_lines(C *s, int log2n, int nl, int stride, const C *
             t = cmulc(x3, w2);
             const C y2 = cadd(x2, t), y3 = csub(x2, t);
             t = cmulc(y2, w1);
-            row[fpad(i0)] = cadd(y0, t);
-            row[fpad(i0 + h)] = csub(y0, t);
+            row[fpad<sizeof(C)>(i0)] = cadd(y0, t);
+            row[fpad<sizeof(C)>(i0 + h)] = csub(y0, t);
             t = cmulc(y3, mul_mi(w1));
-            row[fpad(i0 + q)] = cadd(y1, t);
-            row[fpad(i0 + h + q)] = csub(y1, t);
+            row[fpad<sizeof(C)>(i0 + q)] = cadd(y1, t);
+            row[fpad<sizeof(C)>(i0 + h + q)] = csub(y1, t);
         }
         __syncthreads();
     }
@@ -118,10 +121,10 @@ __device__ void fft_dit_inv_lines(C *s, int log2n, int nl, int stride, const C *
         for (int b = threadIdx.x; b < (nl << hb); b += blockDim.x) {
             const int l = b >> hb, k = b & (half - 1);
             C *row = s + l * stride;
-            const C t = cmulc(row[fpad(k + half)], tw[STAGED ? half - 1 + k : k]);
-            const C a = row[fpad(k)];
-            row[fpad(k + half)] = csub(a, t);
-            row[fpad(k)] = cadd(a, t);
+            const C t = cmulc(row[fpad<sizeof(C)>(k + half)], tw[STAGED ? half - 1 + k : k]);
+            const C a = row[fpad<sizeof(C)>(k)];
+            row[fpad<sizeof(C)>(k + half)] = csub(a, t);
+            row[fpad<sizeof(C)>(k)] = cadd(a, t);
         }
         __syncthreads();
     }

@@ -58,8 +58,8 @@ k_fft2_rows(Fft2Args a, int rb, int staged) {
     const int ne = rb * W;
     const int bd = blockDim.x;
     C *z = static_cast<C *>(a.z);
-    const int LS = fpad_len(W);                       // padded row stride (md_fft.cuh)
-    auto sp = [&](int i) { return (i >> lw) * LS + fpad(i & (W - 1)); };
+    const int LS = fpad_len<sizeof(C)>(W);                       // padded row stride (md_fft.cuh)
+    auto sp = [&](int i) { return (i >> lw) * LS + fpad<sizeof(C)>(i & (W - 1)); };
     // twiddles staged in shared memory behind the rows: the butterflies read them every stage
     C *tw = s + rb * LS;
     {
@@ -186,7 +186,7 @@ k_fft2_cols(Fft2Args a, int lcw) {
     using C = cx_t<T>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C *s = reinterpret_cast<C *>(smem_raw);
-    const int H = a.H, W = a.W, cs = fline_stride(H);      // padded column stride (md_fft.cuh)
+    const int H = a.H, W = a.W, cs = fline_stride<sizeof(C)>(H);      // padded column stride (md_fft.cuh)
     const int cw = 1 << lcw, lh = a.log2H;                  // powers of two: shifts, no division
     const int x0 = blockIdx.x * cw;
     const int64_t base = blockIdx.y * (int64_t)H * W;
@@ -198,8 +198,8 @@ k_fft2_cols(Fft2Args a, int lcw) {
     }
     for (int idx = threadIdx.x; idx < cw * H; idx += blockDim.x) {
         const int y = idx >> lcw, c = idx & (cw - 1);
-        if (x0 + c < W) s[c * cs + fpad(y)] = z[base + (int64_t)y * W + x0 + c];
-        else s[c * cs + fpad(y)] = mkc<T>(T(0), T(0));
+        if (x0 + c < W) s[c * cs + fpad<sizeof(C)>(y)] = z[base + (int64_t)y * W + x0 + c];
+        else s[c * cs + fpad<sizeof(C)>(y)] = mkc<T>(T(0), T(0));
     }
     __syncthreads();
     if (a.log2H > 0) fft_dif_lines<true>(s, a.log2H, cw, cs, tw);
@@ -209,14 +209,14 @@ k_fft2_cols(Fft2Args a, int lcw) {
             const int c = idx >> lh, y = idx & (H - 1);
             if (x0 + c >= W) continue;
             const C f = __ldg(filt + (int64_t)y * W + x0 + c);
-            s[c * cs + fpad(y)] = a.conj_filt ? cmulc(s[c * cs + fpad(y)], f) : cmul(s[c * cs + fpad(y)], f);
+            s[c * cs + fpad<sizeof(C)>(y)] = a.conj_filt ? cmulc(s[c * cs + fpad<sizeof(C)>(y)], f) : cmul(s[c * cs + fpad<sizeof(C)>(y)], f);
         }
         __syncthreads();
     }
     if (a.col_inv && a.log2H > 0) fft_dit_inv_lines<true>(s, a.log2H, cw, cs, tw);
     for (int idx = threadIdx.x; idx < cw * H; idx += blockDim.x) {
         const int y = idx >> lcw, c = idx & (cw - 1);
-        if (x0 + c < W) z[base + (int64_t)y * W + x0 + c] = s[c * cs + fpad(y)];
+        if (x0 + c < W) z[base + (int64_t)y * W + x0 + c] = s[c * cs + fpad<sizeof(C)>(y)];
     }
 }
 
@@ -226,10 +226,10 @@ cudaError_t launch_fft2_rows(const Fft2Args &a, int64_t batch, cudaStream_t st) 
     rb = rb < 1 ? 1 : (rb > a.H ? a.H : rb);
     // stage-major twiddles (W - 1 entries) unless they would not fit (the plan-time float64
     // spectrum of an 8192-sample line): then the natural table (W / 2)
-    size_t smem = ((size_t)rb * fpad_len(a.W) + a.W + 1) * sizeof(cx_t<T>);
+    size_t smem = ((size_t)rb * fpad_len<sizeof(cx_t<T>)>(a.W) + a.W + 1) * sizeof(cx_t<T>);
     int staged = 1;
     if (smem > 227 * 1024) {
-        smem = ((size_t)rb * fpad_len(a.W) + a.W / 2 + 1) * sizeof(cx_t<T>);
+        smem = ((size_t)rb * fpad_len<sizeof(cx_t<T>)>(a.W) + a.W / 2 + 1) * sizeof(cx_t<T>);
         staged = 0;
     }
     cudaError_t e = cudaFuncSetAttribute(k_fft2_rows<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -262,7 +262,7 @@ cudaError_t launch_fft2_cols(const Fft2Args &a, int64_t batch, cudaStream_t st) 
     cw = cw > 16 ? 16 : (cw < 1 ? 1 : cw);          // a power of two (H is)
     int lcw = 0;
     while ((1 << lcw) < cw) ++lcw;
-    const size_t smem = ((size_t)cw * fline_stride(a.H) + a.H + 1) * sizeof(cx_t<T>);
+    const size_t smem = ((size_t)cw * fline_stride<sizeof(cx_t<T>)>(a.H) + a.H + 1) * sizeof(cx_t<T>);
     cudaError_t e = cudaFuncSetAttribute(k_fft2_cols<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int64_t fr = (int64_t)a.H * a.W;

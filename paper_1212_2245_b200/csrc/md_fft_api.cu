@@ -27,7 +27,7 @@ __global__ void __launch_bounds__(256) k_fft_lines_nat(cx_t<T> *z, int log2n, in
     using C = cx_t<T>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C *s = reinterpret_cast<C *>(smem_raw);
-    const int n = 1 << log2n, ls = fline_stride(n);
+    const int n = 1 << log2n, ls = fline_stride<sizeof(C)>(n);
     C *tw = s + G * ls;
     stage_twiddles(tw, twg, log2n);
     const int64_t l0 = (int64_t)blockIdx.x * G;
@@ -36,11 +36,11 @@ __global__ void __launch_bounds__(256) k_fft_lines_nat(cx_t<T> *z, int log2n, in
     for (int i = threadIdx.x; i < gl * n; i += blockDim.x) {
         const int g = i >> log2n, j = i & (n - 1);
         const C v = zb[i];
-        s[g * ls + fpad(inverse ? brev_bits(j, log2n) : j)] = v;
+        s[g * ls + fpad<sizeof(C)>(inverse ? brev_bits(j, log2n) : j)] = v;
     }
     for (int i = gl * n + threadIdx.x; i < G * n; i += blockDim.x) {   // idle lines of a ragged block
         const int g = i >> log2n, j = i & (n - 1);
-        s[g * ls + fpad(j)] = mkc<T>(T(0), T(0));
+        s[g * ls + fpad<sizeof(C)>(j)] = mkc<T>(T(0), T(0));
     }
     __syncthreads();
     if (log2n > 0) {
@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(256) k_fft_lines_nat(cx_t<T> *z, int log2n, in
     const T scale = inverse ? T(1) / T(n) : T(1);
     for (int i = threadIdx.x; i < gl * n; i += blockDim.x) {
         const int g = i >> log2n, k = i & (n - 1);
-        const C v = s[g * ls + fpad(inverse ? k : brev_bits(k, log2n))];
+        const C v = s[g * ls + fpad<sizeof(C)>(inverse ? k : brev_bits(k, log2n))];
         zb[i] = inverse ? cscale(v, scale) : v;
     }
 }
@@ -82,7 +82,7 @@ cudaError_t launch_fft_lines_nat(void *z, int n, int64_t lines, const void *tw, 
     int log2n = 0;
     while ((1 << log2n) < n) ++log2n;
     const int G = std::max(1, std::min(16, 2048 / n));
-    const size_t smem = ((size_t)G * fline_stride(n) + n + 1) * sizeof(C);
+    const size_t smem = ((size_t)G * fline_stride<sizeof(C)>(n) + n + 1) * sizeof(C);
     cudaError_t e = cudaFuncSetAttribute(k_fft_lines_nat<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int64_t blocks = (lines + G - 1) / G;

@@ -26,7 +26,7 @@ k_subfft(SubFftArgs a) {
     using C = cx_t<T>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C *s = reinterpret_cast<C *>(smem_raw);
-    const int L = 1 << a.log2L, G = a.G, ls = fline_stride(L);   // padded line stride (md_fft.cuh)
+    const int L = 1 << a.log2L, G = a.G, ls = fline_stride<sizeof(C)>(L);   // padded line stride (md_fft.cuh)
     const int blocks_b = (a.B + G - 1) / G;
     const int ai = blockIdx.x / blocks_b, b0 = (blockIdx.x - ai * blocks_b) * G;
     const int64_t fr = blockIdx.y;
@@ -64,7 +64,7 @@ k_subfft(SubFftArgs a) {
             if (idx >= n) break;
             int g, e;
             coords(idx, g, e);
-            s[g * ls + fpad(e)] = v[k];
+            s[g * ls + fpad<sizeof(C)>(e)] = v[k];
         }
     }
     C *twL = s + G * ls;                       // sub-transform twiddles staged in shared memory
@@ -78,7 +78,7 @@ k_subfft(SubFftArgs a) {
             coords(idx, g, e);
             if (b0 + g >= a.B) continue;
             const C fl = filt[base + g * sb + e * es];
-            C &v = s[g * ls + fpad(e)];
+            C &v = s[g * ls + fpad<sizeof(C)>(e)];
             v = a.conj_filt ? cmulc(v, fl) : cmul(v, fl);
         }
         __syncthreads();
@@ -124,7 +124,7 @@ k_subfft(SubFftArgs a) {
             int g, e;
             coords(idx, g, e);
             if (idx >= n || b0 + g >= a.B) continue;
-            C v = s[g * ls + fpad(e)];
+            C v = s[g * ls + fpad<sizeof(C)>(e)];
             if (TWM != TW_NONE) v = TWM == TW_FWD ? cmul(v, tw[k]) : cmulc(v, tw[k]);
             if (FILT_EPI && filt) v = a.conj_filt ? cmulc(v, fl[k]) : cmul(v, fl[k]);
             if (scale != T(1)) v = cscale(v, scale);
@@ -166,7 +166,7 @@ cudaError_t launch_subfft(const SubFftArgs &a0, int64_t batch, cudaStream_t st) 
     SubFftArgs a = a0;
     const int L = 1 << a.log2L;
     a.G = std::max(1, std::min(16, 2048 / L));   // power of two (L is)
-    const size_t smem = ((size_t)a.G * fline_stride(L) + L + 1) * sizeof(cx_t<T>);
+    const size_t smem = ((size_t)a.G * fline_stride<sizeof(cx_t<T>)>(L) + L + 1) * sizeof(cx_t<T>);
     auto pick = [&](auto lf) {
         constexpr bool LF = decltype(lf)::value;
         return a.tw_mode == TW_FWD ? k_subfft<T, LF, TW_FWD>

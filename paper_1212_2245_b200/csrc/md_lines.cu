@@ -45,7 +45,7 @@ k_wiener_lines(WienerLinesArgs a) {
     using C = cx_t<T>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int n = a.n, m = a.m, LP = a.lp;
-    const int cs = fline_stride(n);                         // complex line stride (md_fft.cuh padding)
+    const int cs = fline_stride<sizeof(C)>(n);                         // complex line stride (md_fft.cuh padding)
     C *s = reinterpret_cast<C *>(smem_raw);
     T *sfr = reinterpret_cast<T *>(s + LP * cs);             // raw f (only when in_vert)
     const int P = padded_len<T>(n);
@@ -70,7 +70,7 @@ k_wiener_lines(WienerLinesArgs a) {
                 else fpos[(int64_t)line * n + j] = v > floor ? v : floor;
             }
         }
-        C *c = s + (li >> 1) * cs + fpad(j);
+        C *c = s + (li >> 1) * cs + fpad<sizeof(C)>(j);
         if (li & 1) c->y = v; else c->x = v;
     }
     __syncthreads();
@@ -78,7 +78,7 @@ k_wiener_lines(WienerLinesArgs a) {
     const C *mult = static_cast<const C *>(a.mult);
     for (int idx = threadIdx.x; idx < LP * n; idx += blockDim.x) {
         const int l = idx / n, p = idx - l * n;
-        s[l * cs + fpad(p)] = cmul(s[l * cs + fpad(p)], __ldg(mult + p));
+        s[l * cs + fpad<sizeof(C)>(p)] = cmul(s[l * cs + fpad<sizeof(C)>(p)], __ldg(mult + p));
     }
     __syncthreads();
     if (a.log2n > 0) fft_dit_inv_lines(s, a.log2n, LP, cs, static_cast<const C *>(a.tw));
@@ -89,7 +89,7 @@ k_wiener_lines(WienerLinesArgs a) {
         else { li = idx / n; j = idx - li * n; }
         const int line = L0 + li;
         if (line >= m) continue;
-        const C c = s[(li >> 1) * cs + fpad(j)];
+        const C c = s[(li >> 1) * cs + fpad<sizeof(C)>(j)];
         T v = ((li & 1) ? c.y : c.x) * inv_n;
         if (a.clamp) v = v > floor ? v : floor;
         if (a.out_vert) out[(int64_t)j * m + line] = v;
@@ -342,7 +342,7 @@ __global__ void k_clamp2(const T *__restrict__ in, T *__restrict__ o1, T *__rest
 
 template <typename T>
 size_t wiener_lines_smem(int n, int lp, int in_vert, bool with_fpos) {
-    size_t s = (size_t)lp * fline_stride(n) * sizeof(cx_t<T>);
+    size_t s = (size_t)lp * fline_stride<sizeof(cx_t<T>)>(n) * sizeof(cx_t<T>);
     if (in_vert && with_fpos) s += (size_t)2 * lp * padded_len<T>(n) * sizeof(T);
     return s;
 }
