@@ -578,6 +578,21 @@ def main() -> None:
         if i >= 10:                                   # 200 timed single-frame runs
             lat.append(a.elapsed_time(b))
 
+    # host-observed single-frame latency (call -> result ready, synchronised per call): the
+    # direct md_run call vs a replay of the same run captured as a CUDA graph (GpuPlan.capture)
+    g1 = work.latency_plan.capture(f1, u1)
+    host_lat = {}
+    for name, call in (("direct", lambda: work.latency_plan.run(f1, out=u1)), ("cuda_graph", g1.replay)):
+        xs = []
+        for i in range(110):
+            t0 = time.perf_counter()
+            call()
+            torch.cuda.synchronize()
+            if i >= 10:
+                xs.append((time.perf_counter() - t0) * 1e3)
+        host_lat[name] = statistics.median(xs)
+    del g1
+
     # end to end through the public host-buffer entry (DeblurPipeline.run_batch(ndarray) ->
     # md_run_host_ex): pinned host frames in, pinned host results out, copies inside the timed
     # region. Primary: the workload's native 8-bit frames in, float32 results out; also the
@@ -647,6 +662,7 @@ def main() -> None:
                        "plan": work.describe},
             "p50_ms_per_frame_batch1": statistics.median(lat),
             "p99_ms_per_frame_batch1": sorted(lat)[min(len(lat) - 1, int(0.99 * len(lat)))],
+            "host_p50_ms_per_frame_batch1": host_lat,
             "stage_ms_per_step": {k: prof[k] / args.steps for k in ("init_ms", "iter_ms", "layout_ms")},
             "stage_split_source": ("CUDA events between the launch groups of the timed steps" if work.profile_in_loop
                                    else "CUDA events of profiled sequential steps after the timed region"),

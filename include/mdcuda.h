@@ -105,7 +105,10 @@ int32_t md_plan_set_fused(md_plan *plan, int32_t on);
 int32_t md_plan_is_fused(const md_plan *plan);
 
 /* the pipeline: Wiener (or clamp) init + iterations (DeblurPipeline.run, deconv.py:653-693;
- * rrrl_deblur deconv.py:537-559; rl_deblur deconv.py:524-534). f and u are device arrays. */
+ * rrrl_deblur deconv.py:537-559; rl_deblur deconv.py:524-534). f and u are device arrays.
+ * Capturable: between cudaStreamBeginCapture/EndCapture on `stream` it records its launches
+ * into the caller's CUDA graph (call it once uncaptured first with the same batch, so the
+ * plan's scratch is already sized; replays are ordered only by the stream they run on). */
 int32_t md_run(md_plan *plan, const void *f, void *u, int64_t batch, void *stream);
 /* same, but f/u are HOST float64 arrays; H2D, dtype conversion, run, D2H all inside.
  * Copies are chunked through the plan's pinned staging buffers. */

@@ -140,12 +140,17 @@ __global__ void k_embed_taps(double *z, int H, int W, const PlaneTap *taps, int 
     }
 }
 
+// set while this thread enqueues into a stream under capture: buffers cannot be reallocated
+// then (an earlier graph may still reference the old one)
+thread_local bool tl_capturing = false;
+
 struct DevBuf {
     void *p = nullptr;
     size_t bytes = 0;
     void release() { if (p) cudaFree(p); p = nullptr; bytes = 0; }
     int ensure(size_t b) {
         if (b <= bytes) return MD_OK;
+        if (tl_capturing) return fail(MD_EINVAL, "plan scratch must be sized by an uncaptured run before stream capture");
         release();
         if (cudaMalloc(&p, b) != cudaSuccess) { cudaGetLastError(); return fail(MD_ENOMEM, "device allocation failed"); }
         bytes = b;
@@ -408,6 +413,13 @@ class PlanUse {
   public:
     PlanUse(md_plan *P, cudaStream_t st) : P_(P), st_(st), lk_(P->mu) {
         outer_ = P_->use_depth++ == 0;
+        // under stream capture (the caller builds a CUDA graph) the launches are recorded, not
+        // run: no cross-stream event edges -- replays are ordered by the stream they replay on
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (outer_) {
+            if (cudaStreamIsCapturing(st_, &cs) != cudaSuccess) cudaGetLastError();
+            else if (cs != cudaStreamCaptureStatusNone) outer_ = false, captured_ = tl_capturing = true;
+        }
         if (outer_ && P_->use_any && P_->use_stream != st_) cudaStreamWaitEvent(st_, P_->use_done, 0);
     }
     ~PlanUse() {
@@ -418,6 +430,7 @@ class PlanUse {
                 P_->use_any = true;
             }
         }
+        if (captured_) tl_capturing = false;
         --P_->use_depth;
     }
     PlanUse(const PlanUse &) = delete;
@@ -427,7 +440,7 @@ class PlanUse {
     md_plan *P_;
     cudaStream_t st_;
     std::unique_lock<std::recursive_mutex> lk_;
-    bool outer_ = false;
+    bool outer_ = false, captured_ = false;
 };
 
 // ======================================================================== C ABI

@@ -422,6 +422,17 @@ class DeblurPipeline:
         self._check_shape(a.shape[-2:])
         return self._plan.run_host(a, out=out, stream=stream, out_dtype=out_dtype)
 
+    def capture(self, batch: int = 1):
+        """The pipeline for ``batch`` device-resident frames recorded as a CUDA graph
+        (``plan.CapturedRun``): ``g(frames)`` copies the frames into the graph's input buffer and
+        replays; the result is ``g.out``."""
+        import torch
+        if int(batch) < 1:
+            raise ValueError("batch must be positive")
+        f = torch.zeros((int(batch),) + self.shape, dtype=torch_dtype(self.dtype), device="cuda")
+        f.fill_(max(self.params.floor, 1.0))
+        return self._plan.capture(f)
+
     def run_timed(self, f: Image) -> tuple[Image, StageTimes]:
         """Deconvolve one image with per-stage times from CUDA events on the launch stream
         (deconv.py:653-690). The per-iteration kernel path yields one time per iteration; the

@@ -10,6 +10,7 @@ memory / stream plumbing); numpy arrays are staged through the device by the cal
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 
 import numpy as np
@@ -131,6 +132,25 @@ class GpuPlan:
         L.check(self.lib.md_run(self._h, f.data_ptr(), out.data_ptr(), n, _stream_ptr(stream)))
         return out
 
+    def capture(self, f, out=None) -> "CapturedRun":
+        """Record ``run(f, out)`` into a CUDA graph for fixed device buffers (video-rate use: one
+        graph launch per batch instead of one host call per kernel). Runs once uncaptured first,
+        which sizes the plan's scratch; afterwards write new frames into ``f`` and ``replay()``."""
+        import torch
+        self._check_frames(f)
+        out = self.empty_like(f) if out is None else out
+        self._check_frames(out, "out")
+        side = torch.cuda.Stream(device=f.device)
+        side.wait_stream(torch.cuda.current_stream(f.device))
+        with torch.cuda.stream(side):
+            self.run(f, out, stream=side)
+        graph = torch.cuda.CUDAGraph()
+        # relaxed: the launchers set kernel attributes (cudaFuncSetAttribute) while enqueuing
+        with torch.cuda.graph(graph, stream=side, capture_error_mode="relaxed"):
+            self.run(f, out, stream=side)
+        torch.cuda.current_stream(f.device).wait_stream(side)
+        return CapturedRun(self, graph, f, out)
+
     def run_profile(self, f, out=None, stream=None) -> dict:
         """md_run with CUDA events per launch group: {"init_ms", "iter_ms", "layout_ms", "groups"}."""
         n = self._check_frames(f)
@@ -202,6 +222,34 @@ class GpuPlan:
                                       None if d is None else d.data_ptr(),
                                       out.data_ptr(), n, float(alpha), _stream_ptr(stream)))
         return out
+
+
+class CapturedRun:
+    """A ``GpuPlan.run`` recorded as a CUDA graph over fixed buffers ``f`` -> ``out``. The
+    graph holds the plan's device pointers: keep the plan alive and do not use it from another
+    stream while a replay may be running (replays are ordered only by their own stream)."""
+
+    def __init__(self, plan: GpuPlan, graph, f, out):
+        self.plan, self.graph, self.f, self.out = plan, graph, f, out
+
+    def replay(self, stream=None):
+        """Launch the recorded pipeline on ``stream`` (default: the current stream); returns
+        ``out``."""
+        import torch
+        if stream is None:
+            self.graph.replay()
+        else:
+            with torch.cuda.stream(stream):
+                self.graph.replay()
+        return self.out
+
+    def __call__(self, frames=None, stream=None):
+        """Copy ``frames`` (a device tensor of ``f``'s shape) into the input buffer, replay."""
+        if frames is not None:
+            import torch
+            with torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext():
+                self.f.copy_(frames, non_blocking=True)
+        return self.replay(stream)
 
 
 def dtype_code(t) -> int:
