@@ -40,6 +40,7 @@ template <typename T, int R> struct FusedKArgs {
     int has_d;
     LutView lut;
     T box_wi;           // box specialisation: interior weight
+    T alpha_w, guard_w, one_w;   // alpha, the division guard and 1 divided by box_wi
     T box_cb[4], box_ca[4];   // weight corrections at k = -R, -R+1, R-1, R (blur, adjoint)
 };
 
@@ -115,7 +116,12 @@ k_fused_lines(FusedKArgs<T, R> a) {
         }
     }
 
-    const T eps_r2 = a.eps_r2, eps_d2 = a.eps_d2, alpha = a.alpha;
+    const T eps_r2 = a.eps_r2, eps_d2 = a.eps_d2;
+    // plain integer box: the adjoint window sums stay unscaled and alpha, the guard and the
+    // unit denominator carry 1/wi instead -- u (wi S_p + a D+) / (wi S_W - a D-) =
+    // u (S_p + (a/wi) D+) / (S_W - (a/wi) D-): two multiplies per pixel fewer
+    constexpr bool FOLD = BOXR > 0 && !BOXC;
+    const T al = FOLD ? a.alpha_w : a.alpha, gd = FOLD ? a.guard_w : T(kGuard), one = FOLD ? a.one_w : T(1);
     // diffusivity g on logical lines l in [lb, le] (deconv.py:191-203); lines whose stencil
     // touches a halo (l <= 0 or l >= RL-1) need the neighbours' rows of parity `par`
     auto g_lines = [&](int lb, int le, int par, int wl) {
@@ -234,13 +240,13 @@ k_fused_lines(FusedKArgs<T, R> a) {
                     T v[WIN];
 #pragma unroll
                     for (int k = -R; k < SEG + R; ++k) v[k + R] = wp[off + koff(k)];
-                    conv_window<T, R, BOXR, BOXC>(v, a.wa, a.box_wi, a.box_ca, num);
+                    conv_window<T, R, BOXR, BOXC, !FOLD>(v, a.wa, a.box_wi, a.box_ca, num);
                 }
                 if (ROBUST) {
                     T v[WIN];
 #pragma unroll
                     for (int k = -R; k < SEG + R; ++k) v[k + R] = ww[off + koff(k)];
-                    conv_window<T, R, BOXR, BOXC>(v, a.wa, a.box_wi, a.box_ca, den);
+                    conv_window<T, R, BOXR, BOXC, !FOLD>(v, a.wa, a.box_wi, a.box_ca, den);
                 }
                 T ux[SEG + 2];
 #pragma unroll
@@ -262,20 +268,20 @@ k_fused_lines(FusedKArgs<T, R> a) {
                         T d = fr - fl;
                         if (dn_ok) d += (gc + Gd[koff(r)]) * (Ud[koff(r)] - u);
                         if (up_ok) d -= (Gu[koff(r)] + gc) * (u - Uu[koff(r)]);
-                        T nm = num[r] + alpha * (d > T(0) ? d : T(0));
-                        const T neg = alpha * (d < T(0) ? d : T(0));
-                        T dn = (ROBUST ? den[r] : T(1)) - neg;
-                        dn = dn > T(kGuard) ? dn : T(kGuard);
+                        T nm = num[r] + al * (d > T(0) ? d : T(0));
+                        const T neg = al * (d < T(0) ? d : T(0));
+                        T dn = (ROBUST ? den[r] : one) - neg;
+                        dn = fmax(dn, gd);                 // one FMNMX (gd is not a NaN)
                         unew[j][r] = (u * nm) * frcp(dn);
                     }
                 } else {
 #pragma unroll
                     for (int r = 0; r < SEG; ++r) {
                         if (ROBUST) {
-                            const T dn = den[r] > T(kGuard) ? den[r] : T(kGuard);
+                            const T dn = fmax(den[r], gd);
                             unew[j][r] = (ux[r + 1] * num[r]) * frcp(dn);
                         } else {
-                            unew[j][r] = ux[r + 1] * num[r];
+                            unew[j][r] = ux[r + 1] * (FOLD ? num[r] * a.box_wi : num[r]);
                         }
                     }
                 }
@@ -409,6 +415,7 @@ cudaError_t launch_fused_box_r(const FusedLinesArgs &d, int64_t batch, cudaStrea
     a.alpha = T(d.alpha); a.eps_d2 = T(d.eps_d2); a.eps_r2 = T(d.eps_r2); a.has_d = d.has_d;
     a.lut = d.lut;
     a.box_wi = T(d.blur.wi);
+    a.alpha_w = T(d.alpha / d.blur.wi); a.guard_w = T(kGuard / d.blur.wi); a.one_w = T(1.0 / d.blur.wi);
     if (!box_corrections<T, RR>(d.blur, d.blur.wi, a.box_cb) || !box_corrections<T, RR>(d.adj, d.blur.wi, a.box_ca))
         return cudaErrorNotSupported;
     bool corr = false;           // odd integer boxes: the plain sliding sum (no correction code)

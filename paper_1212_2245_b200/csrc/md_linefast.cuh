@@ -30,8 +30,9 @@ template <typename T, int R> struct DenseTaps { T w[2 * R + 1]; };
 // window convolution of 8 outputs: dense taps over [-R, R] (constant-bank FMAs), or, for a
 // box (equal interior weights) of radius BOXR (= R), an O(1)-per-output sliding sum over
 // [-R, R] plus weight corrections at k = -R, -R+1, R-1, R (even-length and fractional boxes:
-// deconv.py box convolver, conv.py:141-173)
-template <typename T, int R, int BOXR, bool BOXC>
+// deconv.py box convolver, conv.py:141-173). SCALE = false (plain integer boxes only) leaves
+// the window sums unscaled by the interior weight, for callers that fold 1/wi elsewhere.
+template <typename T, int R, int BOXR, bool BOXC, bool SCALE = true>
 __device__ __forceinline__ void conv_window(const T (&v)[SEG + 2 * R], const DenseTaps<T, R> &taps, T box_wi,
                                             const T (&corr)[4], T out[SEG]) {
     if constexpr (BOXR > 0) {
@@ -48,12 +49,13 @@ __device__ __forceinline__ void conv_window(const T (&v)[SEG + 2 * R], const Den
         T d[SEG];
 #pragma unroll
         for (int r = 1; r < SEG; ++r) d[r] = v[r + 2 * R] - v[r - 1];
+        static_assert(SCALE || !BOXC, "unscaled windows only for plain boxes");
         T s = t[0];
-        out[0] = s * box_wi;
+        out[0] = SCALE ? s * box_wi : s;
 #pragma unroll
         for (int r = 1; r < SEG; ++r) {
             s += d[r];
-            out[r] = s * box_wi;
+            out[r] = SCALE ? s * box_wi : s;
         }
         if constexpr (BOXC) {
 #pragma unroll

@@ -19,6 +19,7 @@ template <typename T, int R> struct IterFastArgs {
     int has_d;
     LutView lut;
     T box_wi;                    // box specialisation (BOXR > 0): interior weight
+    T alpha_w, guard_w, one_w;   // alpha, the division guard and 1 divided by box_wi
     T box_cb[4], box_ca[4];      // weight corrections at k = -R, -R+1, R-1, R (blur, adjoint)
 };
 

@@ -145,7 +145,10 @@ k_iter_lines_fast(IterFastArgs<T, R> a) {
     __syncthreads();
 
     // ---- phase 2: adjoint pair + TV divergence + multiplicative update (deconv.py:421-446)
-    const T alpha = a.alpha;
+    // plain integer box: adjoint window sums unscaled, 1/wi folded into alpha, the guard and
+    // the unit denominator (as in k_fused_lines)
+    constexpr bool FOLD = BOXR > 0 && !BOXC;
+    const T al = FOLD ? a.alpha_w : a.alpha, gd = FOLD ? a.guard_w : T(kGuard), one = FOLD ? a.one_w : T(1);
     for (int li = warp; li < FTL; li += FWARPS) {
         const int line = l0 + li;
         if (line >= m) continue;
@@ -158,14 +161,14 @@ k_iter_lines_fast(IterFastArgs<T, R> a) {
                 T v[WIN];
 #pragma unroll
                 for (int k = -R; k < SEG + R; ++k) v[k + R] = B[koff(k)];
-                conv_window<T, R, BOXR, BOXC>(v, a.wa, a.box_wi, a.box_ca, num);
+                conv_window<T, R, BOXR, BOXC, !FOLD>(v, a.wa, a.box_wi, a.box_ca, num);
             }
             if (ROBUST) {
                 const T *B = sw + li * ls + off;
                 T v[WIN];
 #pragma unroll
                 for (int k = -R; k < SEG + R; ++k) v[k + R] = B[koff(k)];
-                conv_window<T, R, BOXR, BOXC>(v, a.wa, a.box_wi, a.box_ca, den);
+                conv_window<T, R, BOXR, BOXC, !FOLD>(v, a.wa, a.box_wi, a.box_ca, den);
             }
             const T *U = su + (li + 2) * ls + off;
             T ux[SEG + 2];
@@ -187,11 +190,10 @@ k_iter_lines_fast(IterFastArgs<T, R> a) {
                     T d = fr - fl;
                     if (dn_ok) d += (gc + G[koff(r) + ls]) * (U[koff(r) + ls] - u);
                     if (up_ok) d -= (G[koff(r) - ls] + gc) * (u - U[koff(r) - ls]);
-                    T nm = ROBUST ? num[r] : num[r];
-                    nm += alpha * (d > T(0) ? d : T(0));
-                    const T neg = alpha * (d < T(0) ? d : T(0));
-                    T dn = (ROBUST ? den[r] : T(1)) - neg;
-                    dn = dn > T(kGuard) ? dn : T(kGuard);
+                    const T nm = num[r] + al * (d > T(0) ? d : T(0));
+                    const T neg = al * (d < T(0) ? d : T(0));
+                    T dn = (ROBUST ? den[r] : one) - neg;
+                    dn = fmax(dn, gd);
                     out[r] = (u * nm) * frcp(dn);
                 }
             } else {
@@ -199,10 +201,10 @@ k_iter_lines_fast(IterFastArgs<T, R> a) {
                 for (int r = 0; r < SEG; ++r) {
                     const T u = ux[r + 1];
                     if (ROBUST) {
-                        const T dn = den[r] > T(kGuard) ? den[r] : T(kGuard);
+                        const T dn = fmax(den[r], gd);
                         out[r] = (u * num[r]) * frcp(dn);
                     } else {
-                        out[r] = u * num[r];
+                        out[r] = u * (FOLD ? num[r] * a.box_wi : num[r]);
                     }
                 }
             }
@@ -256,6 +258,7 @@ cudaError_t launch_iter_fast_box_r(const IterFastDesc &d, int64_t batch, cudaStr
     a.alpha = T(d.alpha); a.eps_d2 = T(d.eps_d2); a.eps_r2 = T(d.eps_r2); a.has_d = d.has_d;
     a.lut = d.lut;
     a.box_wi = T(d.blur.wi);
+    a.alpha_w = T(d.alpha / d.blur.wi); a.guard_w = T(kGuard / d.blur.wi); a.one_w = T(1.0 / d.blur.wi);
     if (!box_corrections<T, RR>(d.blur, d.blur.wi, a.box_cb) || !box_corrections<T, RR>(d.adj, d.blur.wi, a.box_ca))
         return cudaErrorNotSupported;
     bool corr = false;           // odd integer boxes: the plain sliding sum
