@@ -501,9 +501,32 @@ int32_t md_plan_create(const md_plan_desc *desc, md_plan **out) {
         P->fast_lines = !(desc->flags & MD_FLAG_GENERIC_LINES) &&
                         iter_fast_supported(desc->dtype, P->n, P->lblur, P->ladj);
         const size_t lim = desc->dtype == MD_F64 ? 4096 : 8192;
-        if (wiener && (size_t)P->n > lim) return bail(fail(MD_EINVAL, "blur-axis length above the on-chip FFT limit"));
-        if (desc->iterations > 0 && !P->fast_lines && !iter_lines_fits(desc->dtype, P->n, 2 * T))
-            return bail(fail(MD_EINVAL, "blur-axis length above the on-chip line-iteration limit"));
+        const char *beyond = nullptr;
+        if (wiener && (size_t)P->n > lim) beyond = "blur-axis length above the on-chip FFT limit";
+        else if (desc->iterations > 0 && !P->fast_lines && !iter_lines_fits(desc->dtype, P->n, 2 * T))
+            beyond = "blur-axis length above the on-chip line-iteration limit";
+        if (beyond) {
+            // lines longer than one CTA holds: the same problem as a plane with a one-row (one-
+            // column) PSF -- two-level FFT Wiener (its spectrum is constant across the lines) and
+            // direct-tap iterations with the same boundary (box and spatial: edge-replicated;
+            // Fourier 1D: periodic along the blur axis). Needs power-of-two sides for the Wiener.
+            delete P;
+            md_plan_desc d2 = *desc;
+            d2.psf_kind = MD_PSF_GENERAL_2D;
+            d2.psf_axis = MD_AXIS_NONE;
+            const bool vert = desc->psf_axis == MD_AXIS_VERTICAL;
+            d2.psf_rows = vert ? T : 1;
+            d2.psf_cols = vert ? 1 : T;
+            d2.center_row = vert ? desc->center_row : 0;
+            d2.center_col = vert ? 0 : desc->center_row;
+            d2.box_length = 0.0;
+            d2.conv = desc->conv == MD_CONV_FOURIER ? MD_CONV_FOURIER2D
+                                                    : (desc->conv == MD_CONV_BOX ? MD_CONV_SPATIAL : desc->conv);
+            d2.flags &= ~MD_FLAG_FORCE_FFT2D;
+            if (md_plan_create(&d2, out) != MD_OK) return fail(MD_EINVAL, beyond);
+            (*out)->describe = std::string("1D PSF beyond the on-chip line limits as a plane; ") + (*out)->describe;
+            return MD_OK;
+        }
         if (is_pow2(P->n)) P->log2n = ilog2(P->n);
         if (is_pow2(P->n) && (size_t)P->n <= lim) {      // line FFT tables (Wiener step)
             if ((rc = build_twiddles(P->n, desc->dtype, &P->d_tw_n))) return bail(rc);

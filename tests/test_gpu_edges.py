@@ -99,12 +99,37 @@ def test_longest_lines_vs_oracle(md):
         assert np.abs(out - ref).max() <= TOL, n
 
 
+@pytest.mark.parametrize("shape,axis,dtype,iters,scenario", [
+    ((16, 16384), "h", "float32", 2, "BOX_1D"),       # past the f32 line FFT (8192)
+    ((16, 8192), "h", "float32", 3, "BOX_1D"),        # past the f32 line-iteration kernel (4096)
+    ((4096, 16), "v", "float64", 2, "BOX_1D"),        # past the f64 line-iteration kernel (2048)
+    ((8192, 16), "v", "float64", 1, "BOX_1D"),        # past the f64 line FFT (4096)
+    ((16, 16384), "h", "float32", 2, "FOURIER_1D"),   # periodic along the blur axis
+])
+def test_lines_beyond_chip_as_plane(md, shape, axis, dtype, iters, scenario):
+    """Blur axes longer than the on-chip line kernels take run as a plane with a one-row (one-
+    column) PSF -- two-level FFT Wiener, direct-tap iterations with the line path's boundary --
+    and still match the oracle's line pipeline."""
+    ax = md.BlurAxis.HORIZONTAL if axis == "h" else md.BlurAxis.VERTICAL
+    psf = md.Psf.uniform_box(ax, 15)
+    params = md.DeconvParams(iterations=iters)
+    g = md.make_test_image(shape[1], shape[0])
+    assert g.values.shape == shape
+    f = md.quantize(md.add_gaussian_noise(md.synth_blur(g, psf), 5.0, seed=3)).values
+    pipe = md.DeblurPipeline(f.shape, psf, params, scenario=getattr(md.Scenario, scenario), dtype=dtype)
+    assert pipe._plan.describe.startswith("1D PSF beyond the on-chip line limits as a plane"), pipe._plan.describe
+    out = pipe.run(md.Image(f)).values
+    ref = _oracle(md, f, psf, params, "box" if scenario == "BOX_1D" else "fourier1d")
+    assert np.abs(out - ref).max() <= TOL, (shape, dtype)
+
+
 def test_limits_raise(md):
-    """Past the on-chip limits -- line FFT (Wiener), line iteration -- and non-power-of-two blur
-    axes, plan creation raises ValueError (the reference's own ValueError cases, fft.py:63-66)."""
+    """Blur axes that are not powers of two, and long blur axes whose other side is not a power
+    of two (the plane route's Wiener needs both), raise ValueError at plan creation (the
+    reference's own ValueError cases, fft.py:63-66)."""
     psf = md.Psf.uniform_box(md.BlurAxis.HORIZONTAL, 15)
-    for shape, dtype, iters in (((16, 16384), "float32", 0), ((16, 8192), "float64", 0),
-                                ((16, 8192), "float32", 5), ((16, 4096), "float64", 5), ((16, 100), "float64", 5)):
+    for shape, dtype, iters in (((16, 100), "float64", 5), ((12, 16384), "float32", 0),
+                                ((12, 8192), "float64", 2)):
         with pytest.raises(ValueError):
             md.DeblurPipeline(shape, psf, md.DeconvParams(iterations=iters), dtype=dtype)
 
