@@ -130,7 +130,7 @@ k_iter_lines_fast(IterFastArgs<T, R> a) {
                 if (ROBUST) {
                     const T x = b * frcp(fp);
                     const T rr = r1_fast<T>(a.lut, x) * fp + eps_d2;
-                    const T w = T(0.5) * frsqrt(rr);
+                    const T w = frsqrt(rr);       // 2 W: the 1/2 moves to alpha and the guard (phase 2)
                     Pw[koff(r)] = w;
                     Pp[koff(r)] = w * ratio;
                 } else {
@@ -148,7 +148,11 @@ k_iter_lines_fast(IterFastArgs<T, R> a) {
     // plain integer box: adjoint window sums unscaled, 1/wi folded into alpha, the guard and
     // the unit denominator (as in k_fused_lines)
     constexpr bool FOLD = BOXR > 0 && !BOXC;
-    const T al = FOLD ? a.alpha_w : a.alpha, gd = FOLD ? a.guard_w : T(kGuard), one = FOLD ? a.one_w : T(1);
+    // robust: p and W are stored as 2 W f / b and 2 W (no 1/2 multiply per pixel), so alpha and
+    // the guard double -- num / den are then exactly twice the reference's (powers of two)
+    constexpr int WS = ROBUST ? 2 : 1;
+    const T al = (FOLD ? a.alpha_w : a.alpha) * T(WS), gd = (FOLD ? a.guard_w : T(kGuard)) * T(WS);
+    const T one = FOLD ? a.one_w : T(1);
     for (int li = warp; li < FTL; li += FWARPS) {
         const int line = l0 + li;
         if (line >= m) continue;
