@@ -76,7 +76,7 @@ k_iter_lines_fast(IterFastArgs<T, R> a) {
     for (int li = warp; li < FTL + 4; li += FWARPS) fill_halo_line<T>(su + li * ls, n, HW, a.periodic, lane, 32);
     __syncthreads();
 
-    const T eps_r2 = a.eps_r2, eps_d2 = a.eps_d2;
+    const T eps_r2 = a.eps_r2, eps_d2 = a.eps_d2, eps_r4 = T(4) * a.eps_r2;
     // ---- phase 1a: diffusivity g on lines l0-1 .. l0+FTL (deconv.py:191-203)
     if (a.has_d) {
         for (int gl = warp; gl < FTL + 2; gl += FWARPS) {
@@ -102,7 +102,8 @@ k_iter_lines_fast(IterFastArgs<T, R> a) {
                     if (r == 0 && s == 0) dxl = T(0);
                     const T dyd = yd[r] - x[r + 1], dyu = x[r + 1] - yu[r];
                     const T q = dxr * dxr + dxl * dxl + dyd * dyd + dyu * dyu;
-                    G[koff(r)] = T(0.5) * frsqrt(T(0.5) * q + eps_r2);
+                    // 0.5 / sqrt(q/2 + eps^2) as 1 / sqrt(2 q + 4 eps^2): bitwise the same (powers of two)
+                    G[koff(r)] = frsqrt(T(2) * q + eps_r4);
                 }
             }
         }
