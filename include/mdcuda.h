@@ -92,6 +92,9 @@ const char *md_last_error(void);
 int32_t md_device_sm_count(void);
 
 /* plans (DeblurPipeline.__init__, deconv.py:611-643; make_convolver, deconv.py:379-403) */
+/* A 1D PSF whose blur axis exceeds the on-chip line kernels (Wiener: 8192 float / 4096 double
+   samples; iterations: 4096 float / 2048 double) is planned as a plane with a one-row (one-column)
+   PSF and the same boundary; that route needs power-of-two sides, else MD_EINVAL.           */
 int32_t md_plan_create(const md_plan_desc *desc, md_plan **out);
 int32_t md_plan_destroy(md_plan *plan);
 /* scratch bytes a run over `batch` frames needs (allocated lazily, owned by the plan) */
