@@ -303,6 +303,10 @@ struct FpGeom {
     size_t smem;
 };
 
+#ifndef MD_FP_MINCL
+#define MD_FP_MINCL 2
+#endif
+
 bool fp_geometry(int H, int W, const PlaneHalo &hb, const PlaneHalo &ha, int dtype, FpGeom *g) {
     if (W != 64 && W != 128 && W != 256) return false;
     const int es = dtype == 0 ? 8 : 4;
@@ -311,7 +315,7 @@ bool fp_geometry(int H, int W, const PlaneHalo &hb, const PlaneHalo &ha, int dty
     if (hx > FP_MAXHX || hx > W / 2) return false;
     const int rs = W + 2 * hx;
     const int ut = std::max(hb.ht, 2), ub = std::max(hb.hb, 2);
-    for (int cl = 2; cl <= 16; cl *= 2) {
+    for (int cl = MD_FP_MINCL; cl <= 16; cl *= 2) {
         if (H % cl) continue;
         const int rl = H / cl;
         if (rl > FP_MAXRL || (rl & 1)) continue;

@@ -10,7 +10,7 @@ from concurrent.futures import ThreadPoolExecutor
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1212_2245_b200 import build as B
 
-VARIED = ("md_fused_box_a.cu", "md_fused_box_b.cu", "md_fused.cu")
+VARIED = tuple(os.environ.get("MD_VARIED", "md_fused_box_a.cu md_fused_box_b.cu md_fused.cu").split())
 tag, defs = sys.argv[1], sys.argv[2:]
 # run the regular build first: its object cache supplies the unchanged translation units
 out_dir = os.path.join(B.ROOT, "build", "variants")
