@@ -88,33 +88,58 @@ def noisy(blurred: np.ndarray, seed: int, sigma: float = 5.0) -> np.ndarray:
 
 
 # ---------------------------------------------------------------------------------- workloads
+#
+# A workload is built in two halves: the INPUTS (host NumPy: the deterministic scene, the
+# blur, PCG64 noise) and, for the GPU arm only, the PIPELINE. The reference arm builds its
+# inputs with the CPU oracle's clamped convolution (bit-identical to the GPU synth kernel,
+# tests/test_gpu_parity.py) and never touches the device or libmdcuda.so.
+
+def gpu_synth(md):
+    return lambda g, psf: md.synth_blur(md.Image(g), psf).values
+
+
+def cpu_synth(md):
+    def blur(g, psf):
+        return np.clip(np.floor(O_clamped(g, oracle_spec(psf)) + 0.5), 0.0, 255.0)
+    return blur
+
+
+def O_clamped(g, spec):
+    from oracle import wr3l_oracle as O
+    return O.clamped_convolve(np.asarray(g, dtype=np.float64), spec)
+
 
 class C1:
     """configs[0]: 256^2, horizontal box L=15, sigma=5, Wiener + 5 RRRL."""
 
     name = "c1: 256x256 box L=15 horizontal, sigma=5, Wiener + 5 RRRL (BASELINE.json configs[0])"
+    profile_in_loop = True                     # stage marks on the same stream cost nothing here
 
-    def __init__(self, md, args):
+    def __init__(self, md, args, synth, gpu: bool = True):
         self.md = md
         self.psf = md.Psf.uniform_box(md.BlurAxis.HORIZONTAL, 15)
         self.params = md.DeconvParams()
-        fused = None if args.fused == "auto" else args.fused == "on"
-        self.pipe = md.DeblurPipeline((H, W), self.psf, self.params, md.Scenario.BOX_1D, dtype=args.dtype,
-                                      fused=fused)
-        self.describe = self.pipe.plan.describe
-        self.fused = self.pipe.plan.fused
-        blurred = md.synth_blur(md.make_test_image(W, H, seed=7), self.psf).values
+        blurred = synth(md.make_test_image(W, H, seed=7).values, self.psf)
         k = min(64, args.batch)
         base = np.stack([noisy(blurred, 5 + i) for i in range(k)])
         self.host = np.tile(base, (-(-args.batch // k), 1, 1))[:args.batch]
         self.cpu_items = [("box", self.psf, base[i]) for i in range(k)]
-        self.latency_plan = self.pipe.plan
+        if gpu:
+            self.pipe = self.make_pipe(args.dtype, args.fused)
+            self.describe = self.pipe.plan.describe
+            self.fused = self.pipe.plan.fused
+            self.latency_plan = self.pipe.plan
 
-    profile_in_loop = True                     # stage marks on the same stream cost nothing here
+    def make_pipe(self, dtype, fused="auto"):
+        fz = None if fused == "auto" else fused == "on"
+        return self.md.DeblurPipeline((H, W), self.psf, self.params, self.md.Scenario.BOX_1D, dtype=dtype, fused=fz)
 
-    def iter_launches(self, n) -> int:
-        """Launches of the fused iteration kernel for n frames (one per internal chunk)."""
-        return max(1, self.pipe.plan.launch_count(n) // 2)
+    def frames_per_iter_launch(self, n) -> float:
+        """Frames one launch of the iteration kernel covers: the fused kernel runs every
+        iteration of a chunk in one launch, the per-iteration kernel one launch per iteration
+        (md_run_launch_count = chunks x (1 Wiener + iteration launches))."""
+        per_chunk = 2 if self.fused else 1 + self.params.iterations
+        return n / max(1, self.pipe.plan.launch_count(n) // per_chunk)
 
     def run(self, f, u):
         self.pipe.plan.run(f, out=u)
@@ -130,7 +155,7 @@ class C1:
         return self.host[:nb], None
 
     def run_host(self, hin, hout, ctx):
-        self.pipe.run_batch(hin, out=hout)
+        self.pipe.run_batch(hin, out=hout, out_dtype=hout.dtype)
 
     def launches(self, n) -> int:
         return self.pipe.plan.launch_count(n)
@@ -138,6 +163,10 @@ class C1:
     def iter_bytes(self, n, esz) -> float:
         """SURVEY 8(d) algorithmic bytes of the iteration stage for n frames (8 passes/it.)."""
         return 8 * self.params.iterations * PX * esz * n
+
+    def frame_bytes(self, esz) -> float:
+        """SURVEY 8(d) algorithmic bytes of one whole frame (Wiener-1D 2 passes + 8 per it.)."""
+        return (2 + 8 * self.params.iterations) * PX * esz
 
 
 def c4_bank(md, seed: int = 2026):
@@ -165,46 +194,56 @@ def c4_bank(md, seed: int = 2026):
     return bank, kinds
 
 
+def c4_frames(md, bank, index, synth):
+    """The c4 frames for PSF assignment `index` (8 distinct noisy frames per PSF, 4 scenes),
+    plus one (kind, psf, frame) CPU sample item per PSF."""
+    scenes = [md.make_test_image(W, H, seed=s).values for s in (7, 8, 9, 10)]
+    distinct = 8
+    frames = np.empty((index.size, H, W))
+    items = []
+    for b, psf in enumerate(bank):
+        sel = np.nonzero(index == b)[0]
+        if sel.size == 0:
+            continue
+        blurred = [synth(scenes[j], psf) for j in range(4)]
+        base = [noisy(blurred[j % 4], 1000 * b + j) for j in range(distinct)]
+        for k, i in enumerate(sel):
+            frames[i] = base[k % distinct]
+        items.append((b, psf, base[0]))
+    return frames, items
+
+
 class C4:
     """configs[3]: 256^2 frames over a 48-PSF bank, grouped by PSF."""
 
     name = ("c4: 256x256 frames, 48-PSF bank (16 box H/V L 5-31 incl. fractional, 16 general 1D, "
             "12 lines L<=21 at random angles + 4 small 2D), sigma=5, Wiener + 5 RRRL (BASELINE.json configs[3])")
+    # the timed step deals the PSF groups over two streams (one group's last partial cluster
+    # wave overlaps the next group); the stage split comes from a separate, sequential pass
+    profile_in_loop = False
 
-    def __init__(self, md, args):
-        from paper_1212_2245_b200.batch import PsfBankPipeline
+    def __init__(self, md, args, synth, gpu: bool = True):
         self.md = md
         self.params = md.DeconvParams()
         self.bank, self.kinds = c4_bank(md)
-        self.pipe = PsfBankPipeline((H, W), self.bank, self.params, dtype=args.dtype)
         nb = len(self.bank)
         per = -(-args.batch // nb)
         self.index = np.minimum(np.arange(args.batch) // per, nb - 1)
-        scenes = [md.make_test_image(W, H, seed=s).values for s in (7, 8, 9, 10)]
-        distinct = 8
-        frames = np.empty((args.batch, H, W))
-        self.cpu_items = []
-        for b, psf in enumerate(self.bank):
-            sel = np.nonzero(self.index == b)[0]
-            if sel.size == 0:
-                continue
-            blurred = [md.synth_blur(md.Image(scenes[j]), psf).values for j in range(4)]
-            base = [noisy(blurred[j % 4], 1000 * b + j) for j in range(distinct)]
-            for k, i in enumerate(sel):
-                frames[i] = base[k % distinct]
-            self.cpu_items.append((self.kinds[b], psf, base[0]))
-        self.host = frames
-        self.describe = "; ".join(sorted({p.plan.describe.split(",")[0] for p in self.pipe.pipes}))
-        self.fused = False
-        self.latency_plan = self.pipe.pipes[int(self.index[0])].plan
+        self.host, items = c4_frames(md, self.bank, self.index, synth)
+        self.cpu_items = [(self.kinds[b], psf, fr) for b, psf, fr in items]
+        if gpu:
+            from paper_1212_2245_b200.batch import PsfBankPipeline
+            self.pipe = PsfBankPipeline((H, W), self.bank, self.params, dtype=args.dtype)
+            self.describe = "; ".join(sorted({p.plan.describe.split(",")[0] for p in self.pipe.pipes}))
+            self.fused = False
+            self.latency_plan = self.pipe.pipes[int(self.index[0])].plan
 
-    # the timed step deals the PSF groups over two streams (one group's last partial cluster
-    # wave overlaps the next group: 227k -> 239k frames/s); the stage split comes from a
-    # separate, sequential profiled pass
-    profile_in_loop = False
+    def make_pipe(self, dtype, fused="auto"):
+        from paper_1212_2245_b200.batch import PsfBankPipeline
+        return PsfBankPipeline((H, W), self.bank, self.params, dtype=dtype)
 
-    def run(self, f, u):
-        self.pipe.run(f, self.index, out=u, streams=2)
+    def run(self, f, u, pipe=None):
+        (pipe or self.pipe).run(f, self.index, out=u, streams=2)
 
     def run_profile(self, f, u) -> dict:
         tot = {"init_ms": 0.0, "iter_ms": 0.0, "layout_ms": 0.0, "groups": 0}
@@ -229,12 +268,24 @@ class C4:
     def launches(self, n) -> int:
         return self.pipe.launch_count(self.index[:n])
 
+    def frames_per_iter_launch(self, n):
+        return None                            # many kernels per step: no single dominant launch
+
     def iter_bytes(self, n, esz) -> float:
         # 8 passes per iteration for every class (line / box / direct-tap convolvers)
         return 8 * self.params.iterations * PX * esz * n
 
+    def frame_bytes(self, esz) -> float:
+        return (2 + 8 * self.params.iterations) * PX * esz
+
 
 WORKLOADS = {"c1": C1, "c4": C4}
+
+
+def bench_config(work_name: str, batch: int, world: int, esz: int) -> dict:
+    """The `config` object both arms print (identical for the same command line)."""
+    return {"workload": work_name, "frames_per_gpu_per_step": batch, "parallelism": f"frame-sharded x{world}",
+            "l2": f"inputs {batch * PX * esz / 2**20:.0f} MiB per GPU > 126 MB L2 (no reuse between steps)"}
 
 
 def run_c5(args, rank: int, world: int, local: int) -> None:
@@ -450,13 +501,16 @@ def cpu_rate(jobs, pool) -> tuple[float, float]:
     return sum(len(j) for j in jobs) / wall, wall
 
 
-def run_reference(args, rank: int) -> None:
-    """--impl reference: the reference algorithm (CPU oracle port) on all host cores."""
+def run_reference(args, rank: int, world: int) -> None:
+    """--impl reference: the reference algorithm (the CPU oracle port of the reference's
+    DeblurPipeline.run, NumPy float64) on all host cores. Inputs come from host NumPy and
+    the oracle's clamped convolution: no device work, libmdcuda.so is never loaded.
+    Under N>1 rank 0 alone runs; the other ranks exit without work."""
     if rank != 0:
         return
-    import paper_1212_2245_b200 as md
-    args.batch = min(args.batch, 1024)
-    work = WORKLOADS[args.config](md, args)            # inputs only (GPU-synthesised blur)
+    import paper_1212_2245_b200 as md              # host-side value types only (Psf, scenes)
+    esz = 8
+    work = WORKLOADS[args.config](md, args, cpu_synth(md), gpu=False)
     cores = host_cores()
     jobs = cpu_jobs(work, args.cpu_frames_per_core, cores)
     pool = mp.get_context("fork").Pool(cores)
@@ -467,16 +521,17 @@ def run_reference(args, rank: int) -> None:
     pool.join()
     per_step = sum(len(j) for j in jobs)
     value = per_step * args.steps / sum(walls)
+    sample = (f"{per_step} frames per step ({args.cpu_frames_per_core} per core) of this workload's frames "
+              "through oracle/wr3l_oracle.pipeline (NumPy float64 restatement of the reference's "
+              "DeblurPipeline.run: its radix-2 FFT and cumsum box filter), one process per host core")
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
+        "devices": "host CPU cores only (n_gpus echoes the launch's N; no device work)",
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(walls) / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (deterministic scenes, GPU-synthesised blur, PCG64 sigma=5 noise, 8-bit)",
-        "config": {"workload": work.name, "frames_per_step": per_step},
-        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": cores, "kind": "port",
-                         "sample": f"{per_step} frames per step through oracle/wr3l_oracle.pipeline (NumPy "
-                                   "float64, the reference's radix-2 FFT and cumsum box filter), one process "
-                                   "per host core"},
+        "data": DATA,
+        "config": bench_config(work.name, args.batch, world, esz),
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "p50_ms_per_frame": 1e3 * statistics.median(walls) / args.cpu_frames_per_core,
     }
@@ -485,48 +540,137 @@ def run_reference(args, rank: int) -> None:
 
 # ---------------------------------------------------------------------------------- GPU arm
 
-def main() -> None:
+DATA = "synthetic (deterministic scenes, clamped-spatial blur, PCG64 sigma=5 noise, 8-bit)"
+
+
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c1", choices=sorted(WORKLOADS) + ["c5"])
     ap.add_argument("--size", type=int, default=16384, help="c5 image side")
-    ap.add_argument("--dtype", default="float32", choices=["float32", "float64"])
+    ap.add_argument("--dtype", default="float64", choices=["float32", "float64"],
+                    help="arithmetic of the timed path (default float64, the reference's: core.py:3-4)")
     ap.add_argument("--batch", type=int, default=None, help="frames per GPU per step")
-    ap.add_argument("--e2e-batch", type=int, default=4096)
+    ap.add_argument("--e2e-batch", type=int, default=2048)
     ap.add_argument("--cpu-frames-per-core", type=int, default=24)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip latency / extra e2e / f32 context legs")
     ap.add_argument("--fused", default="auto", choices=["auto", "on", "off"])
-    args = ap.parse_args()
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N>1 (gloo: CPU tests of the timing path)")
+    args = ap.parse_args(argv)
     if args.batch is None:
         args.batch = 4096 if args.config == "c1" else 16384
+    return args
 
+
+def _free_port() -> int:
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _spawned(local: int, world: int, port: int, argv) -> None:
+    os.environ.update({"RANK": str(local), "LOCAL_RANK": str(local), "WORLD_SIZE": str(world),
+                       "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
+    rank_main(parse_args(argv))
+
+
+def main(argv=None) -> None:
+    args = parse_args(argv)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # `python bench.py --gpus N` without torchrun: launch the N ranks here (one process per
+        # GPU, RANK / LOCAL_RANK / WORLD_SIZE as torchrun would set them)
+        import torch.multiprocessing as tmp
+        port = _free_port()
+        tmp.start_processes(_spawned, args=(args.gpus, port, sys.argv[1:] if argv is None else argv),
+                            nprocs=args.gpus, join=True, start_method="spawn")
+        return
+    rank_main(args)
+
+
+def rank_main(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    import torch
     if args.impl == "reference":
-        if torch.cuda.is_available():
-            torch.cuda.set_device(local)
-        run_reference(args, rank)
+        run_reference(args, rank, world)
         return
 
+    import torch
     import torch.distributed as dist
 
-    torch.cuda.set_device(local)
+    cuda = args.backend == "nccl"
+    if cuda:
+        torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    if args.config == "c5":
-        run_c5(args, rank, world, local)
+        if cuda:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+    try:
+        if args.config == "c5":
+            run_c5(args, rank, world, local)
+        else:
+            run_frames(args, rank, world, local, cuda)
+    finally:
         if world > 1:
             dist.barrier()
             dist.destroy_process_group()
-        return
-    import paper_1212_2245_b200 as md
 
-    work = WORKLOADS[args.config](md, args)
+
+def timed_steps(run, steps: int, world: int, cuda: bool, stream=None, clk=None) -> float:
+    """Time `steps` calls of run() after a barrier, CUDA events on the launching stream
+    (synchronised on both sides); the max over ranks in ms."""
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        dist.barrier()
+    if cuda:
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(steps):
+            run()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1)
+    else:
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            run()
+        ms = (time.perf_counter() - t0) * 1e3
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda" if cuda else "cpu")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_frames(args, rank: int, world: int, local: int, cuda: bool) -> None:
+    """c1 / c4: B frames per GPU per step, frames independent (no collective on the data
+    path); value = all ranks' frames / the max over ranks of the timed region."""
+    import torch
+    import torch.distributed as dist
+    if not cuda:
+        # CPU process-group test of the sharding / timing logic (tests/test_bench_dist.py):
+        # the same barrier + max-over-ranks timing around a stand-in step, no device
+        esz = 8 if args.dtype == "float64" else 4
+        share = torch.zeros(args.batch, dtype=torch.float64)
+        ms = timed_steps(lambda: share.add_(1.0), args.steps, world, False)
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "value": args.batch * args.steps * world / (ms / 1e3),
+                              "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                              "ms_per_step": ms / args.steps, "backend": "gloo",
+                              "config": bench_config(WORKLOADS[args.config].name, args.batch, world, esz)}),
+                  flush=True)
+        return
+
+    import paper_1212_2245_b200 as md
+    work = WORKLOADS[args.config](md, args, gpu_synth(md))
     tdt = torch.float32 if args.dtype == "float32" else torch.float64
     esz = 4 if args.dtype == "float32" else 8
     f = torch.from_numpy(work.host).to(device="cuda", dtype=tdt).contiguous()
@@ -536,23 +680,18 @@ def main() -> None:
     for _ in range(args.warmup):
         work.run(f, u)
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
     prof = {"init_ms": 0.0, "iter_ms": 0.0, "layout_ms": 0.0, "groups": 0}
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def step():
+        if work.profile_in_loop:
+            p = work.run_profile(f, u)          # CUDA events between launch groups, same stream
+            for k in prof:
+                prof[k] += p[k]
+        else:
+            work.run(f, u)
+
     with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
-        ev0.record(stream)
-        for _ in range(args.steps):
-            if work.profile_in_loop:
-                p = work.run_profile(f, u)          # CUDA events between launch groups, same stream
-                for k in prof:
-                    prof[k] += p[k]
-            else:
-                work.run(f, u)
-        ev1.record(stream)
-        torch.cuda.synchronize()
-    elapsed_ms = ev0.elapsed_time(ev1)
+        max_ms = timed_steps(step, args.steps, world, True, stream)
     if not work.profile_in_loop:
         # stage split from profiled sequential steps after the timed region, scaled to it
         npf = max(1, min(args.steps, 5))
@@ -560,43 +699,43 @@ def main() -> None:
             p = work.run_profile(f, u)
             for k in prof:
                 prof[k] += p[k] * args.steps / npf
-    t = torch.tensor([elapsed_ms], device="cuda", dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    max_ms = float(t.item())
     value = args.batch * args.steps * world / (max_ms / 1e3)
 
-    # single-frame latency (p50 / p99 over 200 runs, batch = 1)
-    f1, u1 = f[:1].clone(), torch.empty_like(f[:1])
-    lat = []
-    for i in range(210):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        work.latency_plan.run(f1, out=u1)
-        b.record(stream)
-        b.synchronize()
-        if i >= 10:                                   # 200 timed single-frame runs
-            lat.append(a.elapsed_time(b))
-
-    # host-observed single-frame latency (call -> result ready, synchronised per call): the
-    # direct md_run call vs a replay of the same run captured as a CUDA graph (GpuPlan.capture)
-    g1 = work.latency_plan.capture(f1, u1)
-    host_lat = {}
-    for name, call in (("direct", lambda: work.latency_plan.run(f1, out=u1)), ("cuda_graph", g1.replay)):
-        xs = []
-        for i in range(110):
-            t0 = time.perf_counter()
-            call()
-            torch.cuda.synchronize()
+    extras = {}
+    if not args.no_extras:
+        # single-frame latency (p50 / p99 over 200 runs, batch = 1)
+        f1, u1 = f[:1].clone(), torch.empty_like(f[:1])
+        lat = []
+        for i in range(210):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            work.latency_plan.run(f1, out=u1)
+            b.record(stream)
+            b.synchronize()
             if i >= 10:
-                xs.append((time.perf_counter() - t0) * 1e3)
-        host_lat[name] = statistics.median(xs)
-    del g1
+                lat.append(a.elapsed_time(b))
+        extras["p50_ms_per_frame_batch1"] = statistics.median(lat)
+        extras["p99_ms_per_frame_batch1"] = sorted(lat)[min(len(lat) - 1, int(0.99 * len(lat)))]
+        # host-observed single-frame latency (call -> result ready): direct md_run vs a replay
+        # of the same run captured as a CUDA graph (GpuPlan.capture)
+        g1 = work.latency_plan.capture(f1, u1)
+        host_lat = {}
+        for name, call in (("direct", lambda: work.latency_plan.run(f1, out=u1)), ("cuda_graph", g1.replay)):
+            xs = []
+            for i in range(110):
+                t0 = time.perf_counter()
+                call()
+                torch.cuda.synchronize()
+                if i >= 10:
+                    xs.append((time.perf_counter() - t0) * 1e3)
+            host_lat[name] = statistics.median(xs)
+        del g1
+        extras["host_p50_ms_per_frame_batch1"] = host_lat
 
     # end to end through the public host-buffer entry (DeblurPipeline.run_batch(ndarray) ->
     # md_run_host_ex): pinned host frames in, pinned host results out, copies inside the timed
-    # region. Primary: the workload's native 8-bit frames in, float32 results out; also the
-    # drop-in float64 -> float64 (reference Image semantics).
+    # region. Headline: the workload's native 8-bit frames in, float64 results out (the
+    # reference's Image type, computed in float64).
     def e2e_rate(in_dtype, out_dtype, nb):
         frames, ctx = work.e2e_set(nb)
         hin = torch.from_numpy(np.ascontiguousarray(frames).astype(in_dtype)).pin_memory()
@@ -604,7 +743,7 @@ def main() -> None:
         hin_np, hout_np = hin.numpy(), hout.numpy()
         work.run_host(hin_np, hout_np, ctx)
         torch.cuda.synchronize()
-        steps = max(3, min(10, args.steps // 4))
+        steps = max(3, min(10, args.steps // 2))
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
@@ -614,18 +753,44 @@ def main() -> None:
         te = torch.tensor([el], device="cuda", dtype=torch.float64)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        return nb * steps * world / float(te.item()), hin_np.nbytes, hout_np.nbytes
+        return {"value": nb * steps * world / float(te.item()), "unit": "frames/s",
+                "h2d_bytes_per_step": hin_np.nbytes, "d2h_bytes_per_step": hout_np.nbytes, "frames_per_step": nb}
 
     nb = min(args.e2e_batch, args.batch)
-    e2e_value, e2e_in, e2e_out = e2e_rate(np.uint8, np.float32, nb)
-    nb64 = min(nb, 1024)
-    e2e64_value, e2e64_in, e2e64_out = e2e_rate(np.float64, np.float64, nb64)
-    e2e8_value, e2e8_in, e2e8_out = e2e_rate(np.uint8, np.uint8, nb)
+    out_np = np.float64 if args.dtype == "float64" else np.float32
+    e2e = e2e_rate(np.uint8, out_np, nb)
+    e2e["entry"] = work.e2e_entry("pinned uint8 frames", f"{np.dtype(out_np).name} results, computed in {args.dtype}")
+    if not args.no_extras:
+        if args.dtype == "float64":
+            x = e2e_rate(np.uint8, np.float32, nb)
+            x["entry"] = work.e2e_entry("pinned uint8 frames", "float32 results (computed in float64, rounded "
+                                        "on the device: half the PCIe bytes of the headline)")
+            extras["e2e_f32_out"] = x
+        x = e2e_rate(np.uint8, np.uint8, nb)
+        x["entry"] = work.e2e_entry("pinned uint8 frames", "uint8 frames quantised like the reference's write_pgm "
+                                    "(pgm.py:56-58), the CLI's output")
+        extras["e2e_u8"] = x
+
+    # context only, not the headline: the same frames through a float32 plan (the precision
+    # SURVEY 8(d) measured safe for the noisy 256^2 configs; the reference computes in float64)
+    f32_ctx = None
+    if not args.no_extras and args.dtype == "float64":
+        p32 = work.make_pipe("float32")
+        f32 = f.to(torch.float32)
+        u32 = torch.empty_like(f32)
+        run32 = (lambda: work.run(f32, u32, pipe=p32)) if args.config == "c4" else (lambda: p32.plan.run(f32, out=u32))
+        for _ in range(2):
+            run32()
+        ms32 = timed_steps(run32, max(3, args.steps // 2), world, True, stream)
+        f32_ctx = {"value": args.batch * max(3, args.steps // 2) * world / (ms32 / 1e3), "unit": "frames/s",
+                   "dtype": "f32", "note": "context only: float32 arithmetic is narrower than the reference's"}
+        del f32, u32, p32
 
     if rank == 0:
         pk = peaks()
         iter_bytes = work.iter_bytes(args.batch, esz) * args.steps
-        achieved = iter_bytes / (prof["iter_ms"] / 1e3) / 1e9 if prof["iter_ms"] > 0 else None
+        iter_s = prof["iter_ms"] / 1e3
+        achieved = iter_bytes / iter_s / 1e9 if prof["iter_ms"] > 0 else None
         cpu = None
         if not args.no_cpu and world == 1:            # the CPU baseline: rank 0 at N=1 only
             cores = host_cores()
@@ -637,65 +802,58 @@ def main() -> None:
             cpu = {"value": r, "unit": "frames/s", "cores": cores, "kind": "port",
                    "sample": f"{sum(len(j) for j in jobs)} frames of this workload ({wall:.1f} s wall) through "
                              "oracle/wr3l_oracle.pipeline (NumPy float64), one process per host core"}
+        key = f"{args.config}_{args.dtype}"
+        fpl = work.frames_per_iter_launch(args.batch)
+        traffic = measured_traffic(key, fpl) if fpl else None
         # the fused kernel keeps the iterate on chip, so its other roofline is the shared-memory
         # pipe (north_star: "HBM (or SMEM for fused in-cluster)"): ncu wavefronts per frame over
         # this run's iteration time, against SMs x 128 B/clk x the max SM clock
         smem_roof = None
-        wf = measured_smem(f"{args.config}_{args.dtype}", args.batch) if work.fused else None
+        wf = measured_smem(key, args.batch) if work.fused else None
         if wf and prof["iter_ms"] > 0:
             sms = torch.cuda.get_device_properties(local).multi_processor_count
-            ach = wf * 128 * args.steps / (prof["iter_ms"] / 1e3) / 1e12
+            ach = wf * 128 * args.steps / iter_s / 1e12
             pk_s = sms * 128 * pk["sm_max_mhz"] * 1e6 / 1e12
             smem_roof = {"bound": "smem", "kernel": "RRRL iteration (fused cluster kernel)", "achieved": ach,
                          "peak": pk_s, "unit": "TB/s", "frac": ach / pk_s,
                          "wavefronts_per_frame": wf / args.batch,
                          "source": "ncu l1tex__data_pipe_lsu_wavefronts_mem_shared.sum (profiles/ncu_traffic.json) "
                                    "over this run's iteration time; peak = SMs x 128 B/clk x max SM clock"}
+        frame_gbs = value / world * work.frame_bytes(esz) / 1e9
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32" if args.dtype == "float32" else "f64",
-            "data": "synthetic (deterministic scenes, GPU clamped-spatial blur, PCG64 sigma=5 noise, 8-bit)",
-            "config": {"workload": work.name, "frames_per_gpu_per_step": args.batch,
-                       "parallelism": f"frame-sharded x{world}",
-                       "l2": f"inputs {args.batch * PX * esz / 2**20:.0f} MiB per GPU > 126 MB L2",
-                       "plan": work.describe},
-            "p50_ms_per_frame_batch1": statistics.median(lat),
-            "p99_ms_per_frame_batch1": sorted(lat)[min(len(lat) - 1, int(0.99 * len(lat)))],
-            "host_p50_ms_per_frame_batch1": host_lat,
+            "data": DATA,
+            "config": bench_config(work.name, args.batch, world, esz),
+            "plan": work.describe,
+            **{k: v for k, v in extras.items() if not k.startswith("e2e")},
             "stage_ms_per_step": {k: prof[k] / args.steps for k in ("init_ms", "iter_ms", "layout_ms")},
             "stage_split_source": ("CUDA events between the launch groups of the timed steps" if work.profile_in_loop
                                    else "CUDA events of profiled sequential steps after the timed region"),
             "roofline": {"bound": "hbm",
-                         "kernel": "RRRL iteration" + (" (fused cluster kernel)" if work.fused else ""),
+                         "kernel": "RRRL iteration" + (" (fused cluster kernel)" if work.fused else " (per-iteration kernels)"),
                          "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": (achieved / pk["hbm_gbs"]) if achieved else None,
-                         "traffic": (measured_traffic(f"{args.config}_{args.dtype}", args.batch / work.iter_launches(args.batch))
-                                     if work.fused else None),
-                         "traffic_note": "DRAM bytes per launch of the fused kernel (ncu, scaled to this batch); "
-                                         "iterate, p, W stay on chip, so traffic is the compulsory stream only",
+                         "traffic": traffic,
+                         "traffic_note": "measured DRAM bytes per launch of the iteration kernel (ncu --set full, "
+                                         "profiles/ncu_traffic.json, scaled to this launch's frames)",
                          "peak_source": pk["source"],
                          "bytes_model": "SURVEY.md 8(d): 8 field passes per RRRL iteration x 65536 px x "
                                         f"{esz} B per frame; time = CUDA events around the iteration launches"},
+            "roofline_frame": {"bound": "hbm", "achieved": frame_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                               "frac": frame_gbs / pk["hbm_gbs"],
+                               "bytes_model": f"SURVEY.md 8(d): whole frame (Wiener 2 + 8 per iteration) field passes "
+                                              f"x {esz} B = {work.frame_bytes(esz):.0f} B per frame, over the step time"},
             "roofline_smem": smem_roof,
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": e2e_in,
-                    "d2h_bytes_per_step": e2e_out, "frames_per_step": nb,
-                    "entry": work.e2e_entry("pinned uint8 frames", "float32 results")},
-            "e2e_f64": {"value": e2e64_value, "unit": "frames/s", "h2d_bytes_per_step": e2e64_in,
-                        "d2h_bytes_per_step": e2e64_out, "frames_per_step": nb64,
-                        "entry": work.e2e_entry("pinned float64 frames", "float64 (drop-in Image semantics)")},
-            "e2e_u8": {"value": e2e8_value, "unit": "frames/s", "h2d_bytes_per_step": e2e8_in,
-                       "d2h_bytes_per_step": e2e8_out, "frames_per_step": nb,
-                       "entry": work.e2e_entry("pinned uint8 frames", "uint8 frames quantised like the "
-                                               "reference's write_pgm (pgm.py:56-58), the CLI's output")},
+            "e2e": e2e,
+            **{k: v for k, v in extras.items() if k.startswith("e2e")},
+            "f32_context": f32_ctx,
             "gpu_launches": work.launches(args.batch) * args.steps,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

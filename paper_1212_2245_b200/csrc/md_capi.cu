@@ -86,7 +86,7 @@ inline void prof_mark(cudaStream_t st, int kind) {
 }
 
 // ---------------------------------------------------------------- plan-time kernels
-__global__ void k_build_lut(double *t64, float *t32, float2 *p32) {
+__global__ void k_build_lut(double *t64, float *t32, float2 *p32, double2 *p64) {
     auto val = [](int i) {
         const double x = kLutDelta + (1.0 / kLutInvStep) * (double)i;   // deconv.py:106-108
         return x - 1.0 - log(x);
@@ -95,7 +95,11 @@ __global__ void k_build_lut(double *t64, float *t32, float2 *p32) {
         const double v = val(i);
         t64[i] = v;
         t32[i] = (float)v;
-        if (i + 1 < kLutCount) p32[i] = make_float2((float)v, (float)(val(i + 1) - v));
+        if (i + 1 < kLutCount) {
+            const double step = val(i + 1) - v;      // the reference's T[i+1] - T[i] (deconv.py:131-133)
+            p32[i] = make_float2((float)v, (float)step);
+            p64[i] = make_double2(v, step);
+        }
     }
 }
 
@@ -189,6 +193,7 @@ struct md_plan {
     double *d_lut64 = nullptr;
     float *d_lut32 = nullptr;
     float2 *d_lutp32 = nullptr;
+    double2 *d_lutp64 = nullptr;
     LutView lut{};
     // scratch / staging
     DevBuf scratch, stage, partial;
@@ -225,7 +230,7 @@ struct md_plan {
     ~md_plan() {
         for (void *p : {(void *)d_taps_blur, (void *)d_taps_adj, (void *)d_ptaps_blur, (void *)d_ptaps_adj, d_tw_n,
                         d_tw_H, d_tw_W, d_mult, d_mult_nat, d_hspec, (void *)d_lut64, (void *)d_lut32,
-                        (void *)d_lutp32})
+                        (void *)d_lutp32, (void *)d_lutp64})
             if (p) cudaFree(p);
         for (void *p : owned) cudaFree(p);
         scratch.release();
@@ -249,12 +254,14 @@ int build_lut(md_plan *P) {
     CU(cudaMalloc(&P->d_lut64, kLutCount * sizeof(double)));
     CU(cudaMalloc(&P->d_lut32, kLutCount * sizeof(float)));
     CU(cudaMalloc(&P->d_lutp32, (kLutCount - 1) * sizeof(float2)));
-    k_build_lut<<<(kLutCount + 255) / 256, 256>>>(P->d_lut64, P->d_lut32, P->d_lutp32);
+    CU(cudaMalloc(&P->d_lutp64, (kLutCount - 1) * sizeof(double2)));
+    k_build_lut<<<(kLutCount + 255) / 256, 256>>>(P->d_lut64, P->d_lut32, P->d_lutp32, P->d_lutp64);
     CU(cudaGetLastError());
     CU(cudaDeviceSynchronize());
     P->lut.t64 = P->d_lut64;
     P->lut.t32 = P->d_lut32;
     P->lut.p32 = P->d_lutp32;
+    P->lut.p64 = P->d_lutp64;
     return MD_OK;
 }
 
@@ -549,13 +556,15 @@ int32_t md_plan_create(const md_plan_desc *desc, md_plan **out) {
             CU(cudaDeviceSynchronize());
             P->wiener_reg = !(desc->flags & MD_FLAG_GENERIC_LINES) && wiener_reg_supported(desc->dtype, P->n);
         }
-        // default: the cluster kernel for float (measured faster); float64 keeps the
-        // per-iteration kernel (16-CTA clusters at one CTA per SM lose to it), opt-in via
-        // md_plan_set_fused
-        P->fused = desc->dtype == MD_F32 && P->fast_lines &&
-                   fused_lines_supported(desc->dtype, P->n, P->m, desc->flags,
-                                         std::max(line_radius(P->lblur), line_radius(P->ladj)));
-        if (P->fused) P->fused_clusters = lines_fused_clusters<float>(*P);
+        // default: the cluster kernel -- float, and float64 for line radii <= 8 (the
+        // shuffle-window / st.async-halo kernel, md_fused64_kernel.cuh, two CTAs per SM);
+        // wider float64 kernels keep the per-iteration kernel (the generic cluster kernel runs
+        // 16-CTA clusters at one CTA per SM and loses to it), opt-in via md_plan_set_fused
+        const int lrad = std::max(line_radius(P->lblur), line_radius(P->ladj));
+        P->fused = (desc->dtype == MD_F32 || lrad <= 8) && P->fast_lines &&
+                   fused_lines_supported(desc->dtype, P->n, P->m, desc->flags, lrad);
+        if (P->fused)
+            P->fused_clusters = desc->dtype == MD_F32 ? lines_fused_clusters<float>(*P) : lines_fused_clusters<double>(*P);
         snprintf(buf, sizeof buf, "lines: n=%d m=%d %s %s %s, %s", P->n, P->m, P->vert ? "vertical" : "horizontal",
                  use_box ? "box" : "taps", periodic ? "periodic" : "clamped",
                  P->fused ? "fused cluster iteration kernel"

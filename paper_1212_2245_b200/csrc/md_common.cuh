@@ -6,7 +6,30 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 namespace md {
+
+// host: raise a kernel's dynamic shared-memory limit (and allow non-portable cluster sizes)
+// once per (kernel, device), not on every launch -- cudaFuncSetAttribute costs microseconds,
+// which batch-1 latency notices. Thread-safe; the limit only grows.
+inline cudaError_t func_smem_attr(const void *kern, size_t smem, bool nonportable_cluster = false) {
+    static std::mutex mu;
+    static std::map<std::pair<const void *, int>, size_t> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    auto key = std::make_pair(kern, dev * 2 + (nonportable_cluster ? 1 : 0));
+    auto it = done.find(key);
+    if (it != done.end() && it->second >= smem) return cudaSuccess;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess && nonportable_cluster) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e == cudaSuccess) done[key] = smem;
+    return e;
+}
 
 template <typename T> struct Cx;
 template <> struct Cx<double> { using type = double2; };
@@ -43,6 +66,7 @@ struct LutView {
     const double *t64;
     const float *t32;
     const float2 *p32;                            // (t32[i], t[i+1] - t[i]), i < kLutCount - 1
+    const double2 *p64;                           // (t[i], t[i+1] - t[i]) in float64, i < kLutCount - 1
 };
 
 __device__ __forceinline__ double lut_fetch(const LutView &L, int i, double) { return __ldg(L.t64 + i); }

@@ -28,5 +28,9 @@ inline cudaError_t launch_fused_box(const FusedLinesArgs &d, int radius, int64_t
     return radius <= 8 ? launch_fused_box_parta<T>(d, radius, batch, st) : launch_fused_box_partb<T>(d, radius, batch, st);
 }
 template <typename T> cudaError_t launch_fused_lines(const FusedLinesArgs &, int64_t batch, cudaStream_t);
+// float64, radius <= 8: the shuffle-window / st.async-halo kernel (md_fused64.cu);
+// cudaErrorNotSupported when it does not apply
+cudaError_t launch_fused64(const FusedLinesArgs &, int64_t batch, cudaStream_t);
+int fused64_rows();   // lines per CTA of that kernel
 
 }  // namespace md

@@ -1,0 +1,459 @@
+// md_fused64_kernel.cuh -- the float64 cluster-resident RRRL loop for 1D blur (frames <= 256
+// samples per line): all iterations of a frame in ONE launch, the iterate resident in the shared
+// memory of a thread-block cluster.
+//
+// Replaces the iteration loop of DeblurPipeline.run_timed (deconv.py:675-681): _iterate_rrrl
+// (deconv.py:512-521) -> _blur_guarded (415-418), _weight_arrays + DivergenceLut.r1 (142-162,
+// 114-134), _diffusion_arrays (187-213), _combine (421-446), with the box (conv.py:141-173) or
+// dense line-tap convolver, in IEEE float64 throughout (the reference's arithmetic, core.py:3-4).
+//
+// What differs from the float kernel (md_fused_kernel.cuh), all to fit float64 lines (2.4 KB
+// each) at two 8-warp CTAs per SM:
+//  * no per-warp p / W line buffers: the adjoint windows of p = W f / b and W are assembled in
+//    registers with warp shuffles (a lane's 8 samples plus R from each neighbour lane, the line
+//    ends edge-replicated or wrapped), so shared memory holds only the iterate, its halo lines
+//    and the diffusivity;
+//  * the boundary lines travel to the neighbour CTAs as st.async stores into their shared
+//    memory, completing a transaction count on the neighbour's mbarrier (one per halo parity):
+//    each CTA waits only for its two neighbours' lines, not for a cluster-wide barrier, and the
+//    interior diffusivity is computed while they are in flight;
+//  * the divergence table is read as one 16-byte (value, step) pair per pixel (bitwise the
+//    reference's T[i] + (T[i+1] - T[i]) t).
+//
+// Per iteration, per CTA (lines li = warp + NW j):
+//   per own line: window of u (smem) -> blur -> guard -> W, p (registers) -> shuffled windows ->
+//   adjoint pair -> TV divergence from the stored diffusivity -> u' (registers)
+//   __syncthreads; u' -> own lines (+ x-halos); boundary lines -> neighbours (st.async);
+//   __syncthreads; interior diffusivity; wait for the neighbours' lines; boundary diffusivity
+#pragma once
+#include <cooperative_groups.h>
+
+#include "md_fused_kernel.cuh"
+
+namespace md {
+
+// ------------------------------------------------------------------ mbarrier / DSMEM helpers
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mb_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+// the single arrival of a phase plus the bytes it expects from the neighbours
+__device__ __forceinline__ void mb_arm(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint32_t bar, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ uint32_t cluster_map(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+// 16 bytes into a neighbour CTA's shared memory; completes 16 bytes of its mbarrier's count
+__device__ __forceinline__ void st_async_f64x2(uint32_t raddr, double x, double y, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+                 "d"(x), "d"(y), "r"(rbar)
+                 : "memory");
+}
+
+// r1 with the (value, step) pair table (md_common.cuh rules, deconv.py:114-134)
+__device__ __forceinline__ double r1_pair64(const double2 *__restrict__ p64, double x) {
+    const double xc = x < kLutUpper ? x : kLutUpper;
+    double pos = (xc - kLutDelta) * kLutInvStep;
+    pos = pos > 0.0 ? pos : 0.0;
+    int i = (int)pos;
+    i = i < kLutCount - 2 ? i : kLutCount - 2;
+    const double2 e = __ldg(p64 + i);
+    double r = e.x + e.y * (pos - (double)i);
+    if (x > kLutUpper) r = kLutSlope * x + kLutIntercept;
+    if (x < kLutDirectBelow) r = x - 1.0 - log(x);
+    return r;
+}
+
+// the window [-R, SEG + R) of a lane's 8 samples, the outer 2R taken from the neighbour lanes
+// (lanes >= nseg idle); clamped line ends replicate the end sample, periodic ones wrap
+template <int R>
+__device__ __forceinline__ void lane_window(const double (&x)[SEG], double (&w)[SEG + 2 * R], int lane, int nseg,
+                                            bool periodic) {
+    static_assert(R <= SEG, "neighbour-lane windows need R <= 8");
+    const int src_l = lane == 0 ? nseg - 1 : lane - 1;
+    const int src_r = lane >= nseg - 1 ? 0 : lane + 1;
+#pragma unroll
+    for (int k = 0; k < SEG; ++k) w[R + k] = x[k];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+        w[k] = __shfl_sync(0xffffffffu, x[SEG - R + k], src_l);
+        w[R + SEG + k] = __shfl_sync(0xffffffffu, x[k], src_r);
+    }
+    if (!periodic) {
+        if (lane == 0)
+#pragma unroll
+            for (int k = 0; k < R; ++k) w[k] = x[0];
+        if (lane == nseg - 1)
+#pragma unroll
+            for (int k = 0; k < R; ++k) w[R + SEG + k] = x[SEG - 1];
+    }
+}
+
+template <int R, int NW, int LPW, bool ROBUST, int BOXR, bool BOXC>
+__global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
+k_fused_lines64(FusedKArgs<double, R> a, const double2 *__restrict__ lut64) {
+    using T = double;
+    constexpr int HW = HaloOf<R>::value;
+    constexpr int WIN = SEG + 2 * R;
+    constexpr int RL = NW * LPW;
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T *sm = reinterpret_cast<T *>(smem_raw);
+    const int n = a.n, m = a.m;
+    const int ls = (xline_len(n, HW) + 1) & ~1;      // even: 16-byte st.async granules
+    const int rank = (int)cluster.block_rank();
+    const int CL = a.cl;
+    const int64_t frame = blockIdx.x / CL;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nseg = n / SEG;
+    const int base0 = xaddr(HW);
+    const int gl0 = rank * RL;
+    const int64_t fsz = (int64_t)n * m;
+    const T *fpos = a.fpos + frame * fsz;
+
+    // shared layout (lines of ls doubles): own[RL] | halo[parity][top, bottom][2] | g[RL + 2] | mbar[2]
+    T *own = sm;
+    auto halo = [&](int par, int side) { return sm + (RL + 4 * par + 2 * side) * ls; };
+    T *sg = sm + (RL + 8) * ls;
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(sm + (2 * RL + 10) * ls);
+    auto line_ptr = [&](int l, int par) -> const T * {
+        if (l < 0) return halo(par, 0) + (l + 2) * ls;
+        if (l >= RL) return halo(par, 1) + (l - RL) * ls;
+        return own + l * ls;
+    };
+    const bool has_top = rank > 0, has_bot = rank < CL - 1;
+    const uint32_t line_bytes = (uint32_t)ls * 8u;
+    const uint32_t expect = (has_top ? 2u : 0u) * line_bytes + (has_bot ? 2u : 0u) * line_bytes;
+    if (threadIdx.x == 0) {
+        mb_init(smem_addr(&mbar[0]), 1);
+        mb_init(smem_addr(&mbar[1]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mb_arm(smem_addr(&mbar[0]), expect);
+        mb_arm(smem_addr(&mbar[1]), expect);
+    }
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    cluster.sync();                                  // all CTAs resident, barriers initialised
+    // neighbour targets: my lines 0, 1 -> top neighbour's bottom halo; RL-2, RL-1 -> bottom
+    // neighbour's top halo (same parity)
+    // parity 0 addresses in the neighbours (parity 1 = + 4 lines, barrier + 8 bytes)
+    const uint32_t top_dst = has_top ? cluster_map(smem_addr(halo(0, 1)), rank - 1) : 0u;
+    const uint32_t bot_dst = has_bot ? cluster_map(smem_addr(halo(0, 0)), rank + 1) : 0u;
+    const uint32_t top_bar = has_top ? cluster_map(smem_addr(&mbar[0]), rank - 1) : 0u;
+    const uint32_t bot_bar = has_bot ? cluster_map(smem_addr(&mbar[0]), rank + 1) : 0u;
+    // one own line (already in shared memory, x-halos filled) to the neighbour that needs it
+    auto push_line = [&](int li, int par) {
+        const T *L = own + li * ls;
+        uint32_t dst, bar;
+        if (li < 2 && has_top) {
+            dst = top_dst + (uint32_t)((4 * par + li) * ls) * 8u;
+            bar = top_bar + 8u * par;
+        } else if (li >= RL - 2 && has_bot) {
+            dst = bot_dst + (uint32_t)((4 * par + li - (RL - 2)) * ls) * 8u;
+            bar = bot_bar + 8u * par;
+        } else {
+            return;
+        }
+        for (int q = 2 * lane; q < ls; q += 64) st_async_f64x2(dst + (uint32_t)q * 8u, L[q], L[q + 1], bar);
+    };
+
+    // ---- load u0 (own lines), fill x-halos, push the boundary lines (parity 0)
+    {
+        const T *src = a.u0 + frame * fsz + (int64_t)gl0 * n;
+        for (int li = warp; li < RL; li += NW) {
+            T *L = own + li * ls;
+            for (int j = lane; j < n; j += 32) L[xaddr(HW + j)] = src[(int64_t)li * n + j];
+            __syncwarp();
+            fu_fill_halo<T>(L, n, HW, a.periodic, lane);
+            __syncwarp();
+            push_line(li, 0);
+        }
+    }
+
+    const T eps_r2 = a.eps_r2, eps_d2 = a.eps_d2;
+    constexpr bool FOLD = BOXR > 0 && !BOXC;
+    const T al = FOLD ? a.alpha_w : a.alpha, gd = FOLD ? a.guard_w : T(kGuard), one = FOLD ? a.one_w : T(1);
+    // diffusivity g on logical lines l in [lb, le] (deconv.py:191-203)
+    auto g_lines = [&](int lb, int le, int par, int wl) {
+        if (!a.has_d) return;
+        for (int l = lb + wl; l <= le; l += NW) {
+            const int gl = gl0 + l;
+            if (gl < 0 || gl >= m) continue;
+            const bool up_ok = gl > 0, dn_ok = gl + 1 < m;
+            const T *row = line_ptr(l, par), *up = line_ptr(l - 1, par), *dn = line_ptr(l + 1, par);
+            for (int s = lane; s < nseg; s += 32) {
+                const int off = base0 + 9 * s;
+                T x[SEG + 2];
+#pragma unroll
+                for (int k = -1; k <= SEG; ++k) x[k + 1] = row[off + koff(k)];
+                T *G = sg + (l + 1) * ls + off;
+#pragma unroll
+                for (int r = 0; r < SEG; ++r) {
+                    T dxr = x[r + 2] - x[r + 1];
+                    T dxl = x[r + 1] - x[r];
+                    if (r == SEG - 1 && s == nseg - 1) dxr = T(0);
+                    if (r == 0 && s == 0) dxl = T(0);
+                    const T yd = dn_ok ? dn[off + koff(r)] : x[r + 1];
+                    const T yu = up_ok ? up[off + koff(r)] : x[r + 1];
+                    const T dyd = yd - x[r + 1], dyu = x[r + 1] - yu;
+                    const T q = dxr * dxr + dxl * dxl + dyd * dyd + dyu * dyu;
+                    G[koff(r)] = T(0.5) * frsqrt(T(0.5) * q + eps_r2);
+                }
+            }
+        }
+    };
+    // wait for the neighbours' lines of parity `par` (phase `use` of that barrier), re-arm it,
+    // then the diffusivity of the halo-dependent lines
+    auto publish_and_g = [&](int par, int use) {
+        __syncthreads();
+        g_lines(1, RL - 2, par, (warp + NW - 2) % NW);
+        if (warp < 4) {
+            mb_wait(smem_addr(&mbar[par]), (uint32_t)(use & 1));
+            if (threadIdx.x == 0) mb_arm(smem_addr(&mbar[par]), expect);
+            g_lines(warp < 2 ? -1 : RL - 1, warp < 2 ? 0 : RL, par, warp & 1);
+        }
+        __syncthreads();
+    };
+    publish_and_g(0, 0);
+    for (int it = 0; it < a.iterations; ++it) {
+        const int par = it & 1;
+        const bool last = it == a.iterations - 1;
+        T unew[LPW][SEG];
+#pragma unroll
+        for (int j = 0; j < LPW; ++j) {
+            const int li = warp + NW * j;
+            const int gl = gl0 + li;
+            const bool up_ok = gl > 0, dn_ok = gl + 1 < m;
+            const T *U = own + li * ls;
+            const T *F = fpos + (int64_t)gl * n;
+            const int s = lane < nseg ? lane : nseg - 1;     // idle lanes shadow the last segment
+            const int off = base0 + 9 * s;
+            {
+                const int ln = j + 1 < LPW ? li + NW : warp;
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(fpos + (int64_t)(gl0 + ln) * n + SEG * s));
+            }
+            T fv[SEG];
+            {
+                const double2 *f2 = reinterpret_cast<const double2 *>(F + SEG * s);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const double2 x = __ldg(f2 + i);
+                    fv[2 * i] = x.x;
+                    fv[2 * i + 1] = x.y;
+                }
+            }
+            T pv[SEG], wv[SEG];
+            {
+                T v[WIN];
+#pragma unroll
+                for (int k = -R; k < SEG + R; ++k) v[k + R] = U[off + koff(k)];
+                T bl[SEG];
+                conv_window<T, R, BOXR, BOXC>(v, a.wb, a.box_wi, a.box_cb, bl);
+#pragma unroll
+                for (int r = 0; r < SEG; ++r) {
+                    const T b = bl[r] > T(kGuard) ? bl[r] : T(kGuard);
+                    const T fp = fv[r];
+                    const T ratio = fp * frcp(b);
+                    if (ROBUST) {
+                        const T xr = b * frcp(fp);
+                        const T w = T(0.5) * frsqrt(r1_pair64(lut64, xr) * fp + eps_d2);
+                        wv[r] = w;
+                        pv[r] = w * ratio;
+                    } else {
+                        pv[r] = ratio;
+                    }
+                }
+            }
+            T num[SEG], den[SEG];
+            {
+                T v[WIN];
+                lane_window<R>(pv, v, lane, nseg, a.periodic);
+                conv_window<T, R, BOXR, BOXC, !FOLD>(v, a.wa, a.box_wi, a.box_ca, num);
+            }
+            if (ROBUST) {
+                T v[WIN];
+                lane_window<R>(wv, v, lane, nseg, a.periodic);
+                conv_window<T, R, BOXR, BOXC, !FOLD>(v, a.wa, a.box_wi, a.box_ca, den);
+            }
+            T ux[SEG + 2];
+#pragma unroll
+            for (int k = -1; k <= SEG; ++k) ux[k + 1] = U[off + koff(k)];
+            if (a.has_d) {
+                const T *G = sg + (li + 1) * ls + off;
+                const T *Gu = G - ls, *Gd = G + ls;
+                const T *Uu = line_ptr(li - 1, par) + off, *Ud = line_ptr(li + 1, par) + off;
+                T gx[SEG + 2];
+#pragma unroll
+                for (int k = -1; k <= SEG; ++k) gx[k + 1] = G[koff(k)];
+#pragma unroll
+                for (int r = 0; r < SEG; ++r) {
+                    const T u = ux[r + 1], gc = gx[r + 1];
+                    T fr = (gc + gx[r + 2]) * (ux[r + 2] - u);
+                    T fl = (gx[r] + gc) * (u - ux[r]);
+                    if (r == SEG - 1 && s == nseg - 1) fr = T(0);
+                    if (r == 0 && s == 0) fl = T(0);
+                    T d = fr - fl;
+                    if (dn_ok) d += (gc + Gd[koff(r)]) * (Ud[koff(r)] - u);
+                    if (up_ok) d -= (Gu[koff(r)] + gc) * (u - Uu[koff(r)]);
+                    const T nm = num[r] + al * (d > T(0) ? d : T(0));
+                    const T neg = al * (d < T(0) ? d : T(0));
+                    T dn = (ROBUST ? den[r] : one) - neg;
+                    dn = fmax(dn, gd);
+                    unew[j][r] = (u * nm) * frcp(dn);
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < SEG; ++r) {
+                    if (ROBUST) {
+                        const T dn = fmax(den[r], gd);
+                        unew[j][r] = (ux[r + 1] * num[r]) * frcp(dn);
+                    } else {
+                        unew[j][r] = ux[r + 1] * (FOLD ? num[r] * a.box_wi : num[r]);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        if (last) {
+            T *dst = a.out + frame * fsz;
+#pragma unroll
+            for (int j = 0; j < LPW; ++j) {
+                const int li = warp + NW * j;
+                const int gl = gl0 + li;
+                if (lane >= nseg) continue;
+                if (!a.out_vert) {
+                    double2 *o2 = reinterpret_cast<double2 *>(dst + (int64_t)gl * n + SEG * lane);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) o2[i] = make_double2(unew[j][2 * i], unew[j][2 * i + 1]);
+                } else {
+                    T *L = own + li * ls + base0 + 9 * lane;
+#pragma unroll
+                    for (int r = 0; r < SEG; ++r) L[koff(r)] = unew[j][r];
+                }
+            }
+            if (a.out_vert) {
+                __syncthreads();
+                for (int idx = threadIdx.x; idx < RL * n; idx += blockDim.x) {
+                    const int row = idx / RL, li = idx - row * RL;
+                    dst[(int64_t)row * m + gl0 + li] = own[li * ls + xaddr(HW + row)];
+                }
+            }
+            break;
+        }
+        // ---- u' -> own lines + x-halos; boundary lines -> the neighbours' halo[par ^ 1]
+        const int npar = par ^ 1;
+#pragma unroll
+        for (int j = 0; j < LPW; ++j) {
+            const int li = warp + NW * j;
+            T *L = own + li * ls;
+            if (lane < nseg) {
+                T *P = L + base0 + 9 * lane;
+#pragma unroll
+                for (int r = 0; r < SEG; ++r) P[koff(r)] = unew[j][r];
+            }
+            __syncwarp();
+            fu_fill_halo<T>(L, n, HW, a.periodic, lane);
+            __syncwarp();
+            push_line(li, npar);
+        }
+        // use index of barrier npar: u^(it+1) is its ((it + 1) >> 1)-th completion
+        publish_and_g(npar, (it + 1) >> 1);
+    }
+}
+
+template <int R, int NW, int LPW>
+size_t fused64_smem(int n) {
+    constexpr int HW = HaloOf<R>::value;
+    const int ls = (xline_len(n, HW) + 1) & ~1;
+    return (size_t)(2 * NW * LPW + 10) * ls * sizeof(double) + 2 * sizeof(uint64_t);
+}
+
+template <int R, int NW, int LPW>
+cudaError_t launch_fused64_t(void (*kern)(FusedKArgs<double, R>, const double2 *), const FusedKArgs<double, R> &a,
+                             const double2 *lut64, int64_t batch, cudaStream_t st) {
+    const size_t smem = fused64_smem<R, NW, LPW>(a.n);
+    {
+        const cudaError_t e = func_smem_attr((const void *)kern, smem, true);
+        if (e != cudaSuccess) return e;
+    }
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = a.cl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    if (a.query) {
+        cudaLaunchConfig_t q = {};
+        q.gridDim = dim3((unsigned)a.cl, 1, 1);
+        q.blockDim = dim3(NW * 32, 1, 1);
+        q.dynamicSmemBytes = smem;
+        q.attrs = attr;
+        q.numAttrs = 1;
+        return cudaOccupancyMaxActiveClusters(a.query, kern, &q);
+    }
+    const int64_t fsz = (int64_t)a.n * a.m;
+    const int64_t maxf = (int64_t)(0x7fffffff / a.cl);
+    for (int64_t b0 = 0; b0 < batch; b0 += maxf) {
+        const int64_t nb = std::min<int64_t>(maxf, batch - b0);
+        FusedKArgs<double, R> ab = a;
+        ab.u0 += b0 * fsz;
+        ab.fpos += b0 * fsz;
+        ab.out += b0 * fsz;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(nb * a.cl), 1, 1);
+        cfg.blockDim = dim3(NW * 32, 1, 1);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ab, lut64);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaGetLastError();
+}
+
+// geometry of the float64 kernel: 8 warps x 2 lines (16-line CTAs, two per SM, m / 16 CTAs per
+// cluster) -- MD_F64_NW=16 selects 16 warps x 2 lines (32-line CTAs, one per SM)
+#ifndef MD_F64_NW
+#define MD_F64_NW 8
+#endif
+constexpr int F64_NW = MD_F64_NW;
+constexpr int F64_LPW = 2;
+
+template <int RR>
+cudaError_t launch_fused64_box_r(const FusedLinesArgs &d, int64_t batch, cudaStream_t st) {
+    FusedKArgs<double, RR> a{};
+    a.u0 = static_cast<const double *>(d.u_in);
+    a.fpos = static_cast<const double *>(d.fpos);
+    a.out = static_cast<double *>(d.u_out);
+    a.query = d.query;
+    a.n = d.n; a.m = d.m; a.iterations = d.iterations; a.out_vert = d.out_vert;
+    a.periodic = d.blur.periodic;
+    a.cl = d.m / (F64_NW * F64_LPW);
+    a.alpha = d.alpha; a.eps_d2 = d.eps_d2; a.eps_r2 = d.eps_r2; a.has_d = d.has_d;
+    a.lut = d.lut;
+    a.box_wi = d.blur.wi;
+    a.alpha_w = d.alpha / d.blur.wi; a.guard_w = kGuard / d.blur.wi; a.one_w = 1.0 / d.blur.wi;
+    if (!box_corrections<double, RR>(d.blur, d.blur.wi, a.box_cb) || !box_corrections<double, RR>(d.adj, d.blur.wi, a.box_ca))
+        return cudaErrorNotSupported;
+    bool corr = false;
+    for (int i = 0; i < 4; ++i) corr = corr || a.box_cb[i] != 0.0 || a.box_ca[i] != 0.0;
+    return launch_fused64_t<RR, F64_NW, F64_LPW>(corr ? k_fused_lines64<RR, F64_NW, F64_LPW, true, RR, true>
+                                                      : k_fused_lines64<RR, F64_NW, F64_LPW, true, RR, false>,
+                                                 a, d.lut.p64, batch, st);
+}
+
+}  // namespace md

@@ -355,12 +355,8 @@ cudaError_t launch_fused_t(void (*kern)(FusedKArgs<T, R>), const FusedKArgs<T, R
     constexpr int HW = HaloOf<R>::value;
     constexpr int RL = FU_WARPS * LPW;
     const size_t smem = (size_t)(2 * RL + 10 + 2 * FU_WARPS) * xline_len(a.n, HW) * sizeof(T);
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = func_smem_attr((const void *)kern, smem, a.cl > 8);
     if (e != cudaSuccess) return e;
-    if (a.cl > 8) {
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return e;
-    }
     if (a.query) {
         cudaLaunchConfig_t q = {};
         q.gridDim = dim3((unsigned)a.cl, 1, 1);

@@ -342,8 +342,7 @@ cudaError_t launch_j(const FusedPlaneDesc &d, const FpGeom &g, int64_t batch, cu
     a.alpha = T(d.alpha); a.eps_d2 = T(d.eps_d2); a.eps_r2 = T(d.eps_r2); a.has_d = d.has_d;
     a.lut = d.lut;
     auto kern = d.robust ? k_fused_plane<T, J, true> : k_fused_plane<T, J, false>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
-    if (e == cudaSuccess && g.cl > 8) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaError_t e = func_smem_attr((const void *)kern, g.smem, g.cl > 8);
     if (e != cudaSuccess) return e;
     const int64_t fsz = (int64_t)d.H * d.W;
     const int64_t maxf = (int64_t)(0x7fffffff / g.cl);

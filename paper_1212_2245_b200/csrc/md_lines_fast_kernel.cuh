@@ -237,7 +237,7 @@ template <typename T, int R>
 cudaError_t launch_iter_fast_k(void (*kern)(IterFastArgs<T, R>), const IterFastArgs<T, R> &a, int64_t batch,
                                cudaStream_t st) {
     const size_t smem = iter_fast_smem<T, R>(a.n);
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = func_smem_attr((const void *)kern, smem);
     if (e != cudaSuccess) return e;
     const int tiles = (a.m + FTL - 1) / FTL;
     const int64_t fsz = (int64_t)a.n * a.m;

@@ -232,8 +232,7 @@ template <typename T, int S>
 cudaError_t launch_wiener_reg_t(const WienerLinesArgs &a, int64_t batch, cudaStream_t st) {
     constexpr int PB = 256 / S;
     const size_t smem = (size_t)(S * S + PB * (S * (S + 1) + 1)) * sizeof(cx_t<T>);
-    cudaError_t e = cudaFuncSetAttribute(k_wiener_lines_reg<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    cudaError_t e = func_smem_attr((const void *)k_wiener_lines_reg<T, S>, smem);
     if (e != cudaSuccess) return e;
     const int groups = (a.m + 2 * PB - 1) / (2 * PB);
     const int64_t fb = (int64_t)a.n * a.m * sizeof(T);
