@@ -13,7 +13,9 @@ int fused_lpw(int dtype, int radius) { return dtype == 0 ? 2 : (radius > 8 ? 2 :
 bool fused_lines_supported(int dtype, int n, int m, unsigned flags, int radius) {
     if (flags & 2u) return false;                  // MD_FLAG_NO_FUSED
     if (n % SEG != 0 || n / SEG > 32 || n < 64) return false;
-    const int rl = dtype == 0 && radius <= 8 ? fused64_rows() : FU_WARPS * fused_lpw(dtype, radius);
+    // float64, radius <= 8: any line count the cluster can hold (2..16 CTAs of 4..rows lines)
+    if (dtype == 0 && radius <= 8) return m >= 8 && (m + 15) / 16 <= fused64_rows();
+    const int rl = FU_WARPS * fused_lpw(dtype, radius);
     if (m % rl != 0) return false;
     const int cl = m / rl;
     return cl >= 2 && cl <= 16;

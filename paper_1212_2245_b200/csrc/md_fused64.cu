@@ -34,7 +34,7 @@ cudaError_t launch_fused64(const FusedLinesArgs &d, int64_t batch, cudaStream_t 
         a.query = d.query;
         a.n = d.n; a.m = d.m; a.iterations = d.iterations; a.out_vert = d.out_vert;
         a.periodic = d.blur.periodic;
-        a.cl = d.m / (F64_NW * F64_LPW);
+        a.cl = 0;
         fill_dense<double, RR>(a.wb, d.blur, d.taps_blur_host);
         fill_dense<double, RR>(a.wa, d.adj, d.taps_adj_host);
         a.alpha = d.alpha; a.eps_d2 = d.eps_d2; a.eps_r2 = d.eps_r2; a.has_d = d.has_d;

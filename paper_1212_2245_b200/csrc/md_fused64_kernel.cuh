@@ -28,6 +28,8 @@
 #pragma once
 #include <cooperative_groups.h>
 
+#include <tuple>
+
 #include "md_fused_kernel.cuh"
 
 namespace md {
@@ -65,8 +67,10 @@ __device__ __forceinline__ void st_async_f64x2(uint32_t raddr, double x, double 
                  : "memory");
 }
 
-// r1 with the (value, step) pair table (md_common.cuh rules, deconv.py:114-134)
-__device__ __forceinline__ double r1_pair64(const double2 *__restrict__ p64, double x) {
+// r1 with the (value, step) pair table (md_common.cuh rules, deconv.py:114-134): the table
+// interpolation and the linear continuation above `upper`; the direct formula below
+// `direct_below` is the caller's (taken per warp, see k_fused_lines64)
+__device__ __forceinline__ double r1_table64(const double2 *__restrict__ p64, double x) {
     const double xc = x < kLutUpper ? x : kLutUpper;
     double pos = (xc - kLutDelta) * kLutInvStep;
     pos = pos > 0.0 ? pos : 0.0;
@@ -75,7 +79,6 @@ __device__ __forceinline__ double r1_pair64(const double2 *__restrict__ p64, dou
     const double2 e = __ldg(p64 + i);
     double r = e.x + e.y * (pos - (double)i);
     if (x > kLutUpper) r = kLutSlope * x + kLutIntercept;
-    if (x < kLutDirectBelow) r = x - 1.0 - log(x);
     return r;
 }
 
@@ -110,7 +113,7 @@ k_fused_lines64(FusedKArgs<double, R> a, const double2 *__restrict__ lut64) {
     using T = double;
     constexpr int HW = HaloOf<R>::value;
     constexpr int WIN = SEG + 2 * R;
-    constexpr int RL = NW * LPW;
+    constexpr int RLMAX = NW * LPW;                 // line slots per CTA
     cg::cluster_group cluster = cg::this_cluster();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T *sm = reinterpret_cast<T *>(smem_raw);
@@ -122,15 +125,20 @@ k_fused_lines64(FusedKArgs<double, R> a, const double2 *__restrict__ lut64) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nseg = n / SEG;
     const int base0 = xaddr(HW);
-    const int gl0 = rank * RL;
+    // m lines over CL CTAs as evenly as possible (the cluster size is picked on the host for
+    // GPC fill, so m / CL need not be an integer): RL = m / CL or one more
+    const int lbase = m / CL, lext = m - lbase * CL;
+    const int RL = lbase + (rank < lext ? 1 : 0);
+    const int gl0 = rank * lbase + (rank < lext ? rank : lext);
     const int64_t fsz = (int64_t)n * m;
     const T *fpos = a.fpos + frame * fsz;
 
-    // shared layout (lines of ls doubles): own[RL] | halo[parity][top, bottom][2] | g[RL + 2] | mbar[2]
+    // shared layout (lines of ls doubles, the same offsets in every CTA of the cluster):
+    // own[RLMAX] | halo[parity][top, bottom][2] | g[RLMAX + 2] | mbar[2]
     T *own = sm;
-    auto halo = [&](int par, int side) { return sm + (RL + 4 * par + 2 * side) * ls; };
-    T *sg = sm + (RL + 8) * ls;
-    uint64_t *mbar = reinterpret_cast<uint64_t *>(sm + (2 * RL + 10) * ls);
+    auto halo = [&](int par, int side) { return sm + (RLMAX + 4 * par + 2 * side) * ls; };
+    T *sg = sm + (RLMAX + 8) * ls;
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(sm + (2 * RLMAX + 10) * ls);
     auto line_ptr = [&](int l, int par) -> const T * {
         if (l < 0) return halo(par, 0) + (l + 2) * ls;
         if (l >= RL) return halo(par, 1) + (l - RL) * ls;
@@ -235,7 +243,9 @@ k_fused_lines64(FusedKArgs<double, R> a, const double2 *__restrict__ lut64) {
         T unew[LPW][SEG];
 #pragma unroll
         for (int j = 0; j < LPW; ++j) {
-            const int li = warp + NW * j;
+            // slots past RL (ragged line split) shadow line RL - 1 and store nothing: the loop
+            // stays convergent, so the shuffles need no per-iteration reconvergence
+            const int li = min(warp + NW * j, RL - 1);
             const int gl = gl0 + li;
             const bool up_ok = gl > 0, dn_ok = gl + 1 < m;
             const T *U = own + li * ls;
@@ -243,7 +253,7 @@ k_fused_lines64(FusedKArgs<double, R> a, const double2 *__restrict__ lut64) {
             const int s = lane < nseg ? lane : nseg - 1;     // idle lanes shadow the last segment
             const int off = base0 + 9 * s;
             {
-                const int ln = j + 1 < LPW ? li + NW : warp;
+                const int ln = j + 1 < LPW ? min(li + NW, RL - 1) : warp;
                 asm volatile("prefetch.global.L1 [%0];" ::"l"(fpos + (int64_t)(gl0 + ln) * n + SEG * s));
             }
             T fv[SEG];
@@ -264,18 +274,34 @@ k_fused_lines64(FusedKArgs<double, R> a, const double2 *__restrict__ lut64) {
                 T bl[SEG];
                 conv_window<T, R, BOXR, BOXC>(v, a.wb, a.box_wi, a.box_cb, bl);
 #pragma unroll
-                for (int r = 0; r < SEG; ++r) {
-                    const T b = bl[r] > T(kGuard) ? bl[r] : T(kGuard);
-                    const T fp = fv[r];
-                    const T ratio = fp * frcp(b);
-                    if (ROBUST) {
-                        const T xr = b * frcp(fp);
-                        const T w = T(0.5) * frsqrt(r1_pair64(lut64, xr) * fp + eps_d2);
-                        wv[r] = w;
-                        pv[r] = w * ratio;
-                    } else {
-                        pv[r] = ratio;
+                for (int r = 0; r < SEG; ++r) bl[r] = bl[r] > T(kGuard) ? bl[r] : T(kGuard);   // b
+                if (ROBUST) {
+                    // r1(b / fpos) for the lane's 8 pixels: all 8 table pairs requested before any
+                    // is used (no branch between them), the rare direct-log branch (x < 1/2) taken
+                    // once per warp and only when some lane needs it
+                    T xr[SEG], r1v[SEG];
+                    bool need_log = false;
+#pragma unroll
+                    for (int r = 0; r < SEG; ++r) {
+                        xr[r] = bl[r] * frcp(fv[r]);
+                        need_log |= xr[r] < kLutDirectBelow;
                     }
+#pragma unroll
+                    for (int r = 0; r < SEG; ++r) r1v[r] = r1_table64(lut64, xr[r]);
+                    if (__any_sync(0xffffffffu, need_log)) {
+#pragma unroll
+                        for (int r = 0; r < SEG; ++r)
+                            if (xr[r] < kLutDirectBelow) r1v[r] = xr[r] - 1.0 - log(xr[r]);
+                    }
+#pragma unroll
+                    for (int r = 0; r < SEG; ++r) {
+                        const T w = T(0.5) * frsqrt(r1v[r] * fv[r] + eps_d2);
+                        wv[r] = w;
+                        pv[r] = w * (fv[r] * frcp(bl[r]));
+                    }
+                } else {
+#pragma unroll
+                    for (int r = 0; r < SEG; ++r) pv[r] = fv[r] * frcp(bl[r]);
                 }
             }
             T num[SEG], den[SEG];
@@ -334,7 +360,7 @@ k_fused_lines64(FusedKArgs<double, R> a, const double2 *__restrict__ lut64) {
             for (int j = 0; j < LPW; ++j) {
                 const int li = warp + NW * j;
                 const int gl = gl0 + li;
-                if (lane >= nseg) continue;
+                if (lane >= nseg || li >= RL) continue;
                 if (!a.out_vert) {
                     double2 *o2 = reinterpret_cast<double2 *>(dst + (int64_t)gl * n + SEG * lane);
 #pragma unroll
@@ -359,6 +385,7 @@ k_fused_lines64(FusedKArgs<double, R> a, const double2 *__restrict__ lut64) {
 #pragma unroll
         for (int j = 0; j < LPW; ++j) {
             const int li = warp + NW * j;
+            if (li >= RL) continue;
             T *L = own + li * ls;
             if (lane < nseg) {
                 T *P = L + base0 + 9 * lane;
@@ -382,28 +409,73 @@ size_t fused64_smem(int n) {
     return (size_t)(2 * NW * LPW + 10) * ls * sizeof(double) + 2 * sizeof(uint64_t);
 }
 
+// host: the cluster size for m lines -- every CTA holds at most `rlmax` lines and at least 4, one
+// CTA per SM. Clusters are placed whole inside a GPC, so the resident count does not scale with
+// 1 / size (B200, one CTA per SM: 8-CTA clusters 15 resident = 120 SMs, 9-CTA 15 = 135 SMs,
+// 16-CTA 7 = 112 SMs; scripts/probes/cluster_geom.cu). Among the admissible sizes, the most
+// frames in flight per line round (each warp's lines run in turn); ties to the smaller cluster.
+// Cached per (kernel, smem, m, device).
+inline int pick_cluster(const void *kern, size_t smem, int threads, int m, int rlmax, int *resident) {
+    static std::mutex mu;
+    static std::map<std::tuple<const void *, size_t, int, int>, std::pair<int, int>> memo;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    std::lock_guard<std::mutex> lock(mu);
+    const auto key = std::make_tuple(kern, smem, m, dev);
+    auto it = memo.find(key);
+    if (it == memo.end()) {
+        int best = 0, best_n = 0, best_rounds = 1;
+        for (int cl = std::max(2, (m + rlmax - 1) / rlmax); cl <= 16 && m / cl >= 4; ++cl) {
+            cudaLaunchConfig_t q = {};
+            q.gridDim = dim3((unsigned)cl, 1, 1);
+            q.blockDim = dim3((unsigned)threads, 1, 1);
+            q.dynamicSmemBytes = smem;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = cl;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            q.attrs = at;
+            q.numAttrs = 1;
+            int n = 0;
+            if (cudaOccupancyMaxActiveClusters(&n, kern, &q) != cudaSuccess) {
+                cudaGetLastError();
+                continue;
+            }
+            // throughput ~ frames in flight / line rounds per frame (a warp's lines run in turn)
+            const int nw = threads / 32;
+            const int rounds = ((m + cl - 1) / cl + nw - 1) / nw;
+            if (best == 0 || (int64_t)n * best_rounds > (int64_t)best_n * rounds) {
+                best = cl; best_n = n; best_rounds = rounds;
+            }
+        }
+        it = memo.emplace(key, std::make_pair(best, best_n)).first;
+    }
+    if (resident) *resident = it->second.second;
+    return it->second.first;
+}
+
 template <int R, int NW, int LPW>
-cudaError_t launch_fused64_t(void (*kern)(FusedKArgs<double, R>, const double2 *), const FusedKArgs<double, R> &a,
+cudaError_t launch_fused64_t(void (*kern)(FusedKArgs<double, R>, const double2 *), const FusedKArgs<double, R> &a0,
                              const double2 *lut64, int64_t batch, cudaStream_t st) {
-    const size_t smem = fused64_smem<R, NW, LPW>(a.n);
+    const size_t smem = fused64_smem<R, NW, LPW>(a0.n);
     {
         const cudaError_t e = func_smem_attr((const void *)kern, smem, true);
         if (e != cudaSuccess) return e;
+    }
+    FusedKArgs<double, R> a = a0;
+    int resident = 0;
+    a.cl = pick_cluster((const void *)kern, smem, NW * 32, a.m, NW * LPW, &resident);
+    if (a.cl == 0) return cudaErrorNotSupported;
+    if (a.query) {
+        *a.query = resident;
+        return cudaSuccess;
     }
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = a.cl;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
-    if (a.query) {
-        cudaLaunchConfig_t q = {};
-        q.gridDim = dim3((unsigned)a.cl, 1, 1);
-        q.blockDim = dim3(NW * 32, 1, 1);
-        q.dynamicSmemBytes = smem;
-        q.attrs = attr;
-        q.numAttrs = 1;
-        return cudaOccupancyMaxActiveClusters(a.query, kern, &q);
-    }
     const int64_t fsz = (int64_t)a.n * a.m;
     const int64_t maxf = (int64_t)(0x7fffffff / a.cl);
     for (int64_t b0 = 0; b0 < batch; b0 += maxf) {
@@ -425,10 +497,12 @@ cudaError_t launch_fused64_t(void (*kern)(FusedKArgs<double, R>, const double2 *
     return cudaGetLastError();
 }
 
-// geometry of the float64 kernel: 8 warps x 2 lines (16-line CTAs, two per SM, m / 16 CTAs per
-// cluster) -- MD_F64_NW=16 selects 16 warps x 2 lines (32-line CTAs, one per SM)
+// geometry of the float64 kernel: 16 warps x 2 line slots (up to 32 lines per CTA, one CTA per
+// SM), the cluster size picked per line count (pick_cluster). Measured (c1, 4096 frames):
+// 8 warps x 2 lines at two CTAs per SM in 16-CTA clusters (14 resident = 112 SMs) 20.3 ms of
+// iterations; 16 x 2 in 8-CTA clusters (15 = 120 SMs) 18.7 ms
 #ifndef MD_F64_NW
-#define MD_F64_NW 8
+#define MD_F64_NW 16
 #endif
 constexpr int F64_NW = MD_F64_NW;
 constexpr int F64_LPW = 2;
@@ -442,7 +516,7 @@ cudaError_t launch_fused64_box_r(const FusedLinesArgs &d, int64_t batch, cudaStr
     a.query = d.query;
     a.n = d.n; a.m = d.m; a.iterations = d.iterations; a.out_vert = d.out_vert;
     a.periodic = d.blur.periodic;
-    a.cl = d.m / (F64_NW * F64_LPW);
+    a.cl = 0;                                    // picked at launch (pick_cluster)
     a.alpha = d.alpha; a.eps_d2 = d.eps_d2; a.eps_r2 = d.eps_r2; a.has_d = d.has_d;
     a.lut = d.lut;
     a.box_wi = d.blur.wi;

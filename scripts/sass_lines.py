@@ -1,0 +1,52 @@
+#!/usr/bin/env python
+"""Attribute ncu SASS-level stall samples to CUDA source lines.
+
+    python scripts/sass_lines.py REPORT.ncu-rep CUBIN KERNEL_MANGLED [TOP]
+
+The ncu source page (--print-source sass) gives per-instruction samples by runtime address;
+nvdisasm --print-line-info of the same cubin maps instruction offsets to file:line. The kernel's
+first instruction anchors the offset."""
+import collections
+import csv
+import io
+import re
+import subprocess
+import sys
+
+rep, cubin, kern = sys.argv[1:4]
+top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
+raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                     capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(raw)))
+hi = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
+h = rows[hi]
+si = h.index("Warp Stall Sampling (All Samples)")
+ie = h.index("Instructions Executed")
+sass = [(int(r[0], 16), float(r[si] or 0), float(r[ie] or 0), r[1].strip()) for r in rows[hi + 1:] if len(r) > si]
+base = sass[0][0]
+dis = subprocess.run(["nvdisasm", "--print-line-info", cubin], capture_output=True, text=True).stdout
+line_of = {}
+cur = None
+inside = False
+for ln in dis.splitlines():
+    if ln.startswith(".text."):
+        inside = ln.strip().rstrip(":") == ".text." + kern
+        continue
+    if not inside:
+        continue
+    m = re.search(r'//## File "([^"]+)", line (\d+)', ln)
+    if m:
+        cur = f"{m.group(1).split('/')[-1]}:{m.group(2)}"
+        continue
+    m = re.match(r"\s+/\*([0-9a-f]{4,})\*/\s+(\S.*)", ln)
+    if m and cur:
+        line_of[int(m.group(1), 16)] = cur
+agg = collections.defaultdict(lambda: [0.0, 0.0])
+tot = 0.0
+for addr, s, n, _ in sass:
+    k = line_of.get(addr - base, "?")
+    agg[k][0] += s
+    agg[k][1] += n
+    tot += s
+for k, (s, n) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
+    print(f"{100 * s / tot:5.1f}%  {n / 1e6:8.2f}M inst  {k}")
