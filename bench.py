@@ -509,7 +509,7 @@ def run_reference(args, rank: int, world: int) -> None:
     if rank != 0:
         return
     import paper_1212_2245_b200 as md              # host-side value types only (Psf, scenes)
-    esz = 8
+    esz = 8 if args.dtype == "float64" else 4       # only for the shared config object
     work = WORKLOADS[args.config](md, args, cpu_synth(md), gpu=False)
     cores = host_cores()
     jobs = cpu_jobs(work, args.cpu_frames_per_core, cores)

@@ -1,0 +1,55 @@
+"""bench.py's own logic on CPU: the frame-sharded timing path under `--gpus 2` (ranks
+self-launched, gloo process group, barrier + max over ranks), and the reference arm, which
+must run the CPU oracle without touching the device or loading libmdcuda.so."""
+
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _run(args, extra_env=None, timeout=300):
+    env = dict(os.environ, PYTHONDONTWRITEBYTECODE="1", **(extra_env or {}))
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, *args], cwd=ROOT, env=env, capture_output=True, text=True, timeout=timeout)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    return json.loads(lines[0])
+
+
+def test_gpus2_self_launch_gloo():
+    d = _run(["bench.py", "--gpus", "2", "--backend", "gloo", "--steps", "3", "--warmup", "1", "--batch", "16"])
+    assert d["n_gpus"] == 2 and d["steps"] == 3
+    assert d["config"]["parallelism"] == "frame-sharded x2"
+    assert d["config"]["frames_per_gpu_per_step"] == 16
+    assert d["value"] > 0
+
+
+def test_reference_arm_is_device_free():
+    probe = (
+        "import runpy, sys\n"
+        "sys.argv = ['bench.py', '--impl', 'reference', '--steps', '1', '--warmup', '0', "
+        "'--cpu-frames-per-core', '1', '--batch', '64']\n"
+        "try:\n"
+        "    runpy.run_path('bench.py', run_name='__main__')\n"
+        "finally:\n"
+        "    maps = open('/proc/self/maps').read()\n"
+        "    sys.stderr.write('LIBMDCUDA_MAPPED=%d\\n' % ('libmdcuda' in maps))\n"
+    )
+    env = dict(os.environ, PYTHONDONTWRITEBYTECODE="1", CUDA_VISIBLE_DEVICES="")
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, "-c", probe], cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert "LIBMDCUDA_MAPPED=0" in r.stderr
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][0])
+    assert d["impl"] == "reference" and d["dtype"] == "f64"
+    # the same config object the GPU arm prints for the same command line
+    sys.path.insert(0, ROOT)
+    import bench
+    assert d["config"] == bench.bench_config(bench.C1.name, 64, 1, 8)
+    assert d["cpu_baseline"]["kind"] == "port" and d["e2e"]["h2d_bytes_per_step"] == 0
