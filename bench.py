@@ -194,12 +194,16 @@ def c4_bank(md, seed: int = 2026):
     return bank, kinds
 
 
-def c4_frames(md, bank, index, synth):
+C4_SCENE_SEEDS = (7, 8, 9, 10)
+
+
+def c4_frames(md, bank, index, synth, with_scenes=False):
     """The c4 frames for PSF assignment `index` (8 distinct noisy frames per PSF, 4 scenes),
-    plus one (kind, psf, frame) CPU sample item per PSF."""
-    scenes = [md.make_test_image(W, H, seed=s).values for s in (7, 8, 9, 10)]
+    plus one (kind, psf, frame) CPU sample item per PSF [and each frame's scene number]."""
+    scenes = [md.make_test_image(W, H, seed=s).values for s in C4_SCENE_SEEDS]
     distinct = 8
     frames = np.empty((index.size, H, W))
+    scene_of = np.empty(index.size, dtype=np.int64)
     items = []
     for b, psf in enumerate(bank):
         sel = np.nonzero(index == b)[0]
@@ -209,8 +213,9 @@ def c4_frames(md, bank, index, synth):
         base = [noisy(blurred[j % 4], 1000 * b + j) for j in range(distinct)]
         for k, i in enumerate(sel):
             frames[i] = base[k % distinct]
+            scene_of[i] = (k % distinct) % 4
         items.append((b, psf, base[0]))
-    return frames, items
+    return (frames, items, scene_of) if with_scenes else (frames, items)
 
 
 class C4:

@@ -40,8 +40,18 @@ def box_convolve(image: Image, psf: Psf) -> Image:
 
 def fourier_convolve(image: Image, psf: Psf, plans=None) -> Image:
     """Circular convolution (fft.py:283-307); transformed axes must be powers of two."""
+    h, w = image.shape
+    if psf.kind is PsfKind.GENERAL_2D:
+        if not (_pow2(h) and _pow2(w)):
+            raise ValueError("2D Fourier convolution needs power-of-two dimensions")
+    elif not _pow2(h if psf.axis is BlurAxis.VERTICAL else w):
+        raise ValueError("the blur axis must have power-of-two extent")
     c = make_convolver(psf, image.shape, "fourier2d" if psf.kind is PsfKind.GENERAL_2D else "fourier")
     return _image(c._plan.convolve(_dev(image), 0))
+
+
+def _pow2(n: int) -> bool:
+    return n >= 1 and n & (n - 1) == 0
 
 
 def convolve_array(a: np.ndarray, psf: Psf) -> np.ndarray:

@@ -148,14 +148,36 @@ __global__ void k_embed_taps(double *z, int H, int W, const PlaneTap *taps, int 
 // then (an earlier graph may still reference the old one)
 thread_local bool tl_capturing = false;
 
+// Plan scratch. Once a CUDA graph has captured a run that uses the buffer, the graph holds its
+// address: a later (uncaptured) run that needs more scratch gets a new buffer, and the old one is
+// retired -- kept alive until the plan is destroyed -- so every captured graph stays valid.
 struct DevBuf {
     void *p = nullptr;
     size_t bytes = 0;
-    void release() { if (p) cudaFree(p); p = nullptr; bytes = 0; }
+    bool captured = false;               // some graph recorded launches that use `p`
+    std::vector<void *> retired;
+    void release() {
+        if (p) cudaFree(p);
+        for (void *q : retired) cudaFree(q);
+        retired.clear();
+        p = nullptr;
+        bytes = 0;
+        captured = false;
+    }
     int ensure(size_t b) {
+        if (tl_capturing) captured = true;
         if (b <= bytes) return MD_OK;
         if (tl_capturing) return fail(MD_EINVAL, "plan scratch must be sized by an uncaptured run before stream capture");
-        release();
+        if (captured) {
+            retired.push_back(p);        // still referenced by a graph: keep it
+            p = nullptr;
+            bytes = 0;
+            captured = false;
+        } else if (p) {
+            cudaFree(p);
+            p = nullptr;
+            bytes = 0;
+        }
         if (cudaMalloc(&p, b) != cudaSuccess) { cudaGetLastError(); return fail(MD_ENOMEM, "device allocation failed"); }
         bytes = b;
         return MD_OK;
@@ -405,8 +427,12 @@ int validate(const md_plan_desc *d) {
     if (!(d->wiener_k > 0.0)) return fail(MD_EINVAL, "wiener_k must be positive");
     if (d->alpha < 0.0) return fail(MD_EINVAL, "alpha must be non-negative");
     if (d->iterations < 0) return fail(MD_EINVAL, "iterations must be a non-negative integer");
-    if (!(d->eps_data > 0.0 && d->eps_reg > 0.0 && d->floor > 0.0))
+    if (d->flags & MD_FLAG_RL) {
+        // rl_deblur (deconv.py:524-534) clamps with any floor and has no robust / TV terms
+        if (!std::isfinite(d->floor)) return fail(MD_EINVAL, "floor must be finite");
+    } else if (!(d->eps_data > 0.0 && d->eps_reg > 0.0 && d->floor > 0.0)) {
         return fail(MD_EINVAL, "eps_data, eps_reg and floor must be positive");
+    }
     if (d->conv < MD_CONV_BOX || d->conv > MD_CONV_FOURIER2D) return fail(MD_EINVAL, "unknown convolver mode");
     return MD_OK;
 }
@@ -1144,38 +1170,56 @@ int32_t md_run_host_ex(md_plan *P, const void *f, int32_t in_type, void *u, int3
     const int nstreams = (int)std::min<int64_t>(kHostStreams, (batch + chunk - 1) / chunk);
     rc = P->stage.ensure(per * nstreams);      // one staging slot per stream actually used
     if (rc) return rc;
-    CU(cudaEventRecord(P->ev_start, user));
-    for (int s = 0; s < kHostStreams; ++s) CU(cudaStreamWaitEvent(P->hstream[s], P->ev_start, 0));
-    const int64_t saved_chunk = P->chunk;
-    P->chunk = chunk;
-    for (int64_t b0 = 0, c = 0; b0 < batch; b0 += chunk, ++c) {
-        const int64_t nb = std::min(chunk, batch - b0);
-        const int s = (int)(c % kHostStreams);
-        cudaStream_t st = P->hstream[s];
-        char *base = (char *)P->stage.p + per * s;
-        char *din = base, *dtin = din + align_up(in_b), *dtout = dtin + align_up(tin_b),
-             *dout = dtout + align_up(tout_b), *dscr = dout + align_up(out_b);
-        CU(cudaMemcpyAsync(din, (const char *)f + b0 * fe * ib, nb * fe * ib, cudaMemcpyHostToDevice, st));
-        const void *fin = din;
-        if (in_type != (P->d.dtype == MD_F64 ? MD_IO_F64 : MD_IO_F32)) {
-            CU(P->d.dtype == MD_F64 ? launch_convert_in<double>(din, in_type, dtin, nb * fe, st)
-                                    : launch_convert_in<float>(din, in_type, dtin, nb * fe, st));
-            fin = dtin;
+    // the host chunk size applies to this call only (restored on every exit path); on an error
+    // the internal streams are drained before returning, so no copy into the caller's host
+    // buffers is still in flight when the error comes back
+    struct ChunkGuard {
+        md_plan *P;
+        int64_t saved;
+        ~ChunkGuard() { P->chunk = saved; }
+    } guard{P, P->chunk};
+    auto body = [&]() -> int {
+        CU(cudaEventRecord(P->ev_start, user));
+        for (int s = 0; s < kHostStreams; ++s) CU(cudaStreamWaitEvent(P->hstream[s], P->ev_start, 0));
+        P->chunk = chunk;
+        for (int64_t b0 = 0, c = 0; b0 < batch; b0 += chunk, ++c) {
+            const int64_t nb = std::min(chunk, batch - b0);
+            const int s = (int)(c % kHostStreams);
+            cudaStream_t st = P->hstream[s];
+            char *base = (char *)P->stage.p + per * s;
+            char *din = base, *dtin = din + align_up(in_b), *dtout = dtin + align_up(tin_b),
+                 *dout = dtout + align_up(tout_b), *dscr = dout + align_up(out_b);
+            CU(cudaMemcpyAsync(din, (const char *)f + b0 * fe * ib, nb * fe * ib, cudaMemcpyHostToDevice, st));
+            const void *fin = din;
+            if (in_type != (P->d.dtype == MD_F64 ? MD_IO_F64 : MD_IO_F32)) {
+                CU(P->d.dtype == MD_F64 ? launch_convert_in<double>(din, in_type, dtin, nb * fe, st)
+                                        : launch_convert_in<float>(din, in_type, dtin, nb * fe, st));
+                fin = dtin;
+            }
+            const bool direct_out = out_type == (P->d.dtype == MD_F64 ? MD_IO_F64 : MD_IO_F32);
+            void *uo = direct_out ? (void *)dout : (void *)dtout;
+            const int r = P->d.dtype == MD_F64 ? run_chunk<double>(*P, fin, uo, nb, dscr, st)
+                                               : run_chunk<float>(*P, fin, uo, nb, dscr, st);
+            if (r) return r;
+            if (!direct_out) {
+                CU(P->d.dtype == MD_F64 ? launch_convert_out<double>(dtout, dout, out_type, nb * fe, st)
+                                        : launch_convert_out<float>(dtout, dout, out_type, nb * fe, st));
+            }
+            CU(cudaMemcpyAsync((char *)u + b0 * fe * ob, dout, nb * fe * ob, cudaMemcpyDeviceToHost, st));
         }
-        const bool direct_out = out_type == (P->d.dtype == MD_F64 ? MD_IO_F64 : MD_IO_F32);
-        void *uo = direct_out ? (void *)dout : (void *)dtout;
-        rc = P->d.dtype == MD_F64 ? run_chunk<double>(*P, fin, uo, nb, dscr, st) : run_chunk<float>(*P, fin, uo, nb, dscr, st);
-        if (rc) { P->chunk = saved_chunk; return rc; }
-        if (!direct_out) {
-            CU(P->d.dtype == MD_F64 ? launch_convert_out<double>(dtout, dout, out_type, nb * fe, st)
-                                    : launch_convert_out<float>(dtout, dout, out_type, nb * fe, st));
+        for (int s = 0; s < kHostStreams; ++s) {
+            CU(cudaEventRecord(P->ev_done[s], P->hstream[s]));
+            CU(cudaStreamWaitEvent(user, P->ev_done[s], 0));
         }
-        CU(cudaMemcpyAsync((char *)u + b0 * fe * ob, dout, nb * fe * ob, cudaMemcpyDeviceToHost, st));
-    }
-    P->chunk = saved_chunk;
-    for (int s = 0; s < kHostStreams; ++s) {
-        CU(cudaEventRecord(P->ev_done[s], P->hstream[s]));
-        CU(cudaStreamWaitEvent(user, P->ev_done[s], 0));
+        return MD_OK;
+    };
+    rc = body();
+    if (rc) {
+        const std::string msg = g_err;                // keep the first error's message
+        for (int s = 0; s < kHostStreams; ++s) cudaStreamSynchronize(P->hstream[s]);
+        cudaGetLastError();
+        g_err = msg;
+        return rc;
     }
     CU(cudaStreamSynchronize(user));
     return MD_OK;
@@ -1609,6 +1653,9 @@ int32_t md_slab_iterate(md_plan *P, const void *u, const void *fpos, void *p, vo
     s.H = rows; s.W = P->d.width; s.periodic = P->periodic;
     s.slab = 1; s.gy0 = row0; s.Hg = P->d.height;
     s.row_a0 = -P->hadj.ht; s.rows_a = rows + P->hadj.ht + P->hadj.hb;
+    int32_t top = 0, bot = 0;
+    md_slab_halo(P, &top, &bot);                 // the haloed buffers' extent (slab.py SlabGeometry)
+    s.halo_top = top; s.halo_bot = bot;
     s.hb = P->hblur; s.ha = P->hadj; s.taps_blur = &P->htaps_blur; s.taps_adj = &P->htaps_adj;
     s.alpha = P->d.alpha; s.eps_d2 = P->d.eps_data * P->d.eps_data; s.eps_r2 = P->d.eps_reg * P->d.eps_reg;
     s.has_d = P->has_d; s.lut = P->lut;

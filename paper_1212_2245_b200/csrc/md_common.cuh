@@ -14,21 +14,28 @@ namespace md {
 
 // host: raise a kernel's dynamic shared-memory limit (and allow non-portable cluster sizes)
 // once per (kernel, device), not on every launch -- cudaFuncSetAttribute costs microseconds,
-// which batch-1 latency notices. Thread-safe; the limit only grows.
+// which batch-1 latency notices. The attribute is one value per function, so the limit only
+// ever grows (to the largest size any caller launched with); thread-safe.
 inline cudaError_t func_smem_attr(const void *kern, size_t smem, bool nonportable_cluster = false) {
+    struct State { size_t smem = 0; bool nonportable = false; };
     static std::mutex mu;
-    static std::map<std::pair<const void *, int>, size_t> done;
+    static std::map<std::pair<const void *, int>, State> done;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     std::lock_guard<std::mutex> lock(mu);
-    auto key = std::make_pair(kern, dev * 2 + (nonportable_cluster ? 1 : 0));
-    auto it = done.find(key);
-    if (it != done.end() && it->second >= smem) return cudaSuccess;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess && nonportable_cluster) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e == cudaSuccess) done[key] = smem;
-    return e;
+    State &st = done[std::make_pair(kern, dev)];
+    if (smem > st.smem) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        st.smem = smem;
+    }
+    if (nonportable_cluster && !st.nonportable) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+        st.nonportable = true;
+    }
+    return cudaSuccess;
 }
 
 template <typename T> struct Cx;

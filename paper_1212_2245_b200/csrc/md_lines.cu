@@ -111,7 +111,17 @@ k_wiener_lines(WienerLinesArgs a) {
 
 constexpr int RUN = 8;
 
-template <typename T>
+// a * b + c as the reference's NumPy rounds it (two roundings) when EXACT, else contracted
+template <bool EXACT>
+__device__ __forceinline__ double madd(double a, double b, double c) {
+    return EXACT ? __dadd_rn(__dmul_rn(a, b), c) : a * b + c;
+}
+template <bool EXACT>
+__device__ __forceinline__ float madd(float a, float b, float c) { return a * b + c; }
+
+// EXACT: the public convolve path (synth_blur / convolve_array, conv.py:85-116), which must
+// reproduce the reference's rounding so quantised synthetic inputs match bit for bit
+template <typename T, bool EXACT = false>
 __device__ __forceinline__ void conv_run(const T *line, int n, int j0, const LineConv &c,
                                          const T *taps, T out[RUN]) {
     const int per = c.periodic;
@@ -139,7 +149,7 @@ __device__ __forceinline__ void conv_run(const T *line, int n, int j0, const Lin
             if (w == T(0)) continue;
             const int base = j0 + c.center - t;
 #pragma unroll
-            for (int r = 0; r < RUN; ++r) out[r] += w * line[pidx<T>(resolve(base + r, n, per))];
+            for (int r = 0; r < RUN; ++r) out[r] = madd<EXACT>(w, line[pidx<T>(resolve(base + r, n, per))], out[r]);
         }
     }
 }
@@ -292,7 +302,7 @@ k_conv_lines(ConvLinesArgs a) {
         const int li = q / runs, j0 = (q - li * runs) * RUN;
         if (l0 + li >= m) continue;
         T v[RUN];
-        conv_run<T>(sa + li * P, n, j0, a.c, stap, v);
+        conv_run<T, true>(sa + li * P, n, j0, a.c, stap, v);
         for (int r = 0; r < RUN && j0 + r < n; ++r) out[(int64_t)(l0 + li) * n + j0 + r] = v[r];
     }
 }

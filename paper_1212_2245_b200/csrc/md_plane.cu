@@ -88,6 +88,21 @@ __device__ __forceinline__ T tap_sum(const T *s, int ss, int ty, int tx, const P
     return acc;
 }
 
+// the same sum with the reference's rounding (conv.py:85-116: acc += w * shifted, a multiply
+// and an add per tap, in tap order) -- the public convolve / synth_blur path, which must
+// reproduce the reference's quantised test inputs bit for bit at any size; float keeps FMAs
+__device__ __forceinline__ double tap_sum_ref(const double *s, int ss, int ty, int tx, const PlaneTap *taps, int nt,
+                                              int oy, int ox) {
+    double acc = 0.0;
+    const double *base = s + (ty + oy) * ss + (tx + ox);
+    for (int t = 0; t < nt; ++t) acc = __dadd_rn(acc, __dmul_rn(taps[t].w, base[taps[t].dy * ss + taps[t].dx]));
+    return acc;
+}
+__device__ __forceinline__ float tap_sum_ref(const float *s, int ss, int ty, int tx, const PlaneTap *taps, int nt,
+                                             int oy, int ox) {
+    return tap_sum<float>(s, ss, ty, tx, taps, nt, oy, ox);
+}
+
 template <typename T, bool ROBUST>
 __global__ void __launch_bounds__(PTHREADS)
 k_stage_a_plane(StagePlaneArgs a) {
@@ -194,7 +209,7 @@ k_conv_plane(ConvPlaneArgs a) {
         const int ty = k / PT, tx = k - ty * PT;
         const int y = y0 + ty, x = x0 + tx;
         if (y >= H || x >= W) continue;
-        out[(int64_t)y * W + x] = tap_sum<T>(s, ss, ty, tx, st, h.nt, h.ht, h.hl);
+        out[(int64_t)y * W + x] = tap_sum_ref(s, ss, ty, tx, st, h.nt, h.ht, h.hl);
     }
 }
 
@@ -234,6 +249,24 @@ template <typename T>
 __global__ void k_lut_r1(const T *__restrict__ x, T *__restrict__ out, int64_t n, LutView lut) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         out[i] = r1_lut<T>(lut, x[i]);
+}
+
+// DivergenceLut.r1 as the public API evaluates it (deconv.py:114-134), in the reference's
+// rounding order: (T[i+1] - T[i]) * t + T[i] and slope * x + intercept as separate roundings
+// (NumPy applies them as separate array operations; the in-kernel form contracts to FMAs)
+__global__ void k_lut_r1_ref(const double *__restrict__ x, double *__restrict__ out, int64_t n, LutView lut) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double xi = x[i];
+        double pos = __dmul_rn(__dsub_rn(xi < kLutUpper ? xi : kLutUpper, kLutDelta), kLutInvStep);
+        long long idx = (long long)pos;                   // astype(int64): truncation toward zero
+        idx = idx < 0 ? 0 : (idx > kLutCount - 2 ? kLutCount - 2 : idx);
+        pos = __dsub_rn(pos, (double)idx);
+        const double lo = lut.t64[idx], hi = lut.t64[idx + 1];
+        double r = __dadd_rn(__dmul_rn(__dsub_rn(hi, lo), pos), lo);
+        if (xi > kLutUpper) r = __dadd_rn(__dmul_rn(kLutSlope, xi), kLutIntercept);
+        if (xi < kLutDirectBelow) r = __dsub_rn(__dsub_rn(xi, 1.0), log(xi));
+        out[i] = r;
+    }
 }
 
 // ratio = f / b, optionally times w (first half of _combine)
@@ -398,7 +431,10 @@ cudaError_t launch_robust_weight(const void *f, const void *b, void *out, int64_
 
 template <typename T>
 cudaError_t launch_lut_r1(const void *x, void *out, int64_t n, const LutView &lut, cudaStream_t st) {
-    k_lut_r1<T><<<ew_blocks(n), 256, 0, st>>>(static_cast<const T *>(x), static_cast<T *>(out), n, lut);
+    if (sizeof(T) == 8)
+        k_lut_r1_ref<<<ew_blocks(n), 256, 0, st>>>(static_cast<const double *>(x), static_cast<double *>(out), n, lut);
+    else
+        k_lut_r1<T><<<ew_blocks(n), 256, 0, st>>>(static_cast<const T *>(x), static_cast<T *>(out), n, lut);
     return cudaGetLastError();
 }
 

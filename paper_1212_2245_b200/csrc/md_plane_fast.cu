@@ -32,7 +32,7 @@ __device__ __forceinline__ int pf_resolve(int k, int n, int periodic) {
 constexpr int PF_CJ = 4;                  // cols <= 32 * PF_CJ (FX + x-halos <= 128)
 template <typename T, typename E, typename Get>
 __device__ void pf_load(E *s, int ss, int H, int W, int y0, int x0, const PlaneHalo &h, int periodic, int slab,
-                        Get get) {
+                        int ylo, int yhi, Get get) {
     const int rows = FY + h.ht + h.hb, cols = FX + h.hl + h.hr;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     int xr[PF_CJ];
@@ -42,8 +42,11 @@ __device__ void pf_load(E *s, int ss, int H, int W, int y0, int x0, const PlaneH
         xr[c] = j < cols ? pf_resolve(x0 - h.hl + j, W, periodic) : -1;
     }
     auto yres = [&](int i) {
-        // slab mode: the caller's buffer carries the neighbours' rows (halo), read them as is
-        return slab ? y0 - h.ht + i : pf_resolve(y0 - h.ht + i, H, periodic);
+        // slab mode: the caller's buffer carries the neighbours' rows (halo), read them as is; the
+        // last tile row band may reach past the halo (rows_a is not a multiple of FY): those rows
+        // only feed outputs that are not stored, so they read the nearest existing row
+        const int y = y0 - h.ht + i;
+        return slab ? (y < ylo ? ylo : (y >= yhi ? yhi - 1 : y)) : pf_resolve(y, H, periodic);
     };
     for (int i = warp; i < rows; i += 2 * nw) {
         const int i2 = i + nw;
@@ -88,7 +91,7 @@ k_plane_a_fast(PlaneFastArgs<T> a) {
     T *w = a.w + fr * fsz;
     const int y0 = blockIdx.y * FY, x0 = blockIdx.x * FX;
     const int ss = a.ssa;
-    pf_load<T>(su, ss, H, W, y0, x0, a.hb, a.periodic, a.slab, [&](int64_t o) { return u[o]; });
+    pf_load<T>(su, ss, H, W, y0, x0, a.hb, a.periodic, a.slab, a.ylo, a.yhi, [&](int64_t o) { return u[o]; });
     __syncthreads();
     const int tp = threadIdx.x >> 4, cx = threadIdx.x & 15;
     const int yp = y0 + 2 * tp;
@@ -145,7 +148,7 @@ k_plane_b_fast(PlaneFastArgs<T> a) {
     const int y0 = blockIdx.y * FY, x0 = blockIdx.x * FX;
     {
         const T *pp = a.p + fr * fsz, *ww = a.w + fr * fsz;
-        pf_load<T>(spw, ss, H, W, y0, x0, a.ha, a.periodic, a.slab, [&](int64_t o) {
+        pf_load<T>(spw, ss, H, W, y0, x0, a.ha, a.periodic, a.slab, a.ylo, a.yhi, [&](int64_t o) {
             T2 v;
             v.x = pp[o];
             v.y = ROBUST ? ww[o] : T(0);
@@ -165,7 +168,8 @@ k_plane_b_fast(PlaneFastArgs<T> a) {
                 if (idx >= n) continue;
                 const int i = idx / UC, j = idx - i * UC;
                 const int yy = y0 - 2 + i, xx = x0 - 2 + j;
-                const bool rok = gy0 + yy >= 0 && gy0 + yy < Hg && (a.slab || (yy >= 0 && yy < H));
+                const bool rok = gy0 + yy >= 0 && gy0 + yy < Hg &&
+                                 (a.slab ? (yy >= a.ylo && yy < a.yhi) : (yy >= 0 && yy < H));
                 if (rok && xx >= 0 && xx < W) v[k] = u[(int64_t)yy * W + xx];
             }
 #pragma unroll
@@ -285,10 +289,14 @@ cudaError_t launch_plane_fast(const PlaneFastDesc &d, bool robust, int64_t batch
     if (e != cudaSuccess) return e;
     if (d.slab) {
         // stage A over the extended rows [row_a0, row_a0 + rows_a), stage B over the own rows
+        a.ylo = -d.halo_top;
+        a.yhi = d.H + d.halo_bot;
         PlaneFastArgs<T> aa = a;
         const int64_t off = (int64_t)d.row_a0 * d.W;
         aa.u += off; aa.f += off; aa.p += off; aa.w += off;
         aa.H = d.rows_a; aa.gy0 = d.gy0 + d.row_a0;
+        aa.ylo = a.ylo - d.row_a0;
+        aa.yhi = a.yhi - d.row_a0;
         ka<<<dim3((d.W + FX - 1) / FX, (d.rows_a + FY - 1) / FY, 1), 256, sa, st>>>(aa);
         kb<<<dim3((d.W + FX - 1) / FX, (d.H + FY - 1) / FY, 1), 256, sb, st>>>(a);
         return cudaGetLastError();

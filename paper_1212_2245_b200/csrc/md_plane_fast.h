@@ -14,6 +14,8 @@ template <typename T> struct PlaneFastArgs {
     T *p, *w, *u_out;
     int H, W, periodic;
     int slab, gy0, Hg;  // slab mode: rows read directly (halo present); global row of row 0; global height
+    int ylo, yhi;       // slab mode: rows [ylo, yhi) of the buffers exist (relative to the base pointers);
+                        // tile rows outside only feed discarded outputs and read the nearest valid row
     PlaneHalo hb, ha;
     int ssa, ssb;       // shared row strides of the stage-A u tile and the stage-B (p, W) tile
     ColTaps<T> tb, ta;  // column-grouped taps for those strides
@@ -28,6 +30,7 @@ struct PlaneFastDesc {
     int H, W, periodic;
     int slab, gy0, Hg;         // see PlaneFastArgs
     int rows_a, row_a0;        // slab: stage A computes rows [row_a0, row_a0 + rows_a) (relative to own row 0)
+    int halo_top, halo_bot;    // slab: rows present above / below the own rows in every buffer
     PlaneHalo hb, ha;
     const std::vector<PlaneTap> *taps_blur, *taps_adj;   // host copies
     double alpha, eps_d2, eps_r2;

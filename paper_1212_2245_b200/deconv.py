@@ -48,6 +48,15 @@ def _cached_plan(shape, psf_key, psf_ref, params, conv, init, dtype, rl, force_f
     return GpuPlan(shape, psf_ref[0], params, conv, init=init, dtype=dtype, rl=rl, force_fft2d=force_fft2d)
 
 
+def _unchecked_params(**fields) -> DeconvParams:
+    """A DeconvParams carrying `fields` without its validation (callers whose reference
+    counterpart does not validate, e.g. rl_deblur's floor)."""
+    p = object.__new__(DeconvParams)
+    for k, v in {**DeconvParams().__dict__, **fields}.items():
+        object.__setattr__(p, k, v)
+    return p
+
+
 def _plan(shape, psf: Psf, params: DeconvParams, conv: str, init="wiener", dtype="float64", rl=False,
           force_fft2d=False) -> GpuPlan:
     # psf_ref is a 1-tuple so the Psf (unhashable by value) rides along without keying the cache
@@ -305,9 +314,12 @@ def rrrl_step(state: SharpeningState, f: Image, h: Psf, params: DeconvParams, co
 
 def rl_deblur(f: Image, h: Psf, iterations: int, convolver=None, floor: float = DEFAULT_FLOOR,
               dtype: str = "float64") -> Image:
-    """Richardson-Lucy from the clamped input (deconv.py:524-534)."""
+    """Richardson-Lucy from the clamped input (deconv.py:524-534). As in the reference the
+    iteration count is a ``range`` bound (non-integers raise TypeError, negative counts run
+    none) and ``floor`` is only the clamp value: no DeconvParams validation applies."""
+    count = len(range(iterations))
     conv = _convolver(h, f.shape, convolver, dtype)
-    params = DeconvParams(iterations=int(iterations), floor=floor)
+    params = _unchecked_params(iterations=count, floor=float(floor))
     p = _plan(f.shape, h, params, conv.mode, init="clamped", dtype=dtype, rl=True)
     return _image(p.run(_dev(f, dtype)))
 

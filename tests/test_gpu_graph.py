@@ -79,3 +79,23 @@ def test_capture_cannot_grow_scratch(md):
             plan.run(big, stream=side)
     torch.cuda.synchronize()
     np.testing.assert_array_equal(plan.run(f).cpu().numpy(), plan.run(f).cpu().numpy())
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+def test_graph_survives_scratch_growth(md, dtype):
+    """A graph captured for one frame stays valid after an uncaptured run of a larger batch grew
+    the plan's scratch (the captured buffer is retired, not freed): replay still equals run."""
+    import torch
+    psf = md.Psf.uniform_box(md.BlurAxis.HORIZONTAL, 15.0)
+    pipe = md.DeblurPipeline((64, 128), psf, md.DeconvParams(), md.Scenario.BOX_1D, dtype=dtype)
+    g = pipe.capture(1)
+    tdt = torch.float32 if dtype == "float32" else torch.float64
+    big = torch.from_numpy(_frames(md, (64, 128), psf, 64, 3)).to("cuda", tdt)
+    pipe.run_batch(big)                                   # grows the scratch
+    junk = torch.full((1 << 22,), 7.0, device="cuda")     # reuse of freed memory would show here
+    x = torch.from_numpy(_frames(md, (64, 128), psf, 1, 90)).to("cuda", tdt)
+    got = g(x).clone()
+    want = pipe.run_batch(x)
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
+    del junk

@@ -84,7 +84,11 @@ def test_components_golden(md, name):
     d = load_golden(name)
     entry = str(d["entry"])
     if entry == "lut_r1":
-        pytest.skip("table evaluated inside the weight kernel; covered by comp_robust_weight")
+        # the public DivergenceLut.r1 (md_lut_r1, the reference's rounding order) at 1e-12
+        got = md.default_divergence_lut().r1(d["x"])
+        np.testing.assert_allclose(got, d["out"], rtol=0, atol=1e-12)
+        assert float(np.mean(got == d["out"])) > 0.99     # bitwise except a log ulp here and there
+        return
     if entry == "robust_weight":
         got = md.robust_weight(md.Image(d["f"]), md.Image(d["b"]), eps_data=1.0, floor=0.1).values
         np.testing.assert_allclose(got, d["out"], rtol=0, atol=1e-13)

@@ -219,3 +219,43 @@ def test_benchmark_report_formats_match_reference():
     assert ts.mean_ms == st["total"].mean_ms and ts.max_ms == 4.5
     with pytest.raises(ValueError):
         report(ts, "xml")
+
+
+@pytest.mark.parametrize("kw, expect", [
+    (dict(wiener_k=0, iterations=float("inf")), ("ValueError", "wiener_k must be positive")),
+    (dict(wiener_k=0, eps_data=None), ("ValueError", "wiener_k must be positive")),
+    (dict(iterations=float("nan")), ("ValueError", "cannot convert float NaN to integer")),
+    (dict(iterations=float("inf")), ("OverflowError", "cannot convert float infinity to integer")),
+    (dict(iterations=2.5), ("ValueError", "iterations must be a non-negative integer")),
+    (dict(alpha=-1), ("ValueError", "alpha must be non-negative")),
+    (dict(alpha=float("nan")), None),
+    (dict(floor=0), ("ValueError", "eps_data, eps_reg and floor must be positive")),
+    (dict(eps_reg=float("nan")), ("ValueError", "eps_data, eps_reg and floor must be positive")),
+    (dict(eps_data=None), ("TypeError", None)),
+])
+def test_deconv_params_checks_short_circuit_like_reference(kw, expect):
+    """Outcomes recorded from the reference's DeconvParams (core.py:249-257): the first failing
+    check raises, with the reference's comparison forms (NaN / inf / None behave the same)."""
+    import paper_1212_2245_b200 as md
+    if expect is None:
+        md.DeconvParams(**kw)
+        return
+    with pytest.raises(Exception) as ei:
+        md.DeconvParams(**kw)
+    assert type(ei.value).__name__ == expect[0]
+    if expect[1]:
+        assert str(ei.value) == expect[1]
+
+
+def test_fft_module_exports_fourier_convolve():
+    from paper_1212_2245_b200 import fft
+    assert "fourier_convolve" in fft.__all__ and callable(fft.fourier_convolve)
+
+
+def test_rl_deblur_iterations_are_a_range_bound():
+    """rl_deblur's iteration count is a range() bound as in the reference (deconv.py:531):
+    a fractional count raises TypeError before any device work."""
+    import paper_1212_2245_b200 as md
+    f = md.Image(np.full((8, 8), 10.0))
+    with pytest.raises(TypeError):
+        md.rl_deblur(f, md.Psf.uniform_box(md.BlurAxis.HORIZONTAL, 3), 2.5)
