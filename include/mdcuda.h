@@ -175,6 +175,34 @@ int32_t md_fft(int32_t dtype, void *z, int32_t n, int64_t lines, int32_t inverse
 /* min over n elements, written to *out_host (positivity contracts, deconv.py:410-412) */
 int32_t md_min(int32_t dtype, const void *x, int64_t n, double *out_host, void *stream);
 
+/* ---- DivergenceLut with non-default parameters (DivergenceLut.build, deconv.py:95-112): the
+ * caller owns a device table of `count` doubles; slope / intercept as the reference derives
+ * them (deconv.py:108-111). Evaluation follows the reference's rounding order. */
+/* table[i] = (delta + step i) - 1 - ln(delta + step i) */
+int32_t md_lut_build(double *table, int64_t count, double delta, double step, void *stream);
+/* DivergenceLut.r1 (deconv.py:114-134) with that table, float64 */
+int32_t md_lut_r1_custom(const double *table, int64_t count, double delta, double step, double upper,
+                         double direct_below, double slope, double intercept, const double *x,
+                         double *out, int64_t n, void *stream);
+/* _weight_arrays / robust_weight (deconv.py:142-180) with that table */
+int32_t md_robust_weight_custom(int32_t dtype, const double *table, int64_t count, double delta,
+                                double step, double upper, double direct_below, double slope,
+                                double intercept, const void *f, const void *b, void *out, int64_t n,
+                                double eps_data, double floor, int32_t assume_floored, void *stream);
+
+/* ---- plan-free pointwise steps for a caller-supplied convolver object (the reference's
+ * duck-typed protocol, deconv.py:456-457, 549-550): the caller's blur / adjoint_pair run
+ * wherever they run, these two run here */
+/* out = max(in, floor)  (np.maximum(f, floor): rl_deblur / rrrl_deblur, deconv.py:529, 554) */
+int32_t md_clamp(int32_t dtype, const void *in, void *out, int64_t n, double floor, void *stream);
+/* out = (w ?) f / b  (_combine's ratio, deconv.py:425-430) */
+int32_t md_ratio(int32_t dtype, const void *f, const void *b, const void *w, void *out, int64_t n,
+                 void *stream);
+/* out = u * (num + a D+) / max(den - a D-, 1e-12); den NULL = RL form, d NULL = no TV
+ * (_combine, deconv.py:421-446) */
+int32_t md_combine(int32_t dtype, const void *u, const void *num, const void *den, const void *d,
+                   void *out, int64_t n, double alpha, void *stream);
+
 /* ---- one image split into row slabs over ranks (c5; driver: paper_1212_2245_b200/slab.py).
  * Plans must be 2D direct-tap plans created with MD_FLAG_BIG_FFT. Slab buffers hold the
  * rank's rows plus `top`/`bottom` halo rows; pointers passed to md_slab_iterate point at the

@@ -78,6 +78,12 @@ SIGNATURES = {
     "md_diffusion": (_I32, [_I32, _P, _P, _I64, _I32, _I32, _D, _P]),
     "md_rrrl_step": (_I32, [_P, _P, _P, _P, _P, _P, _P, _I64, _D, _P]),
     "md_guard": (_I32, [_I32, _P, _I64, _P]),
+    "md_lut_build": (_I32, [_P, _I64, _D, _D, _P]),
+    "md_lut_r1_custom": (_I32, [_P, _I64, _D, _D, _D, _D, _D, _D, _P, _P, _I64, _P]),
+    "md_robust_weight_custom": (_I32, [_I32, _P, _I64, _D, _D, _D, _D, _D, _D, _P, _P, _P, _I64, _D, _D, _I32, _P]),
+    "md_clamp": (_I32, [_I32, _P, _P, _I64, _D, _P]),
+    "md_ratio": (_I32, [_I32, _P, _P, _P, _P, _I64, _P]),
+    "md_combine": (_I32, [_I32, _P, _P, _P, _P, _P, _I64, _D, _P]),
     "md_lut_r1": (_I32, [_I32, _P, _P, _I64, _P]),
     "md_lut_table": (_I32, [ctypes.POINTER(_D), _I64]),
     "md_min": (_I32, [_I32, _P, _I64, ctypes.POINTER(_D), _P]),

@@ -132,6 +132,10 @@ def _param_flags(p):
     p.add_argument("--floor", type=float, default=0.1)
     p.add_argument("--scenario", default="auto", choices=["auto", "box", "fourier1d", "fourier2d"])
     p.add_argument("--dtype", default="float64", choices=["float64", "float32"])
+    # the reference's thread-engine width (cli.py:215); accepted for drop-in command lines -- the
+    # device runs the whole frame whatever its value (results do not depend on it, as in the
+    # reference, parallel.py:10-13)
+    p.add_argument("--threads", type=int, default=1, help="accepted for compatibility; the GPU runs the frame")
 
 
 def build_parser() -> argparse.ArgumentParser:

@@ -477,6 +477,11 @@ class PlanUse {
 };
 
 // ======================================================================== C ABI
+// error reporting for the C-ABI entries defined in other translation units (md_custom_lut.cu)
+namespace md {
+int set_error(int code, const char *msg) { return fail(code, msg); }
+}  // namespace md
+
 extern "C" {
 
 int32_t md_abi_version(void) { return MDCUDA_ABI_VERSION; }

@@ -11,6 +11,9 @@ namespace md {
 
 enum { LINE_BOX = 0, LINE_TAPS = 1 };
 
+// md_last_error() for C-ABI entries outside md_capi.cu; returns `code`
+int set_error(int code, const char *msg);
+
 // One direction (blur or adjoint) of a 1D convolution along a line (conv.py:85-173,
 // deconv.py:310-326). Box: out[j] = wi * sum_{k=lo..hi} a[j+k] (+ we*(a[j+elo] + a[j+ehi])).
 // Taps: out[j] = sum_t w[t] * a[j + center - t]. Indices clamp or wrap.

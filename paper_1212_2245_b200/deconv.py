@@ -99,8 +99,14 @@ def _image(t) -> Image:
 
 
 # ------------------------------------------------------------------------------------------
-# divergence table descriptor (deconv.py:81-139). The table itself is built and evaluated on
-# the device (md_common.cuh r1_lut); this object carries the same parameters for API parity.
+# divergence table (deconv.py:81-139). The table is built and evaluated on the device: the
+# reference parameters are compiled into the pipeline kernels (md_common.cuh); any other
+# parameters get a device table of their own (md_lut_build) evaluated with runtime parameters
+# (md_lut_r1_custom / md_robust_weight_custom), and the entries that take a `lut` then run the
+# iteration step by step (the fused kernels know only the default table).
+
+_DEFAULT_LUT = (1.0 / 32.0, 1.0 / 2048.0, 65.0, 0.5)
+
 
 @dataclass(frozen=True, eq=False)
 class DivergenceLut:
@@ -116,29 +122,72 @@ class DivergenceLut:
               direct_below: float = 0.5) -> "DivergenceLut":
         if not 0.0 < delta < direct_below < upper:
             raise ValueError("need 0 < delta < direct_below < upper")
-        if (delta, step, upper, direct_below) != (1.0 / 32.0, 1.0 / 2048.0, 65.0, 0.5):
-            raise ValueError("the device divergence table supports the reference defaults only")
         slope = 1.0 - 1.0 / upper
         return cls(delta, step, upper, direct_below, slope, (upper - 1.0 - math.log(upper)) - slope * upper)
 
     @property
+    def count(self) -> int:
+        return int(round((self.upper - self.delta) / self.step)) + 1      # deconv.py:104
+
+    @property
+    def is_default(self) -> bool:
+        return (self.delta, self.step, self.upper, self.direct_below) == _DEFAULT_LUT
+
+    def _device_table(self):
+        """The custom table on the current device (built once per object and device)."""
+        import torch
+        from . import _lib as L
+        dev = torch.cuda.current_device()
+        cache = self.__dict__.setdefault("_tables", {})
+        if dev not in cache:
+            t = torch.empty(self.count, dtype=torch.float64, device="cuda")
+            L.check(L.lib().md_lut_build(t.data_ptr(), t.numel(), self.delta, self.step, None))
+            cache[dev] = t
+        return cache[dev]
+
+    def _args(self):
+        t = self._device_table()
+        return (t.data_ptr(), t.numel(), self.delta, self.step, self.upper, self.direct_below, self.linear_slope,
+                self.linear_intercept)
+
+    @property
     def table(self) -> np.ndarray:
-        """The 133,057 nodes x_i - 1 - ln x_i, built on the device (copied to the host)."""
+        """The nodes x_i - 1 - ln x_i, built on the device (copied to the host)."""
         import ctypes
         from . import _lib as L
-        out = np.empty(133057)
-        L.check(L.lib().md_lut_table(out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), out.size))
+        if self.is_default:
+            out = np.empty(133057)
+            L.check(L.lib().md_lut_table(out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), out.size))
+        else:
+            out = _host(self._device_table())
         out.setflags(write=False)
         return out
 
     def r1(self, x) -> np.ndarray:
-        """r1 by table interpolation with the linear / exact extensions, on the device."""
+        """r1 by table interpolation with the linear / exact extensions, on the device, in the
+        reference's rounding order."""
         from . import _lib as L
         from .plan import _stream_ptr
         xd = _dev(np.asarray(x, dtype=np.float64))
         out = xd.new_empty(xd.shape)
-        L.check(L.lib().md_lut_r1(L.MD_F64, xd.data_ptr(), out.data_ptr(), xd.numel(), _stream_ptr(None)))
+        if self.is_default:
+            L.check(L.lib().md_lut_r1(L.MD_F64, xd.data_ptr(), out.data_ptr(), xd.numel(), _stream_ptr(None)))
+        else:
+            L.check(L.lib().md_lut_r1_custom(*self._args(), xd.data_ptr(), out.data_ptr(), xd.numel(),
+                                             _stream_ptr(None)))
         return _host(out)
+
+    def weight_dev(self, f, b, eps_data: float, floor: float, assume_floored: bool = False):
+        """_weight_arrays (deconv.py:142-162) with this table, device tensors in and out."""
+        if self.is_default:
+            return robust_weight_dev(f, b, eps_data, floor, assume_floored)
+        from . import _lib as L
+        from .plan import _stream_ptr, dtype_code
+        out = b.new_empty(b.shape)
+        L.check(L.lib().md_robust_weight_custom(dtype_code(f), *self._args(), f.data_ptr(), b.data_ptr(),
+                                                out.data_ptr(), f.numel(), eps_data, floor,
+                                                1 if assume_floored else 0, _stream_ptr(None)))
+        return out
 
 
 @functools.lru_cache(maxsize=1)
@@ -163,7 +212,8 @@ def robust_weight(f: Image, b: Image, lut: DivergenceLut | None = None, eps_data
     bd = _dev(b)
     if device_min(bd) <= 0.0:
         raise ContractError("blurred iterate must be strictly positive")
-    return _image(robust_weight_dev(_dev(f), bd, eps_data, floor))
+    lut = default_divergence_lut() if lut is None else lut
+    return _image(lut.weight_dev(_dev(f), bd, eps_data, floor))
 
 
 def diffusion_term(u: Image, eps_reg: float) -> Image:
@@ -257,12 +307,100 @@ def make_convolver(psf: Psf, shape: tuple[int, int], mode: str | None = None, dt
     return GpuConvolver(psf, shape, mode, dtype)
 
 
-def _convolver(h: Psf, shape, convolver, dtype="float64") -> GpuConvolver:
+def _convolver(h: Psf, shape, convolver, dtype="float64"):
+    """A mode string / None -> the device convolver; a GpuConvolver as is; any other object with
+    the reference's convolver protocol (blur / adjoint / adjoint_pair on float64 arrays,
+    deconv.py:295-376; accepted wherever the reference accepts one, deconv.py:456-457, 549-550)
+    -> wrapped so it is called with host arrays while every other step stays on the device."""
     if convolver is None or isinstance(convolver, str):
         return make_convolver(h, shape, convolver, dtype)
     if isinstance(convolver, GpuConvolver):
         return convolver
-    raise TypeError("the GPU path needs a convolver from make_convolver() or a mode string")
+    for name in ("blur", "adjoint", "adjoint_pair"):
+        if not callable(getattr(convolver, name, None)):
+            raise TypeError(f"convolver object lacks {name}() (the protocol of deconv.py:295-376)")
+    return _ForeignConvolver(convolver, dtype)
+
+
+class _ForeignConvolver:
+    """A caller's convolver object behind device-tensor blur / adjoint / adjoint_pair: tensors go
+    to the host as float64 arrays, through the object, and back. Only the object's own work runs
+    where the object runs it; ratio, weights, diffusion and the update are device kernels."""
+
+    def __init__(self, obj, dtype: str):
+        self.obj, self.dtype = obj, dtype
+
+    def blur(self, t):
+        return _dev(np.asarray(self.obj.blur(_host(t)), dtype=np.float64), self.dtype)
+
+    def adjoint(self, t):
+        return _dev(np.asarray(self.obj.adjoint(_host(t)), dtype=np.float64), self.dtype)
+
+    def adjoint_pair(self, p, q):
+        a, b = self.obj.adjoint_pair(_host(p), _host(q))
+        return _dev(np.asarray(a, dtype=np.float64), self.dtype), _dev(np.asarray(b, dtype=np.float64), self.dtype)
+
+
+def _dev_ops(conv):
+    """Device-tensor blur / adjoint / adjoint_pair of a GpuConvolver or a wrapped object."""
+    if isinstance(conv, GpuConvolver):
+        return (lambda t: conv._plan.convolve(t, 0), lambda t: conv._plan.convolve(t, 1),
+                lambda p, q: conv._plan.adjoint_pair(p, q))
+    return conv.blur, conv.adjoint, conv.adjoint_pair
+
+
+# ------------------------------------------------------------------------------------------
+# device step toolkit (deconv.py:415-446, 512-521) for the step-by-step paths: a caller's
+# convolver object, or a DivergenceLut with non-default parameters
+
+def _clamp_dev(t, floor: float):
+    from . import _lib as L
+    from .plan import _stream_ptr, dtype_code
+    out = t.new_empty(t.shape)
+    L.check(L.lib().md_clamp(dtype_code(t), t.data_ptr(), out.data_ptr(), t.numel(), float(floor), _stream_ptr(None)))
+    return out
+
+
+def _ratio_dev(f, b, w=None):
+    from . import _lib as L
+    from .plan import _stream_ptr, dtype_code
+    out = b.new_empty(b.shape)
+    L.check(L.lib().md_ratio(dtype_code(b), f.data_ptr(), b.data_ptr(), None if w is None else w.data_ptr(),
+                             out.data_ptr(), b.numel(), _stream_ptr(None)))
+    return out
+
+
+def _combine_dev(u, num, den, d, alpha: float):
+    """_combine's assembly (deconv.py:421-446): u (num + a D+) / max(den - a D-, 1e-12)."""
+    from . import _lib as L
+    from .plan import _stream_ptr, dtype_code
+    out = u.new_empty(u.shape)
+    L.check(L.lib().md_combine(dtype_code(u), u.data_ptr(), num.data_ptr(), None if den is None else den.data_ptr(),
+                               None if d is None else d.data_ptr(), out.data_ptr(), u.numel(), float(alpha),
+                               _stream_ptr(None)))
+    return out
+
+
+def _combine_steps(u, f, b, w, d, alpha, conv):
+    """_combine (deconv.py:421-446) with the convolver's adjoint(s)."""
+    _, adjoint, adjoint_pair = _dev_ops(conv)
+    if w is None:
+        return _combine_dev(u, adjoint(_ratio_dev(f, b)), None, d, alpha)
+    num, den = adjoint_pair(_ratio_dev(f, b, w), w)
+    return _combine_dev(u, num, den, d, alpha)
+
+
+def _iterate_steps(u, fpos, conv, params: DeconvParams, lut: "DivergenceLut", robust: bool = True):
+    """_iterate_rrrl (deconv.py:512-521), one device step at a time."""
+    blur = _dev_ops(conv)[0]
+    b = guard_(blur(u))
+    w = lut.weight_dev(fpos, b, params.eps_data, params.floor, assume_floored=True) if robust else None
+    d = diffusion_dev(u, params.eps_reg) if params.alpha > 0.0 else None
+    return _combine_steps(u, fpos, b, w, d, params.alpha, conv)
+
+
+def _stepwise(conv, lut) -> bool:
+    return not isinstance(conv, GpuConvolver) or (lut is not None and not lut.is_default)
 
 
 # ------------------------------------------------------------------------------------------
@@ -284,6 +422,8 @@ def rl_step(u: Image, f: Image, h: Psf, convolver=None) -> Image:
     _require_positive(ud, "RL iterate")
     _require_positive(fd, "RL observation")
     conv = _convolver(h, u.shape, convolver)
+    if not isinstance(conv, GpuConvolver):
+        return _image(_combine_steps(ud, fd, guard_(conv.blur(ud)), None, None, 0.0, conv))
     b = guard_(conv._plan.convolve(ud, 0))
     return _image(conv._plan.rrrl_step(ud, fd, b))
 
@@ -295,8 +435,9 @@ def prepare_state(u: Image, f: Image, h: Psf, params: DeconvParams, convolver=No
     _require_positive(ud, "RRRL iterate")
     _require_positive(fd, "RRRL observation")
     conv = _convolver(h, u.shape, convolver)
-    b = guard_(conv._plan.convolve(ud, 0))
-    w = robust_weight_dev(fd, b, params.eps_data, params.floor) if robust else None
+    lut = default_divergence_lut() if lut is None else lut
+    b = guard_(_dev_ops(conv)[0](ud))
+    w = lut.weight_dev(fd, b, params.eps_data, params.floor) if robust else None
     d = diffusion_dev(ud, params.eps_reg) if params.alpha > 0.0 else None
     return SharpeningState(u, _image(b), None if w is None else _image(w), None if d is None else _image(d))
 
@@ -308,6 +449,8 @@ def rrrl_step(state: SharpeningState, f: Image, h: Psf, params: DeconvParams, co
     conv = _convolver(h, state.iterate.shape, convolver)
     w = None if state.weight is None else _dev(state.weight)
     d = None if state.diffusion is None else _dev(state.diffusion)
+    if not isinstance(conv, GpuConvolver):
+        return _image(_combine_steps(ud, _dev(f), _dev(state.blurred), w, d, params.alpha, conv))
     out = conv._plan.rrrl_step(ud, _dev(f), _dev(state.blurred), w, d, alpha=params.alpha)
     return _image(out)
 
@@ -319,6 +462,12 @@ def rl_deblur(f: Image, h: Psf, iterations: int, convolver=None, floor: float = 
     none) and ``floor`` is only the clamp value: no DeconvParams validation applies."""
     count = len(range(iterations))
     conv = _convolver(h, f.shape, convolver, dtype)
+    if not isinstance(conv, GpuConvolver):
+        fpos = _clamp_dev(_dev(f, dtype), floor)
+        u = fpos.clone()
+        for _ in range(count):
+            u = _combine_steps(u, fpos, guard_(conv.blur(u)), None, None, 0.0, conv)
+        return _image(u)
     params = _unchecked_params(iterations=count, floor=float(floor))
     p = _plan(f.shape, h, params, conv.mode, init="clamped", dtype=dtype, rl=True)
     return _image(p.run(_dev(f, dtype)))
@@ -327,8 +476,16 @@ def rl_deblur(f: Image, h: Psf, iterations: int, convolver=None, floor: float = 
 def rrrl_deblur(f: Image, h: Psf, params: DeconvParams, convolver=None,
                 lut: DivergenceLut | None = None, dtype: str = "float64") -> Image:
     """RRRL from the clamped input (deconv.py:537-559); default convolver is box for box
-    kernels and clamped direct summation otherwise."""
+    kernels and clamped direct summation otherwise. A caller's convolver object or a
+    non-default divergence table runs the iterations step by step on the device."""
     conv = _convolver(h, f.shape, convolver, dtype)
+    if _stepwise(conv, lut):
+        lut = default_divergence_lut() if lut is None else lut
+        fpos = _clamp_dev(_dev(f, dtype), params.floor)
+        u = fpos.clone()
+        for _ in range(params.iterations):
+            u = _iterate_steps(u, fpos, conv, params, lut)
+        return _image(u)
     p = _plan(f.shape, h, params, conv.mode, init="clamped", dtype=dtype)
     return _image(p.run(_dev(f, dtype)))
 
@@ -413,6 +570,24 @@ class DeblurPipeline:
                              force_fft2d=force_fft2d, fused=fused, generic_lines=generic_lines,
                              big_fft=big_fft)
         self._wiener_plan = None
+        # a non-default divergence table: the Wiener step through a 0-iteration plan, then the
+        # iterations step by step with the scenario's device convolver (deconv.py:653-690)
+        self.lut = lut
+        self._steps = None
+        if lut is not None and not lut.is_default:
+            p0 = DeconvParams(params.wiener_k, params.alpha, 0, params.eps_data, params.eps_reg, params.floor)
+            self._steps = (GpuPlan(self.shape, psf, p0, _SCENARIO_CONV[scenario], init="wiener", dtype=dtype,
+                                   force_fft2d=force_fft2d, big_fft=big_fft),
+                           make_convolver(psf, self.shape, _SCENARIO_CONV[scenario], dtype))
+
+    def _run_steps(self, f):
+        """Wiener -> clamp -> iterations with the custom table, device tensors [.., H, W]."""
+        wplan, conv = self._steps
+        u = wplan.run(f)
+        fpos = _clamp_dev(f, self.params.floor)
+        for _ in range(self.params.iterations):
+            u = _iterate_steps(u, fpos, conv, self.params, self.lut)
+        return u
 
     @property
     def plan(self) -> GpuPlan:
@@ -427,12 +602,31 @@ class DeblurPipeline:
         array in (uint8 camera frames, float32 or float64) -> host array out (float64 by
         default, float32 on request), copies pipelined inside the C ABI (md_run_host_ex)."""
         import torch
+        if self._steps is not None:
+            return self._run_batch_steps(frames, out, out_dtype)
         if isinstance(frames, torch.Tensor):
             self._check_shape(frames.shape[-2:])
             return self._plan.run(frames, out=out, stream=stream)
         a = np.asarray(frames)
         self._check_shape(a.shape[-2:])
         return self._plan.run_host(a, out=out, stream=stream, out_dtype=out_dtype)
+
+    def _run_batch_steps(self, frames, out, out_dtype):
+        import torch
+        host = not isinstance(frames, torch.Tensor)
+        t = _dev(np.asarray(frames, dtype=np.float64), self.dtype) if host else _dev(frames, self.dtype)
+        self._check_shape(t.shape[-2:])
+        u = self._run_steps(t)
+        if not host:
+            if out is not None:
+                out.copy_(u)
+                return out
+            return u
+        res = _host(u).astype(out_dtype, copy=False)
+        if out is not None:
+            out[...] = res
+            return out
+        return res
 
     def capture(self, batch: int = 1):
         """The pipeline for ``batch`` device-resident frames recorded as a CUDA graph
@@ -441,6 +635,9 @@ class DeblurPipeline:
         import torch
         if int(batch) < 1:
             raise ValueError("batch must be positive")
+        if self._steps is not None:
+            raise ValueError("a pipeline with a non-default divergence table runs step by step; capture needs "
+                             "the default table")
         f = torch.zeros((int(batch),) + self.shape, dtype=torch_dtype(self.dtype), device="cuda")
         f.fill_(max(self.params.floor, 1.0))
         return self._plan.capture(f)
@@ -452,6 +649,8 @@ class DeblurPipeline:
         import torch
         self._check_shape(f.shape)
         fd = _dev(f, self.dtype)
+        if self._steps is not None:
+            return self._run_timed_steps(fd)
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record()
@@ -466,8 +665,26 @@ class DeblurPipeline:
         total = max(t0.elapsed_time(t1), wiener_ms + sum(iters))
         return _image(out), StageTimes(wiener_ms=wiener_ms, iteration_ms=iters if k else [], total_ms=total)
 
+    def _run_timed_steps(self, fd):
+        import torch
+        wplan, conv = self._steps
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(self.params.iterations + 2)]
+        ev[0].record()
+        u = wplan.run(fd)
+        fpos = _clamp_dev(fd, self.params.floor)
+        ev[1].record()
+        for k in range(self.params.iterations):
+            u = _iterate_steps(u, fpos, conv, self.params, self.lut)
+            ev[k + 2].record()
+        torch.cuda.synchronize()
+        iters = [ev[k + 1].elapsed_time(ev[k + 2]) for k in range(self.params.iterations)]
+        return _image(u), StageTimes(wiener_ms=ev[0].elapsed_time(ev[1]), iteration_ms=iters,
+                                     total_ms=ev[0].elapsed_time(ev[-1]))
+
     def run(self, f: Image) -> Image:
         self._check_shape(f.shape)
+        if self._steps is not None:
+            return _image(self._run_steps(_dev(f, self.dtype)))
         return _image(self._plan.run(_dev(f, self.dtype)))
 
 

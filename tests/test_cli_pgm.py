@@ -49,3 +49,9 @@ def test_cli_usage_errors(tmp_path):
     assert main(["deblur", str(tmp_path / "t.pgm"), str(tmp_path / "o.pgm"), "--psf", "nope"]) == 1
     assert main(["nosuchcommand"]) == 1
     assert main(["deblur", str(tmp_path / "missing.pgm"), str(tmp_path / "o.pgm"), "--psf", "box:h:3"]) == 2
+
+
+def test_deblur_parser_accepts_reference_threads_flag():
+    from paper_1212_2245_b200.cli import build_parser
+    a = build_parser().parse_args(["deblur", "in.pgm", "out.pgm", "--psf", "box:h:15", "--threads", "8"])
+    assert a.threads == 8

@@ -28,6 +28,26 @@ def test_cli_deblur_matches_api(md, tmp_path, capsys):
     want = md.wr3l(f, psf, md.DeconvParams())
     got = md.read_pgm(tmp_path / "u.pgm").values
     np.testing.assert_array_equal(got, np.clip(np.floor(want.values + 0.5), 0, 255))
+    # and against the CPU oracle of the reference's `motiondeblur deblur` (cli.py:132-167: wr3l,
+    # then write_pgm's round-half-up quantisation); a pixel may differ by one grey level only
+    # where the unquantised values straddle a .5 boundary within the parity bar
+    from oracle import wr3l_oracle as O
+    ref = O.pipeline(f.values, O.make_psf("box", axis="h", length=9), O.OParams(), "box")
+    ref_q = np.clip(np.floor(ref + 0.5), 0, 255)
+    diff = np.abs(got - ref_q)
+    assert diff.max() <= 1.0
+    near = np.abs((ref + 0.5) - np.round(ref + 0.5)) <= 1e-4 * 255
+    assert np.all((diff == 0) | near)
+
+
+def test_cli_deblur_threads_flag(md, tmp_path):
+    """The reference's --threads (cli.py:215) is accepted; the output does not depend on it."""
+    from paper_1212_2245_b200.cli import main
+    psf = md.Psf.uniform_box(md.BlurAxis.VERTICAL, 7)
+    md.write_pgm(md.synth_blur(md.make_test_image(64, 32), psf), tmp_path / "f.pgm")
+    assert main(["deblur", str(tmp_path / "f.pgm"), str(tmp_path / "a.pgm"), "--psf", "box:v:7"]) == 0
+    assert main(["deblur", str(tmp_path / "f.pgm"), str(tmp_path / "b.pgm"), "--psf", "box:v:7", "--threads", "4"]) == 0
+    np.testing.assert_array_equal(md.read_pgm(tmp_path / "a.pgm").values, md.read_pgm(tmp_path / "b.pgm").values)
 
 
 def test_cli_bench_csv(md, tmp_path, capsys):

@@ -110,3 +110,44 @@ def test_periodic_direct_equals_fourier_convolver(rng):
     p1 = O.make_psf("1d", rng.uniform(0, 1, 9), center=2, axis="h")
     np.testing.assert_allclose(O.periodic_convolve(a, p1), O.make_convolver(p1, a.shape, "fourier").blur(a),
                                rtol=0, atol=1e-9)
+
+
+# ---- drop-in boundary fixtures (oracle/gen_golden_boundary.py, produced by the reference)
+
+LUT_ARGS = dict(delta=1.0 / 16.0, step=1.0 / 1000.0, upper=40.0, direct_below=0.4)
+
+
+def test_oracle_custom_lut_golden():
+    from oracle import wr3l_oracle as O
+    d = load_golden("bnd_lut_custom")
+    lut = O.build_lut(**LUT_ARGS)
+    np.testing.assert_array_equal(lut.table, d["table"])
+    np.testing.assert_allclose(O.r1(d["x"], lut), d["out"], rtol=0, atol=1e-15)
+
+
+def test_oracle_custom_lut_pipelines_golden():
+    from oracle import wr3l_oracle as O
+    lut = O.build_lut(**LUT_ARGS)
+    d = load_golden("bnd_pipe_lut_custom")
+    got = O.pipeline(d["f"].astype(np.float64), O.make_psf("box", axis="h", length=9), O.OParams(), "box", lut=lut)
+    assert np.abs(got - d["out"]).max() <= 1e-8
+    d = load_golden("bnd_rrrl_lut_custom")
+    spec = O.OPsf("1d", d["psf_weights"], int(d["psf_center"]), "v")
+    conv = O.make_convolver(spec, d["f"].shape, "fourier")
+    fpos = np.maximum(d["f"].astype(np.float64), 0.1)
+    u = fpos.copy()
+    for _ in range(4):
+        u = O.rrrl_iteration(u, fpos, conv, O.OParams(iterations=4), lut)
+    assert np.abs(u - d["out"]).max() <= 1e-8
+
+
+def test_oracle_object_convolver_golden():
+    from oracle import wr3l_oracle as O
+    spec = O.make_psf("box", axis="h", length=9)
+    conv = O.SpatialConv(O.OPsf("1d", spec.weights, spec.center, "h"))
+    d = load_golden("bnd_rrrl_object")
+    fpos = np.maximum(d["f"].astype(np.float64), 0.1)
+    u = fpos.copy()
+    for _ in range(5):
+        u = O.rrrl_iteration(u, fpos, conv, O.OParams())
+    assert np.abs(u - d["out"]).max() <= 1e-8
