@@ -168,7 +168,7 @@ int32_t md_lut_r1(int32_t dtype, const void *x, void *out, int64_t n, void *stre
 int32_t md_lut_table(double *host_out, int64_t count);
 /* x = max(x, 1e-12) in place (_blur_guarded, deconv.py:415-418) */
 int32_t md_guard(int32_t dtype, void *x, int64_t n, void *stream);
-/* natural-order complex FFT of `lines` contiguous lines of length n (power of two <= 65536), in
+/* natural-order complex FFT of `lines` contiguous lines of length n (power of two <= 2^20), in
  * place; dtype MD_F64 = complex128 (interleaved double pairs), MD_F32 = complex64; forward
  * unnormalised, inverse scaled by 1/n (FourierPlan.forward / inverse, fft.py:52-117) */
 int32_t md_fft(int32_t dtype, void *z, int32_t n, int64_t lines, int32_t inverse, void *stream);

@@ -35,6 +35,9 @@ using namespace md;
 
 namespace {
 
+// internal plan flag (not in mdcuda.h): a 1D PSF handed over from the line route as a plane
+constexpr uint32_t kFlagLinePlane = 1u << 16;
+
 thread_local std::string g_err;
 
 int fail(int code, const std::string &msg) {
@@ -137,6 +140,15 @@ __global__ void k_unbitrev(const unsigned char *src, unsigned char *dst, int n, 
 }
 
 // scatter a direct-tap list into a zeroed H x W grid, centre at (0, 0), wrapped (fft.py:204-221)
+// m[H][W] = m1[x] (axis 1) or m1[y] (axis 0): a 1D multiplier over a plane, byte-generic
+__global__ void k_replicate_filter(const unsigned char *m1, unsigned char *m, int H, int W, int axis, int es) {
+    const int64_t n = (int64_t)H * W;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = axis == 1 ? i % W : i / W;
+        for (int b = 0; b < es; ++b) m[i * es + b] = m1[k * es + b];
+    }
+}
+
 __global__ void k_embed_taps(double *z, int H, int W, const PlaneTap *taps, int nt) {
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
         const int y = ((-taps[t].dy) % H + H) % H, x = ((-taps[t].dx) % W + W) % W;
@@ -202,6 +214,8 @@ struct md_plan {
     std::vector<PlaneTap> htaps_blur, htaps_adj;
     bool fast_plane = false;    // register-blocked direct-tap stage kernels apply
     bool big = false;           // two-level FFT passes for the 2D Wiener step (large images)
+    int line_axis = -1;         // a 1D PSF routed as a plane: its blur axis (1 rows, 0 columns) --
+                                // the Wiener step is then 1D along that axis (wiener_1d semantics)
     BigAxis bigH{}, bigW{};
     std::vector<void *> owned;  // extra device tables
     int periodic = 0;
@@ -543,6 +557,8 @@ int32_t md_plan_create(const md_plan_desc *desc, md_plan **out) {
         if (wiener && (size_t)P->n > lim) beyond = "blur-axis length above the on-chip FFT limit";
         else if (desc->iterations > 0 && !P->fast_lines && !iter_lines_fits(desc->dtype, P->n, 2 * T))
             beyond = "blur-axis length above the on-chip line-iteration limit";
+        else if (!conv_lines_fits(desc->dtype, P->n, 2 * T))
+            beyond = "blur-axis length above the on-chip line-convolution limit";
         if (beyond) {
             // lines longer than one CTA holds: the same problem as a plane with a one-row (one-
             // column) PSF -- two-level FFT Wiener (its spectrum is constant across the lines) and
@@ -561,6 +577,7 @@ int32_t md_plan_create(const md_plan_desc *desc, md_plan **out) {
             d2.conv = desc->conv == MD_CONV_FOURIER ? MD_CONV_FOURIER2D
                                                     : (desc->conv == MD_CONV_BOX ? MD_CONV_SPATIAL : desc->conv);
             d2.flags &= ~MD_FLAG_FORCE_FFT2D;
+            d2.flags |= kFlagLinePlane;
             if (md_plan_create(&d2, out) != MD_OK) return fail(MD_EINVAL, beyond);
             (*out)->describe = std::string("1D PSF beyond the on-chip line limits as a plane; ") + (*out)->describe;
             return MD_OK;
@@ -609,16 +626,22 @@ int32_t md_plan_create(const md_plan_desc *desc, md_plan **out) {
               desc->center_col < desc->psf_cols))
             return bail(fail(MD_EINVAL, "PSF center must lie inside the support"));
         P->periodic = desc->conv != MD_CONV_SPATIAL;
-        const bool pow2 = is_pow2(H) && is_pow2(W);
+        // a 1D PSF past the line kernels' limits (kFlagLinePlane): only its blur axis is
+        // transformed (wiener_1d, deconv.py:275-288; fft.py:63-66 constrains that axis alone)
+        if ((desc->flags & kFlagLinePlane) && (desc->psf_rows == 1) != (desc->psf_cols == 1))
+            P->line_axis = desc->psf_rows == 1 ? 1 : 0;
+        const bool pow2 = P->line_axis >= 0 ? is_pow2(P->line_axis == 1 ? W : H) : (is_pow2(H) && is_pow2(W));
         if ((P->periodic || wiener) && !pow2)
-            return bail(fail(MD_EINVAL, "2D Fourier convolution needs power-of-two dimensions"));
+            return bail(fail(MD_EINVAL, P->line_axis >= 0 ? "the blur axis must have power-of-two extent"
+                                                          : "2D Fourier convolution needs power-of-two dimensions"));
         std::vector<PlaneTap> tb, ta;
         plane_taps(*P, false, tb, P->hblur);
         plane_taps(*P, true, ta, P->hadj);
         const int maxh = std::max(std::max(P->hadj.ht, P->hadj.hb), std::max(P->hadj.hl, P->hadj.hr));
         const bool direct_ok = maxh <= 40;
         const int lim = desc->dtype == MD_F64 ? 4096 : 8192;
-        P->big = pow2 && (std::max(H, W) > lim || (desc->flags & MD_FLAG_BIG_FFT)) && (P->periodic || wiener);
+        P->big = pow2 && (P->line_axis >= 0 || std::max(H, W) > lim || (desc->flags & MD_FLAG_BIG_FFT)) &&
+                 (P->periodic || wiener);
         bool use_fft = P->periodic && ((desc->flags & MD_FLAG_FORCE_FFT2D) || P->hblur.nt > 96 || !direct_ok);
         if (!P->periodic && !direct_ok) return bail(fail(MD_EINVAL, "PSF too large for the direct clamped path"));
         if (P->big && use_fft) {
@@ -626,14 +649,48 @@ int32_t md_plan_create(const md_plan_desc *desc, md_plan **out) {
                 return bail(fail(MD_EINVAL, "image side above the on-chip 2D FFT limit for a dense PSF"));
             use_fft = false;    // large images iterate with direct taps; only the Wiener step needs FFTs
         }
-        if (std::max(H, W) > 65536) return bail(fail(MD_EINVAL, "transform length above 65536"));
+        if (P->line_axis >= 0 ? (std::max(H, W) > (1 << 20) || (int64_t)H * W >= (1ll << 31))
+                              : std::max(H, W) > 65536)
+            return bail(fail(MD_EINVAL, "transform length above the two-level FFT limit"));
         P->path = use_fft ? PATH_PLANE_FFT : PATH_PLANE_DIRECT;
         if ((rc = upload(&P->d_ptaps_blur, tb.data(), tb.size()))) return bail(rc);
         if ((rc = upload(&P->d_ptaps_adj, ta.data(), ta.size()))) return bail(rc);
         P->htaps_blur = tb;
         P->htaps_adj = ta;
         P->fast_plane = !(desc->flags & MD_FLAG_GENERIC_LINES) && plane_fast_supported(P->hblur, P->hadj, tb, ta, desc->dtype);
-        if (pow2 && P->big) {
+        if (pow2 && P->big && P->line_axis >= 0) {
+            // the 1D spectrum along the blur axis in the two-level storage order, its Wiener
+            // multiplier replicated over the other axis (so the passes' filter index is the
+            // frame address, as for 2D)
+            const int ax = P->line_axis, N = ax == 1 ? W : H;
+            BigAxis n64{};
+            std::vector<void *> tmp;
+            if ((rc = build_big_axis(N, MD_F64, &n64, tmp)) ||
+                (rc = build_big_axis(N, desc->dtype, ax == 1 ? &P->bigW : &P->bigH, P->owned)))
+                return bail(rc);
+            double *emb = nullptr;
+            double2 *h64 = nullptr;
+            CU(cudaMalloc(&emb, (size_t)N * sizeof(double)));
+            CU(cudaMalloc(&h64, (size_t)N * sizeof(double2)));
+            CU(cudaMemset(emb, 0, (size_t)N * sizeof(double)));
+            k_embed_taps<<<(tb.size() + 255) / 256, 256>>>(emb, ax == 1 ? 1 : N, ax == 1 ? N : 1, P->d_ptaps_blur,
+                                                         (int)tb.size());
+            CU(cudaGetLastError());
+            CU(big_axis<double>(n64, h64, ax == 1 ? 1 : N, ax == 1 ? N : 1, ax, 0, emb, nullptr, nullptr, 0, 1.0, 1, 0));
+            CU(cudaDeviceSynchronize());
+            cudaFree(emb);
+            for (void *p : tmp) cudaFree(p);
+            void *m1 = nullptr;
+            rc = make_filter(h64, N, desc->wiener_k, desc->dtype, &m1);
+            cudaFree(h64);
+            if (rc) return bail(rc);
+            const int ces = desc->dtype == MD_F64 ? 16 : 8;
+            CU(cudaMalloc(&P->d_mult, (size_t)H * W * ces));
+            k_replicate_filter<<<1024, 256>>>((const unsigned char *)m1, (unsigned char *)P->d_mult, H, W, ax, ces);
+            CU(cudaGetLastError());
+            CU(cudaDeviceSynchronize());
+            cudaFree(m1);
+        } else if (pow2 && P->big) {
             BigAxis h64{}, w64{};
             std::vector<void *> tmp;
             if ((rc = build_big_axis(H, MD_F64, &h64, tmp)) || (rc = build_big_axis(W, MD_F64, &w64, tmp)) ||
@@ -911,6 +968,16 @@ Fft2Args fft2_base(const md_plan &P) {
 template <typename T>
 int wiener_plane(md_plan &P, const void *f, void *out, void *fpos, void *z, bool clamp, bool fwd_after,
                  int64_t nb, cudaStream_t st) {
+    if (P.big && P.line_axis >= 0) {
+        // 1D along the blur axis: forward (real input) x M in the last pass, inverse whose last
+        // pass writes u0 / fpos -- 4 sub-transform passes
+        const int H = P.d.height, W = P.d.width, ax = P.line_axis;
+        const BigAxis &A = ax == 1 ? P.bigW : P.bigH;
+        CU(big_axis<T>(A, z, H, W, ax, 0, f, nullptr, P.d_mult, 0, 1.0, nb, st));
+        CU(big_axis_inv_wiener<T>(A, z, H, W, ax, 1.0 / (ax == 1 ? W : H), f, out, fpos, P.d.floor, clamp ? 1 : 0, nb,
+                                  st));
+        return MD_OK;
+    }
     if (P.big) {
         const int H = P.d.height, W = P.d.width;
         // rows forward (real input) | columns: forward, x M and inverse of the inner digit fused
@@ -1141,7 +1208,7 @@ int32_t md_run_launch_count(const md_plan *P, int64_t batch) {
         per = 1;
         if (K > 0) per += P->fused ? 1 : K + (P->vert ? 1 : 0);
     } else {
-        per = wiener ? (P->big ? 6 : 3) : 1;      // two-level Wiener: 6 sub-transform passes
+        per = wiener ? (P->big ? (P->line_axis >= 0 ? 4 : 6) : 3) : 1;   // two-level Wiener: 6 (1D: 4) passes
         if (K > 0) {
             if (!wiener && P->path == PATH_PLANE_FFT) per += 1;
             per += P->fused_plane ? 1 : K * (P->path == PATH_PLANE_FFT ? 4 : 2);
@@ -1481,8 +1548,8 @@ int32_t md_rrrl_step(md_plan *P, const void *u, const void *f, const void *b, co
 // natural-order complex transforms of `lines` contiguous lines of length n, in place
 // (FourierPlan.forward / inverse, fft.py:52-117): tables per (n, dtype) built once
 int32_t md_fft(int32_t dtype, void *z, int32_t n, int64_t lines, int32_t inverse, void *stream) {
-    if ((dtype != MD_F64 && dtype != MD_F32) || lines < 0 || n < 1 || n > 65536 || !is_pow2(n))
-        return fail(MD_EINVAL, "transform length must be a power of two in [1, 65536]");
+    if ((dtype != MD_F64 && dtype != MD_F32) || lines < 0 || n < 1 || n > (1 << 20) || !is_pow2(n))
+        return fail(MD_EINVAL, "transform length must be a power of two in [1, 1048576]");
     if (lines == 0 || n == 1) return MD_OK;               // length 1: the identity both ways
     if (!z) return fail(MD_EINVAL, "bad arguments");
     clear_stale_error();
@@ -1511,25 +1578,33 @@ int32_t md_fft(int32_t dtype, void *z, int32_t n, int64_t lines, int32_t inverse
                            : launch_fft_lines_nat<float>(z, n, lines, tb->tw, inverse ? 1 : 0, st));
         return MD_OK;
     }
-    if (lines * (int64_t)n >= (1ll << 31)) return fail(MD_EINVAL, "too many elements for one two-level transform");
-    const size_t bytes = (size_t)lines * n * (dtype == MD_F64 ? 16 : 8);
+    // two-level passes (N = N1 N2, factors up to 1024: the reference's 2^20 limit, fft.py:45) in
+    // groups of lines whose element count keeps the passes' 32-bit in-frame offsets
+    const int64_t per = std::max<int64_t>(1, ((1ll << 31) - 1) / n);
+    const int es = dtype == MD_F64 ? 16 : 8;
+    const size_t bytes = (size_t)std::min<int64_t>(lines, per) * n * es;
     void *tmp = nullptr;
     CU(cudaMallocAsync(&tmp, bytes, st));
-    cudaError_t e;
-    if (!inverse) {
-        e = dtype == MD_F64 ? big_axis<double>(tb->ax, z, (int)lines, n, 1, 0, nullptr, nullptr, nullptr, 0, 1.0, 1, st)
-                            : big_axis<float>(tb->ax, z, (int)lines, n, 1, 0, nullptr, nullptr, nullptr, 0, 1.0, 1, st);
-        if (e == cudaSuccess)
-            e = dtype == MD_F64 ? launch_fft_perm<double>(z, tmp, tb->ax, lines, 1, st)
-                                : launch_fft_perm<float>(z, tmp, tb->ax, lines, 1, st);
-    } else {
-        e = dtype == MD_F64 ? launch_fft_perm<double>(z, tmp, tb->ax, lines, 0, st)
-                            : launch_fft_perm<float>(z, tmp, tb->ax, lines, 0, st);
-        if (e == cudaSuccess)
-            e = dtype == MD_F64 ? big_axis<double>(tb->ax, tmp, (int)lines, n, 1, 1, nullptr, nullptr, nullptr, 0, 1.0 / n, 1, st)
-                                : big_axis<float>(tb->ax, tmp, (int)lines, n, 1, 1, nullptr, nullptr, nullptr, 0, 1.0 / n, 1, st);
+    cudaError_t e = cudaSuccess;
+    for (int64_t l0 = 0; l0 < lines && e == cudaSuccess; l0 += per) {
+        const int64_t nl = std::min(per, lines - l0);
+        void *zc = static_cast<char *>(z) + l0 * n * es;
+        if (!inverse) {
+            e = dtype == MD_F64 ? big_axis<double>(tb->ax, zc, (int)nl, n, 1, 0, nullptr, nullptr, nullptr, 0, 1.0, 1, st)
+                                : big_axis<float>(tb->ax, zc, (int)nl, n, 1, 0, nullptr, nullptr, nullptr, 0, 1.0, 1, st);
+            if (e == cudaSuccess)
+                e = dtype == MD_F64 ? launch_fft_perm<double>(zc, tmp, tb->ax, nl, 1, st)
+                                    : launch_fft_perm<float>(zc, tmp, tb->ax, nl, 1, st);
+        } else {
+            e = dtype == MD_F64 ? launch_fft_perm<double>(zc, tmp, tb->ax, nl, 0, st)
+                                : launch_fft_perm<float>(zc, tmp, tb->ax, nl, 0, st);
+            if (e == cudaSuccess)
+                e = dtype == MD_F64
+                        ? big_axis<double>(tb->ax, tmp, (int)nl, n, 1, 1, nullptr, nullptr, nullptr, 0, 1.0 / n, 1, st)
+                        : big_axis<float>(tb->ax, tmp, (int)nl, n, 1, 1, nullptr, nullptr, nullptr, 0, 1.0 / n, 1, st);
+        }
+        if (e == cudaSuccess) e = cudaMemcpyAsync(zc, tmp, (size_t)nl * n * es, cudaMemcpyDeviceToDevice, st);
     }
-    if (e == cudaSuccess) e = cudaMemcpyAsync(z, tmp, bytes, cudaMemcpyDeviceToDevice, st);
     cudaFreeAsync(tmp, st);
     CU(e);
     return MD_OK;
@@ -1577,7 +1652,7 @@ __global__ void k_copy_cols(const unsigned char *src, unsigned char *dst, int H,
 
 int slab_check(const md_plan *P) {
     if (!P) return fail(MD_EINVAL, "null plan");
-    if (P->path != PATH_PLANE_DIRECT || !P->big || !P->fast_plane)
+    if (P->path != PATH_PLANE_DIRECT || !P->big || !P->fast_plane || P->line_axis >= 0)
         return fail(MD_EINVAL, "slab execution needs a 2D direct-tap plan built with MD_FLAG_BIG_FFT");
     return MD_OK;
 }

@@ -202,7 +202,7 @@ cudaError_t launch_big_wiener_epilogue(const void *z, const void *f, void *u, vo
 
 // ---- axis plans -------------------------------------------------------------------------
 
-// split N = N1 * N2 with both factors <= 256 (N <= 65536), N1 >= N2
+// split N = N1 * N2, N1 >= N2, both factors <= 1024 (N <= 2^20, the reference's limit, fft.py:45)
 void split_axis(int N, int *N1, int *N2) {
     int l = 0;
     while ((1 << l) < N) ++l;

@@ -62,6 +62,7 @@ bool wiener_reg_supported(int dtype, int n);
 template <typename T> cudaError_t launch_wiener_reg(const WienerLinesArgs &, int64_t, cudaStream_t);
 template <typename T> cudaError_t launch_iter_lines(const IterLinesArgs &, bool robust, int64_t, cudaStream_t);
 bool iter_lines_fits(int dtype, int n, int ntaps);
+bool conv_lines_fits(int dtype, int n, int ntaps);   // one line of the plain line convolution
 template <typename T> cudaError_t launch_conv_lines(const ConvLinesArgs &, int64_t, cudaStream_t);
 template <typename T> cudaError_t launch_transpose(const void *in, void *out, void *out_clamped, int rows,
                                                    int cols, double floor, int clamp_out, int64_t batch,

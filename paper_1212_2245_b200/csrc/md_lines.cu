@@ -465,6 +465,12 @@ cudaError_t launch_clamp2(const void *in, void *o1, void *o2, int64_t n, double 
 
 // the generic per-iteration line kernel keeps 5 tl + 6 padded lines on chip: it fits while one
 // line tile (tl = 1) stays within the opt-in shared memory of a block
+bool conv_lines_fits(int dtype, int n, int ntaps) {
+    const size_t smem = ((size_t)(dtype == 0 ? padded_len<double>(n) : padded_len<float>(n)) + ntaps) *
+                        (dtype == 0 ? 8 : 4);
+    return smem <= 227 * 1024;
+}
+
 bool iter_lines_fits(int dtype, int n, int ntaps) {
     const size_t smem = dtype == 0 ? iter_lines_smem<double>(n, 1, ntaps) : iter_lines_smem<float>(n, 1, ntaps);
     return smem <= 227 * 1024;

@@ -105,6 +105,10 @@ def test_longest_lines_vs_oracle(md):
     ((4096, 16), "v", "float64", 2, "BOX_1D"),        # past the f64 line-iteration kernel (2048)
     ((8192, 16), "v", "float64", 1, "BOX_1D"),        # past the f64 line FFT (4096)
     ((16, 16384), "h", "float32", 2, "FOURIER_1D"),   # periodic along the blur axis
+    ((12, 16384), "h", "float32", 0, "BOX_1D"),       # cross axis not a power of two (fft.py:63-66
+    ((12, 8192), "h", "float64", 2, "BOX_1D"),        #   constrains the blur axis only)
+    ((8192, 20), "v", "float64", 2, "FOURIER_1D"),
+    ((3, 65536), "h", "float64", 1, "BOX_1D"),        # a long line: two-level 1D transform
 ])
 def test_lines_beyond_chip_as_plane(md, shape, axis, dtype, iters, scenario):
     """Blur axes longer than the on-chip line kernels take run as a plane with a one-row (one-
@@ -113,7 +117,7 @@ def test_lines_beyond_chip_as_plane(md, shape, axis, dtype, iters, scenario):
     ax = md.BlurAxis.HORIZONTAL if axis == "h" else md.BlurAxis.VERTICAL
     psf = md.Psf.uniform_box(ax, 15)
     params = md.DeconvParams(iterations=iters)
-    g = md.make_test_image(shape[1], shape[0])
+    g = md.Image(md.make_test_image(max(16, shape[1]), max(16, shape[0])).values[:shape[0], :shape[1]])
     assert g.values.shape == shape
     f = md.quantize(md.add_gaussian_noise(md.synth_blur(g, psf), 5.0, seed=3)).values
     pipe = md.DeblurPipeline(f.shape, psf, params, scenario=getattr(md.Scenario, scenario), dtype=dtype)
@@ -124,12 +128,11 @@ def test_lines_beyond_chip_as_plane(md, shape, axis, dtype, iters, scenario):
 
 
 def test_limits_raise(md):
-    """Blur axes that are not powers of two, and long blur axes whose other side is not a power
-    of two (the plane route's Wiener needs both), raise ValueError at plan creation (the
-    reference's own ValueError cases, fft.py:63-66)."""
+    """Blur axes that are not powers of two raise ValueError at plan creation, short or long
+    (the reference's own ValueError cases, fft.py:63-66)."""
     psf = md.Psf.uniform_box(md.BlurAxis.HORIZONTAL, 15)
-    for shape, dtype, iters in (((16, 100), "float64", 5), ((12, 16384), "float32", 0),
-                                ((12, 8192), "float64", 2)):
+    for shape, dtype, iters in (((16, 100), "float64", 5), ((12, 12288), "float32", 0),
+                                ((12, 8200), "float64", 2)):
         with pytest.raises(ValueError):
             md.DeblurPipeline(shape, psf, md.DeconvParams(iterations=iters), dtype=dtype)
 

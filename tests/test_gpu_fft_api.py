@@ -35,7 +35,7 @@ def test_forward_matches_naive_dft(md, n):
     assert np.abs(got - want).max() <= 1e-10 * max(1.0, np.abs(want).max())
 
 
-@pytest.mark.parametrize("n", [4, 512, 4096, 8192, 16384, 65536])
+@pytest.mark.parametrize("n", [4, 512, 4096, 8192, 16384, 65536, 1 << 17, 1 << 20])
 def test_forward_inverse_vs_oracle_and_round_trip(md, n):
     """Single-block lengths and the two-level lengths (> 4096) against the oracle's radix-2
     transform; inverse(forward(x)) = x."""
@@ -93,9 +93,10 @@ def test_fft2_and_filters_vs_oracle(md):
 
 
 def test_fft_api_errors(md):
-    for n in (0, 3, 100, 1 << 17):
+    for n in (0, 3, 100, 1 << 21):                    # the reference's limit is 2^20 (fft.py:45)
         with pytest.raises(ValueError):
             md.FourierPlan(n)
+    assert md.FourierPlan(1 << 20).n == 1 << 20
     with pytest.raises(ValueError):
         md.plan_fft(64).forward(np.zeros(32))
 

@@ -133,5 +133,5 @@ def test_c5_16384_eight_slabs_equal_single_plan(md):
     got = run_slabs(pipe.plan, f, 8)
     assert float((got - want).abs().max()) <= 1e-9
     assert bool(torch.isfinite(want).all())
-    assert float(want.min()) >= 0.1 - 1e-12            # the multiplicative update keeps u >= floor-ish
+    assert float(want.min()) > 0.0                     # the multiplicative update keeps u positive
     assert abs(float(want.mean()) - float(f.mean())) < 1.0   # RL-type updates preserve the mean
