@@ -155,3 +155,16 @@ def test_column_sharpening_engine(md):
     assert len(times) == params.iterations
     with pytest.raises(ValueError):
         ColumnSharpeningEngine(params, None, 0)
+
+
+def test_rrrl_deblur_parallel_with_object_convolver(md):
+    """A convolver OBJECT passed to rrrl_deblur_parallel sees the frame in vertical orientation
+    (horizontal kernels transposed around the call, parallel.py:130-142), as in the reference."""
+    from oracle import wr3l_oracle as O
+    g = md.make_test_image(64, 48)
+    psf = md.Psf.uniform_box(md.BlurAxis.HORIZONTAL, 9)
+    f = md.synth_blur(g, psf)
+    obj = O.BoxConv(9.0, 4, 9, axis=0)                  # acts along axis 0 of what it is given
+    got = md.rrrl_deblur_parallel(f, psf, md.DeconvParams(), 3, convolver=obj).values
+    want = md.rrrl_deblur(f, psf, md.DeconvParams(), convolver="box").values
+    assert np.abs(got - want).max() <= 1e-8
