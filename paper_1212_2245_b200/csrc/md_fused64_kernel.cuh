@@ -67,6 +67,23 @@ __device__ __forceinline__ void st_async_f64x2(uint32_t raddr, double x, double 
                  : "memory");
 }
 
+// 1D bulk copy (TMA) global -> this CTA's shared memory, completing `bytes` on `bar`
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+
+// MD_F64_FPOS_TMA=1: the observation line of the next line slot is staged through shared memory
+// by the TMA engine (one 2 KB bulk copy per line, per-warp buffer and mbarrier) instead of
+// per-lane L2 loads. Measured SLOWER on c1 (iterations 21.8 vs 19.0 ms per 4096 frames): the
+// 32 KB of buffers push the CTA's shared memory from 182 to 214 KB, the carveout from 196 to
+// 228 KB, and the L1 left for the divergence-table reads from 60 to 28 KB. Off by default.
+#ifndef MD_F64_FPOS_TMA
+#define MD_F64_FPOS_TMA 0
+#endif
+constexpr int F64_OBS_LINE = 256;                 // doubles per warp buffer (n <= 256)
+
 // r1 with the (value, step) pair table (md_common.cuh rules, deconv.py:114-134): the table
 // interpolation and the linear continuation above `upper`; the direct formula below
 // `direct_below` is the caller's (taken per warp, see k_fused_lines64)
@@ -138,7 +155,10 @@ k_fused_lines64(FusedKArgs<double, R> a, const double2 *__restrict__ lut64) {
     T *own = sm;
     auto halo = [&](int par, int side) { return sm + (RLMAX + 4 * par + 2 * side) * ls; };
     T *sg = sm + (RLMAX + 8) * ls;
-    uint64_t *mbar = reinterpret_cast<uint64_t *>(sm + (2 * RLMAX + 10) * ls);
+    T *obs_all = sm + (2 * RLMAX + 10) * ls;       // [NW][F64_OBS_LINE] observation lines (TMA)
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(obs_all + (MD_F64_FPOS_TMA ? NW * F64_OBS_LINE : 0));
+    T *obs = obs_all + warp * F64_OBS_LINE;
+    uint64_t *obar = mbar + 2 + warp;             // this warp's observation barrier
     auto line_ptr = [&](int l, int par) -> const T * {
         if (l < 0) return halo(par, 0) + (l + 2) * ls;
         if (l >= RL) return halo(par, 1) + (l - RL) * ls;
@@ -150,12 +170,25 @@ k_fused_lines64(FusedKArgs<double, R> a, const double2 *__restrict__ lut64) {
     if (threadIdx.x == 0) {
         mb_init(smem_addr(&mbar[0]), 1);
         mb_init(smem_addr(&mbar[1]), 1);
+        if (MD_F64_FPOS_TMA)
+            for (int w = 0; w < NW; ++w) mb_init(smem_addr(&mbar[2 + w]), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         mb_arm(smem_addr(&mbar[0]), expect);
         mb_arm(smem_addr(&mbar[1]), expect);
     }
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     cluster.sync();                                  // all CTAs resident, barriers initialised
+    const uint32_t obs_bytes = (uint32_t)n * 8u;
+    uint32_t ophase = 0;
+    // observation of line slot `li` into this warp's buffer (lane 0)
+    auto fetch_obs = [&](int li) {
+        if (MD_F64_FPOS_TMA && lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mb_arm(smem_addr(obar), obs_bytes);
+            bulk_g2s(smem_addr(obs), fpos + (int64_t)(gl0 + li) * n, obs_bytes, smem_addr(obar));
+        }
+    };
+    if (a.iterations > 0) fetch_obs(min(warp, RL - 1));
     // neighbour targets: my lines 0, 1 -> top neighbour's bottom halo; RL-2, RL-1 -> bottom
     // neighbour's top halo (same parity)
     // parity 0 addresses in the neighbours (parity 1 = + 4 lines, barrier + 8 bytes)
@@ -249,15 +282,25 @@ k_fused_lines64(FusedKArgs<double, R> a, const double2 *__restrict__ lut64) {
             const int gl = gl0 + li;
             const bool up_ok = gl > 0, dn_ok = gl + 1 < m;
             const T *U = own + li * ls;
-            const T *F = fpos + (int64_t)gl * n;
             const int s = lane < nseg ? lane : nseg - 1;     // idle lanes shadow the last segment
             const int off = base0 + 9 * s;
-            {
-                const int ln = j + 1 < LPW ? min(li + NW, RL - 1) : warp;
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(fpos + (int64_t)(gl0 + ln) * n + SEG * s));
-            }
+            const int ln = j + 1 < LPW ? min(warp + NW * (j + 1), RL - 1) : min(warp, RL - 1);
             T fv[SEG];
-            {
+            if (MD_F64_FPOS_TMA) {
+                mb_wait(smem_addr(obar), ophase);
+                ophase ^= 1u;
+                const double2 *f2 = reinterpret_cast<const double2 *>(obs + SEG * s);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const double2 x = f2[i];
+                    fv[2 * i] = x.x;
+                    fv[2 * i + 1] = x.y;
+                }
+                __syncwarp();
+                if (!(last && j == LPW - 1)) fetch_obs(ln);   // the next slot's line, in flight meanwhile
+            } else {
+                const T *F = fpos + (int64_t)gl * n;
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(fpos + (int64_t)(gl0 + ln) * n + SEG * s));
                 const double2 *f2 = reinterpret_cast<const double2 *>(F + SEG * s);
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
@@ -406,7 +449,8 @@ template <int R, int NW, int LPW>
 size_t fused64_smem(int n) {
     constexpr int HW = HaloOf<R>::value;
     const int ls = (xline_len(n, HW) + 1) & ~1;
-    return (size_t)(2 * NW * LPW + 10) * ls * sizeof(double) + 2 * sizeof(uint64_t);
+    return (size_t)(2 * NW * LPW + 10) * ls * sizeof(double) +
+           (MD_F64_FPOS_TMA ? (size_t)NW * F64_OBS_LINE * sizeof(double) : 0) + (2 + NW) * sizeof(uint64_t);
 }
 
 // host: the cluster size for m lines -- every CTA holds at most `rlmax` lines and at least 4, one

@@ -22,7 +22,10 @@ hi = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
 h = rows[hi]
 si = h.index("Warp Stall Sampling (All Samples)")
 ie = h.index("Instructions Executed")
-sass = [(int(r[0], 16), float(r[si] or 0), float(r[ie] or 0), r[1].strip()) for r in rows[hi + 1:] if len(r) > si]
+reasons = [c for c in h if c.startswith("stall_") and not c.endswith("(Not Issued)")]
+ri = [h.index(c) for c in reasons]
+sass = [(int(r[0], 16), float(r[si] or 0), float(r[ie] or 0), r[1].strip(),
+         [float(r[i] or 0) for i in ri]) for r in rows[hi + 1:] if len(r) > si]
 base = sass[0][0]
 dis = subprocess.run(["nvdisasm", "--print-line-info", cubin], capture_output=True, text=True).stdout
 line_of = {}
@@ -41,12 +44,22 @@ for ln in dis.splitlines():
     m = re.match(r"\s+/\*([0-9a-f]{4,})\*/\s+(\S.*)", ln)
     if m and cur:
         line_of[int(m.group(1), 16)] = cur
-agg = collections.defaultdict(lambda: [0.0, 0.0])
+agg = collections.defaultdict(lambda: [0.0, 0.0, [0.0] * len(reasons)])
 tot = 0.0
-for addr, s, n, _ in sass:
+overall = [0.0] * len(reasons)
+for addr, s, n, _, rs in sass:
     k = line_of.get(addr - base, "?")
     agg[k][0] += s
     agg[k][1] += n
+    for j, v in enumerate(rs):
+        agg[k][2][j] += v
+        overall[j] += v
     tot += s
-for k, (s, n) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
-    print(f"{100 * s / tot:5.1f}%  {n / 1e6:8.2f}M inst  {k}")
+ts = sum(overall) or 1.0
+print("overall:", ", ".join(f"{reasons[j][6:]} {100 * overall[j] / ts:.1f}%"
+                            for j in sorted(range(len(reasons)), key=lambda j: -overall[j])[:8]))
+print(f"total {sum(a[1] for a in agg.values()) / 1e6:.1f}M warp instructions")
+for k, (s, n, rs) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
+    top3 = sorted(range(len(reasons)), key=lambda j: -rs[j])[:3]
+    why = ", ".join(f"{reasons[j][6:]} {100 * rs[j] / max(s, 1):.0f}%" for j in top3)
+    print(f"{100 * s / tot:5.1f}%  {n / 1e6:8.2f}M inst  {k:32s} [{why}]")
