@@ -604,12 +604,11 @@ int32_t md_plan_create(const md_plan_desc *desc, md_plan **out) {
             CU(cudaDeviceSynchronize());
             P->wiener_reg = !(desc->flags & MD_FLAG_GENERIC_LINES) && wiener_reg_supported(desc->dtype, P->n);
         }
-        // default: the cluster kernel -- float, and float64 for line radii <= 8 (the
-        // shuffle-window / st.async-halo kernel, md_fused64_kernel.cuh, two CTAs per SM);
-        // wider float64 kernels keep the per-iteration kernel (the generic cluster kernel runs
-        // 16-CTA clusters at one CTA per SM and loses to it), opt-in via md_plan_set_fused
+        // default: the cluster kernel -- float, and float64 for line radii <= 16 (the
+        // shuffle-window / st.async-halo kernel, md_fused64_kernel.cuh); wider float64 kernels
+        // keep the per-iteration kernel, opt-in via md_plan_set_fused
         const int lrad = std::max(line_radius(P->lblur), line_radius(P->ladj));
-        P->fused = (desc->dtype == MD_F32 || lrad <= 8) && P->fast_lines &&
+        P->fused = (desc->dtype == MD_F32 || lrad <= 16) && P->fast_lines &&
                    fused_lines_supported(desc->dtype, P->n, P->m, desc->flags, lrad);
         if (P->fused)
             P->fused_clusters = desc->dtype == MD_F32 ? lines_fused_clusters<float>(*P) : lines_fused_clusters<double>(*P);

@@ -13,8 +13,8 @@ int fused_lpw(int dtype, int radius) { return dtype == 0 ? 2 : (radius > 8 ? 2 :
 bool fused_lines_supported(int dtype, int n, int m, unsigned flags, int radius) {
     if (flags & 2u) return false;                  // MD_FLAG_NO_FUSED
     if (n % SEG != 0 || n / SEG > 32 || n < 64) return false;
-    // float64, radius <= 8: any line count the cluster can hold (2..16 CTAs of 4..rows lines)
-    if (dtype == 0 && radius <= 8) return m >= 8 && (m + 15) / 16 <= fused64_rows();
+    // float64, radius <= 16: any line count the cluster can hold (2..16 CTAs of 4..rows lines)
+    if (dtype == 0 && radius <= 16) return m >= 8 && (m + 15) / 16 <= fused64_rows();
     const int rl = FU_WARPS * fused_lpw(dtype, radius);
     if (m % rl != 0) return false;
     const int cl = m / rl;
@@ -24,7 +24,7 @@ bool fused_lines_supported(int dtype, int n, int m, unsigned flags, int radius) 
 template <typename T>
 cudaError_t launch_fused_lines(const FusedLinesArgs &d, int64_t batch, cudaStream_t st) {
     const int r = std::max(line_radius(d.blur), line_radius(d.adj));
-    if (sizeof(T) == 8 && r <= 8) return launch_fused64(d, batch, st);
+    if (sizeof(T) == 8 && r <= 16) return launch_fused64(d, batch, st);
     // boxes (odd, even, fractional length): O(1) sliding sum + end corrections
     if (d.blur.kind == LINE_BOX && d.adj.kind == LINE_BOX && r >= 1 && r <= 15 && d.robust) {
         const cudaError_t e = launch_fused_box<T>(d, r, batch, st);

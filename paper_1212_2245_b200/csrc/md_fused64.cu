@@ -1,5 +1,6 @@
 // md_fused64.cu -- host dispatch of the float64 cluster-resident iteration kernel
-// (md_fused64_kernel.cuh): box radii 1..8 (sliding sums) and dense line taps up to radius 8.
+// (md_fused64_kernel.cuh): box radii 1..16 (sliding sums; 9..16 in md_fused64_b.cu) and dense
+// line taps up to radius 16.
 
 #include "md_fused64_kernel.cuh"
 
@@ -7,9 +8,11 @@ namespace md {
 
 int fused64_rows() { return F64_NW * F64_LPW; }
 
+cudaError_t launch_fused64_box_hi(const FusedLinesArgs &d, int radius, int64_t batch, cudaStream_t st);
+
 cudaError_t launch_fused64(const FusedLinesArgs &d, int64_t batch, cudaStream_t st) {
     const int r = std::max(line_radius(d.blur), line_radius(d.adj));
-    if (r > 8 || !d.lut.p64) return cudaErrorNotSupported;
+    if (r > 16 || !d.lut.p64) return cudaErrorNotSupported;
     if (d.blur.kind == LINE_BOX && d.adj.kind == LINE_BOX && r >= 1 && d.robust) {
         cudaError_t e = cudaErrorNotSupported;
         switch (r) {
@@ -21,7 +24,7 @@ cudaError_t launch_fused64(const FusedLinesArgs &d, int64_t batch, cudaStream_t 
             case 6: e = launch_fused64_box_r<6>(d, batch, st); break;
             case 7: e = launch_fused64_box_r<7>(d, batch, st); break;
             case 8: e = launch_fused64_box_r<8>(d, batch, st); break;
-            default: break;
+            default: e = launch_fused64_box_hi(d, r, batch, st); break;
         }
         if (e != cudaErrorNotSupported) return e;
     }
@@ -44,7 +47,8 @@ cudaError_t launch_fused64(const FusedLinesArgs &d, int64_t batch, cudaStream_t 
                                                      a, d.lut.p64, batch, st);
     };
     if (r <= 4) return go(std::integral_constant<int, 4>{});
-    return go(std::integral_constant<int, 8>{});
+    if (r <= 8) return go(std::integral_constant<int, 8>{});
+    return go(std::integral_constant<int, 16>{});
 }
 
 }  // namespace md

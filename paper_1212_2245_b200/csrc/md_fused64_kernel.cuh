@@ -99,28 +99,49 @@ __device__ __forceinline__ double r1_table64(const double2 *__restrict__ p64, do
     return r;
 }
 
-// the window [-R, SEG + R) of a lane's 8 samples, the outer 2R taken from the neighbour lanes
-// (lanes >= nseg idle); clamped line ends replicate the end sample, periodic ones wrap
+// the window [-R, SEG + R) of a lane's 8 samples, the outer 2R taken from the lanes one or two
+// segments away (R <= 16; lanes >= nseg idle); clamped line ends replicate the end sample,
+// periodic ones wrap
 template <int R>
 __device__ __forceinline__ void lane_window(const double (&x)[SEG], double (&w)[SEG + 2 * R], int lane, int nseg,
                                             bool periodic) {
-    static_assert(R <= SEG, "neighbour-lane windows need R <= 8");
-    const int src_l = lane == 0 ? nseg - 1 : lane - 1;
-    const int src_r = lane >= nseg - 1 ? 0 : lane + 1;
+    static_assert(R <= 2 * SEG, "neighbour-lane windows need R <= 16");
+    auto src = [&](int d) {                       // lane d segments away, wrapped over the line
+        int t = lane + d;
+        t = t < 0 ? t + nseg : (t >= nseg ? t - nseg : t);
+        return t;
+    };
+    const int l1 = src(-1), r1 = src(1);
+    const int l2 = R > SEG ? src(-2) : l1, r2 = R > SEG ? src(2) : r1;
 #pragma unroll
     for (int k = 0; k < SEG; ++k) w[R + k] = x[k];
 #pragma unroll
     for (int k = 0; k < R; ++k) {
-        w[k] = __shfl_sync(0xffffffffu, x[SEG - R + k], src_l);
-        w[R + SEG + k] = __shfl_sync(0xffffffffu, x[k], src_r);
+        const int pl = k - R;                     // left position relative to the segment start
+        const int el = pl + (pl < -SEG ? 2 * SEG : SEG);
+        w[k] = __shfl_sync(0xffffffffu, x[el], pl < -SEG ? l2 : l1);
+        const int pr = SEG + k;                   // right position
+        const int er = pr - (pr >= 2 * SEG ? 2 * SEG : SEG);
+        w[R + SEG + k] = __shfl_sync(0xffffffffu, x[er], pr >= 2 * SEG ? r2 : r1);
     }
     if (!periodic) {
-        if (lane == 0)
+        if constexpr (R <= SEG) {                 // only the end lanes reach past the line
+            if (lane == 0)
 #pragma unroll
-            for (int k = 0; k < R; ++k) w[k] = x[0];
-        if (lane == nseg - 1)
+                for (int k = 0; k < R; ++k) w[k] = x[0];
+            if (lane == nseg - 1)
 #pragma unroll
-            for (int k = 0; k < R; ++k) w[R + SEG + k] = x[SEG - 1];
+                for (int k = 0; k < R; ++k) w[R + SEG + k] = x[SEG - 1];
+        } else {                                  // two lanes at each end do
+            const double first = __shfl_sync(0xffffffffu, x[0], 0);
+            const double last = __shfl_sync(0xffffffffu, x[SEG - 1], nseg - 1);
+            const int g0 = SEG * lane;            // line position of the segment start
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+                if (g0 + k - R < 0) w[k] = first;
+                if (g0 + SEG + k >= SEG * nseg) w[R + SEG + k] = last;
+            }
+        }
     }
 }
 

@@ -1,4 +1,5 @@
-"""c4 bank: device time per PSF class (all 48 PSFs, the bench's own frames per group), float32."""
+"""c4 bank: device time per PSF class (all 48 PSFs, the bench's own frames per group).
+usage: python scripts/c4_breakdown.py [float32|float64]"""
 import os, sys, types
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import collections
@@ -6,8 +7,10 @@ import torch
 import paper_1212_2245_b200 as md
 from bench import C4
 
-work = C4(md, types.SimpleNamespace(dtype="float32", batch=16384))
-f_all = torch.from_numpy(work.host).cuda().float()
+from bench import gpu_synth
+dt = sys.argv[1] if len(sys.argv) > 1 else "float32"
+work = C4(md, types.SimpleNamespace(dtype=dt, batch=16384), gpu_synth(md))
+f_all = torch.from_numpy(work.host).cuda().to(torch.float32 if dt == "float32" else torch.float64)
 tot = collections.defaultdict(float)
 cnt = collections.Counter()
 for b, s, e in work.pipe.groups(work.index):
