@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <cstdio>
 #include <stdint.h>
 
 #include <map>
@@ -11,6 +12,42 @@
 #include <utility>
 
 namespace md {
+
+// ---- checked build (-DMD_CHECKED; scripts/build_checked.sh): device-side bounds and protocol
+// assertions in the cluster kernels plus NaN-poisoned shared memory, the substitute for
+// compute-sanitizer (closed on this pool). Compiled out of the production library.
+#ifdef MD_CHECKED
+#define MD_CHECK(cond)                                                                                  \
+    do {                                                                                                \
+        if (!(cond)) {                                                                                  \
+            printf("MD_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__,          \
+                   (int)blockIdx.x, (int)threadIdx.x);                                                  \
+            __trap();                                                                                   \
+        }                                                                                               \
+    } while (0)
+#else
+#define MD_CHECK(cond) \
+    do {               \
+    } while (0)
+#endif
+
+// bytes of dynamic shared memory this launch has (PTX %dynamic_smem_size)
+__device__ __forceinline__ uint32_t dyn_smem_bytes() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(r));
+    return r;
+}
+// checked build: fill this CTA's dynamic shared memory with NaN bytes before first use, so a
+// read of a never-written element that reaches a result turns the result into NaN
+__device__ __forceinline__ void poison_smem(unsigned char *smem) {
+#ifdef MD_CHECKED
+    const uint32_t n = dyn_smem_bytes();
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) smem[i] = 0xff;
+    __syncthreads();
+#else
+    (void)smem;
+#endif
+}
 
 // host: raise a kernel's dynamic shared-memory limit (and allow non-portable cluster sizes)
 // once per (kernel, device), not on every launch -- cudaFuncSetAttribute costs microseconds,

@@ -45,7 +45,13 @@ __device__ __forceinline__ void mb_arm(uint32_t bar, uint32_t bytes) {
 }
 __device__ __forceinline__ void mb_wait(uint32_t bar, uint32_t parity) {
     uint32_t done;
+#ifdef MD_CHECKED
+    long long spins = 0;
+#endif
     do {
+#ifdef MD_CHECKED
+        MD_CHECK(++spins < (1ll << 28));          // a lost arrival / byte count would hang here
+#endif
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
             "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
@@ -180,7 +186,11 @@ k_fused_lines64(FusedKArgs<double, R> a, const double2 *__restrict__ lut64) {
     uint64_t *mbar = reinterpret_cast<uint64_t *>(obs_all + (MD_F64_FPOS_TMA ? NW * F64_OBS_LINE : 0));
     T *obs = obs_all + warp * F64_OBS_LINE;
     uint64_t *obar = mbar + 2 + warp;             // this warp's observation barrier
+    poison_smem(smem_raw);
+    MD_CHECK(n % SEG == 0 && nseg <= 32 && RL >= 4 && RL <= RLMAX && CL >= 2 && CL <= 16);
+    MD_CHECK((size_t)(2 * RLMAX + 10) * ls * sizeof(T) + 2 * sizeof(uint64_t) <= dyn_smem_bytes());
     auto line_ptr = [&](int l, int par) -> const T * {
+        MD_CHECK(l >= -2 && l <= RL + 1 && (par == 0 || par == 1));
         if (l < 0) return halo(par, 0) + (l + 2) * ls;
         if (l >= RL) return halo(par, 1) + (l - RL) * ls;
         return own + l * ls;
@@ -230,6 +240,7 @@ k_fused_lines64(FusedKArgs<double, R> a, const double2 *__restrict__ lut64) {
         } else {
             return;
         }
+        MD_CHECK(li >= 0 && li < RL && (par == 0 || par == 1) && (ls & 1) == 0);
         for (int q = 2 * lane; q < ls; q += 64) st_async_f64x2(dst + (uint32_t)q * 8u, L[q], L[q + 1], bar);
     };
 
@@ -262,6 +273,7 @@ k_fused_lines64(FusedKArgs<double, R> a, const double2 *__restrict__ lut64) {
                 T x[SEG + 2];
 #pragma unroll
                 for (int k = -1; k <= SEG; ++k) x[k + 1] = row[off + koff(k)];
+                MD_CHECK(l >= -1 && l <= RL);
                 T *G = sg + (l + 1) * ls + off;
 #pragma unroll
                 for (int r = 0; r < SEG; ++r) {

@@ -86,7 +86,11 @@ k_fused_lines(FusedKArgs<T, R> a) {
     T *sg = sm + (RL + 8) * ls;                      // RL+2 lines: logical -1..RL
     T *wp = sm + (2 * RL + 10 + 2 * warp) * ls;      // warp buffers: p, W
     T *ww = wp + ls;
+    poison_smem(smem_raw);
+    MD_CHECK(m == RL * CL && n % SEG == 0 && n / SEG <= 32);
+    MD_CHECK((size_t)(2 * RL + 10 + 2 * FU_WARPS) * ls * sizeof(T) <= dyn_smem_bytes());
     auto line_ptr = [&](int l, int par) -> T * {
+        MD_CHECK(l >= -2 && l <= RL + 1 && (par == 0 || par == 1));
         if (l < 0) return halo_top(par) + (l + 2) * ls;
         if (l >= RL) return halo_bot(par) + (l - RL) * ls;
         return own + l * ls;

@@ -136,8 +136,16 @@ k_fused_plane(FusedPlaneKArgs<T> a) {
     const T *fpos = a.fpos + frame * fsz;
     const FpLayout L = fp_layout(RL, rs, W, a.ut, a.ub, a.pt, a.pb);
     const int ut = a.ut, ub = a.ub, pt = a.pt, pb = a.pb;
-    auto urow = [&](T *base, int r) { return base + L.u + (r + ut) * rs; };
-    auto pwrow = [&](T *base, int r) { return reinterpret_cast<T2 *>(base + L.pw) + (r + pt) * rs; };
+    poison_smem(smem_raw);
+    MD_CHECK((size_t)L.total * sizeof(T) <= dyn_smem_bytes() && RL * CL == H && (RL & 1) == 0);
+    auto urow = [&](T *base, int r) {
+        MD_CHECK(r >= -ut && r < RL + ub);
+        return base + L.u + (r + ut) * rs;
+    };
+    auto pwrow = [&](T *base, int r) {
+        MD_CHECK(r >= -pt && r < RL + pb);
+        return reinterpret_cast<T2 *>(base + L.pw) + (r + pt) * rs;
+    };
     T *G = sm + L.g + rs;                    // row r at G + r * rs, r in [-1, RL]
     T *stash = sm + L.stash;                 // U rows -1 and RL, columns 0..W-1
 

@@ -16,8 +16,11 @@ constexpr int PT = 32;          // output tile edge
 constexpr int PTHREADS = 256;   // 32 x 8
 
 __device__ __forceinline__ int resolve2(int k, int n, int periodic) {
-    // halos never exceed the extent, so one conditional wrap suffices (no integer modulo)
-    if (periodic) return k < 0 ? k + n : (k >= n ? k - n : k);
+    // a tile plus halo may be larger than a small frame: a full wrap (see pf_resolve)
+    if (periodic) {
+        k %= n;
+        return k < 0 ? k + n : k;
+    }
     return k < 0 ? 0 : (k >= n ? n - 1 : k);
 }
 

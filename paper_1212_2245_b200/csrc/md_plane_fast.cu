@@ -21,8 +21,14 @@ constexpr int PJ = 4;                     // outputs per row per thread (column 
 constexpr int PS = 72;                    // u / g tile stride: 2 * PS = 16 (mod 32) -> half-warps on disjoint banks
 
 __device__ __forceinline__ int pf_resolve(int k, int n, int periodic) {
-    // halos never exceed the extent, so one conditional wrap suffices (no integer modulo)
-    if (periodic) return k < 0 ? k + n : (k >= n ? k - n : k);
+    // a tile (64 x 32 plus halos) may be wider / taller than a small frame, so positions can lie
+    // more than one extent outside: a full wrap (resolved once per tile column / row, not per
+    // element). Found by the checked build: a 32-wide frame read past its buffer with the
+    // single conditional wrap this replaced.
+    if (periodic) {
+        k %= n;
+        return k < 0 ? k + n : k;
+    }
     return k < 0 ? 0 : (k >= n ? n - 1 : k);
 }
 
@@ -46,6 +52,7 @@ __device__ void pf_load(E *s, int ss, int H, int W, int y0, int x0, const PlaneH
         // last tile row band may reach past the halo (rows_a is not a multiple of FY): those rows
         // only feed outputs that are not stored, so they read the nearest existing row
         const int y = y0 - h.ht + i;
+        MD_CHECK(!slab || ylo < yhi);
         return slab ? (y < ylo ? ylo : (y >= yhi ? yhi - 1 : y)) : pf_resolve(y, H, periodic);
     };
     for (int i = warp; i < rows; i += 2 * nw) {
