@@ -18,7 +18,15 @@ top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
 raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
-hi = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
+# one block per profiled kernel ("Kernel Name" row, then the "Address" header): take the block
+# whose name matches the kernel (mangled names contain the demangled base name)
+mm = re.match(r"^_ZN\d+md(\d+)", kern)
+want = kern[mm.end():mm.end() + int(mm.group(1))] if mm else kern       # e.g. k_fused_lines64
+starts = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"] or [0]
+blk = next((i for i in starts if want in " ".join(rows[i][1:])), starts[0])
+hi = next(i for i, r in enumerate(rows) if i >= blk and r and r[0] == "Address")
+end = next((i for i in starts if i > hi), len(rows))
+rows = rows[:end]
 h = rows[hi]
 si = h.index("Warp Stall Sampling (All Samples)")
 ie = h.index("Instructions Executed")
