@@ -28,7 +28,7 @@ import numpy as np
 
 from . import _lib as L
 
-__all__ = ["SlabGeometry", "DistComm", "LocalComm", "CudaSlabBackend", "SlabWorker", "run_slabs"]
+__all__ = ["SlabGeometry", "DistComm", "HostStagedComm", "LocalComm", "CudaSlabBackend", "SlabWorker", "run_slabs"]
 
 
 class SlabGeometry:
@@ -83,6 +83,32 @@ class DistComm:
     def barrier(self, rank):
         if self.world > 1:
             self.dist.barrier(self.group)
+
+
+class HostStagedComm:
+    """A DistComm over a backend that moves only host tensors (gloo): device buffers are
+    staged through host copies around each exchange. Lets several processes share ONE GPU
+    with a real process group -- the multi-process slab test (tests/test_gpu_slab_dist.py);
+    on 8 GPUs NCCL moves device memory directly (DistComm)."""
+
+    def __init__(self, comm: DistComm):
+        self.c = comm
+        self.rank, self.world = comm.rank, comm.world
+
+    def exchange(self, rank, send_up, send_down, recv_up, recv_down):
+        h = [t.detach().to("cpu").contiguous() for t in (send_up, send_down)]
+        r_up, r_down = recv_up.new_empty(recv_up.shape, device="cpu"), recv_down.new_empty(recv_down.shape, device="cpu")
+        self.c.exchange(rank, h[0], h[1], r_up, r_down)
+        recv_up.copy_(r_up)
+        recv_down.copy_(r_down)
+
+    def all_to_all(self, rank, recv, send):
+        r = recv.new_empty(recv.shape, device="cpu")
+        self.c.all_to_all(rank, r, send.detach().to("cpu").contiguous())
+        recv.copy_(r)
+
+    def barrier(self, rank):
+        self.c.barrier(rank)
 
 
 class LocalComm:
