@@ -174,7 +174,7 @@ cudaError_t launch_subfft(const SubFftArgs &a0, int64_t batch, cudaStream_t st) 
                                       : (a.tw_mode == TW_FILT_INV ? k_subfft<T, LF, TW_FILT_INV> : k_subfft<T, LF, TW_NONE>));
     };
     auto kern = a.es == 1 ? pick(std::true_type{}) : pick(std::false_type{});
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = func_smem_attr((const void *)kern, smem);
     if (e != cudaSuccess) return e;
     const int blocks_b = (a.B + a.G - 1) / a.G;
     for (int64_t b0 = 0; b0 < batch; b0 += 65535) {

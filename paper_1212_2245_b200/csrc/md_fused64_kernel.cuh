@@ -151,8 +151,11 @@ __device__ __forceinline__ void lane_window(const double (&x)[SEG], double (&w)[
     }
 }
 
+#ifndef MD_F64_BLOCKS_PER_SM
+#define MD_F64_BLOCKS_PER_SM 1
+#endif
 template <int R, int NW, int LPW, bool ROBUST, int BOXR, bool BOXC>
-__global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
+__global__ void __launch_bounds__(NW * 32, MD_F64_BLOCKS_PER_SM)
 k_fused_lines64(FusedKArgs<double, R> a, const double2 *__restrict__ lut64) {
     using T = double;
     constexpr int HW = HaloOf<R>::value;
@@ -582,7 +585,10 @@ cudaError_t launch_fused64_t(void (*kern)(FusedKArgs<double, R>, const double2 *
 #define MD_F64_NW 16
 #endif
 constexpr int F64_NW = MD_F64_NW;
-constexpr int F64_LPW = 2;
+#ifndef MD_F64_LPW
+#define MD_F64_LPW 2
+#endif
+constexpr int F64_LPW = MD_F64_LPW;
 
 template <int RR>
 cudaError_t launch_fused64_box_r(const FusedLinesArgs &d, int64_t batch, cudaStream_t st) {
