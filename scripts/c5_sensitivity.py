@@ -3,8 +3,13 @@ run the 4096^2 c5 pipeline (line L=21@30deg, noise-free, 5 RRRL iterations, FOUR
 the second time with the Wiener start perturbed by 1e-13 relative noise, and report how far
 the results drift; also the oracle against the reference's own run (tests/golden/big_c5_4096.npz).
 About 4 minutes of CPU. Output recorded in profiles/r2_c5_sensitivity.txt."""
-import sys, time, numpy as np
-import os\nROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))\nsys.path.insert(0, ROOT)
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
 from oracle import wr3l_oracle as O
 import paper_1212_2245_b200 as md
 d = np.load(os.path.join(ROOT, 'tests/golden/big_c5_4096.npz'))
