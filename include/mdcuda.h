@@ -223,6 +223,17 @@ int32_t md_slab_wiener_epilogue(md_plan *plan, const void *z, const void *f, voi
 /* one RRRL iteration of a slab whose first own row is global row `row0` */
 int32_t md_slab_iterate(md_plan *plan, const void *u, const void *fpos, void *p, void *w,
                         void *u_out, int32_t rows, int32_t row0, void *stream);
+/* the same iteration in pieces, so the halo exchange can overlap the rows that do not need it:
+ * stage A (blur -> p, W) over rows [a_begin, a_end) of [-adj.ht, rows + adj.hb), stage B
+ * (adjoint pair + TV + update) over own rows [b_begin, b_end); empty ranges are skipped */
+int32_t md_slab_stage(md_plan *plan, const void *u, const void *fpos, void *p, void *w,
+                      void *u_out, int32_t rows, int32_t row0, int32_t a_begin, int32_t a_end,
+                      int32_t b_begin, int32_t b_end, void *stream);
+/* margins of the halo-free bands: stage A rows [a_in, S - a_in) read no halo u, stage B rows
+ * [b_in, S - b_in) need only those p / W rows (slab.py: interior first, boundary after the
+ * exchange); adj_top / adj_bottom: the full stage A range is [-adj_top, S + adj_bottom) */
+int32_t md_slab_bands(const md_plan *plan, int32_t *a_in, int32_t *b_in, int32_t *adj_top,
+                      int32_t *adj_bottom);
 
 #ifdef __cplusplus
 }

@@ -94,6 +94,9 @@ SIGNATURES = {
     "md_slab_cols_filter": (_I32, [_P, _P, _I32, _P, _P]),
     "md_slab_wiener_epilogue": (_I32, [_P, _P, _P, _P, _P, _I32, _P]),
     "md_slab_iterate": (_I32, [_P, _P, _P, _P, _P, _P, _I32, _I32, _P]),
+    "md_slab_stage": (_I32, [_P, _P, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _P]),
+    "md_slab_bands": (_I32, [_P, ctypes.POINTER(_I32), ctypes.POINTER(_I32), ctypes.POINTER(_I32),
+                             ctypes.POINTER(_I32)]),
 }
 
 _lib = None

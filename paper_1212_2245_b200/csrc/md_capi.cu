@@ -1721,17 +1721,19 @@ int32_t md_slab_wiener_epilogue(md_plan *P, const void *z, const void *f, void *
     return MD_OK;
 }
 
-int32_t md_slab_iterate(md_plan *P, const void *u, const void *fpos, void *p, void *w, void *u_out, int32_t rows,
-                        int32_t row0, void *stream) {
+int32_t md_slab_stage(md_plan *P, const void *u, const void *fpos, void *p, void *w, void *u_out, int32_t rows,
+                      int32_t row0, int32_t a_begin, int32_t a_end, int32_t b_begin, int32_t b_end, void *stream) {
     int rc = slab_check(P);
     if (rc) return rc;
+    if (a_begin < -P->hadj.ht || a_end > rows + P->hadj.hb || b_begin < 0 || b_end > rows)
+        return fail(MD_EINVAL, "slab stage rows out of range");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     PlanUse use(P, st);
     PlaneFastDesc s{};
     s.u = u; s.f = fpos; s.p = p; s.w = w; s.u_out = u_out;     // all point at own row 0 of haloed buffers
     s.H = rows; s.W = P->d.width; s.periodic = P->periodic;
     s.slab = 1; s.gy0 = row0; s.Hg = P->d.height;
-    s.row_a0 = -P->hadj.ht; s.rows_a = rows + P->hadj.ht + P->hadj.hb;
+    s.a_begin = a_begin; s.a_end = a_end; s.b_begin = b_begin; s.b_end = b_end;
     int32_t top = 0, bot = 0;
     md_slab_halo(P, &top, &bot);                 // the haloed buffers' extent (slab.py SlabGeometry)
     s.halo_top = top; s.halo_bot = bot;
@@ -1740,6 +1742,24 @@ int32_t md_slab_iterate(md_plan *P, const void *u, const void *fpos, void *p, vo
     s.has_d = P->has_d; s.lut = P->lut;
     CU(P->d.dtype == MD_F64 ? launch_plane_fast<double>(s, P->robust, 1, st)
                             : launch_plane_fast<float>(s, P->robust, 1, st));
+    return MD_OK;
+}
+
+int32_t md_slab_iterate(md_plan *P, const void *u, const void *fpos, void *p, void *w, void *u_out, int32_t rows,
+                        int32_t row0, void *stream) {
+    if (!P) return fail(MD_EINVAL, "null plan");
+    return md_slab_stage(P, u, fpos, p, w, u_out, rows, row0, -P->hadj.ht, rows + P->hadj.hb, 0, rows, stream);
+}
+
+int32_t md_slab_bands(const md_plan *P, int32_t *a_in, int32_t *b_in, int32_t *adj_top, int32_t *adj_bottom) {
+    int rc = slab_check(P);
+    if (rc) return rc;
+    *adj_top = P->hadj.ht;
+    *adj_bottom = P->hadj.hb;
+    // stage A rows that read no halo u: [blur.ht, S - blur.hb); stage B rows whose p / W come from
+    // those rows only (and whose TV stencil stays inside): [adj.ht + blur.ht, S - blur.hb - adj.hb)
+    *a_in = std::max(P->hblur.ht, P->hblur.hb);
+    *b_in = std::max(std::max(P->hadj.ht, P->hadj.hb) + *a_in, 2);
     return MD_OK;
 }
 

@@ -289,23 +289,33 @@ cudaError_t launch_plane_fast(const PlaneFastDesc &d, bool robust, int64_t batch
     a.alpha = T(d.alpha); a.eps_d2 = T(d.eps_d2); a.eps_r2 = T(d.eps_r2); a.has_d = d.has_d;
     a.lut = d.lut;
     const size_t sa = smem_a(d.hb, sizeof(T), a.ssa), sb = smem_b(d.ha, sizeof(T), a.ssb);
+#define MD_CHECK_HOST(c) \
+    if (!(c)) return cudaErrorInvalidValue
     auto ka = robust ? k_plane_a_fast<T, true> : k_plane_a_fast<T, false>;
     auto kb = robust ? k_plane_b_fast<T, true> : k_plane_b_fast<T, false>;
     cudaError_t e = cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sa);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
     if (e != cudaSuccess) return e;
     if (d.slab) {
-        // stage A over the extended rows [row_a0, row_a0 + rows_a), stage B over the own rows
+        // stage A over rows [a_begin, a_end) (at most the extended rows [-adj.ht, H + adj.hb)),
+        // stage B over own rows [b_begin, b_end): the row-slab driver runs the rows that do not
+        // need the neighbours' halo while the halo exchange is in flight (slab.py)
         a.ylo = -d.halo_top;
         a.yhi = d.H + d.halo_bot;
-        PlaneFastArgs<T> aa = a;
-        const int64_t off = (int64_t)d.row_a0 * d.W;
-        aa.u += off; aa.f += off; aa.p += off; aa.w += off;
-        aa.H = d.rows_a; aa.gy0 = d.gy0 + d.row_a0;
-        aa.ylo = a.ylo - d.row_a0;
-        aa.yhi = a.yhi - d.row_a0;
-        ka<<<dim3((d.W + FX - 1) / FX, (d.rows_a + FY - 1) / FY, 1), 256, sa, st>>>(aa);
-        kb<<<dim3((d.W + FX - 1) / FX, (d.H + FY - 1) / FY, 1), 256, sb, st>>>(a);
+        auto sub = [&](int r0, int r1) {
+            PlaneFastArgs<T> s2 = a;
+            const int64_t off = (int64_t)r0 * d.W;
+            s2.u += off; s2.f += off; s2.p += off; s2.w += off; s2.u_out += off;
+            s2.H = r1 - r0; s2.gy0 = d.gy0 + r0;
+            s2.ylo = a.ylo - r0; s2.yhi = a.yhi - r0;
+            return s2;
+        };
+        if (d.a_end > d.a_begin) {
+            MD_CHECK_HOST(d.a_begin >= -d.ha.ht && d.a_end <= d.H + d.ha.hb);
+            ka<<<dim3((d.W + FX - 1) / FX, (d.a_end - d.a_begin + FY - 1) / FY, 1), 256, sa, st>>>(sub(d.a_begin, d.a_end));
+        }
+        if (d.b_end > d.b_begin)
+            kb<<<dim3((d.W + FX - 1) / FX, (d.b_end - d.b_begin + FY - 1) / FY, 1), 256, sb, st>>>(sub(d.b_begin, d.b_end));
         return cudaGetLastError();
     }
     const int64_t fsz = (int64_t)d.H * d.W;

@@ -29,7 +29,9 @@ struct PlaneFastDesc {
     void *p, *w, *u_out;
     int H, W, periodic;
     int slab, gy0, Hg;         // see PlaneFastArgs
-    int rows_a, row_a0;        // slab: stage A computes rows [row_a0, row_a0 + rows_a) (relative to own row 0)
+    int a_begin, a_end;        // slab: stage A computes rows [a_begin, a_end) (relative to own row 0;
+                               // the full stage is [-adj.ht, H + adj.hb)); empty = skipped
+    int b_begin, b_end;        // slab: stage B computes own rows [b_begin, b_end) (full: [0, H))
     int halo_top, halo_bot;    // slab: rows present above / below the own rows in every buffer
     PlaneHalo hb, ha;
     const std::vector<PlaneTap> *taps_blur, *taps_adj;   // host copies

@@ -62,16 +62,28 @@ class DistComm:
         """send_up -> rank-1 (its bottom halo); send_down -> rank+1 (its top halo); periodic."""
         dist = self.dist
         prev, nxt = (self.rank - 1) % self.world, (self.rank + 1) % self.world
+        self.exchange_async(rank, send_up, send_down, recv_up, recv_down)()
+
+    def exchange_async(self, rank, send_up, send_down, recv_up, recv_down):
+        """Post the halo exchange; returns a wait() callable. On NCCL the transfers run on the
+        communicator's stream while the caller's stream computes; wait() orders the caller's
+        stream after them."""
+        dist = self.dist
+        prev, nxt = (self.rank - 1) % self.world, (self.rank + 1) % self.world
         if self.world == 1:
             recv_up.copy_(send_down)
             recv_down.copy_(send_up)
-            return
+            return lambda: None
         ops = [dist.P2POp(dist.isend, send_up.contiguous(), prev, self.group),
                dist.P2POp(dist.irecv, recv_down, nxt, self.group),
                dist.P2POp(dist.isend, send_down.contiguous(), nxt, self.group),
                dist.P2POp(dist.irecv, recv_up, prev, self.group)]
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
+        reqs = dist.batch_isend_irecv(ops)
+
+        def wait():
+            for req in reqs:
+                req.wait()
+        return wait
 
     def all_to_all(self, rank, recv, send):
         """send[q] goes to rank q, recv[q] comes from rank q (equal splits along dim 0)."""
@@ -102,6 +114,10 @@ class HostStagedComm:
         recv_up.copy_(r_up)
         recv_down.copy_(r_down)
 
+    def exchange_async(self, rank, send_up, send_down, recv_up, recv_down):
+        self.exchange(rank, send_up, send_down, recv_up, recv_down)      # host-side: done on return
+        return lambda: None
+
     def all_to_all(self, rank, recv, send):
         r = recv.new_empty(recv.shape, device="cpu")
         self.c.all_to_all(rank, r, send.detach().to("cpu").contiguous())
@@ -126,6 +142,10 @@ class LocalComm:
         recv_up.copy_(self._box[prev][1])       # prev's bottom rows -> my top halo
         recv_down.copy_(self._box[nxt][0])      # next's top rows -> my bottom halo
         self._bar.wait()
+
+    def exchange_async(self, rank, send_up, send_down, recv_up, recv_down):
+        self.exchange(rank, send_up, send_down, recv_up, recv_down)
+        return lambda: None
 
     def all_to_all(self, rank, recv, send):
         self._box[rank] = send
@@ -169,6 +189,24 @@ class CudaSlabBackend:
     def epilogue(self, z, f, u0, fpos, rows, stream=None):
         L.check(self.lib.md_slab_wiener_epilogue(self.plan._h, z.data_ptr(), f.data_ptr(), u0.data_ptr(),
                                                  fpos.data_ptr(), rows, _sp(stream)))
+
+    def bands(self):
+        """(a_in, b_in): stage-A rows [a_in, S - a_in) and stage-B rows [b_in, S - b_in) need no
+        halo rows (md_slab_bands)."""
+        a, b, t, u = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        L.check(self.lib.md_slab_bands(self.plan._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(t),
+                                       ctypes.byref(u)))
+        self.adj_halo = (t.value, u.value)
+        return a.value, b.value
+
+    def stage(self, u_ext, fpos_ext, p_ext, w_ext, out_ext, geo: SlabGeometry, a_rows, b_rows, stream=None):
+        """Part of one iteration: stage A over rows a_rows = (begin, end) of [-adj.ht, S + adj.hb),
+        stage B over own rows b_rows (md_slab_stage)."""
+        off = geo.top * geo.W * u_ext.element_size()
+        ptr = lambda t: t.data_ptr() + off
+        L.check(self.lib.md_slab_stage(self.plan._h, ptr(u_ext), ptr(fpos_ext), ptr(p_ext), ptr(w_ext),
+                                       ptr(out_ext), geo.S, geo.row0, a_rows[0], a_rows[1], b_rows[0], b_rows[1],
+                                       _sp(stream)))
 
     def iterate(self, u_ext, fpos_ext, p_ext, w_ext, out_ext, geo: SlabGeometry, stream=None):
         """One iteration on haloed [top + S + bottom, W] buffers (pointers at own row 0)."""
@@ -231,11 +269,30 @@ class SlabWorker:
         cur = 0
         b.epilogue(self.z, f_own, self.own(self.u[cur]), self.own(self.fpos), g.S)
         self._exchange(comm, self.fpos)
-        # ---- iterations: halo exchange of u, then one fused-stage iteration on the slab
+        # ---- iterations. With a backend that runs stages by row band (CudaSlabBackend), the
+        # rows that need no halo are computed while the halo exchange is in flight: stage A on
+        # [a_in, S - a_in) and stage B on [b_in, S - b_in) first, then the boundary bands after
+        # the exchange (on NCCL the transfer overlaps the interior kernels). Otherwise exchange,
+        # then the whole iteration.
+        bands = b.bands() if hasattr(b, "bands") else None
+        ha_t, ha_b = getattr(b, "adj_halo", (None, None))
+        overlap = bands is not None and 2 * bands[1] <= g.S and ha_t is not None
         for k in range(self.K):
-            self._exchange(comm, self.u[cur])
             nxt = 1 - cur
-            b.iterate(self.u[cur], self.fpos, self.p, self.w, self.u[nxt], g)
+            if overlap:
+                a_in, b_in = bands
+                t = self.u[cur]
+                wait = comm.exchange_async(g.rank, self.own(t)[:g.bottom], self.own(t)[g.S - g.top:],
+                                           t[:g.top], t[g.top + g.S:])
+                b.stage(self.u[cur], self.fpos, self.p, self.w, self.u[nxt], g, (a_in, g.S - a_in),
+                        (b_in, g.S - b_in))
+                wait()
+                for ar, br in (((-ha_t, a_in), (0, b_in)), ((g.S - a_in, g.S + ha_b), (g.S - b_in, g.S))):
+                    b.stage(self.u[cur], self.fpos, self.p, self.w, self.u[nxt], g, ar, (0, 0))
+                    b.stage(self.u[cur], self.fpos, self.p, self.w, self.u[nxt], g, (0, 0), br)
+            else:
+                self._exchange(comm, self.u[cur])
+                b.iterate(self.u[cur], self.fpos, self.p, self.w, self.u[nxt], g)
             cur = nxt
         return self.own(self.u[cur])
 

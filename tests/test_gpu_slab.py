@@ -135,3 +135,18 @@ def test_c5_16384_eight_slabs_equal_single_plan(md):
     assert bool(torch.isfinite(want).all())
     assert float(want.min()) > 0.0                     # the multiplicative update keeps u positive
     assert abs(float(want.mean()) - float(f.mean())) < 1.0   # RL-type updates preserve the mean
+
+
+def test_slab_bands_enable_overlap(md):
+    """The band split the worker uses to overlap the halo exchange with the interior rows
+    (md_slab_bands / md_slab_stage): margins cover the blur and adjoint halos, and the c5 slabs
+    (2048 rows at 8 ranks) are deep enough for it."""
+    from paper_1212_2245_b200.slab import CudaSlabBackend
+    pipe = md.DeblurPipeline((512, 512), md.Psf.line(21.0, 30.0), md.DeconvParams(), big_fft=True)
+    be = CudaSlabBackend(pipe.plan)
+    a_in, b_in = be.bands()
+    top, bot = be.halo_rows()
+    ht, hb = be.adj_halo
+    assert a_in >= 1 and b_in >= a_in + max(ht, hb) and b_in >= 2
+    assert top >= ht + a_in - 1 and bot >= hb + a_in - 1
+    assert 2 * b_in <= 16384 // 8
