@@ -240,7 +240,6 @@ class SlabWorker:
         self.p = torch.zeros(ext, dtype=dtype, device=device)
         self.w = torch.zeros(ext, dtype=dtype, device=device)
         self.z = torch.zeros((g.S, g.W, 2), dtype=dtype, device=device)          # complex as (re, im)
-        self.zc = torch.zeros((g.H, g.Wb, 2), dtype=dtype, device=device)
         self.send = torch.zeros((g.world, g.S, g.Wb, 2), dtype=dtype, device=device)
         self.recv = torch.zeros_like(self.send)
         backend.prepare(geo)
@@ -257,14 +256,14 @@ class SlabWorker:
     def run(self, comm, f_own):
         g, b = self.g, self.b
         # ---- Wiener: rows (local) -> transpose -> columns x M -> transpose back -> rows
+        # the column block arrives as [world][S][Wb] = [H][Wb]: filtered in place in the receive
+        # buffer and sent back from it (no staging copies around the column pass)
         b.rows_fft(self.z, f_own, g.S, 0)
         self.send.copy_(self.z.view(g.S, g.world, g.Wb, 2).permute(1, 0, 2, 3))
         comm.all_to_all(g.rank, self.recv, self.send)
-        self.zc.view(g.world, g.S, g.Wb, 2).copy_(self.recv)
-        b.cols_filter(self.zc, g.Wb)
-        self.send.copy_(self.zc.view(g.world, g.S, g.Wb, 2))
-        comm.all_to_all(g.rank, self.recv, self.send)
-        self.z.view(g.S, g.world, g.Wb, 2).copy_(self.recv.permute(1, 0, 2, 3))
+        b.cols_filter(self.recv.view(g.H, g.Wb, 2), g.Wb)
+        comm.all_to_all(g.rank, self.send, self.recv)
+        self.z.view(g.S, g.world, g.Wb, 2).copy_(self.send.permute(1, 0, 2, 3))
         b.rows_fft(self.z, None, g.S, 1)
         cur = 0
         b.epilogue(self.z, f_own, self.own(self.u[cur]), self.own(self.fpos), g.S)
