@@ -825,6 +825,9 @@ def run_frames(args, rank: int, world: int, local: int, cuda: bool) -> None:
                          "source": "ncu l1tex__data_pipe_lsu_wavefronts_mem_shared.sum (profiles/ncu_traffic.json) "
                                    "over this run's iteration time; peak = SMs x 128 B/clk x max SM clock"}
         frame_gbs = value / world * work.frame_bytes(esz) / 1e9
+        geom = work.pipe.plan.fused_geometry() if (work.fused and hasattr(work, "pipe")) else None
+        if geom:
+            geom["sms"] = torch.cuda.get_device_properties(local).multi_processor_count
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
@@ -845,7 +848,8 @@ def run_frames(args, rank: int, world: int, local: int, cuda: bool) -> None:
                                          "profiles/ncu_traffic.json, scaled to this launch's frames)",
                          "peak_source": pk["source"],
                          "bytes_model": "SURVEY.md 8(d): 8 field passes per RRRL iteration x 65536 px x "
-                                        f"{esz} B per frame; time = CUDA events around the iteration launches"},
+                                        f"{esz} B per frame; time = CUDA events around the iteration launches",
+                         "launch_geometry": geom},
             "roofline_frame": {"bound": "hbm", "achieved": frame_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
                                "frac": frame_gbs / pk["hbm_gbs"],
                                "bytes_model": f"SURVEY.md 8(d): whole frame (Wiener 2 + 8 per iteration) field passes "

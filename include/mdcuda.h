@@ -106,6 +106,10 @@ int32_t md_plan_set_chunk(md_plan *plan, int64_t frames);
 /* enable / disable the fused persistent kernel where the plan supports it */
 int32_t md_plan_set_fused(md_plan *plan, int32_t on);
 int32_t md_plan_is_fused(const md_plan *plan);
+/* the 1D cluster kernel's launch geometry: CTAs per cluster, co-resident clusters, CTAs per SM
+ * (all 0 when the plan does not use it); SMs busy = clusters x CTAs / CTAs per SM */
+int32_t md_plan_fused_geometry(const md_plan *plan, int32_t *cluster_ctas, int32_t *resident_clusters,
+                               int32_t *ctas_per_sm);
 
 /* the pipeline: Wiener (or clamp) init + iterations (DeblurPipeline.run, deconv.py:653-693;
  * rrrl_deblur deconv.py:537-559; rl_deblur deconv.py:524-534). f and u are device arrays.

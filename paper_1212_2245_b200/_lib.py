@@ -63,6 +63,7 @@ SIGNATURES = {
     "md_plan_set_chunk": (_I32, [_P, _I64]),
     "md_plan_set_fused": (_I32, [_P, _I32]),
     "md_plan_is_fused": (_I32, [_P]),
+    "md_plan_fused_geometry": (_I32, [_P, ctypes.POINTER(_I32), ctypes.POINTER(_I32), ctypes.POINTER(_I32)]),
     "md_run": (_I32, [_P, _P, _P, _I64, _P]),
     "md_run_host": (_I32, [_P, _P, _P, _I64, _P]),
     "md_run_host_ex": (_I32, [_P, _P, _I32, _P, _I32, _I64, _P]),

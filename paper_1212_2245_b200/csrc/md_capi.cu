@@ -250,6 +250,7 @@ struct md_plan {
         return MD_OK;
     }
     int fused_clusters = 0;     // resident clusters of the fused-lines kernel (0 = unknown)
+    int fused_geom[2] = {0, 0}; // its cluster size (CTAs) and CTAs per SM
     // concurrent use: host-side enqueue under a per-plan lock; a call on another stream than the
     // previous one waits (device side) for it, since both would use the plan's scratch
     std::recursive_mutex mu;
@@ -826,6 +827,7 @@ int lines_fused_clusters(md_plan &P) {
     int n = 0;
     FusedLinesArgs fa = fused_args<T>(P, nullptr, nullptr, nullptr);
     fa.query = &n;
+    fa.query_geom = P.fused_geom;
     return launch_fused_lines<T>(fa, 1, nullptr) == cudaSuccess ? n : 0;
 }
 
@@ -1136,6 +1138,16 @@ int32_t md_plan_set_fused(md_plan *P, int32_t on) {
 }
 
 int32_t md_plan_is_fused(const md_plan *P) { return P && (P->fused || P->fused_plane) ? 1 : 0; }
+
+int32_t md_plan_fused_geometry(const md_plan *P, int32_t *cluster_ctas, int32_t *resident_clusters,
+                               int32_t *ctas_per_sm) {
+    if (!P || !cluster_ctas || !resident_clusters || !ctas_per_sm) return fail(MD_EINVAL, "bad arguments");
+    const bool on = P->fused && P->fused_clusters > 0;
+    *cluster_ctas = on ? P->fused_geom[0] : 0;
+    *resident_clusters = on ? P->fused_clusters : 0;
+    *ctas_per_sm = on ? P->fused_geom[1] : 0;
+    return MD_OK;
+}
 
 int32_t md_run(md_plan *P, const void *f, void *u, int64_t batch, void *stream) {
     if (!P || batch < 0) return fail(MD_EINVAL, "bad arguments");

@@ -47,7 +47,7 @@ cudaError_t launch_fused_lines(const FusedLinesArgs &d, int64_t batch, cudaStrea
         a.lut = d.lut;
         return launch_fused_t<T, RR, LP>(d.robust ? k_fused_lines<T, RR, LP, true, 0, false>
                                                   : k_fused_lines<T, RR, LP, false, 0, false>,
-                                         a, batch, st);
+                                         a, batch, st, d.query_geom);
     };
     if (r <= 4) return go(std::integral_constant<int, 4>{});
     if (r <= 8) return go(std::integral_constant<int, 8>{});

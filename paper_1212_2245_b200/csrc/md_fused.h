@@ -16,6 +16,7 @@ struct FusedLinesArgs {
     int has_d, robust;
     LutView lut;
     int *query;            // non-null: store the resident cluster count, launch nothing
+    int *query_geom;       // with query: [cluster CTAs, CTAs per SM] of that launch (optional)
 };
 
 // radius: max(blur, adjoint) line radius (line_radius, md_lines_fast.h)

@@ -12,7 +12,7 @@ cudaError_t launch_fused64_box_hi(const FusedLinesArgs &d, int radius, int64_t b
 
 cudaError_t launch_fused64(const FusedLinesArgs &d, int64_t batch, cudaStream_t st) {
     const int r = std::max(line_radius(d.blur), line_radius(d.adj));
-    if (r > 16 || !d.lut.p64) return cudaErrorNotSupported;
+    if (r > 16 || (!d.lut.p64 && !d.query)) return cudaErrorNotSupported;   // plan-time queries run before the table exists
     if (d.blur.kind == LINE_BOX && d.adj.kind == LINE_BOX && r >= 1 && d.robust) {
         cudaError_t e = cudaErrorNotSupported;
         switch (r) {
@@ -44,7 +44,7 @@ cudaError_t launch_fused64(const FusedLinesArgs &d, int64_t batch, cudaStream_t 
         a.lut = d.lut;
         return launch_fused64_t<RR, F64_NW, F64_LPW>(d.robust ? k_fused_lines64<RR, F64_NW, F64_LPW, true, 0, false>
                                                               : k_fused_lines64<RR, F64_NW, F64_LPW, false, 0, false>,
-                                                     a, d.lut.p64, batch, st);
+                                                     a, d.lut.p64, batch, st, d.query_geom);
     };
     if (r <= 4) return go(std::integral_constant<int, 4>{});
     if (r <= 8) return go(std::integral_constant<int, 8>{});

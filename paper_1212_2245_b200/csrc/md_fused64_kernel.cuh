@@ -537,7 +537,7 @@ inline int pick_cluster(const void *kern, size_t smem, int threads, int m, int r
 
 template <int R, int NW, int LPW>
 cudaError_t launch_fused64_t(void (*kern)(FusedKArgs<double, R>, const double2 *), const FusedKArgs<double, R> &a0,
-                             const double2 *lut64, int64_t batch, cudaStream_t st) {
+                             const double2 *lut64, int64_t batch, cudaStream_t st, int *query_geom = nullptr) {
     const size_t smem = fused64_smem<R, NW, LPW>(a0.n);
     {
         const cudaError_t e = func_smem_attr((const void *)kern, smem, true);
@@ -549,6 +549,12 @@ cudaError_t launch_fused64_t(void (*kern)(FusedKArgs<double, R>, const double2 *
     if (a.cl == 0) return cudaErrorNotSupported;
     if (a.query) {
         *a.query = resident;
+        if (query_geom) {
+            query_geom[0] = a.cl;
+            int per_sm = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32, smem);
+            query_geom[1] = per_sm;
+        }
         return cudaSuccess;
     }
     cudaLaunchAttribute attr[1];
@@ -610,7 +616,7 @@ cudaError_t launch_fused64_box_r(const FusedLinesArgs &d, int64_t batch, cudaStr
     for (int i = 0; i < 4; ++i) corr = corr || a.box_cb[i] != 0.0 || a.box_ca[i] != 0.0;
     return launch_fused64_t<RR, F64_NW, F64_LPW>(corr ? k_fused_lines64<RR, F64_NW, F64_LPW, true, RR, true>
                                                       : k_fused_lines64<RR, F64_NW, F64_LPW, true, RR, false>,
-                                                 a, d.lut.p64, batch, st);
+                                                 a, d.lut.p64, batch, st, d.query_geom);
 }
 
 }  // namespace md

@@ -355,7 +355,7 @@ k_fused_lines(FusedKArgs<T, R> a) {
 // launch one instantiation of k_fused_lines (cluster of a.cl CTAs per frame)
 template <typename T, int R, int LPW>
 cudaError_t launch_fused_t(void (*kern)(FusedKArgs<T, R>), const FusedKArgs<T, R> &a, int64_t batch,
-                           cudaStream_t st) {
+                           cudaStream_t st, int *query_geom = nullptr) {
     constexpr int HW = HaloOf<R>::value;
     constexpr int RL = FU_WARPS * LPW;
     const size_t smem = (size_t)(2 * RL + 10 + 2 * FU_WARPS) * xline_len(a.n, HW) * sizeof(T);
@@ -373,7 +373,14 @@ cudaError_t launch_fused_t(void (*kern)(FusedKArgs<T, R>), const FusedKArgs<T, R
         qa[0].val.clusterDim.z = 1;
         q.attrs = qa;
         q.numAttrs = 1;
-        return cudaOccupancyMaxActiveClusters(a.query, kern, &q);
+        e = cudaOccupancyMaxActiveClusters(a.query, kern, &q);
+        if (e == cudaSuccess && query_geom) {
+            query_geom[0] = a.cl;
+            int per_sm = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
+            query_geom[1] = per_sm;
+        }
+        return e;
     }
     const int64_t fsz = (int64_t)a.n * a.m;
     const int64_t maxf = (int64_t)(0x7fffffff / a.cl);
@@ -421,7 +428,7 @@ cudaError_t launch_fused_box_r(const FusedLinesArgs &d, int64_t batch, cudaStrea
     bool corr = false;           // odd integer boxes: the plain sliding sum (no correction code)
     for (int i = 0; i < 4; ++i) corr = corr || a.box_cb[i] != T(0) || a.box_ca[i] != T(0);
     return launch_fused_t<T, RR, LP>(corr ? k_fused_lines<T, RR, LP, true, RR, true> : k_fused_lines<T, RR, LP, true, RR, false>,
-                                     a, batch, st);
+                                     a, batch, st, d.query_geom);
 }
 
 // lines per warp: 4 in float (32-line CTAs, 8-CTA clusters, two CTAs per SM); for radii above 8

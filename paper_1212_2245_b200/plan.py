@@ -97,6 +97,14 @@ class GpuPlan:
     def fused(self) -> bool:
         return bool(self.lib.md_plan_is_fused(self._h))
 
+    def fused_geometry(self) -> dict:
+        """The 1D cluster kernel's launch shape: CTAs per cluster, co-resident clusters, CTAs per
+        SM and the SMs they keep busy (zeros when the plan does not use it)."""
+        c, r, p = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        L.check(self.lib.md_plan_fused_geometry(self._h, ctypes.byref(c), ctypes.byref(r), ctypes.byref(p)))
+        busy = -(-(c.value * r.value) // p.value) if p.value else 0
+        return {"cluster_ctas": c.value, "resident_clusters": r.value, "ctas_per_sm": p.value, "sms_busy": busy}
+
     def set_fused(self, on: bool) -> None:
         L.check(self.lib.md_plan_set_fused(self._h, 1 if on else 0))
 
