@@ -93,12 +93,15 @@ constexpr int F64_OBS_LINE = 256;                 // doubles per warp buffer (n 
 // r1 with the (value, step) pair table (md_common.cuh rules, deconv.py:114-134): the table
 // interpolation and the linear continuation above `upper`; the direct formula below
 // `direct_below` is the caller's (taken per warp, see k_fused_lines64)
+// The reference clamps x to `upper` and the position to >= 0 before indexing; both clamps only
+// matter where the result is replaced anyway (x > upper: the linear continuation below; x <
+// delta < direct_below: the caller's direct formula), so the index is clamped as an integer
+// instead (saturating conversion, two integer min/max) -- bitwise the same r1 wherever it is used,
+// without the float64 compare-and-select pairs
 __device__ __forceinline__ double r1_table64(const double2 *__restrict__ p64, double x) {
-    const double xc = x < kLutUpper ? x : kLutUpper;
-    double pos = (xc - kLutDelta) * kLutInvStep;
-    pos = pos > 0.0 ? pos : 0.0;
-    int i = (int)pos;
-    i = i < kLutCount - 2 ? i : kLutCount - 2;
+    const double pos = (x - kLutDelta) * kLutInvStep;
+    int i = __double2int_rz(pos);
+    i = min(max(i, 0), kLutCount - 2);
     const double2 e = __ldg(p64 + i);
     double r = e.x + e.y * (pos - (double)i);
     if (x > kLutUpper) r = kLutSlope * x + kLutIntercept;
@@ -269,8 +272,10 @@ k_fused_lines64(FusedKArgs<double, R> a, const double2 *__restrict__ lut64) {
         for (int l = lb + wl; l <= le; l += NW) {
             const int gl = gl0 + l;
             if (gl < 0 || gl >= m) continue;
-            const bool up_ok = gl > 0, dn_ok = gl + 1 < m;
-            const T *row = line_ptr(l, par), *up = line_ptr(l - 1, par), *dn = line_ptr(l + 1, par);
+            // Neumann at the frame's first / last line: the missing neighbour aliases the line
+            // itself, so its difference is exactly zero (no per-pixel selects)
+            const T *row = line_ptr(l, par);
+            const T *up = gl > 0 ? line_ptr(l - 1, par) : row, *dn = gl + 1 < m ? line_ptr(l + 1, par) : row;
             for (int s = lane; s < nseg; s += 32) {
                 const int off = base0 + 9 * s;
                 T x[SEG + 2];
@@ -284,9 +289,7 @@ k_fused_lines64(FusedKArgs<double, R> a, const double2 *__restrict__ lut64) {
                     T dxl = x[r + 1] - x[r];
                     if (r == SEG - 1 && s == nseg - 1) dxr = T(0);
                     if (r == 0 && s == 0) dxl = T(0);
-                    const T yd = dn_ok ? dn[off + koff(r)] : x[r + 1];
-                    const T yu = up_ok ? up[off + koff(r)] : x[r + 1];
-                    const T dyd = yd - x[r + 1], dyu = x[r + 1] - yu;
+                    const T dyd = dn[off + koff(r)] - x[r + 1], dyu = x[r + 1] - up[off + koff(r)];
                     const T q = dxr * dxr + dxl * dxl + dyd * dyd + dyu * dyu;
                     G[koff(r)] = T(0.5) * frsqrt(T(0.5) * q + eps_r2);
                 }
@@ -398,9 +401,12 @@ k_fused_lines64(FusedKArgs<double, R> a, const double2 *__restrict__ lut64) {
 #pragma unroll
             for (int k = -1; k <= SEG; ++k) ux[k + 1] = U[off + koff(k)];
             if (a.has_d) {
+                // Neumann at the frame's first / last line by aliasing (see g_lines): the vertical
+                // flux to a missing neighbour is (g + g) (u - u) = 0 exactly
                 const T *G = sg + (li + 1) * ls + off;
-                const T *Gu = G - ls, *Gd = G + ls;
-                const T *Uu = line_ptr(li - 1, par) + off, *Ud = line_ptr(li + 1, par) + off;
+                const T *Gu = up_ok ? G - ls : G, *Gd = dn_ok ? G + ls : G;
+                const T *Uu = up_ok ? line_ptr(li - 1, par) + off : U + off;
+                const T *Ud = dn_ok ? line_ptr(li + 1, par) + off : U + off;
                 T gx[SEG + 2];
 #pragma unroll
                 for (int k = -1; k <= SEG; ++k) gx[k + 1] = G[koff(k)];
@@ -412,10 +418,11 @@ k_fused_lines64(FusedKArgs<double, R> a, const double2 *__restrict__ lut64) {
                     if (r == SEG - 1 && s == nseg - 1) fr = T(0);
                     if (r == 0 && s == 0) fl = T(0);
                     T d = fr - fl;
-                    if (dn_ok) d += (gc + Gd[koff(r)]) * (Ud[koff(r)] - u);
-                    if (up_ok) d -= (Gu[koff(r)] + gc) * (u - Uu[koff(r)]);
-                    const T nm = num[r] + al * (d > T(0) ? d : T(0));
-                    const T neg = al * (d < T(0) ? d : T(0));
+                    d += (gc + Gd[koff(r)]) * (Ud[koff(r)] - u);
+                    d -= (Gu[koff(r)] + gc) * (u - Uu[koff(r)]);
+                    const T dp = fmax(d, T(0));          // max(D, 0); D - max(D, 0) = min(D, 0) exactly
+                    const T nm = num[r] + al * dp;
+                    const T neg = al * (d - dp);
                     T dn = (ROBUST ? den[r] : one) - neg;
                     dn = fmax(dn, gd);
                     unew[j][r] = (u * nm) * frcp(dn);
