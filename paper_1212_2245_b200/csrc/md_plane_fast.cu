@@ -36,6 +36,9 @@ __device__ __forceinline__ int pf_resolve(int k, int n, int periodic) {
 // walks rows, its lanes the columns (CJ column slots per lane, resolved once per block, so
 // no per-element division or wrap); two rows per step keep 2 CJ global loads in flight.
 constexpr int PF_CJ = 4;                  // cols <= 32 * PF_CJ (FX + x-halos <= 128)
+#ifndef MD_PLANE_CP_ASYNC
+#define MD_PLANE_CP_ASYNC 1
+#endif
 template <typename T, typename E, typename Get>
 __device__ void pf_load(E *s, int ss, int H, int W, int y0, int x0, const PlaneHalo &h, int periodic, int slab,
                         int ylo, int yhi, Get get) {
@@ -77,6 +80,42 @@ __device__ void pf_load(E *s, int ss, int H, int W, int y0, int x0, const PlaneH
     }
 }
 
+// the same tile of up to two fields, loaded with cp.async (LDGSTS: global -> shared without a
+// register round trip, every element of the tile in flight at once) -- field a into the first
+// element of each E slot, field b (optional) into the second. Caller: cp_async_wait_all() and
+// __syncthreads() before use.
+__device__ __forceinline__ void cp_async_elem(void *dst, const void *src, int bytes) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+    if (bytes == 8) asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+    else asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+template <typename T, typename E>
+__device__ void pf_load_async(E *s, int ss, int H, int W, int y0, int x0, const PlaneHalo &h, int periodic, int slab,
+                              int ylo, int yhi, const T *fa, const T *fb) {
+    const int rows = FY + h.ht + h.hb, cols = FX + h.hl + h.hr;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    int xr[PF_CJ];
+#pragma unroll
+    for (int c = 0; c < PF_CJ; ++c) {
+        const int j = lane + 32 * c;
+        xr[c] = j < cols ? pf_resolve(x0 - h.hl + j, W, periodic) : -1;
+    }
+    for (int i = warp; i < rows; i += nw) {
+        const int y = y0 - h.ht + i;
+        const int yy = slab ? (y < ylo ? ylo : (y >= yhi ? yhi - 1 : y)) : pf_resolve(y, H, periodic);
+        const int64_t b = (int64_t)yy * W;
+#pragma unroll
+        for (int c = 0; c < PF_CJ; ++c) {
+            if (xr[c] < 0) continue;
+            T *d = reinterpret_cast<T *>(s + i * ss + lane + 32 * c);
+            cp_async_elem(d, fa + b + xr[c], (int)sizeof(T));
+            if (fb) cp_async_elem(d + 1, fb + b + xr[c], (int)sizeof(T));
+        }
+    }
+}
+
 // f32 u-tile stride for stage A: 8 (mod 16) so the two half-warps (rows 2 apart) use disjoint banks
 template <typename T> __host__ __device__ inline int pf_stride_a(const PlaneHalo &h) {
     const int base = FX + h.hl + h.hr;
@@ -98,7 +137,12 @@ k_plane_a_fast(PlaneFastArgs<T> a) {
     T *w = a.w + fr * fsz;
     const int y0 = blockIdx.y * FY, x0 = blockIdx.x * FX;
     const int ss = a.ssa;
+#if MD_PLANE_CP_ASYNC
+    pf_load_async<T, T>(su, ss, H, W, y0, x0, a.hb, a.periodic, a.slab, a.ylo, a.yhi, u, nullptr);
+    cp_async_wait_all();
+#else
     pf_load<T>(su, ss, H, W, y0, x0, a.hb, a.periodic, a.slab, a.ylo, a.yhi, [&](int64_t o) { return u[o]; });
+#endif
     __syncthreads();
     const int tp = threadIdx.x >> 4, cx = threadIdx.x & 15;
     const int yp = y0 + 2 * tp;
@@ -155,12 +199,17 @@ k_plane_b_fast(PlaneFastArgs<T> a) {
     const int y0 = blockIdx.y * FY, x0 = blockIdx.x * FX;
     {
         const T *pp = a.p + fr * fsz, *ww = a.w + fr * fsz;
+#if MD_PLANE_CP_ASYNC
+        // (p, W) tile by cp.async: issued here, in flight while the u tile loads below
+        pf_load_async<T, T2>(spw, ss, H, W, y0, x0, a.ha, a.periodic, a.slab, a.ylo, a.yhi, pp, ROBUST ? ww : nullptr);
+#else
         pf_load<T>(spw, ss, H, W, y0, x0, a.ha, a.periodic, a.slab, a.ylo, a.yhi, [&](int64_t o) {
             T2 v;
             v.x = pp[o];
             v.y = ROBUST ? ww[o] : T(0);
             return v;
         });
+#endif
     }
     const int gy0 = a.gy0, Hg = a.Hg;
     {
@@ -188,6 +237,9 @@ k_plane_b_fast(PlaneFastArgs<T> a) {
             }
         }
     }
+#if MD_PLANE_CP_ASYNC
+    cp_async_wait_all();
+#endif
     __syncthreads();
     const T eps_r2 = a.eps_r2;
     if (a.has_d) {
