@@ -18,8 +18,12 @@ constexpr int PTHREADS = 256;   // 32 x 8
 __device__ __forceinline__ int resolve2(int k, int n, int periodic) {
     // a tile plus halo may be larger than a small frame: a full wrap (see pf_resolve)
     if (periodic) {
-        k %= n;
-        return k < 0 ? k + n : k;
+        k = k < 0 ? k + n : (k >= n ? k - n : k);
+        if ((unsigned)k >= (unsigned)n) {
+            k %= n;
+            k = k < 0 ? k + n : k;
+        }
+        return k;
     }
     return k < 0 ? 0 : (k >= n ? n - 1 : k);
 }

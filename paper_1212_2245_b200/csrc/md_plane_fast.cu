@@ -26,8 +26,12 @@ __device__ __forceinline__ int pf_resolve(int k, int n, int periodic) {
     // element). Found by the checked build: a 32-wide frame read past its buffer with the
     // single conditional wrap this replaced.
     if (periodic) {
-        k %= n;
-        return k < 0 ? k + n : k;
+        k = k < 0 ? k + n : (k >= n ? k - n : k);          // the common case: within one extent
+        if ((unsigned)k >= (unsigned)n) {                   // small frames: a full wrap
+            k %= n;
+            k = k < 0 ? k + n : k;
+        }
+        return k;
     }
     return k < 0 ? 0 : (k >= n ? n - 1 : k);
 }
