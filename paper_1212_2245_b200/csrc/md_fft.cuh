@@ -39,22 +39,26 @@ __device__ __forceinline__ C mul_mi(C a) {          // a * (-i)
 // W_{2h}^k, k < h, at tws[h - 1 + k] (n - 1 entries in all), so consecutive lanes of a stage
 // read consecutive entries -- the natural table read at tw[k << shift] strides the banks. Filled
 // by a block from the plan's natural table twg[k] = W_n^k, k < n/2.
-template <typename C>
+// BD: the block size when the caller knows it at compile time (0: blockDim.x) -- with the
+// length also a compile-time constant the loops below unroll and their index math folds
+template <int BD = 0, typename C>
 __device__ __forceinline__ void stage_twiddles(C *tws, const C *__restrict__ twg, int log2n) {
     const int n = 1 << log2n;
-    for (int i = threadIdx.x; i < n - 1; i += blockDim.x) {
+    const int bd = BD ? BD : (int)blockDim.x;
+    for (int i = threadIdx.x; i < n - 1; i += bd) {
         const int lh = 31 - __clz(i + 1), h = 1 << lh;     // stage of entry i
         tws[i] = twg[(i - (h - 1)) << (log2n - 1 - lh)];   // W_{2h}^k = W_n^{k n / 2h}
     }
 }
 
-template <bool STAGED = false, typename C>
-__device__ void fft_dif_lines(C *s, int log2n, int nl, int stride, const C *__restrict__ tw) {
+template <bool STAGED = false, int BD = 0, typename C>
+__device__ __forceinline__ void fft_dif_lines(C *s, int log2n, int nl, int stride, const C *__restrict__ tw) {
     const int n = 1 << log2n;
+    const int bd = BD ? BD : (int)blockDim.x;
     int lh = log2n - 1;
     if (log2n & 1) {                               // lone radix-2 stage, half = n/2
         const int half = n >> 1;
-        for (int b = threadIdx.x; b < (nl << lh); b += blockDim.x) {
+        for (int b = threadIdx.x; b < (nl << lh); b += bd) {
             const int l = b >> lh, k = b & (half - 1);
             C *row = s + l * stride;
             const C a = row[fpad<sizeof(C)>(k)], c = row[fpad<sizeof(C)>(k + half)];
@@ -67,7 +71,7 @@ __device__ void fft_dif_lines(C *s, int log2n, int nl, int stride, const C *__re
     const int lu = log2n - 2;                      // log2(n/4) units per line
     for (; lh >= 1; lh -= 2) {
         const int h = 1 << lh, q = h >> 1;
-        for (int u = threadIdx.x; u < (nl << lu); u += blockDim.x) {
+        for (int u = threadIdx.x; u < (nl << lu); u += bd) {
             const int l = u >> lu, uu = u & ((n >> 2) - 1);
             const int k = uu & (q - 1);
             const int i0 = ((uu >> (lh - 1)) << (lh + 1)) + k;
@@ -87,15 +91,16 @@ __device__ void fft_dif_lines(C *s, int log2n, int nl, int stride, const C *__re
 }
 
 // inverse (conjugate twiddles), bit-reversed in -> natural out, unscaled
-template <bool STAGED = false, typename C>
-__device__ void fft_dit_inv_lines(C *s, int log2n, int nl, int stride, const C *__restrict__ tw) {
+template <bool STAGED = false, int BD = 0, typename C>
+__device__ __forceinline__ void fft_dit_inv_lines(C *s, int log2n, int nl, int stride, const C *__restrict__ tw) {
     const int n = 1 << log2n;
+    const int bd = BD ? BD : (int)blockDim.x;
     const int hb = log2n - 1;
     const int lu = log2n - 2;
     int lh = 0;
     for (; lh + 1 <= hb; lh += 2) {                // stages half = 2^lh and 2^(lh+1)
         const int q = 1 << lh, h = q << 1;
-        for (int u = threadIdx.x; u < (nl << lu); u += blockDim.x) {
+        for (int u = threadIdx.x; u < (nl << lu); u += bd) {
             const int l = u >> lu, uu = u & ((n >> 2) - 1);
             const int k = uu & (q - 1);
             const int i0 = ((uu >> lh) << (lh + 2)) + k;
@@ -118,7 +123,7 @@ __device__ void fft_dit_inv_lines(C *s, int log2n, int nl, int stride, const C *
     }
     if (lh == hb) {                                // lone radix-2 stage, half = n/2
         const int half = n >> 1;
-        for (int b = threadIdx.x; b < (nl << hb); b += blockDim.x) {
+        for (int b = threadIdx.x; b < (nl << hb); b += bd) {
             const int l = b >> hb, k = b & (half - 1);
             C *row = s + l * stride;
             const C t = cmulc(row[fpad<sizeof(C)>(k + half)], tw[STAGED ? half - 1 + k : k]);

@@ -13,136 +13,9 @@
 //
 // Generic line geometry: line (a, b) starts at a*sa + b*sb and has L elements at stride es;
 // a block transforms G lines with consecutive b.
-#include "md_fft.cuh"
-#include "md_fft_big.h"
+#include "md_fft_big_kernel.cuh"
 
 namespace md {
-
-// LINE_FAST: contiguous lines (es == 1); TW: the inter-pass twiddle mode (TW_NONE / FWD / INV),
-// compile-time so that each pass carries only its own epilogue
-template <typename T, bool LINE_FAST, int TW>
-__global__ void __launch_bounds__(256)
-k_subfft(SubFftArgs a) {
-    using C = cx_t<T>;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    C *s = reinterpret_cast<C *>(smem_raw);
-    const int L = 1 << a.log2L, G = a.G, ls = fline_stride<sizeof(C)>(L);   // padded line stride (md_fft.cuh)
-    const int blocks_b = (a.B + G - 1) / G;
-    const int ai = blockIdx.x / blocks_b, b0 = (blockIdx.x - ai * blocks_b) * G;
-    const int64_t fr = blockIdx.y;
-    C *z = static_cast<C *>(a.z) + fr * a.frame;
-    const T *ra = a.ra ? static_cast<const T *>(a.ra) + fr * a.rframe : nullptr;
-    const T *rb = a.rb ? static_cast<const T *>(a.rb) + fr * a.rframe : nullptr;
-    // offsets within a frame fit 32 bits (launch_subfft checks frame < 2^31): cheaper address math
-    const int sb = (int)a.sb, es = (int)a.es;
-    const int base = ai * (int)a.sa + b0 * sb;
-    constexpr bool line_fast = LINE_FAST;      // contiguous lines: iterate along the line
-    constexpr int U = 4;                       // global loads in flight per thread
-    const int n = G * L, bd = blockDim.x;
-    const int lg = 31 - __clz(G);              // G is a power of two
-    auto coords = [&](int idx, int &g, int &e) {
-        if (line_fast) { g = idx >> a.log2L; e = idx & (L - 1); }
-        else { e = idx >> lg; g = idx & (G - 1); }
-    };
-    for (int i0 = threadIdx.x; i0 < n; i0 += U * bd) {
-        C v[U];
-#pragma unroll
-        for (int k = 0; k < U; ++k) {
-            const int idx = i0 + k * bd;
-            int g, e;
-            coords(idx, g, e);
-            v[k] = mkc<T>(T(0), T(0));
-            if (idx < n && b0 + g < a.B) {
-                const int o = base + g * sb + e * es;
-                if (ra) v[k] = mkc<T>(ra[o], rb ? rb[o] : T(0));
-                else v[k] = z[o];
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < U; ++k) {
-            const int idx = i0 + k * bd;
-            if (idx >= n) break;
-            int g, e;
-            coords(idx, g, e);
-            s[g * ls + fpad<sizeof(C)>(e)] = v[k];
-        }
-    }
-    C *twL = s + G * ls;                       // sub-transform twiddles staged in shared memory
-    stage_twiddles(twL, static_cast<const C *>(a.twL), a.log2L);   // stage-major (md_fft.cuh)
-    __syncthreads();
-    const C *filt = static_cast<const C *>(a.filt);
-    if (TW == TW_FILT_INV) {
-        fft_dif_lines<true>(s, a.log2L, G, ls, twL);
-        for (int idx = threadIdx.x; idx < n; idx += bd) {
-            int g, e;
-            coords(idx, g, e);
-            if (b0 + g >= a.B) continue;
-            const C fl = filt[base + g * sb + e * es];
-            C &v = s[g * ls + fpad<sizeof(C)>(e)];
-            v = a.conj_filt ? cmulc(v, fl) : cmul(v, fl);
-        }
-        __syncthreads();
-        fft_dit_inv_lines<true>(s, a.log2L, G, ls, twL);
-    } else if (a.inv) {
-        fft_dit_inv_lines<true>(s, a.log2L, G, ls, twL);
-    } else {
-        fft_dif_lines<true>(s, a.log2L, G, ls, twL);
-    }
-    // inter-pass twiddle W_N^{+-(digit * rev(pos))}, digit = line (FWD) or element (INV) index
-    const C *twN = static_cast<const C *>(a.twN);
-    const int N = a.N;
-    const T scale = T(a.scale);
-    constexpr bool FILT_EPI = TW != TW_FILT_INV;        // the fused mode filtered in shared memory
-    constexpr int TWM = TW == TW_FILT_INV ? TW_INV : TW;
-    T *wu = static_cast<T *>(a.wu), *wfp = static_cast<T *>(a.wfpos);
-    const T *wf = static_cast<const T *>(a.wf);
-    const T wfloor = T(a.floor);
-    for (int i0 = threadIdx.x; i0 < n; i0 += U * bd) {
-        // table and filter operands first: loads after the z stores below would wait on them
-        C tw[U], fl[U];
-#pragma unroll
-        for (int k = 0; k < U; ++k) {
-            const int idx = i0 + k * bd;
-            int g, e;
-            coords(idx, g, e);
-            tw[k] = fl[k] = mkc<T>(T(1), T(0));
-            if (idx >= n || b0 + g >= a.B) continue;
-            if (TWM != TW_NONE) {
-                const int lb = a.tw_digit_is_a ? ai : b0 + g;                 // line digit
-                const int re = (int)(__brev((unsigned)e) >> (32 - a.log2L));   // rev(pos) in the line
-                const int rl = (int)(__brev((unsigned)lb) >> (32 - a.log2Lother));
-                // FWD (after F1): W_N^{line * rev(e)};  INV (after I2): conj W_N^{e * rev(line)}
-                const int kk = TWM == TW_FWD ? (int)(((int64_t)lb * re) & (N - 1)) : (int)(((int64_t)e * rl) & (N - 1));
-                const C w = twN[kk & (N / 2 - 1)];
-                tw[k] = kk < N / 2 ? w : mkc<T>(-w.x, -w.y);
-            }
-            if (FILT_EPI && filt) fl[k] = filt[base + g * sb + e * es];
-        }
-#pragma unroll
-        for (int k = 0; k < U; ++k) {
-            const int idx = i0 + k * bd;
-            int g, e;
-            coords(idx, g, e);
-            if (idx >= n || b0 + g >= a.B) continue;
-            C v = s[g * ls + fpad<sizeof(C)>(e)];
-            if (TWM != TW_NONE) v = TWM == TW_FWD ? cmul(v, tw[k]) : cmulc(v, tw[k]);
-            if (FILT_EPI && filt) v = a.conj_filt ? cmulc(v, fl[k]) : cmul(v, fl[k]);
-            if (scale != T(1)) v = cscale(v, scale);
-            const int o = base + g * sb + e * es;
-            if (TW == TW_NONE && wu) {
-                // Wiener epilogue (deconv.py:666-672): real part, clamp, floored observation
-                const T x = v.x;
-                wu[fr * a.rframe + o] = a.clamp ? (x > wfloor ? x : wfloor) : x;
-                if (wfp) {
-                    const T fv = wf[fr * a.rframe + o];
-                    wfp[fr * a.rframe + o] = fv > wfloor ? fv : wfloor;
-                }
-            } else {
-                z[o] = v;
-            }
-        }
-    }
-}
 
 // u0 = max(Re z * scale, floor) (or unclamped), fpos = max(f, floor)
 template <typename T>
@@ -169,11 +42,13 @@ cudaError_t launch_subfft(const SubFftArgs &a0, int64_t batch, cudaStream_t st) 
     const size_t smem = ((size_t)a.G * fline_stride<sizeof(cx_t<T>)>(L) + L + 1) * sizeof(cx_t<T>);
     auto pick = [&](auto lf) {
         constexpr bool LF = decltype(lf)::value;
-        return a.tw_mode == TW_FWD ? k_subfft<T, LF, TW_FWD>
-               : (a.tw_mode == TW_INV ? k_subfft<T, LF, TW_INV>
-                                      : (a.tw_mode == TW_FILT_INV ? k_subfft<T, LF, TW_FILT_INV> : k_subfft<T, LF, TW_NONE>));
+        return a.tw_mode == TW_FWD ? k_subfft<T, LF, TW_FWD, 0>
+               : (a.tw_mode == TW_INV ? k_subfft<T, LF, TW_INV, 0>
+                                      : (a.tw_mode == TW_FILT_INV ? k_subfft<T, LF, TW_FILT_INV, 0> : k_subfft<T, LF, TW_NONE, 0>));
     };
-    auto kern = a.es == 1 ? pick(std::true_type{}) : pick(std::false_type{});
+    using KernT = void (*)(SubFftArgs);
+    KernT kern = subfft_ct_kernel<T>(a.log2L, a.es == 1, a.tw_mode);      // compile-time length, if any
+    if (!kern) kern = a.es == 1 ? pick(std::true_type{}) : pick(std::false_type{});
     cudaError_t e = func_smem_attr((const void *)kern, smem);
     if (e != cudaSuccess) return e;
     const int blocks_b = (a.B + a.G - 1) / a.G;

@@ -39,6 +39,9 @@ struct BigAxis {
 
 void split_axis(int N, int *N1, int *N2);
 template <typename T> cudaError_t launch_subfft(const SubFftArgs &, int64_t batch, cudaStream_t);
+// the pass kernel specialised for a compile-time sub-transform length 2^6 .. 2^10 (float64;
+// md_fft_big_ct.cu), or nullptr (then the generic kernel runs)
+template <typename T> void (*subfft_ct_kernel(int log2L, bool line_fast, int tw_mode))(SubFftArgs);
 template <typename T>
 cudaError_t big_axis(const BigAxis &ax, void *z, int H, int W, int axis, int inv, const void *ra, const void *rb,
                      const void *filt, int conj_filt, double scale_last, int64_t batch, cudaStream_t st);
