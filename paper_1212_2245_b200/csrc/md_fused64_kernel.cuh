@@ -29,6 +29,7 @@
 #include <cooperative_groups.h>
 
 #include <tuple>
+#include <cstdlib>
 
 #include "md_fused_kernel.cuh"
 
@@ -512,7 +513,11 @@ inline int pick_cluster(const void *kern, size_t smem, int threads, int m, int r
     auto it = memo.find(key);
     if (it == memo.end()) {
         int best = 0, best_n = 0, best_rounds = 1;
+        // MD_F64_CLUSTER=k (measurement knob): only cluster size k is considered
+        const char *force = std::getenv("MD_F64_CLUSTER");
+        const int fcl = force ? std::atoi(force) : 0;
         for (int cl = std::max(2, (m + rlmax - 1) / rlmax); cl <= 16 && m / cl >= 4; ++cl) {
+            if (fcl > 0 && cl != fcl) continue;
             cudaLaunchConfig_t q = {};
             q.gridDim = dim3((unsigned)cl, 1, 1);
             q.blockDim = dim3((unsigned)threads, 1, 1);
@@ -529,10 +534,13 @@ inline int pick_cluster(const void *kern, size_t smem, int threads, int m, int r
                 cudaGetLastError();
                 continue;
             }
-            // throughput ~ frames in flight / line rounds per frame (a warp's lines run in turn)
+            // throughput ~ frames in flight / line rounds per frame (a warp's lines run in turn);
+            // on a tie the size that keeps more SMs busy (c1: 9 x 15 = 135 SMs at 29 lines per
+            // CTA ran 1.7 % faster than 8 x 15 = 120 at 32 lines, scripts/r2_cl_ab.sh)
             const int nw = threads / 32;
             const int rounds = ((m + cl - 1) / cl + nw - 1) / nw;
-            if (best == 0 || (int64_t)n * best_rounds > (int64_t)best_n * rounds) {
+            const int64_t lhs = (int64_t)n * best_rounds, rhs = (int64_t)best_n * rounds;
+            if (best == 0 || lhs > rhs || (lhs == rhs && n * cl > best_n * best)) {
                 best = cl; best_n = n; best_rounds = rounds;
             }
         }
