@@ -128,4 +128,109 @@ __device__ __forceinline__ void col_taps_pair2(const typename Vec2<T>::type *s, 
     }
 }
 
+// R output rows per thread (the pair kernels above are R = 2): walking a column of len taps
+// from its first tap, loaded value i feeds output row r with tap i - r (0 <= i - r < len), so
+// R rows cost len + R - 1 loads per column instead of R (len + 1) / 2 -- each row's sum still
+// runs over the same taps in the same order (columns in turn, taps top to bottom), so the
+// results equal the pair kernels' bit for bit. The head (i < R - 1) and tail (i >= len) steps,
+// where only some rows take part, are unrolled; the middle steps feed all R rows. The R
+// weights of a step are a register window shifted by one table read per step.
+// V: the loaded element (T, or Vec2<T> for the adjoint pair); F(acc_row, w, v): the update
+template <typename T, typename V, int R, int J, int XS, bool SHORT, typename Acc, typename F>
+__device__ __forceinline__ void col_walk_one(const V *p, int rs, const T *wc, int len, Acc (&acc)[R][J], F upd) {
+    // SHORT = false: len >= R - 1, so every head step is a tap of its rows and every tail step
+    // lies past the head -- no per-step predicates (the common case); SHORT: any len
+    T w[R];                                       // w[r] = wc[i - r] at step i
+#pragma unroll
+    for (int r = 0; r < R; ++r) w[r] = T(0);
+    // head: steps 0 .. R-2 (rows 0 .. i)
+#pragma unroll
+    for (int i = 0; i < R - 1; ++i) {
+#pragma unroll
+        for (int r = R - 1; r > 0; --r) w[r] = w[r - 1];
+        w[0] = (!SHORT || i < len) ? wc[i] : T(0);
+        V v[J];
+#pragma unroll
+        for (int j = 0; j < J; ++j) v[j] = p[XS * j];
+#pragma unroll
+        for (int r = 0; r <= i; ++r)
+            if (!SHORT || i - r < len) {
+#pragma unroll
+                for (int j = 0; j < J; ++j) upd(acc[r][j], w[r], v[j]);
+            }
+        p += rs;
+    }
+    // middle: steps R-1 .. len-1, every row
+    for (int i = R - 1; i < len; ++i) {
+#pragma unroll
+        for (int r = R - 1; r > 0; --r) w[r] = w[r - 1];
+        w[0] = wc[i];
+        V v[J];
+#pragma unroll
+        for (int j = 0; j < J; ++j) v[j] = p[XS * j];
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int j = 0; j < J; ++j) upd(acc[r][j], w[r], v[j]);
+        p += rs;
+    }
+    // tail: steps i = len + t (t = 0 .. R-2) not already taken by the head; rows t+1 .. R-1
+    // (and r <= i). When len < R - 1 the pointer already stands at step R - 1.
+#pragma unroll
+    for (int t = 0; t < R - 1; ++t) {
+        const int i = len + t;
+        if (SHORT && i < R - 1) continue;
+#pragma unroll
+        for (int r = R - 1; r > 0; --r) w[r] = w[r - 1];
+        w[0] = T(0);
+        V v[J];
+#pragma unroll
+        for (int j = 0; j < J; ++j) v[j] = p[XS * j];
+#pragma unroll
+        for (int r = t + 1; r < R; ++r)
+            if (!SHORT || r <= i) {
+#pragma unroll
+                for (int j = 0; j < J; ++j) upd(acc[r][j], w[r], v[j]);
+            }
+        p += rs;
+    }
+}
+
+template <typename T, typename V, int R, int J, int XS, typename Acc, typename F>
+__device__ __forceinline__ void col_walk_rows(const V *s, int rs, const ColTaps<T> &tp, Acc (&acc)[R][J], F upd) {
+    for (int c = 0; c < tp.ncol; ++c) {
+        const int2 ci = tp.c[c];
+        const int len = ci.y & 0xffff;
+        const T *wc = tp.w + (ci.y >> 16);
+        // the branch is uniform (every thread walks the same column)
+        if (len >= R - 1) col_walk_one<T, V, R, J, XS, false>(s + ci.x, rs, wc, len, acc, upd);
+        else col_walk_one<T, V, R, J, XS, true>(s + ci.x, rs, wc, len, acc, upd);
+    }
+}
+
+// blur of R rows: a[r][j] = sum w u
+template <typename T, int R, int J, int XS>
+__device__ __forceinline__ void col_taps_rows(const T *s, int rs, const ColTaps<T> &tp, T (&a)[R][J]) {
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int j = 0; j < J; ++j) a[r][j] = T(0);
+    col_walk_rows<T, T, R, J, XS>(s, rs, tp, a, [](T &acc, T w, T v) { acc += w * v; });
+}
+
+// adjoint pair of R rows over interleaved (p, W): nd[r][j].x = sum w p, .y = sum w W
+template <typename T, int R, int J, int XS>
+__device__ __forceinline__ void col_taps_rows2(const typename Vec2<T>::type *s, int rs, const ColTaps<T> &tp,
+                                               typename Vec2<T>::type (&nd)[R][J]) {
+    using T2 = typename Vec2<T>::type;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int j = 0; j < J; ++j) nd[r][j].x = nd[r][j].y = T(0);
+    col_walk_rows<T, T2, R, J, XS>(s, rs, tp, nd, [](T2 &acc, T w, T2 v) {
+        acc.x += w * v.x;
+        acc.y += w * v.y;
+    });
+}
+
 }  // namespace md

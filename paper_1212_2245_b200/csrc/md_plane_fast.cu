@@ -5,11 +5,12 @@
 // 359-376, 512-521) together with _weight_arrays (142-162), _diffusion_arrays (187-213) and
 // _combine (421-446).
 //
-// Tile 64 x 32 outputs per block, 256 threads; thread (pair tp, column cx) owns the outputs
-// of rows 2tp, 2tp+1 at x = cx + 16 r (r = 0..3), so a half-warp reads 16 consecutive
-// shared-memory words per tap. Taps are regrouped on the host into columns (md_coltaps.cuh):
-// each loaded value feeds both rows of the pair. Stage B stages p and W interleaved, so one
-// load feeds both halves of the adjoint pair.
+// Tile 64 x 32 outputs per block, 256 threads; thread (row group tp, column cx) owns the
+// outputs of rows PR tp .. PR tp + PR-1 at x = cx + PX r (round 2: PR = 4 rows x 2 columns at
+// stride 32, a warp reads 32 consecutive shared-memory elements per tap; round 1: row pairs x 4
+// columns at stride 16). Taps are regrouped on the host into columns (md_coltaps.cuh): each
+// loaded value feeds all PR rows. Stage B stages p and W interleaved, so one load feeds both
+// halves of the adjoint pair.
 #include "md_plane.h"
 #include "md_plane_fast.h"
 #include "md_linefast.cuh"
@@ -17,7 +18,16 @@
 namespace md {
 
 constexpr int FX = 64, FY = 32;           // output tile
-constexpr int PJ = 4;                     // outputs per row per thread (column stride 16)
+#ifndef MD_PLANE_ROWS
+#define MD_PLANE_ROWS 4
+#endif
+// thread = PR consecutive output rows x PJ columns at stride PX (256 threads cover the tile):
+// PR = 4 rows cost len + 3 shared loads per tap column for 4 rows, the row pair len + 1 for 2
+// (md_coltaps.cuh); the sums, and so the results, are the same
+constexpr int PR = MD_PLANE_ROWS;
+constexpr int PJ = 8 / PR;                // outputs per row per thread
+constexpr int PX = FX / PJ;               // their column stride (= the threads per row)
+static_assert(PR * PJ == 8 && (FY / PR) * PX == 256, "tile / thread mapping");
 constexpr int PS = 72;                    // u / g tile stride: 2 * PS = 16 (mod 32) -> half-warps on disjoint banks
 
 __device__ __forceinline__ int pf_resolve(int k, int n, int periodic) {
@@ -148,28 +158,28 @@ k_plane_a_fast(PlaneFastArgs<T> a) {
     pf_load<T>(su, ss, H, W, y0, x0, a.hb, a.periodic, a.slab, a.ylo, a.yhi, [&](int64_t o) { return u[o]; });
 #endif
     __syncthreads();
-    const int tp = threadIdx.x >> 4, cx = threadIdx.x & 15;
-    const int yp = y0 + 2 * tp;
+    const int tp = threadIdx.x / PX, cx = threadIdx.x % PX;
+    const int yp = y0 + PR * tp;
     if (yp >= H) return;
     // observation first: loads issued after the p / W stores below would wait for them
-    T fv[2][PJ];
+    T fv[PR][PJ];
 #pragma unroll
-    for (int k = 0; k < 2; ++k)
+    for (int k = 0; k < PR; ++k)
 #pragma unroll
         for (int r = 0; r < PJ; ++r) {
-            const int x = x0 + cx + 16 * r;
+            const int x = x0 + cx + PX * r;
             fv[k][r] = (x < W && yp + k < H) ? f[(int64_t)(yp + k) * W + x] : T(1);
         }
-    T b[2][PJ];
-    col_taps_pair<T, PJ, 16>(su + (2 * tp + a.hb.ht) * ss + a.hb.hl + cx, ss, a.tb, b[0], b[1]);
+    T b[PR][PJ];
+    col_taps_rows<T, PR, PJ, PX>(su + (PR * tp + a.hb.ht) * ss + a.hb.hl + cx, ss, a.tb, b);
     const T eps_d2 = a.eps_d2;
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < PR; ++k) {
         const int y = yp + k;
         if (y >= H) break;
 #pragma unroll
         for (int r = 0; r < PJ; ++r) {
-            const int x = x0 + cx + 16 * r;
+            const int x = x0 + cx + PX * r;
             if (x >= W) continue;
             const int64_t o = (int64_t)y * W + x;
             const T bb = b[k][r] > T(kGuard) ? b[k][r] : T(kGuard);
@@ -216,6 +226,26 @@ k_plane_b_fast(PlaneFastArgs<T> a) {
 #endif
     }
     const int gy0 = a.gy0, Hg = a.Hg;
+#if MD_PLANE_CP_ASYNC
+    {
+        // u with a 2-pixel halo (zero outside the frame / slab): cp.async as well (zero-fill
+        // for the outside positions), so the whole tile set is in flight before one wait
+        constexpr int UC = FX + 4;
+        const int n = (FY + 4) * UC;
+        for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
+            const int i = idx / UC, j = idx - i * UC;
+            const int yy = y0 - 2 + i, xx = x0 - 2 + j;
+            const bool ok = gy0 + yy >= 0 && gy0 + yy < Hg && (a.slab ? (yy >= a.ylo && yy < a.yhi) : (yy >= 0 && yy < H)) &&
+                            xx >= 0 && xx < W;
+            const uint32_t d = (uint32_t)__cvta_generic_to_shared(su + i * PS + j);
+            const T *src = ok ? u + (int64_t)yy * W + xx : u;
+            if (sizeof(T) == 8)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(ok ? 8 : 0) : "memory");
+            else
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(ok ? 4 : 0) : "memory");
+        }
+    }
+#else
     {
         constexpr int U = 4, UC = FX + 4;
         const int n = (FY + 4) * UC, bd = blockDim.x;
@@ -241,6 +271,7 @@ k_plane_b_fast(PlaneFastArgs<T> a) {
             }
         }
     }
+#endif
 #if MD_PLANE_CP_ASYNC
     cp_async_wait_all();
 #endif
@@ -266,20 +297,20 @@ k_plane_b_fast(PlaneFastArgs<T> a) {
         }
         __syncthreads();
     }
-    const int tp = threadIdx.x >> 4, cx = threadIdx.x & 15;
-    const int ty0 = 2 * tp;
+    const int tp = threadIdx.x / PX, cx = threadIdx.x % PX;
+    const int ty0 = PR * tp;
     if (y0 + ty0 >= H) return;
-    T num[2][PJ], den[2][PJ];
-    col_taps_pair2<T, PJ, 16>(spw + (ty0 + a.ha.ht) * ss + a.ha.hl + cx, ss, a.ta, num[0], num[1], den[0], den[1]);
+    T2 nd[PR][PJ];
+    col_taps_rows2<T, PR, PJ, PX>(spw + (ty0 + a.ha.ht) * ss + a.ha.hl + cx, ss, a.ta, nd);
     const T alpha = a.alpha;
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < PR; ++k) {
         const int ty = ty0 + k;
         const int y = y0 + ty;
         if (y >= H) break;
 #pragma unroll
         for (int r = 0; r < PJ; ++r) {
-            const int tx = cx + 16 * r;
+            const int tx = cx + PX * r;
             const int x = x0 + tx;
             if (x >= W) continue;
             const T *c = su + (ty + 2) * PS + (tx + 2);
@@ -293,8 +324,8 @@ k_plane_b_fast(PlaneFastArgs<T> a) {
                 if (gy0 + y + 1 < Hg) d += (gc + g[PS]) * (c[PS] - uv);
                 if (gy0 + y > 0) d -= (g[-PS] + gc) * (uv - c[-PS]);
             }
-            T nm = num[k][r];
-            T dn = ROBUST ? den[k][r] : T(1);
+            T nm = nd[k][r].x;
+            T dn = ROBUST ? nd[k][r].y : T(1);
             if (a.has_d) {
                 nm += alpha * (d > T(0) ? d : T(0));
                 dn -= alpha * (d < T(0) ? d : T(0));
