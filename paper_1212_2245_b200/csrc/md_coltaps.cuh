@@ -196,13 +196,52 @@ __device__ __forceinline__ void col_walk_one(const V *p, int rs, const T *wc, in
     }
 }
 
+// a column of exactly LEN taps, fully unrolled: no loop, no predicates; the LEN weights are
+// read once (uniform registers) -- the common short columns of line / small 2D PSFs
+template <typename T, typename V, int R, int J, int XS, int LEN, typename Acc, typename F>
+__device__ __forceinline__ void col_walk_fixed(const V *p, int rs, const T *wc, Acc (&acc)[R][J], F upd) {
+    T w[LEN];
+#pragma unroll
+    for (int k = 0; k < LEN; ++k) w[k] = wc[k];
+#pragma unroll
+    for (int i = 0; i < LEN + R - 1; ++i) {
+        V v[J];
+#pragma unroll
+        for (int j = 0; j < J; ++j) v[j] = p[XS * j];
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+            if (i - r >= 0 && i - r < LEN) {
+#pragma unroll
+                for (int j = 0; j < J; ++j) upd(acc[r][j], w[i - r], v[j]);
+            }
+        p += rs;
+    }
+}
+
+#ifndef MD_COL_FIXED_MAX
+#define MD_COL_FIXED_MAX 8          // columns of up to this many taps take the unrolled walk
+#endif
+template <typename T, typename V, int R, int J, int XS, int LEN, typename Acc, typename F>
+__device__ __forceinline__ bool col_walk_dispatch(const V *p, int rs, const T *wc, int len, Acc (&acc)[R][J], F upd) {
+    if constexpr (LEN > MD_COL_FIXED_MAX) {
+        return false;
+    } else {
+        if (len == LEN) {
+            col_walk_fixed<T, V, R, J, XS, LEN>(p, rs, wc, acc, upd);
+            return true;
+        }
+        return col_walk_dispatch<T, V, R, J, XS, LEN + 1>(p, rs, wc, len, acc, upd);
+    }
+}
+
 template <typename T, typename V, int R, int J, int XS, typename Acc, typename F>
 __device__ __forceinline__ void col_walk_rows(const V *s, int rs, const ColTaps<T> &tp, Acc (&acc)[R][J], F upd) {
     for (int c = 0; c < tp.ncol; ++c) {
         const int2 ci = tp.c[c];
         const int len = ci.y & 0xffff;
         const T *wc = tp.w + (ci.y >> 16);
-        // the branch is uniform (every thread walks the same column)
+        // the branches are uniform (every thread walks the same column)
+        if (col_walk_dispatch<T, V, R, J, XS, 1>(s + ci.x, rs, wc, len, acc, upd)) continue;
         if (len >= R - 1) col_walk_one<T, V, R, J, XS, false>(s + ci.x, rs, wc, len, acc, upd);
         else col_walk_one<T, V, R, J, XS, true>(s + ci.x, rs, wc, len, acc, upd);
     }

@@ -24,10 +24,15 @@ constexpr int FX = 64, FY = 32;           // output tile
 // thread = PR consecutive output rows x PJ columns at stride PX (256 threads cover the tile):
 // PR = 4 rows cost len + 3 shared loads per tap column for 4 rows, the row pair len + 1 for 2
 // (md_coltaps.cuh); the sums, and so the results, are the same
-constexpr int PR = MD_PLANE_ROWS;
-constexpr int PJ = 8 / PR;                // outputs per row per thread
-constexpr int PX = FX / PJ;               // their column stride (= the threads per row)
-static_assert(PR * PJ == 8 && (FY / PR) * PX == 256, "tile / thread mapping");
+#ifndef MD_PLANE_ROWS_B
+#define MD_PLANE_ROWS_B MD_PLANE_ROWS
+#endif
+template <int R> struct PlaneMap {
+    static constexpr int PR = R;
+    static constexpr int PJ = 8 / R;           // outputs per row per thread
+    static constexpr int PX = FX / PJ;         // their column stride (= the threads per row)
+    static_assert(PR * PJ == 8 && (FY / PR) * PX == 256, "tile / thread mapping");
+};
 constexpr int PS = 72;                    // u / g tile stride: 2 * PS = 16 (mod 32) -> half-warps on disjoint banks
 
 __device__ __forceinline__ int pf_resolve(int k, int n, int periodic) {
@@ -140,6 +145,7 @@ template <typename T> __host__ __device__ inline int pf_stride_b(const PlaneHalo
 template <typename T, bool ROBUST>
 __global__ void __launch_bounds__(256)
 k_plane_a_fast(PlaneFastArgs<T> a) {
+    constexpr int PR = PlaneMap<MD_PLANE_ROWS>::PR, PJ = PlaneMap<MD_PLANE_ROWS>::PJ, PX = PlaneMap<MD_PLANE_ROWS>::PX;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T *su = reinterpret_cast<T *>(smem_raw);
     const int H = a.H, W = a.W;
@@ -198,6 +204,7 @@ k_plane_a_fast(PlaneFastArgs<T> a) {
 template <typename T, bool ROBUST>
 __global__ void __launch_bounds__(256)
 k_plane_b_fast(PlaneFastArgs<T> a) {
+    constexpr int PR = PlaneMap<MD_PLANE_ROWS_B>::PR, PJ = PlaneMap<MD_PLANE_ROWS_B>::PJ, PX = PlaneMap<MD_PLANE_ROWS_B>::PX;
     using T2 = typename Vec2<T>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int H = a.H, W = a.W;
