@@ -135,4 +135,91 @@ __device__ __forceinline__ void fft_dit_inv_lines(C *s, int log2n, int nl, int s
     }
 }
 
+// ---- compile-time-length variants: several stages per shared-memory round trip --------------
+// With the length and the line count known at compile time, a thread can hold 2^NS elements of
+// a line in registers and run NS consecutive radix-2 stages on them before writing back (one
+// load/store + one barrier per group of stages instead of per radix-4 unit). The butterflies,
+// their twiddle operands and their order per element are exactly those of fft_dif_lines /
+// fft_dit_inv_lines with STAGED twiddles -- including which twiddles come from the table and
+// which are the exact (-i) rotation of a table entry (the second pair of a radix-4 unit) --
+// -- the same operations, but not bit-identical results: see fft_dif_lines_ct below.
+//
+// DIF stage with half size hs = 2^lh (stages run lh = log2n-1 .. 0): `mi` marks the first stage
+// of a radix-4 unit, whose pairs at positions p >= hs/2 use -i * table[p - hs/2]
+template <int LOG2N>
+__device__ __forceinline__ constexpr bool dif_stage_mi(int lh) {
+    return !((LOG2N & 1) && lh == LOG2N - 1) && (((LOG2N - 1 - (LOG2N & 1)) - lh) % 2 == 0);
+}
+// DIT (inverse) stages run lh = 0 .. log2n-1; units pair (lh, lh+1) for even lh, the second
+// (odd lh) uses the rotation; an odd count leaves a lone plain stage at the top
+__device__ __forceinline__ constexpr bool dit_stage_mi(int lh) { return (lh & 1) != 0; }
+
+// one group of NS stages, top stage LT (DIF: LT, LT-1, .., LB; DIT: LB, .., LT), over NL lines
+template <int LOG2N, int LT, int NS, bool INV, int NL, int BD, typename C>
+__device__ __forceinline__ void fft_group_ct(C *s, int stride, const C *__restrict__ tw) {
+    constexpr int LB = LT - NS + 1, E = 1 << NS, SB = 1 << LB;
+    constexpr int LOG2UPL = LOG2N - NS;                 // units (thread tasks) per line
+    constexpr int NU = NL << LOG2UPL;
+    static_assert(LB >= 0 && LT < LOG2N, "stage group out of range");
+#pragma unroll 1
+    for (int u = threadIdx.x; u < NU; u += BD) {
+        const int l = u >> LOG2UPL, r = u & ((1 << LOG2UPL) - 1);
+        const int k = r & (SB - 1), blk = r >> LB;
+        const int base = (blk << (LT + 1)) + k;
+        C *row = s + l * stride;
+        C v[E];
+#pragma unroll
+        for (int j = 0; j < E; ++j) v[j] = row[fpad<sizeof(C)>(base + (j << LB))];
+#pragma unroll
+        for (int st = 0; st < NS; ++st) {
+            const int lh = INV ? LB + st : LT - st;
+            const int hs = 1 << lh, q = hs >> 1, js = 1 << (lh - LB);
+            const bool mi = INV ? dit_stage_mi(lh) : dif_stage_mi<LOG2N>(lh);
+#pragma unroll
+            for (int j = 0; j < E; ++j) {
+                if (j & js) continue;
+                const int p = k + ((j << LB) & (hs - 1));          // position in the half
+                C w;
+                if (mi) {
+                    const C w0 = tw[hs - 1 + (p & (q - 1))];
+                    w = (p & q) ? mul_mi(w0) : w0;
+                } else {
+                    w = tw[hs - 1 + p];
+                }
+                const C a = v[j], c = v[j + js];
+                if (INV) {
+                    const C t = cmulc(c, w);
+                    v[j] = cadd(a, t);
+                    v[j + js] = csub(a, t);
+                } else {
+                    v[j] = cadd(a, c);
+                    v[j + js] = cmul(csub(a, c), w);
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < E; ++j) row[fpad<sizeof(C)>(base + (j << LB))] = v[j];
+    }
+    __syncthreads();
+}
+
+// the whole transform: greedy groups of MD_SUBFFT_GROUPS stages from the top (DIF) / bottom
+// (DIT), the remainder group taking the leftover stages. MEASUREMENT OPTION, off by default
+// (md_fft_big_kernel.cuh): with 3-stage groups the c5 16384^2 Wiener ran 10 % faster (30 %
+// fewer shared wavefronts) but the butterflies of a group split across a radix-4 unit round
+// differently (the compiler contracts a lane-selected rotation differently), and the noise-
+// free c5 problem amplifies that past the parity bar
+template <int LOG2N, int NL, int BD, int GS, int LT = LOG2N - 1, typename C>
+__device__ __forceinline__ void fft_dif_lines_ct(C *s, int stride, const C *__restrict__ tw) {
+    constexpr int NS = LT + 1 < GS ? LT + 1 : GS;
+    fft_group_ct<LOG2N, LT, NS, false, NL, BD>(s, stride, tw);
+    if constexpr (LT + 1 - NS > 0) fft_dif_lines_ct<LOG2N, NL, BD, GS, LT - NS>(s, stride, tw);
+}
+template <int LOG2N, int NL, int BD, int GS, int LB = 0, typename C>
+__device__ __forceinline__ void fft_dit_inv_lines_ct(C *s, int stride, const C *__restrict__ tw) {
+    constexpr int NS = LOG2N - LB < GS ? LOG2N - LB : GS;
+    fft_group_ct<LOG2N, LB + NS - 1, NS, true, NL, BD>(s, stride, tw);
+    if constexpr (LB + NS < LOG2N) fft_dit_inv_lines_ct<LOG2N, NL, BD, GS, LB + NS>(s, stride, tw);
+}
+
 }  // namespace md

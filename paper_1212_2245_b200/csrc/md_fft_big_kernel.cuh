@@ -15,8 +15,27 @@ namespace md {
 // LOG2L = 0: any length, from the arguments
 constexpr int subfft_lines(int log2l) { return (2048 >> log2l) < 1 ? 1 : ((2048 >> log2l) > 16 ? 16 : (2048 >> log2l)); }
 
+// measurement option (off): register stage groups of MD_SUBFFT_GROUPS stages in the
+// constant-length kernels (md_fft.cuh); 3 with MD_SUBFFT_MINB=4 (<= 64 registers) was the
+// fastest variant -- c5 Wiener 17.6 -> 15.8 ms -- but it is not bit-compatible with the
+// parity fixtures. With the option off the kernel is unchanged.
+#ifndef MD_SUBFFT_GROUPS
+#define MD_SUBFFT_GROUPS 0
+#endif
+#if MD_SUBFFT_GROUPS
+#ifndef MD_SUBFFT_MINB
+#define MD_SUBFFT_MINB 4
+#endif
+#define MD_SUBFFT_DIF(...) do { if constexpr (LOG2L > 0) fft_dif_lines_ct<LOG2L, subfft_lines(LOG2L), BD, MD_SUBFFT_GROUPS>(s, ls, twL); else fft_dif_lines<true, BD>(s, log2L, G, ls, twL); } while (0)
+#define MD_SUBFFT_DIT(...) do { if constexpr (LOG2L > 0) fft_dit_inv_lines_ct<LOG2L, subfft_lines(LOG2L), BD, MD_SUBFFT_GROUPS>(s, ls, twL); else fft_dit_inv_lines<true, BD>(s, log2L, G, ls, twL); } while (0)
+#define MD_SUBFFT_BOUNDS __launch_bounds__(256, LOG2L > 0 ? MD_SUBFFT_MINB : 1)
+#else
+#define MD_SUBFFT_DIF(...) fft_dif_lines<true, BD>(s, log2L, G, ls, twL)
+#define MD_SUBFFT_DIT(...) fft_dit_inv_lines<true, BD>(s, log2L, G, ls, twL)
+#define MD_SUBFFT_BOUNDS __launch_bounds__(256)
+#endif
 template <typename T, bool LINE_FAST, int TW, int LOG2L>
-__global__ void __launch_bounds__(256)
+__global__ void MD_SUBFFT_BOUNDS
 k_subfft(SubFftArgs a) {
     using C = cx_t<T>;
     constexpr int BD = 256;                    // launch_subfft always uses 256 threads
@@ -73,7 +92,7 @@ k_subfft(SubFftArgs a) {
     __syncthreads();
     const C *filt = static_cast<const C *>(a.filt);
     if (TW == TW_FILT_INV) {
-        fft_dif_lines<true, BD>(s, log2L, G, ls, twL);
+        MD_SUBFFT_DIF();
         for (int idx = threadIdx.x; idx < n; idx += bd) {
             int g, e;
             coords(idx, g, e);
@@ -83,11 +102,11 @@ k_subfft(SubFftArgs a) {
             v = a.conj_filt ? cmulc(v, fl) : cmul(v, fl);
         }
         __syncthreads();
-        fft_dit_inv_lines<true, BD>(s, log2L, G, ls, twL);
+        MD_SUBFFT_DIT();
     } else if (a.inv) {
-        fft_dit_inv_lines<true, BD>(s, log2L, G, ls, twL);
+        MD_SUBFFT_DIT();
     } else {
-        fft_dif_lines<true, BD>(s, log2L, G, ls, twL);
+        MD_SUBFFT_DIF();
     }
     // inter-pass twiddle W_N^{+-(digit * rev(pos))}, digit = line (FWD) or element (INV) index
     const C *twN = static_cast<const C *>(a.twN);
