@@ -1,7 +1,10 @@
 #!/usr/bin/env python
 """Attribute ncu SASS-level stall samples to CUDA source lines.
 
-    python scripts/sass_lines.py REPORT.ncu-rep CUBIN KERNEL_MANGLED [TOP]
+    python scripts/sass_lines.py REPORT.ncu-rep CUBIN KERNEL_MANGLED [TOP] [COLUMN]
+
+COLUMN (optional): rank lines by that source-page column instead of stall samples, e.g.
+"L1 Wavefronts Shared" (shared-memory wavefronts per source line).
 
 The ncu source page (--print-source sass) gives per-instruction samples by runtime address;
 nvdisasm --print-line-info of the same cubin maps instruction offsets to file:line. The kernel's
@@ -15,6 +18,7 @@ import sys
 
 rep, cubin, kern = sys.argv[1:4]
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
+col = sys.argv[5] if len(sys.argv) > 5 else None
 raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
@@ -32,7 +36,17 @@ si = h.index("Warp Stall Sampling (All Samples)")
 ie = h.index("Instructions Executed")
 reasons = [c for c in h if c.startswith("stall_") and not c.endswith("(Not Issued)")]
 ri = [h.index(c) for c in reasons]
-sass = [(int(r[0], 16), float(r[si] or 0), float(r[ie] or 0), r[1].strip(),
+ci = h.index(col) if col else si
+
+
+def num(x):
+    try:
+        return float(x)
+    except ValueError:
+        return 0.0
+
+
+sass = [(int(r[0], 16), num(r[ci]), float(r[ie] or 0), r[1].strip(),
          [float(r[i] or 0) for i in ri]) for r in rows[hi + 1:] if len(r) > si]
 base = sass[0][0]
 dis = subprocess.run(["nvdisasm", "--print-line-info", cubin], capture_output=True, text=True).stdout
@@ -70,4 +84,5 @@ print(f"total {sum(a[1] for a in agg.values()) / 1e6:.1f}M warp instructions")
 for k, (s, n, rs) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
     top3 = sorted(range(len(reasons)), key=lambda j: -rs[j])[:3]
     why = ", ".join(f"{reasons[j][6:]} {100 * rs[j] / max(s, 1):.0f}%" for j in top3)
-    print(f"{100 * s / tot:5.1f}%  {n / 1e6:8.2f}M inst  {k:32s} [{why}]")
+    extra = f"  {s / 1e6:9.2f}M {col}" if col else ""
+    print(f"{100 * s / tot:5.1f}%  {n / 1e6:8.2f}M inst  {k:32s} [{why}]{extra}")
