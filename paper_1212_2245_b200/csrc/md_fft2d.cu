@@ -187,7 +187,7 @@ k_fft2_cols(Fft2Args a, int lcw) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C *s = reinterpret_cast<C *>(smem_raw);
     const int H = a.H, W = a.W, cs = fline_stride<sizeof(C)>(H);      // padded column stride (md_fft.cuh)
-    const int cw = 1 << lcw, lh = a.log2H;                  // powers of two: shifts, no division
+    const int cw = 1 << lcw;                                // a power of two: shifts, no division
     const int x0 = blockIdx.x * cw;
     const int64_t base = blockIdx.y * (int64_t)H * W;
     C *z = static_cast<C *>(a.z);
@@ -196,20 +196,50 @@ k_fft2_cols(Fft2Args a, int lcw) {
         const C *twg = static_cast<const C *>(a.twH);
         stage_twiddles(tw, twg, a.log2H);
     }
-    for (int idx = threadIdx.x; idx < cw * H; idx += blockDim.x) {
-        const int y = idx >> lcw, c = idx & (cw - 1);
-        if (x0 + c < W) s[c * cs + fpad<sizeof(C)>(y)] = z[base + (int64_t)y * W + x0 + c];
-        else s[c * cs + fpad<sizeof(C)>(y)] = mkc<T>(T(0), T(0));
+    // element idx -> (row y, column c), columns fastest: a warp reads whole row segments of the
+    // block's columns (coalesced), and the padded column stride (= 1 mod 8) keeps the shared
+    // stores conflict-free. U loads in flight per thread (a load after a shared store could not
+    // be hoisted above it: z may alias as far as the compiler knows)
+    constexpr int U = 4;
+    const int n = cw * H, bd = blockDim.x;
+    for (int i0 = threadIdx.x; i0 < n; i0 += U * bd) {
+        C v[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const int idx = i0 + k * bd;
+            const int y = idx >> lcw, c = idx & (cw - 1);
+            v[k] = (idx < n && x0 + c < W) ? z[base + (int64_t)y * W + x0 + c] : mkc<T>(T(0), T(0));
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const int idx = i0 + k * bd;
+            if (idx >= n) break;
+            const int y = idx >> lcw, c = idx & (cw - 1);
+            s[c * cs + fpad<sizeof(C)>(y)] = v[k];
+        }
     }
     __syncthreads();
     if (a.log2H > 0) fft_dif_lines<true>(s, a.log2H, cw, cs, tw);
     if (a.filt) {
+        // the same row-segment order for the (natural-layout) multiplier: coalesced reads (a
+        // column-major walk read one 16-byte element per 4 KB row)
         const C *filt = static_cast<const C *>(a.filt);
-        for (int idx = threadIdx.x; idx < cw * H; idx += blockDim.x) {
-            const int c = idx >> lh, y = idx & (H - 1);
-            if (x0 + c >= W) continue;
-            const C f = __ldg(filt + (int64_t)y * W + x0 + c);
-            s[c * cs + fpad<sizeof(C)>(y)] = a.conj_filt ? cmulc(s[c * cs + fpad<sizeof(C)>(y)], f) : cmul(s[c * cs + fpad<sizeof(C)>(y)], f);
+        for (int i0 = threadIdx.x; i0 < n; i0 += U * bd) {
+            C f[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const int idx = i0 + k * bd;
+                const int y = idx >> lcw, c = idx & (cw - 1);
+                f[k] = (idx < n && x0 + c < W) ? __ldg(filt + (int64_t)y * W + x0 + c) : mkc<T>(T(0), T(0));
+            }
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const int idx = i0 + k * bd;
+                const int y = idx >> lcw, c = idx & (cw - 1);
+                if (idx >= n || x0 + c >= W) continue;
+                C &e = s[c * cs + fpad<sizeof(C)>(y)];
+                e = a.conj_filt ? cmulc(e, f[k]) : cmul(e, f[k]);
+            }
         }
         __syncthreads();
     }
@@ -258,8 +288,12 @@ cudaError_t launch_fft2_rows(const Fft2Args &a, int64_t batch, cudaStream_t st) 
 
 template <typename T>
 cudaError_t launch_fft2_cols(const Fft2Args &a, int64_t batch, cudaStream_t st) {
+    // columns per block: up to one 128-byte line per row (8 float64 / 16 float32 complex
+    // columns) -- 16 float64 columns (78 KB of shared memory, 2 blocks/SM) ran the 256^2
+    // Wiener column pass 20 % slower than 8 (39 KB); 4 was slower again
+    constexpr int kColW = 128 / (int)sizeof(cx_t<T>);
     int cw = 4096 / a.H;
-    cw = cw > 16 ? 16 : (cw < 1 ? 1 : cw);          // a power of two (H is)
+    cw = cw > kColW ? kColW : (cw < 1 ? 1 : cw);          // a power of two (H is)
     int lcw = 0;
     while ((1 << lcw) < cw) ++lcw;
     const size_t smem = ((size_t)cw * fline_stride<sizeof(cx_t<T>)>(a.H) + a.H + 1) * sizeof(cx_t<T>);
