@@ -219,31 +219,30 @@ __device__ __forceinline__ void col_walk_fixed(const V *p, int rs, const T *wc, 
 }
 
 #ifndef MD_COL_FIXED_MAX
-#define MD_COL_FIXED_MAX 8          // columns of up to this many taps take the unrolled walk
+#define MD_COL_FIXED_MAX 8          // columns of up to 8 taps take the unrolled walk (0: never)
 #endif
-template <typename T, typename V, int R, int J, int XS, int LEN, typename Acc, typename F>
-__device__ __forceinline__ bool col_walk_dispatch(const V *p, int rs, const T *wc, int len, Acc (&acc)[R][J], F upd) {
-    if constexpr (LEN > MD_COL_FIXED_MAX) {
-        return false;
-    } else {
-        if (len == LEN) {
-            col_walk_fixed<T, V, R, J, XS, LEN>(p, rs, wc, acc, upd);
-            return true;
-        }
-        return col_walk_dispatch<T, V, R, J, XS, LEN + 1>(p, rs, wc, len, acc, upd);
-    }
-}
-
 template <typename T, typename V, int R, int J, int XS, typename Acc, typename F>
 __device__ __forceinline__ void col_walk_rows(const V *s, int rs, const ColTaps<T> &tp, Acc (&acc)[R][J], F upd) {
     for (int c = 0; c < tp.ncol; ++c) {
         const int2 ci = tp.c[c];
         const int len = ci.y & 0xffff;
         const T *wc = tp.w + (ci.y >> 16);
-        // the branches are uniform (every thread walks the same column)
-        if (col_walk_dispatch<T, V, R, J, XS, 1>(s + ci.x, rs, wc, len, acc, upd)) continue;
-        if (len >= R - 1) col_walk_one<T, V, R, J, XS, false>(s + ci.x, rs, wc, len, acc, upd);
-        else col_walk_one<T, V, R, J, XS, true>(s + ci.x, rs, wc, len, acc, upd);
+        // the branches are uniform (every thread walks the same column); a switch, so the
+        // length selects its walk through one indexed branch instead of a compare chain
+        const V *p = s + ci.x;
+        switch (MD_COL_FIXED_MAX >= 8 ? len : 0) {
+            case 1: col_walk_fixed<T, V, R, J, XS, 1>(p, rs, wc, acc, upd); break;
+            case 2: col_walk_fixed<T, V, R, J, XS, 2>(p, rs, wc, acc, upd); break;
+            case 3: col_walk_fixed<T, V, R, J, XS, 3>(p, rs, wc, acc, upd); break;
+            case 4: col_walk_fixed<T, V, R, J, XS, 4>(p, rs, wc, acc, upd); break;
+            case 5: col_walk_fixed<T, V, R, J, XS, 5>(p, rs, wc, acc, upd); break;
+            case 6: col_walk_fixed<T, V, R, J, XS, 6>(p, rs, wc, acc, upd); break;
+            case 7: col_walk_fixed<T, V, R, J, XS, 7>(p, rs, wc, acc, upd); break;
+            case 8: col_walk_fixed<T, V, R, J, XS, 8>(p, rs, wc, acc, upd); break;
+            default:
+                if (len >= R - 1) col_walk_one<T, V, R, J, XS, false>(p, rs, wc, len, acc, upd);
+                else col_walk_one<T, V, R, J, XS, true>(p, rs, wc, len, acc, upd);
+        }
     }
 }
 
