@@ -218,8 +218,8 @@ __device__ __forceinline__ void col_walk_fixed(const V *p, int rs, const T *wc, 
     }
 }
 
-#ifndef MD_COL_FIXED_MAX
-#define MD_COL_FIXED_MAX 8          // columns of up to 8 taps take the unrolled walk (0: never)
+#ifndef MD_COL_FIXED
+#define MD_COL_FIXED 1              // columns of up to 8 taps take the unrolled walk (0: never)
 #endif
 template <typename T, typename V, int R, int J, int XS, typename Acc, typename F>
 __device__ __forceinline__ void col_walk_rows(const V *s, int rs, const ColTaps<T> &tp, Acc (&acc)[R][J], F upd) {
@@ -230,7 +230,7 @@ __device__ __forceinline__ void col_walk_rows(const V *s, int rs, const ColTaps<
         // the branches are uniform (every thread walks the same column); a switch, so the
         // length selects its walk through one indexed branch instead of a compare chain
         const V *p = s + ci.x;
-        switch (MD_COL_FIXED_MAX >= 8 ? len : 0) {
+        switch (MD_COL_FIXED ? len : 0) {
             case 1: col_walk_fixed<T, V, R, J, XS, 1>(p, rs, wc, acc, upd); break;
             case 2: col_walk_fixed<T, V, R, J, XS, 2>(p, rs, wc, acc, upd); break;
             case 3: col_walk_fixed<T, V, R, J, XS, 3>(p, rs, wc, acc, upd); break;
