@@ -1119,14 +1119,23 @@ int32_t md_plan_set_chunk(md_plan *P, int64_t frames) {
     return MD_OK;
 }
 
+// the plan's description names the iteration kernel: keep it in step with the switch
+static void describe_swap(std::string &d, const char *from, const char *to) {
+    const size_t i = d.find(from);
+    if (i != std::string::npos) d.replace(i, std::strlen(from), to);
+}
+
 int32_t md_plan_set_fused(md_plan *P, int32_t on) {
     if (!P) return fail(MD_EINVAL, "null plan");
     std::lock_guard<std::recursive_mutex> lock(P->mu);
+    static const char *kFused = "fused cluster iteration kernel";
     if (P->path == PATH_PLANE_DIRECT) {
         if (on && !(P->fast_plane && !P->big &&
                     fused_plane_supported(P->d.height, P->d.width, P->hblur, P->hadj, P->htaps_blur, P->htaps_adj, P->d.dtype)))
             return fail(MD_EINVAL, "fused kernel not available for this plan");
         P->fused_plane = on != 0;
+        if (on) describe_swap(P->describe, "direct taps (2 launches/iteration)", "direct taps, fused cluster iteration kernel");
+        else describe_swap(P->describe, "direct taps, fused cluster iteration kernel", "direct taps (2 launches/iteration)");
         return MD_OK;
     }
     if (on && !(P->path == PATH_LINES && P->fast_lines && fused_lines_supported(P->d.dtype, P->n, P->m, 0,
@@ -1134,6 +1143,12 @@ int32_t md_plan_set_fused(md_plan *P, int32_t on) {
         return fail(MD_EINVAL, "fused kernel not available for this plan");
     P->fused = on != 0;
     P->fused_clusters = !on ? 0 : (P->d.dtype == MD_F64 ? lines_fused_clusters<double>(*P) : lines_fused_clusters<float>(*P));
+    if (P->path == PATH_LINES) {
+        const char *per_it = P->fast_lines ? "k_wiener_lines + k_iter_lines_fast per iteration"
+                                           : "k_wiener_lines + k_iter_lines per iteration";
+        if (on) describe_swap(P->describe, per_it, kFused);
+        else describe_swap(P->describe, kFused, per_it);
+    }
     return MD_OK;
 }
 

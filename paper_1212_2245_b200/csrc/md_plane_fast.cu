@@ -14,6 +14,9 @@
 #include "md_plane.h"
 #include "md_plane_fast.h"
 #include "md_linefast.cuh"
+#include "md_tma.cuh"
+
+#include <cstdlib>
 
 namespace md {
 
@@ -57,6 +60,9 @@ __device__ __forceinline__ int pf_resolve(int k, int n, int periodic) {
 constexpr int PF_CJ = 4;                  // cols <= 32 * PF_CJ (FX + x-halos <= 128)
 #ifndef MD_PLANE_CP_ASYNC
 #define MD_PLANE_CP_ASYNC 1
+#endif
+#ifndef MD_PLANE_TMA
+#define MD_PLANE_TMA 1             // u tiles by TMA (md_tma.cuh) in whole-frame launches
 #endif
 template <typename T, typename E, typename Get>
 __device__ void pf_load(E *s, int ss, int H, int W, int y0, int x0, const PlaneHalo &h, int periodic, int slab,
@@ -135,18 +141,30 @@ __device__ void pf_load_async(E *s, int ss, int H, int W, int y0, int x0, const 
     }
 }
 
-// f32 u-tile stride for stage A: 8 (mod 16) so the two half-warps (rows 2 apart) use disjoint banks
-template <typename T> __host__ __device__ inline int pf_stride_a(const PlaneHalo &h) {
-    const int base = FX + h.hl + h.hr;
-    return sizeof(T) == 4 ? base + ((8 - base) % 16 + 16) % 16 : base;
+// Stage A's u tile in shared memory, laid out for TMA: a box must start on a 16-byte column
+// boundary (measured: an unaligned inner start coordinate is an illegal instruction), so the
+// tile row starts at column xoff = (-hl) mod (16 / sizeof(T)) of an smem row of pf_stride_a
+// elements (a multiple of 16 bytes, >= xoff + the tile width); x0 is a multiple of 64, so xoff
+// is the same for every tile of a launch. (A warp reads 32 consecutive columns of one row: any
+// stride is conflict-free.)
+template <typename T> __host__ __device__ inline int pf_xoff_a(const PlaneHalo &h) {
+    constexpr int g = 16 / (int)sizeof(T);
+    return ((-h.hl) % g + g) % g;
 }
+template <typename T> __host__ __device__ inline int pf_stride_a(const PlaneHalo &h) {
+    constexpr int g = 16 / (int)sizeof(T);
+    const int need = FX + h.hl + h.hr + pf_xoff_a<T>(h);
+    return (need + g - 1) / g * g;
+}
+// stage B's u tile (columns x0-2 ..): the same rule, a constant offset for float
+template <typename T> constexpr int pf_xoff_b() { return sizeof(T) == 4 ? 2 : 0; }
 template <typename T> __host__ __device__ inline int pf_stride_b(const PlaneHalo &h) { return FX + h.hl + h.hr; }
 
 template <typename T, bool ROBUST>
 __global__ void __launch_bounds__(256)
-k_plane_a_fast(PlaneFastArgs<T> a) {
+k_plane_a_fast(PlaneFastArgs<T> a, const __grid_constant__ CUtensorMap tmu) {
     constexpr int PR = PlaneMap<MD_PLANE_ROWS>::PR, PJ = PlaneMap<MD_PLANE_ROWS>::PJ, PX = PlaneMap<MD_PLANE_ROWS>::PX;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     T *su = reinterpret_cast<T *>(smem_raw);
     const int H = a.H, W = a.W;
     const int64_t fsz = (int64_t)H * W;
@@ -157,12 +175,27 @@ k_plane_a_fast(PlaneFastArgs<T> a) {
     T *w = a.w + fr * fsz;
     const int y0 = blockIdx.y * FY, x0 = blockIdx.x * FX;
     const int ss = a.ssa;
+    const int trows = FY + a.hb.ht + a.hb.hb;
+    const int xo = pf_xoff_a<T>(a.hb);
+    T *st = su + xo;                                  // the tile's column 0 (x0 - hl)
+    // interior tiles (no wrap / clamp inside the halo): one TMA box of trows x ss elements (the
+    // padding columns past the halo read whatever lies there, or zeros past the frame)
+    if (a.tma_a && x0 - a.hb.hl >= 0 && x0 + FX + a.hb.hr <= W && y0 - a.hb.ht >= 0 && y0 + FY + a.hb.hb <= H) {
+        uint64_t *bar = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(su + trows * ss) + 7) & ~uintptr_t(7));
+        if (threadIdx.x == 0) {
+            tma_bar_arm(bar, (uint32_t)(trows * ss * sizeof(T)));
+            tma_load_3d(su, &tmu, x0 - a.hb.hl - xo, y0 - a.hb.ht, (int)blockIdx.z, bar);
+        }
+        __syncthreads();                            // the barrier is initialised
+        tma_bar_wait(bar);
+    } else {
 #if MD_PLANE_CP_ASYNC
-    pf_load_async<T, T>(su, ss, H, W, y0, x0, a.hb, a.periodic, a.slab, a.ylo, a.yhi, u, nullptr);
-    cp_async_wait_all();
+        pf_load_async<T, T>(st, ss, H, W, y0, x0, a.hb, a.periodic, a.slab, a.ylo, a.yhi, u, nullptr);
+        cp_async_wait_all();
 #else
-    pf_load<T>(su, ss, H, W, y0, x0, a.hb, a.periodic, a.slab, a.ylo, a.yhi, [&](int64_t o) { return u[o]; });
+        pf_load<T>(st, ss, H, W, y0, x0, a.hb, a.periodic, a.slab, a.ylo, a.yhi, [&](int64_t o) { return u[o]; });
 #endif
+    }
     __syncthreads();
     const int tp = threadIdx.x / PX, cx = threadIdx.x % PX;
     const int yp = y0 + PR * tp;
@@ -177,7 +210,7 @@ k_plane_a_fast(PlaneFastArgs<T> a) {
             fv[k][r] = (x < W && yp + k < H) ? f[(int64_t)(yp + k) * W + x] : T(1);
         }
     T b[PR][PJ];
-    col_taps_rows<T, PR, PJ, PX>(su + (PR * tp + a.hb.ht) * ss + a.hb.hl + cx, ss, a.tb, b);
+    col_taps_rows<T, PR, PJ, PX>(st + (PR * tp + a.hb.ht) * ss + a.hb.hl + cx, ss, a.tb, b);
     const T eps_d2 = a.eps_d2;
 #pragma unroll
     for (int k = 0; k < PR; ++k) {
@@ -203,16 +236,19 @@ k_plane_a_fast(PlaneFastArgs<T> a) {
 
 template <typename T, bool ROBUST>
 __global__ void __launch_bounds__(256)
-k_plane_b_fast(PlaneFastArgs<T> a) {
+k_plane_b_fast(PlaneFastArgs<T> a, const __grid_constant__ CUtensorMap tmu) {
     constexpr int PR = PlaneMap<MD_PLANE_ROWS_B>::PR, PJ = PlaneMap<MD_PLANE_ROWS_B>::PJ, PX = PlaneMap<MD_PLANE_ROWS_B>::PX;
     using T2 = typename Vec2<T>::type;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     const int H = a.H, W = a.W;
     const int ss = a.ssb;
     const int rows = FY + a.ha.ht + a.ha.hb;
     T2 *spw = reinterpret_cast<T2 *>(smem_raw);
-    T *su = reinterpret_cast<T *>(spw + rows * ss);  // (FY+4) x PS: u with a 2-pixel halo
-    T *sg = su + (FY + 4) * PS;                      // (FY+2) x PS: diffusivity
+    // (FY+4) x PS: u with a 2-pixel halo, 128-byte aligned (a TMA destination)
+    T *su_box = reinterpret_cast<T *>(smem_raw + ((rows * ss * sizeof(T2) + 127) & ~size_t(127)));
+    T *su = su_box + pf_xoff_b<T>();                 // column 0 = x0 - 2 (TMA boxes start 16-byte aligned)
+    T *sg = su_box + (FY + 4) * PS;                  // (FY+2) x PS: diffusivity
+    uint64_t *bar = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(sg + (FY + 2) * PS) + 7) & ~uintptr_t(7));
     const int64_t fsz = (int64_t)H * W;
     const int64_t fr = blockIdx.z;
     const T *u = a.u + fr * fsz;
@@ -233,8 +269,16 @@ k_plane_b_fast(PlaneFastArgs<T> a) {
 #endif
     }
     const int gy0 = a.gy0, Hg = a.Hg;
+    if (a.tma_b) {
+        // u tile by TMA: one box of (FY+4) x PS at (x0-2, y0-2); positions outside the frame
+        // arrive as zeros (whole-frame launches only: a slab reads its halo rows as they are)
+        if (threadIdx.x == 0) {
+            tma_bar_arm(bar, (uint32_t)((FY + 4) * PS * sizeof(T)));
+            tma_load_3d(su_box, &tmu, x0 - 2 - pf_xoff_b<T>(), y0 - 2, (int)blockIdx.z, bar);
+        }
+    }
 #if MD_PLANE_CP_ASYNC
-    {
+    else {
         // u with a 2-pixel halo (zero outside the frame / slab): cp.async as well (zero-fill
         // for the outside positions), so the whole tile set is in flight before one wait
         constexpr int UC = FX + 4;
@@ -253,7 +297,7 @@ k_plane_b_fast(PlaneFastArgs<T> a) {
         }
     }
 #else
-    {
+    else {
         constexpr int U = 4, UC = FX + 4;
         const int n = (FY + 4) * UC, bd = blockDim.x;
         for (int i0 = threadIdx.x; i0 < n; i0 += U * bd) {
@@ -282,7 +326,11 @@ k_plane_b_fast(PlaneFastArgs<T> a) {
 #if MD_PLANE_CP_ASYNC
     cp_async_wait_all();
 #endif
-    __syncthreads();
+    __syncthreads();                                 // (also: the TMA barrier is initialised)
+    if (a.tma_b) {
+        tma_bar_wait(bar);
+        __syncthreads();
+    }
     const T eps_r2 = a.eps_r2;
     if (a.has_d) {
         for (int i = threadIdx.x / 32; i < FY + 2; i += 8) {
@@ -348,9 +396,12 @@ k_plane_b_fast(PlaneFastArgs<T> a) {
 
 // ---------------------------------------------------------------------------------- host
 
-static size_t smem_a(const PlaneHalo &hb, size_t es, int ssa) { return (size_t)(FY + hb.ht + hb.hb) * ssa * es; }
+// + an 8-byte-aligned TMA barrier behind the tile(s); stage B's u tile starts 128-byte aligned
+static size_t smem_a(const PlaneHalo &hb, size_t es, int ssa) {
+    return (((size_t)(FY + hb.ht + hb.hb) * ssa * es + 7) & ~size_t(7)) + 8;
+}
 static size_t smem_b(const PlaneHalo &ha, size_t es, int ssb) {
-    return (size_t)(FY + ha.ht + ha.hb) * ssb * 2 * es + (size_t)(2 * FY + 6) * PS * es;
+    return (((size_t)(FY + ha.ht + ha.hb) * ssb * 2 * es + 127) & ~size_t(127)) + (size_t)(2 * FY + 6) * PS * es + 16 + 8;
 }
 
 bool plane_fast_supported(const PlaneHalo &hb, const PlaneHalo &ha, const std::vector<PlaneTap> &taps_blur,
@@ -390,6 +441,8 @@ cudaError_t launch_plane_fast(const PlaneFastDesc &d, bool robust, int64_t batch
     cudaError_t e = cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sa);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
     if (e != cudaSuccess) return e;
+    const CUtensorMap no_map{};                      // slab launches: per-element tile loads
+    a.tma_a = a.tma_b = 0;
     if (d.slab) {
         // stage A over rows [a_begin, a_end) (at most the extended rows [-adj.ht, H + adj.hb)),
         // stage B over own rows [b_begin, b_end): the row-slab driver runs the rows that do not
@@ -406,10 +459,10 @@ cudaError_t launch_plane_fast(const PlaneFastDesc &d, bool robust, int64_t batch
         };
         if (d.a_end > d.a_begin) {
             MD_CHECK_HOST(d.a_begin >= -d.ha.ht && d.a_end <= d.H + d.ha.hb);
-            ka<<<dim3((d.W + FX - 1) / FX, (d.a_end - d.a_begin + FY - 1) / FY, 1), 256, sa, st>>>(sub(d.a_begin, d.a_end));
+            ka<<<dim3((d.W + FX - 1) / FX, (d.a_end - d.a_begin + FY - 1) / FY, 1), 256, sa, st>>>(sub(d.a_begin, d.a_end), no_map);
         }
         if (d.b_end > d.b_begin)
-            kb<<<dim3((d.W + FX - 1) / FX, (d.b_end - d.b_begin + FY - 1) / FY, 1), 256, sb, st>>>(sub(d.b_begin, d.b_end));
+            kb<<<dim3((d.W + FX - 1) / FX, (d.b_end - d.b_begin + FY - 1) / FY, 1), 256, sb, st>>>(sub(d.b_begin, d.b_end), no_map);
         return cudaGetLastError();
     }
     const int64_t fsz = (int64_t)d.H * d.W;
@@ -418,8 +471,13 @@ cudaError_t launch_plane_fast(const PlaneFastDesc &d, bool robust, int64_t batch
         PlaneFastArgs<T> ab = a;
         ab.u += b0 * fsz; ab.f += b0 * fsz; ab.p += b0 * fsz; ab.w += b0 * fsz; ab.u_out += b0 * fsz;
         const dim3 grid((d.W + FX - 1) / FX, (d.H + FY - 1) / FY, nb);
-        ka<<<grid, 256, sa, st>>>(ab);
-        kb<<<grid, 256, sb, st>>>(ab);
+        // the u tiles by TMA where the maps can be made (16-byte row pitch and box rows)
+        CUtensorMap tm_a{}, tm_b{};
+        static const int tma_mask = [] { const char *e = std::getenv("MD_PLANE_TMA_MASK"); return e ? std::atoi(e) : 3; }();
+        ab.tma_a = MD_PLANE_TMA && (tma_mask & 1) && make_tmap_3d(&tm_a, ab.u, sizeof(T), d.W, d.H, nb, a.ssa, FY + d.hb.ht + d.hb.hb);
+        ab.tma_b = MD_PLANE_TMA && (tma_mask & 2) && make_tmap_3d(&tm_b, ab.u, sizeof(T), d.W, d.H, nb, PS, FY + 4);
+        ka<<<grid, 256, sa, st>>>(ab, tm_a);
+        kb<<<grid, 256, sb, st>>>(ab, tm_b);
     }
     return cudaGetLastError();
 }

@@ -22,6 +22,7 @@ template <typename T> struct PlaneFastArgs {
     T alpha, eps_d2, eps_r2;
     int has_d;
     LutView lut;
+    int tma_a, tma_b;   // the u tiles come by TMA (md_tma.cuh): stage A's interior tiles, all of stage B's
 };
 
 struct PlaneFastDesc {

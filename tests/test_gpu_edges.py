@@ -182,3 +182,53 @@ def test_bench_pipeline_stage_samples(md):
         assert st.per_stage["rrrl_later_iterations"].samples == 12
         assert st.mean_ms > 0 and st.per_stage["wiener"].mean_ms > 0
         assert md.report(st, "csv").startswith("scenario,stage,runs,mean_ms,std_ms,min_ms,max_ms\n")
+
+
+# The per-iteration 2D-PSF stage kernels load their u tiles by TMA (md_tma.cuh) where the
+# tensor map can be made, the rest per element: boxes must start on 16-byte column boundaries
+# (an odd left halo shifts the tile inside its shared-memory row), frames whose row pitch is not
+# a multiple of 16 bytes take the per-element path, and edge tiles of stage A wrap / clamp per
+# element while interior tiles arrive by TMA. Every combination against the oracle.
+def _tile_psf(md, kind):
+    if kind == "line_odd":
+        return md.Psf.line(9.0, 30.0)
+    if kind == "line_even":
+        return md.Psf.line(12.0, 75.0)
+    w = np.random.default_rng(11).uniform(0.2, 1.0, size=(4, 5))
+    return md.Psf.general_2d(w / w.sum(), center=(1, 3))
+
+
+def _tile_input(md, shape, psf):
+    g = md.make_test_image(shape[1], shape[0], seed=3)          # (width, height)
+    return md.quantize(md.add_gaussian_noise(md.synth_blur(g, psf), 5.0, seed=4)).values
+
+
+@pytest.mark.parametrize("shape", [(64, 64), (128, 256), (256, 512)])
+@pytest.mark.parametrize("psf_kind", ["line_odd", "line_even", "small2d"])
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_plane_tile_loads_periodic_vs_oracle(md, shape, psf_kind, dtype):
+    psf = _tile_psf(md, psf_kind)
+    f = _tile_input(md, shape, psf)
+    params = md.DeconvParams(iterations=3)
+    pipe = md.DeblurPipeline(shape, psf, params, md.Scenario.FOURIER_2D, dtype=dtype, fused=False)
+    assert "direct taps" in pipe.plan.describe and "fused" not in pipe.plan.describe
+    out = pipe.run(md.Image(f)).values
+    ref = _oracle(md, f, psf, params, "fourier2d")
+    err = float(np.abs(out - ref).max())
+    assert err <= (1e-6 if dtype == "float64" else TOL), err
+
+
+@pytest.mark.parametrize("shape", [(96, 192), (128, 136), (130, 130), (200, 264), (72, 300)])
+@pytest.mark.parametrize("psf_kind", ["line_odd", "small2d"])
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_plane_tile_loads_clamped_vs_oracle(md, shape, psf_kind, dtype):
+    from oracle import wr3l_oracle as O
+    psf = _tile_psf(md, psf_kind)
+    f = _tile_input(md, shape, psf)
+    params = md.DeconvParams(iterations=3)
+    out = md.rrrl_deblur(md.Image(f), psf, params, convolver="spatial", dtype=dtype).values
+    p = O.OParams(wiener_k=params.wiener_k, alpha=params.alpha, iterations=params.iterations,
+                  eps_data=params.eps_data, eps_reg=params.eps_reg, floor=params.floor)
+    ref = O.rrrl_deblur(np.asarray(f, dtype=np.float64), O.OPsf("2d", psf.weights, psf.center), p, mode="spatial")
+    err = float(np.abs(out - ref).max())
+    assert err <= (1e-6 if dtype == "float64" else TOL), err
