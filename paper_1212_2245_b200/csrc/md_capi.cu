@@ -1055,6 +1055,7 @@ int run_plane(md_plan &P, const void *f, void *u, int64_t nb, char *scr, cudaStr
         } else if (P.fast_plane) {
             PlaneFastDesc s{};
             s.u = cur; s.f = FP; s.p = X; s.w = Y; s.u_out = dst;
+            s.pw_pairs = 1;                                           // (p, W) pairs over X and Y
             s.H = P.d.height; s.W = P.d.width; s.periodic = P.periodic;
             s.hb = P.hblur; s.ha = P.hadj; s.taps_blur = &P.htaps_blur; s.taps_adj = &P.htaps_adj;
             s.alpha = P.d.alpha; s.eps_d2 = P.d.eps_data * P.d.eps_data; s.eps_r2 = P.d.eps_reg * P.d.eps_reg;

@@ -111,14 +111,17 @@ __device__ void pf_load(E *s, int ss, int H, int W, int y0, int x0, const PlaneH
 // __syncthreads() before use.
 __device__ __forceinline__ void cp_async_elem(void *dst, const void *src, int bytes) {
     const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
-    if (bytes == 8) asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+    if (bytes == 16) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+    else if (bytes == 8) asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
     else asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+// fpair (optional, E = the pair type): the two fields interleaved in one array -- one copy of
+// sizeof(E) bytes per element instead of two
 template <typename T, typename E>
 __device__ void pf_load_async(E *s, int ss, int H, int W, int y0, int x0, const PlaneHalo &h, int periodic, int slab,
-                              int ylo, int yhi, const T *fa, const T *fb) {
+                              int ylo, int yhi, const T *fa, const T *fb, const E *fpair = nullptr) {
     const int rows = FY + h.ht + h.hb, cols = FX + h.hl + h.hr;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     int xr[PF_CJ];
@@ -134,6 +137,10 @@ __device__ void pf_load_async(E *s, int ss, int H, int W, int y0, int x0, const 
 #pragma unroll
         for (int c = 0; c < PF_CJ; ++c) {
             if (xr[c] < 0) continue;
+            if (fpair) {
+                cp_async_elem(s + i * ss + lane + 32 * c, fpair + b + xr[c], (int)sizeof(E));
+                continue;
+            }
             T *d = reinterpret_cast<T *>(s + i * ss + lane + 32 * c);
             cp_async_elem(d, fa + b + xr[c], (int)sizeof(T));
             if (fb) cp_async_elem(d + 1, fb + b + xr[c], (int)sizeof(T));
@@ -158,10 +165,22 @@ template <typename T> __host__ __device__ inline int pf_stride_a(const PlaneHalo
 }
 // stage B's u tile (columns x0-2 ..): the same rule, a constant offset for float
 template <typename T> constexpr int pf_xoff_b() { return sizeof(T) == 4 ? 2 : 0; }
-template <typename T> __host__ __device__ inline int pf_stride_b(const PlaneHalo &h) { return FX + h.hl + h.hr; }
+// stage B's (p, W) pair tile: pairs of 16 (float64) / 8 (float32) bytes, the same rule
+template <typename T> __host__ __device__ inline int pf_xoff_pw(const PlaneHalo &h) {
+    constexpr int g = 16 / (2 * (int)sizeof(T));
+    return ((-h.hl) % g + g) % g;
+}
+template <typename T> __host__ __device__ inline int pf_stride_b(const PlaneHalo &h) {
+    constexpr int g = 16 / (2 * (int)sizeof(T));
+    const int need = FX + h.hl + h.hr + pf_xoff_pw<T>(h);
+    return (need + g - 1) / g * g;
+}
 
+#ifndef MD_PLANE_A_MINB
+#define MD_PLANE_A_MINB 4          // <= 64 registers: 4 blocks per SM (the interleaved-store branch pushed it to 76 and 3)
+#endif
 template <typename T, bool ROBUST>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, MD_PLANE_A_MINB)
 k_plane_a_fast(PlaneFastArgs<T> a, const __grid_constant__ CUtensorMap tmu) {
     constexpr int PR = PlaneMap<MD_PLANE_ROWS>::PR, PJ = PlaneMap<MD_PLANE_ROWS>::PJ, PX = PlaneMap<MD_PLANE_ROWS>::PX;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -223,12 +242,20 @@ k_plane_a_fast(PlaneFastArgs<T> a, const __grid_constant__ CUtensorMap tmu) {
             const int64_t o = (int64_t)y * W + x;
             const T bb = b[k][r] > T(kGuard) ? b[k][r] : T(kGuard);
             const T ratio = fv[k][r] * frcp(bb);
+            T pv = ratio, wv = T(0);
             if (ROBUST) {
-                const T wv = T(0.5) * frsqrt(r1_fast<T>(a.lut, bb * frcp(fv[k][r])) * fv[k][r] + eps_d2);
-                w[o] = wv;
-                p[o] = wv * ratio;
+                wv = T(0.5) * frsqrt(r1_fast<T>(a.lut, bb * frcp(fv[k][r])) * fv[k][r] + eps_d2);
+                pv = wv * ratio;
+            }
+            if (a.pwi) {                              // interleaved (p, W): one store
+                using T2 = typename Vec2<T>::type;
+                T2 v;
+                v.x = pv;
+                v.y = wv;
+                reinterpret_cast<T2 *>(a.p)[fr * fsz + o] = v;
             } else {
-                p[o] = ratio;
+                p[o] = pv;
+                if (ROBUST) w[o] = wv;
             }
         }
     }
@@ -236,7 +263,7 @@ k_plane_a_fast(PlaneFastArgs<T> a, const __grid_constant__ CUtensorMap tmu) {
 
 template <typename T, bool ROBUST>
 __global__ void __launch_bounds__(256)
-k_plane_b_fast(PlaneFastArgs<T> a, const __grid_constant__ CUtensorMap tmu) {
+k_plane_b_fast(PlaneFastArgs<T> a, const __grid_constant__ CUtensorMap tmu, const __grid_constant__ CUtensorMap tmpw) {
     constexpr int PR = PlaneMap<MD_PLANE_ROWS_B>::PR, PJ = PlaneMap<MD_PLANE_ROWS_B>::PJ, PX = PlaneMap<MD_PLANE_ROWS_B>::PX;
     using T2 = typename Vec2<T>::type;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -254,13 +281,21 @@ k_plane_b_fast(PlaneFastArgs<T> a, const __grid_constant__ CUtensorMap tmu) {
     const T *u = a.u + fr * fsz;
     T *uo = a.u_out + fr * fsz;
     const int y0 = blockIdx.y * FY, x0 = blockIdx.x * FX;
-    {
+    const int xpw = pf_xoff_pw<T>(a.ha);
+    T2 *sp = spw + xpw;                              // the (p, W) tile's column 0 (x0 - hl)
+    // interleaved (p, W) and an interior tile: the whole pair tile as one TMA box (rows x ss
+    // pairs, started on a 16-byte boundary); otherwise per element (wrap / clamp at the edges)
+    const bool pw_tma = a.tma_pw && x0 - a.ha.hl >= 0 && x0 + FX + a.ha.hr <= W && y0 - a.ha.ht >= 0 &&
+                        y0 + FY + a.ha.hb <= H;
+    if (!pw_tma) {
         const T *pp = a.p + fr * fsz, *ww = a.w + fr * fsz;
+        const T2 *ppw = a.pwi ? reinterpret_cast<const T2 *>(a.p) + fr * fsz : nullptr;
 #if MD_PLANE_CP_ASYNC
         // (p, W) tile by cp.async: issued here, in flight while the u tile loads below
-        pf_load_async<T, T2>(spw, ss, H, W, y0, x0, a.ha, a.periodic, a.slab, a.ylo, a.yhi, pp, ROBUST ? ww : nullptr);
+        pf_load_async<T, T2>(sp, ss, H, W, y0, x0, a.ha, a.periodic, a.slab, a.ylo, a.yhi, pp, ROBUST ? ww : nullptr, ppw);
 #else
-        pf_load<T>(spw, ss, H, W, y0, x0, a.ha, a.periodic, a.slab, a.ylo, a.yhi, [&](int64_t o) {
+        pf_load<T>(sp, ss, H, W, y0, x0, a.ha, a.periodic, a.slab, a.ylo, a.yhi, [&](int64_t o) {
+            if (ppw) return ppw[o];
             T2 v;
             v.x = pp[o];
             v.y = ROBUST ? ww[o] : T(0);
@@ -269,16 +304,16 @@ k_plane_b_fast(PlaneFastArgs<T> a, const __grid_constant__ CUtensorMap tmu) {
 #endif
     }
     const int gy0 = a.gy0, Hg = a.Hg;
-    if (a.tma_b) {
-        // u tile by TMA: one box of (FY+4) x PS at (x0-2, y0-2); positions outside the frame
-        // arrive as zeros (whole-frame launches only: a slab reads its halo rows as they are)
-        if (threadIdx.x == 0) {
-            tma_bar_arm(bar, (uint32_t)((FY + 4) * PS * sizeof(T)));
-            tma_load_3d(su_box, &tmu, x0 - 2 - pf_xoff_b<T>(), y0 - 2, (int)blockIdx.z, bar);
-        }
+    if (threadIdx.x == 0 && (a.tma_b || pw_tma)) {
+        // TMA boxes on one barrier: u (FY+4) x PS at (x0-2, y0-2), positions outside the frame
+        // arriving as zeros (whole-frame launches only: a slab reads its halo rows as they are);
+        // the (p, W) pairs as 2 ss elements per row
+        tma_bar_arm(bar, (uint32_t)((a.tma_b ? (FY + 4) * PS * sizeof(T) : 0) + (pw_tma ? rows * ss * sizeof(T2) : 0)));
+        if (a.tma_b) tma_load_3d(su_box, &tmu, x0 - 2 - pf_xoff_b<T>(), y0 - 2, (int)blockIdx.z, bar);
+        if (pw_tma) tma_load_3d(spw, &tmpw, 2 * (x0 - a.ha.hl - xpw), y0 - a.ha.ht, (int)blockIdx.z, bar);
     }
 #if MD_PLANE_CP_ASYNC
-    else {
+    if (!a.tma_b) {
         // u with a 2-pixel halo (zero outside the frame / slab): cp.async as well (zero-fill
         // for the outside positions), so the whole tile set is in flight before one wait
         constexpr int UC = FX + 4;
@@ -297,7 +332,7 @@ k_plane_b_fast(PlaneFastArgs<T> a, const __grid_constant__ CUtensorMap tmu) {
         }
     }
 #else
-    else {
+    if (!a.tma_b) {
         constexpr int U = 4, UC = FX + 4;
         const int n = (FY + 4) * UC, bd = blockDim.x;
         for (int i0 = threadIdx.x; i0 < n; i0 += U * bd) {
@@ -327,7 +362,7 @@ k_plane_b_fast(PlaneFastArgs<T> a, const __grid_constant__ CUtensorMap tmu) {
     cp_async_wait_all();
 #endif
     __syncthreads();                                 // (also: the TMA barrier is initialised)
-    if (a.tma_b) {
+    if (a.tma_b || pw_tma) {
         tma_bar_wait(bar);
         __syncthreads();
     }
@@ -356,7 +391,7 @@ k_plane_b_fast(PlaneFastArgs<T> a, const __grid_constant__ CUtensorMap tmu) {
     const int ty0 = PR * tp;
     if (y0 + ty0 >= H) return;
     T2 nd[PR][PJ];
-    col_taps_rows2<T, PR, PJ, PX>(spw + (ty0 + a.ha.ht) * ss + a.ha.hl + cx, ss, a.ta, nd);
+    col_taps_rows2<T, PR, PJ, PX>(sp + (ty0 + a.ha.ht) * ss + a.ha.hl + cx, ss, a.ta, nd);
     const T alpha = a.alpha;
 #pragma unroll
     for (int k = 0; k < PR; ++k) {
@@ -442,7 +477,9 @@ cudaError_t launch_plane_fast(const PlaneFastDesc &d, bool robust, int64_t batch
     if (e == cudaSuccess) e = cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
     if (e != cudaSuccess) return e;
     const CUtensorMap no_map{};                      // slab launches: per-element tile loads
-    a.tma_a = a.tma_b = 0;
+    a.tma_a = a.tma_b = a.tma_pw = 0;
+    a.pwi = d.pw_pairs;
+    if (d.slab && d.pw_pairs) return cudaErrorInvalidValue;   // slabs exchange p and W rows separately
     if (d.slab) {
         // stage A over rows [a_begin, a_end) (at most the extended rows [-adj.ht, H + adj.hb)),
         // stage B over own rows [b_begin, b_end): the row-slab driver runs the rows that do not
@@ -462,7 +499,7 @@ cudaError_t launch_plane_fast(const PlaneFastDesc &d, bool robust, int64_t batch
             ka<<<dim3((d.W + FX - 1) / FX, (d.a_end - d.a_begin + FY - 1) / FY, 1), 256, sa, st>>>(sub(d.a_begin, d.a_end), no_map);
         }
         if (d.b_end > d.b_begin)
-            kb<<<dim3((d.W + FX - 1) / FX, (d.b_end - d.b_begin + FY - 1) / FY, 1), 256, sb, st>>>(sub(d.b_begin, d.b_end), no_map);
+            kb<<<dim3((d.W + FX - 1) / FX, (d.b_end - d.b_begin + FY - 1) / FY, 1), 256, sb, st>>>(sub(d.b_begin, d.b_end), no_map, no_map);
         return cudaGetLastError();
     }
     const int64_t fsz = (int64_t)d.H * d.W;
@@ -472,12 +509,15 @@ cudaError_t launch_plane_fast(const PlaneFastDesc &d, bool robust, int64_t batch
         ab.u += b0 * fsz; ab.f += b0 * fsz; ab.p += b0 * fsz; ab.w += b0 * fsz; ab.u_out += b0 * fsz;
         const dim3 grid((d.W + FX - 1) / FX, (d.H + FY - 1) / FY, nb);
         // the u tiles by TMA where the maps can be made (16-byte row pitch and box rows)
-        CUtensorMap tm_a{}, tm_b{};
-        static const int tma_mask = [] { const char *e = std::getenv("MD_PLANE_TMA_MASK"); return e ? std::atoi(e) : 3; }();
+        CUtensorMap tm_a{}, tm_b{}, tm_pw{};
+        static const int tma_mask = [] { const char *e = std::getenv("MD_PLANE_TMA_MASK"); return e ? std::atoi(e) : 7; }();
         ab.tma_a = MD_PLANE_TMA && (tma_mask & 1) && make_tmap_3d(&tm_a, ab.u, sizeof(T), d.W, d.H, nb, a.ssa, FY + d.hb.ht + d.hb.hb);
         ab.tma_b = MD_PLANE_TMA && (tma_mask & 2) && make_tmap_3d(&tm_b, ab.u, sizeof(T), d.W, d.H, nb, PS, FY + 4);
+        // interleaved (p, W) pairs as 2W elements per row
+        ab.tma_pw = MD_PLANE_TMA && (tma_mask & 4) && ab.pwi &&
+                    make_tmap_3d(&tm_pw, ab.p, sizeof(T), 2 * (int64_t)d.W, d.H, nb, 2 * a.ssb, FY + d.ha.ht + d.ha.hb);
         ka<<<grid, 256, sa, st>>>(ab, tm_a);
-        kb<<<grid, 256, sb, st>>>(ab, tm_b);
+        kb<<<grid, 256, sb, st>>>(ab, tm_b, tm_pw);
     }
     return cudaGetLastError();
 }

@@ -23,6 +23,8 @@ template <typename T> struct PlaneFastArgs {
     int has_d;
     LutView lut;
     int tma_a, tma_b;   // the u tiles come by TMA (md_tma.cuh): stage A's interior tiles, all of stage B's
+    int pwi;            // p and W interleaved as pairs in the p buffer (2 elements per pixel; w unused)
+    int tma_pw;         // ... and stage B's interior (p, W) tiles come by TMA
 };
 
 struct PlaneFastDesc {
@@ -39,6 +41,7 @@ struct PlaneFastDesc {
     double alpha, eps_d2, eps_r2;
     int has_d;
     LutView lut;
+    int pw_pairs;              // whole-frame launches: p / W interleaved in the p buffer (2 elements per pixel)
 };
 
 bool plane_fast_supported(const PlaneHalo &hb, const PlaneHalo &ha, const std::vector<PlaneTap> &taps_blur,
