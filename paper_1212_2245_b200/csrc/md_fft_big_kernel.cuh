@@ -64,6 +64,42 @@ k_subfft(SubFftArgs a) {
         if (line_fast) { g = idx >> log2L; e = idx & (L - 1); }
         else { e = idx >> lg; g = idx & (G - 1); }
     };
+#ifndef MD_SUBFFT_CP_ASYNC
+#define MD_SUBFFT_CP_ASYNC 1
+#endif
+    if (MD_SUBFFT_CP_ASYNC) {
+        // cp.async (global -> shared, no register round trip, every element of the block in
+        // flight at once): one 16-byte copy per complex element, two 8-byte (4-byte) copies for a
+        // real pair; lines past the batch and a missing second field zero-filled
+        for (int idx = threadIdx.x; idx < n; idx += bd) {
+            int g, e;
+            coords(idx, g, e);
+            const bool ok = b0 + g < a.B;
+            const int o = ok ? base + g * sb + e * es : 0;
+            C *d = &s[g * ls + fpad<sizeof(C)>(e)];
+            const uint32_t da = (uint32_t)__cvta_generic_to_shared(d);
+            if (ra) {
+                constexpr int ES = (int)sizeof(T);
+                const uint32_t db = da + ES;
+                const T *pa = ra + o, *pb = rb ? rb + o : ra;
+                const int na = ok ? ES : 0, nb2 = ok && rb ? ES : 0;
+                if (ES == 8) {
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(da), "l"(pa), "r"(na) : "memory");
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(db), "l"(pb), "r"(nb2) : "memory");
+                } else {
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(da), "l"(pa), "r"(na) : "memory");
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(db), "l"(pb), "r"(nb2) : "memory");
+                }
+            } else {
+                const C *pz = z + o;
+                if (sizeof(C) == 16)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(da), "l"(pz), "r"(ok ? 16 : 0) : "memory");
+                else
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(da), "l"(pz), "r"(ok ? 8 : 0) : "memory");
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    } else {
     for (int i0 = threadIdx.x; i0 < n; i0 += U * bd) {
         C v[U];
 #pragma unroll
@@ -87,8 +123,10 @@ k_subfft(SubFftArgs a) {
             s[g * ls + fpad<sizeof(C)>(e)] = v[k];
         }
     }
+    }
     C *twL = s + G * ls;                       // sub-transform twiddles staged in shared memory
     stage_twiddles<BD>(twL, static_cast<const C *>(a.twL), log2L);   // stage-major (md_fft.cuh)
+    if (MD_SUBFFT_CP_ASYNC) asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
     const C *filt = static_cast<const C *>(a.filt);
     if (TW == TW_FILT_INV) {
