@@ -43,6 +43,7 @@ __device__ __forceinline__ void poison_smem(unsigned char *smem) {
 #ifdef MD_CHECKED
     const uint32_t n = dyn_smem_bytes();
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) smem[i] = 0xff;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // before TMA writes the same bytes
     __syncthreads();
 #else
     (void)smem;

@@ -196,6 +196,9 @@ k_plane_a_fast(PlaneFastArgs<T> a, const __grid_constant__ CUtensorMap tmu) {
     const int ss = a.ssa;
     const int trows = FY + a.hb.ht + a.hb.hb;
     const int xo = pf_xoff_a<T>(a.hb);
+    poison_smem(smem_raw);
+    MD_CHECK((smem_addr_of(su) & 127) == 0 && (size_t)trows * ss * sizeof(T) + 8 <= dyn_smem_bytes() &&
+             ((x0 - a.hb.hl - xo) * (int)sizeof(T)) % 16 == 0);
     T *st = su + xo;                                  // the tile's column 0 (x0 - hl)
     // interior tiles (no wrap / clamp inside the halo): one TMA box of trows x ss elements (the
     // padding columns past the halo read whatever lies there, or zeros past the frame)
@@ -283,6 +286,10 @@ k_plane_b_fast(PlaneFastArgs<T> a, const __grid_constant__ CUtensorMap tmu, cons
     const int y0 = blockIdx.y * FY, x0 = blockIdx.x * FX;
     const int xpw = pf_xoff_pw<T>(a.ha);
     T2 *sp = spw + xpw;                              // the (p, W) tile's column 0 (x0 - hl)
+    poison_smem(smem_raw);
+    MD_CHECK((smem_addr_of(spw) & 127) == 0 && (smem_addr_of(su_box) & 127) == 0 &&
+             (size_t)(reinterpret_cast<unsigned char *>(bar + 1) - smem_raw) <= dyn_smem_bytes() &&
+             ((x0 - a.ha.hl - xpw) * 2 * (int)sizeof(T)) % 16 == 0 && ((x0 - 2 - pf_xoff_b<T>()) * (int)sizeof(T)) % 16 == 0);
     // interleaved (p, W) and an interior tile: the whole pair tile as one TMA box (rows x ss
     // pairs, started on a 16-byte boundary); otherwise per element (wrap / clamp at the edges)
     const bool pw_tma = a.tma_pw && x0 - a.ha.hl >= 0 && x0 + FX + a.ha.hr <= W && y0 - a.ha.ht >= 0 &&

@@ -19,6 +19,7 @@ namespace md {
 
 // ------------------------------------------------------------------------------ device side
 __device__ __forceinline__ uint32_t tma_smem(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t smem_addr_of(const void *p) { return tma_smem(p); }
 
 // one-thread setup of a single-use barrier: init (one arrival), make it visible to the async
 // proxy, arm it with the bytes of the copies that will complete on it
