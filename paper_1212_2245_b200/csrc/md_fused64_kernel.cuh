@@ -155,6 +155,14 @@ __device__ __forceinline__ void lane_window(const double (&x)[SEG], double (&w)[
     }
 }
 
+#ifndef MD_F64_SELMAX
+#define MD_F64_SELMAX 1            // guards as compare + select (dmax_sel) instead of fmax
+#endif
+#if MD_F64_SELMAX
+#define MD_F64_MAX(a, b) dmax_sel(a, b)
+#else
+#define MD_F64_MAX(a, b) fmax(a, b)
+#endif
 #ifndef MD_F64_BLOCKS_PER_SM
 #define MD_F64_BLOCKS_PER_SM 1
 #endif
@@ -357,7 +365,7 @@ k_fused_lines64(FusedKArgs<double, R> a, const double2 *__restrict__ lut64) {
                 T bl[SEG];
                 conv_window<T, R, BOXR, BOXC>(v, a.wb, a.box_wi, a.box_cb, bl);
 #pragma unroll
-                for (int r = 0; r < SEG; ++r) bl[r] = bl[r] > T(kGuard) ? bl[r] : T(kGuard);   // b
+                for (int r = 0; r < SEG; ++r) bl[r] = MD_F64_MAX(bl[r], T(kGuard));   // b
                 if (ROBUST) {
                     // r1(b / fpos) for the lane's 8 pixels: all 8 table pairs requested before any
                     // is used (no branch between them), the rare direct-log branch (x < 1/2) taken
@@ -421,18 +429,18 @@ k_fused_lines64(FusedKArgs<double, R> a, const double2 *__restrict__ lut64) {
                     T d = fr - fl;
                     d += (gc + Gd[koff(r)]) * (Ud[koff(r)] - u);
                     d -= (Gu[koff(r)] + gc) * (u - Uu[koff(r)]);
-                    const T dp = fmax(d, T(0));          // max(D, 0); D - max(D, 0) = min(D, 0) exactly
+                    const T dp = MD_F64_MAX(d, T(0));    // max(D, 0); D - max(D, 0) = min(D, 0) exactly
                     const T nm = num[r] + al * dp;
                     const T neg = al * (d - dp);
                     T dn = (ROBUST ? den[r] : one) - neg;
-                    dn = fmax(dn, gd);
+                    dn = MD_F64_MAX(dn, gd);
                     unew[j][r] = (u * nm) * frcp(dn);
                 }
             } else {
 #pragma unroll
                 for (int r = 0; r < SEG; ++r) {
                     if (ROBUST) {
-                        const T dn = fmax(den[r], gd);
+                        const T dn = MD_F64_MAX(den[r], gd);
                         unew[j][r] = (ux[r + 1] * num[r]) * frcp(dn);
                     } else {
                         unew[j][r] = ux[r + 1] * (FOLD ? num[r] * a.box_wi : num[r]);

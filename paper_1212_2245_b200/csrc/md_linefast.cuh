@@ -112,6 +112,23 @@ __device__ __forceinline__ float flog(float x) {
 }
 __device__ __forceinline__ double flog(double x) { return log(x); }
 
+// max(x, y) as one compare and a select (x > y ? x : y): the reference's guards and D+ parts
+// (np.maximum) on ordinary numbers. fmax() and the same ternary in C compile to a min/max
+// compare plus NaN / signed-zero fix-ups (4-5 instructions per double); the operands here are
+// finite, and where they compare equal (+-0 against 0) the sign of a zero never reaches a result
+__device__ __forceinline__ double dmax_sel(double x, double y) {
+    double r;
+    asm("{\n\t.reg .pred p;\n\tsetp.gt.f64 p, %1, %2;\n\tselp.f64 %0, %1, %2, p;\n\t}" : "=d"(r) : "d"(x), "d"(y));
+    return r;
+}
+__device__ __forceinline__ float dmax_sel(float x, float y) { return x > y ? x : y; }
+__device__ __forceinline__ double dmin_sel(double x, double y) {
+    double r;
+    asm("{\n\t.reg .pred p;\n\tsetp.lt.f64 p, %1, %2;\n\tselp.f64 %0, %1, %2, p;\n\t}" : "=d"(r) : "d"(x), "d"(y));
+    return r;
+}
+__device__ __forceinline__ float dmin_sel(float x, float y) { return x < y ? x : y; }
+
 __device__ __forceinline__ float lut_interp(const LutView &L, int i, float t) {
     const float2 p = __ldg(L.p32 + i);            // one 8-byte load: value and step
     return p.x + p.y * t;

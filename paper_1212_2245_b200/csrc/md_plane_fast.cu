@@ -243,7 +243,7 @@ k_plane_a_fast(PlaneFastArgs<T> a, const __grid_constant__ CUtensorMap tmu) {
             const int x = x0 + cx + PX * r;
             if (x >= W) continue;
             const int64_t o = (int64_t)y * W + x;
-            const T bb = b[k][r] > T(kGuard) ? b[k][r] : T(kGuard);
+            const T bb = dmax_sel(b[k][r], T(kGuard));
             const T ratio = fv[k][r] * frcp(bb);
             T pv = ratio, wv = T(0);
             if (ROBUST) {
@@ -424,13 +424,13 @@ k_plane_b_fast(PlaneFastArgs<T> a, const __grid_constant__ CUtensorMap tmu, cons
             T nm = nd[k][r].x;
             T dn = ROBUST ? nd[k][r].y : T(1);
             if (a.has_d) {
-                nm += alpha * (d > T(0) ? d : T(0));
-                dn -= alpha * (d < T(0) ? d : T(0));
+                nm += alpha * dmax_sel(d, T(0));
+                dn -= alpha * dmin_sel(d, T(0));
             } else if (!ROBUST) {
                 uo[(int64_t)y * W + x] = uv * nm;
                 continue;
             }
-            dn = dn > T(kGuard) ? dn : T(kGuard);
+            dn = dmax_sel(dn, T(kGuard));
             uo[(int64_t)y * W + x] = (uv * nm) * frcp(dn);
         }
     }
