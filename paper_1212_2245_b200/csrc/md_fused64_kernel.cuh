@@ -166,6 +166,12 @@ __device__ __forceinline__ void lane_window(const double (&x)[SEG], double (&w)[
 #ifndef MD_F64_BLOCKS_PER_SM
 #define MD_F64_BLOCKS_PER_SM 1
 #endif
+// MD_F64_SKIP_SHADOW=1: a warp whose last line slot lies past RL (ragged split: 28-29 lines on
+// 16 warps x 2 slots in 9-CTA clusters) skips that slot's arithmetic instead of recomputing line
+// RL - 1 (the branch is warp-uniform, so the shuffles inside stay full-warp)
+#ifndef MD_F64_SKIP_SHADOW
+#define MD_F64_SKIP_SHADOW 1
+#endif
 template <int R, int NW, int LPW, bool ROBUST, int BOXR, bool BOXC>
 __global__ void __launch_bounds__(NW * 32, MD_F64_BLOCKS_PER_SM)
 k_fused_lines64(FusedKArgs<double, R> a, const double2 *__restrict__ lut64) {
@@ -326,6 +332,8 @@ k_fused_lines64(FusedKArgs<double, R> a, const double2 *__restrict__ lut64) {
         for (int j = 0; j < LPW; ++j) {
             // slots past RL (ragged line split) shadow line RL - 1 and store nothing: the loop
             // stays convergent, so the shuffles need no per-iteration reconvergence
+            // (MD_F64_SKIP_SHADOW: the whole warp skips such a slot -- the test is warp-uniform)
+            if (MD_F64_SKIP_SHADOW && j > 0 && warp + NW * j >= RL) continue;
             const int li = min(warp + NW * j, RL - 1);
             const int gl = gl0 + li;
             const bool up_ok = gl > 0, dn_ok = gl + 1 < m;
