@@ -154,6 +154,10 @@ class C1:
     def e2e_set(self, nb):
         return self.host[:nb], None
 
+    def device_frames(self, dtype):
+        import torch
+        return torch.from_numpy(self.host).to(device="cuda", dtype=dtype).contiguous()
+
     def run_host(self, hin, hout, ctx):
         self.pipe.run_batch(hin, out=hout, out_dtype=hout.dtype)
 
@@ -197,24 +201,41 @@ def c4_bank(md, seed: int = 2026):
 C4_SCENE_SEEDS = (7, 8, 9, 10)
 
 
+C4_DISTINCT = 8                      # distinct noisy frames per PSF (4 scenes x 2 noise draws)
+
+
+def c4_distinct(md, bank, synth, used=None):
+    """[len(bank), C4_DISTINCT, H, W]: the distinct noisy frames of every PSF in `used` (default all;
+    the others stay zero) -- 8 per PSF over the 4 scenes, noise seeded by (PSF, frame)."""
+    scenes = [md.make_test_image(W, H, seed=s).values for s in C4_SCENE_SEEDS]
+    out = np.zeros((len(bank), C4_DISTINCT, H, W))
+    for b, psf in enumerate(bank):
+        if used is not None and b not in used:
+            continue
+        blurred = [synth(scenes[j], psf) for j in range(4)]
+        out[b] = np.stack([noisy(blurred[j % 4], 1000 * b + j) for j in range(C4_DISTINCT)])
+    return out
+
+
+def c4_source(index):
+    """Frame i (PSF index[i], k-th frame of its PSF) is distinct frame (index[i], k mod 8)."""
+    idx = np.asarray(index)
+    k = np.zeros(idx.size, dtype=np.int64)
+    for b in np.unique(idx):
+        sel = np.nonzero(idx == b)[0]
+        k[sel] = np.arange(sel.size)
+    return idx * C4_DISTINCT + k % C4_DISTINCT
+
+
 def c4_frames(md, bank, index, synth, with_scenes=False):
     """The c4 frames for PSF assignment `index` (8 distinct noisy frames per PSF, 4 scenes),
     plus one (kind, psf, frame) CPU sample item per PSF [and each frame's scene number]."""
-    scenes = [md.make_test_image(W, H, seed=s).values for s in C4_SCENE_SEEDS]
-    distinct = 8
-    frames = np.empty((index.size, H, W))
-    scene_of = np.empty(index.size, dtype=np.int64)
-    items = []
-    for b, psf in enumerate(bank):
-        sel = np.nonzero(index == b)[0]
-        if sel.size == 0:
-            continue
-        blurred = [synth(scenes[j], psf) for j in range(4)]
-        base = [noisy(blurred[j % 4], 1000 * b + j) for j in range(distinct)]
-        for k, i in enumerate(sel):
-            frames[i] = base[k % distinct]
-            scene_of[i] = (k % distinct) % 4
-        items.append((b, psf, base[0]))
+    used = set(int(b) for b in np.unique(index))
+    base = c4_distinct(md, bank, synth, used).reshape(-1, H, W)
+    src = c4_source(index)
+    frames = base[src]
+    scene_of = (src % C4_DISTINCT) % 4
+    items = [(b, bank[b], base[b * C4_DISTINCT]) for b in sorted(used)]
     return (frames, items, scene_of) if with_scenes else (frames, items)
 
 
@@ -232,10 +253,18 @@ class C4:
         self.params = md.DeconvParams()
         self.bank, self.kinds = c4_bank(md)
         nb = len(self.bank)
-        per = -(-args.batch // nb)
-        self.index = np.minimum(np.arange(args.batch) // per, nb - 1)
-        self.host, items = c4_frames(md, self.bank, self.index, synth)
-        self.cpu_items = [(self.kinds[b], psf, fr) for b, psf, fr in items]
+        # strong scaling (configs[3], the default): ONE batch of args.global_batch frames over the
+        # ranks, rank r taking frames r, r + N, ... (every rank sees every PSF class); weak (an
+        # explicit --batch): args.batch frames per rank
+        G = args.global_batch or args.batch
+        per = -(-G // nb)
+        gidx = np.minimum(np.arange(G) // per, nb - 1)
+        gsrc = c4_source(gidx)
+        sel = slice(args.rank, None, args.world) if args.global_batch else slice(None)
+        self.index, self.src = gidx[sel], gsrc[sel]
+        assert self.index.size == args.batch, (self.index.size, args.batch)
+        self.distinct = c4_distinct(md, self.bank, synth).reshape(-1, H, W)
+        self.cpu_items = [(self.kinds[b], psf, self.distinct[b * C4_DISTINCT]) for b, psf in enumerate(self.bank)]
         if gpu:
             from paper_1212_2245_b200.batch import PsfBankPipeline
             self.pipe = PsfBankPipeline((H, W), self.bank, self.params, dtype=args.dtype)
@@ -243,12 +272,18 @@ class C4:
             self.fused = False
             self.latency_plan = self.pipe.pipes[int(self.index[0])].plan
 
+    def device_frames(self, dtype):
+        """The rank's frames in HBM, gathered on the device from the distinct ones."""
+        import torch
+        d = torch.from_numpy(self.distinct).to(device="cuda", dtype=dtype)
+        return d[torch.from_numpy(self.src).cuda()].contiguous()
+
     def make_pipe(self, dtype, fused="auto"):
         from paper_1212_2245_b200.batch import PsfBankPipeline
         return PsfBankPipeline((H, W), self.bank, self.params, dtype=dtype)
 
-    def run(self, f, u, pipe=None):
-        (pipe or self.pipe).run(f, self.index, out=u, streams=2)
+    def run(self, f, u, pipe=None, index=None):
+        (pipe or self.pipe).run(f, self.index if index is None else index, out=u, streams=2)
 
     def run_profile(self, f, u) -> dict:
         tot = {"init_ms": 0.0, "iter_ms": 0.0, "layout_ms": 0.0, "groups": 0}
@@ -260,7 +295,7 @@ class C4:
 
     def e2e_set(self, nb):
         sel = np.linspace(0, self.index.size - 1, nb).astype(np.int64)   # every PSF class, sorted
-        return self.host[sel], self.index[sel]
+        return self.distinct[self.src[sel]], self.index[sel]
 
     def run_host(self, hin, hout, ctx):
         self.pipe.run_host(hin, ctx, out=hout)
@@ -287,10 +322,14 @@ class C4:
 WORKLOADS = {"c1": C1, "c4": C4}
 
 
-def bench_config(work_name: str, batch: int, world: int, esz: int) -> dict:
+def bench_config(work_name: str, batch: int, world: int, esz: int, global_batch=None) -> dict:
     """The `config` object both arms print (identical for the same command line)."""
-    return {"workload": work_name, "frames_per_gpu_per_step": batch, "parallelism": f"frame-sharded x{world}",
-            "l2": f"inputs {batch * PX * esz / 2**20:.0f} MiB per GPU > 126 MB L2 (no reuse between steps)"}
+    c = {"workload": work_name, "frames_per_gpu_per_step": batch, "parallelism": f"frame-sharded x{world}",
+         "l2": f"inputs {batch * PX * esz / 2**20:.0f} MiB per GPU > 126 MB L2 (no reuse between steps)"}
+    if global_batch:
+        c["global_batch"] = global_batch
+        c["parallelism"] = f"one {global_batch}-frame batch, frames dealt round-robin over {world} rank(s)"
+    return c
 
 
 def run_c5(args, rank: int, world: int, local: int) -> None:
@@ -536,9 +575,9 @@ def run_reference(args, rank: int, world: int) -> None:
         "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
         "devices": "host CPU cores only (n_gpus echoes the launch's N; no device work)",
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(walls) / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": DATA,
-        "config": bench_config(work.name, args.batch, world, esz),
+        "config": bench_config(work.name, args.batch, world, esz, args.global_batch),
         "cpu_baseline": {"value": value, "unit": "frames/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "p50_ms_per_frame": 1e3 * statistics.median(walls) / args.cpu_frames_per_core,
@@ -561,7 +600,10 @@ def parse_args(argv=None):
     ap.add_argument("--size", type=int, default=16384, help="c5 image side")
     ap.add_argument("--dtype", default="float64", choices=["float32", "float64"],
                     help="arithmetic of the timed path (default float64, the reference's: core.py:3-4)")
-    ap.add_argument("--batch", type=int, default=None, help="frames per GPU per step")
+    ap.add_argument("--batch", type=int, default=None,
+                    help="frames per GPU per step (weak scaling; c1 default 4096)")
+    ap.add_argument("--global-batch", type=int, default=None,
+                    help="c4: frames per step over ALL ranks (strong scaling; default 65536, configs[3])")
     ap.add_argument("--e2e-batch", type=int, default=2048)
     ap.add_argument("--cpu-frames-per-core", type=int, default=24)
     ap.add_argument("--no-cpu", action="store_true")
@@ -570,8 +612,19 @@ def parse_args(argv=None):
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N>1 (gloo: CPU tests of the timing path)")
     args = ap.parse_args(argv)
-    if args.batch is None:
-        args.batch = 4096 if args.config == "c1" else 16384
+    args.world = int(os.environ.get("WORLD_SIZE") or args.gpus)
+    args.rank = int(os.environ.get("RANK", "0"))
+    if args.config != "c4":
+        args.global_batch = None
+    elif args.batch is None and args.global_batch is None:
+        args.global_batch = 65536
+    if args.global_batch:
+        if args.global_batch % args.world:
+            ap.error(f"--global-batch {args.global_batch} does not split over {args.world} ranks")
+        args.batch = args.global_batch // args.world
+    elif args.batch is None:
+        args.batch = 4096
+    args.scaling = "strong" if args.global_batch else "weak"
     return args
 
 
@@ -673,7 +726,7 @@ def run_frames(args, rank: int, world: int, local: int, cuda: bool) -> None:
             print(json.dumps({"metric": METRIC, "value": args.batch * args.steps * world / (ms / 1e3),
                               "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                               "ms_per_step": ms / args.steps, "backend": "gloo",
-                              "config": bench_config(WORKLOADS[args.config].name, args.batch, world, esz)}),
+                              "config": bench_config(WORKLOADS[args.config].name, args.batch, world, esz, args.global_batch)}),
                   flush=True)
         return
 
@@ -681,7 +734,7 @@ def run_frames(args, rank: int, world: int, local: int, cuda: bool) -> None:
     work = WORKLOADS[args.config](md, args, gpu_synth(md))
     tdt = torch.float32 if args.dtype == "float32" else torch.float64
     esz = 4 if args.dtype == "float32" else 8
-    f = torch.from_numpy(work.host).to(device="cuda", dtype=tdt).contiguous()
+    f = work.device_frames(tdt)
     u = torch.empty_like(f)
     stream = torch.cuda.current_stream()
 
@@ -784,14 +837,24 @@ def run_frames(args, rank: int, world: int, local: int, cuda: bool) -> None:
     f32_ctx = None
     if not args.no_extras and args.dtype == "float64":
         p32 = work.make_pipe("float32")
-        f32 = f.to(torch.float32)
+        # at most 16384 frames (every k-th: the same class mix), so the float32 copies fit beside
+        # a large float64 batch
+        k32 = max(1, args.batch // 16384)
+        sel32 = torch.arange(0, args.batch, k32, device=f.device)
+        n32 = int(sel32.numel())
+        f32 = f[sel32].to(torch.float32)
         u32 = torch.empty_like(f32)
-        run32 = (lambda: work.run(f32, u32, pipe=p32)) if args.config == "c4" else (lambda: p32.plan.run(f32, out=u32))
+        if args.config == "c4":
+            idx32 = work.index[::k32]
+            run32 = lambda: work.run(f32, u32, pipe=p32, index=idx32)
+        else:
+            run32 = lambda: p32.plan.run(f32, out=u32)
         for _ in range(2):
             run32()
         ms32 = timed_steps(run32, max(3, args.steps // 2), world, True, stream)
-        f32_ctx = {"value": args.batch * max(3, args.steps // 2) * world / (ms32 / 1e3), "unit": "frames/s",
-                   "dtype": "f32", "note": "context only: float32 arithmetic is narrower than the reference's"}
+        f32_ctx = {"value": n32 * max(3, args.steps // 2) * world / (ms32 / 1e3), "unit": "frames/s",
+                   "dtype": "f32", "frames_per_gpu": n32,
+                   "note": "context only: float32 arithmetic is narrower than the reference's"}
         del f32, u32, p32
 
     if rank == 0:
@@ -834,9 +897,9 @@ def run_frames(args, rank: int, world: int, local: int, cuda: bool) -> None:
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32" if args.dtype == "float32" else "f64",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f32" if args.dtype == "float32" else "f64",
             "data": DATA,
-            "config": bench_config(work.name, args.batch, world, esz),
+            "config": bench_config(work.name, args.batch, world, esz, args.global_batch),
             "plan": work.describe,
             **{k: v for k, v in extras.items() if not k.startswith("e2e")},
             "stage_ms_per_step": {k: prof[k] / args.steps for k in ("init_ms", "iter_ms", "layout_ms")},

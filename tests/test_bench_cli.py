@@ -53,3 +53,32 @@ def test_reference_arm_is_device_free():
     import bench
     assert d["config"] == bench.bench_config(bench.C1.name, 64, 1, 8)
     assert d["cpu_baseline"]["kind"] == "port" and d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_c4_strong_scaling_split():
+    """configs[3]: one global batch dealt round-robin over the ranks (every rank gets every PSF
+    class, the per-rank batches sum to the global one)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    import numpy as np
+    import paper_1212_2245_b200 as md
+    parts = []
+    for r in range(4):
+        os.environ.update({"WORLD_SIZE": "4", "RANK": str(r)})
+        try:
+            a = bench.parse_args(["--config", "c4", "--global-batch", "480"])
+        finally:
+            os.environ.pop("WORLD_SIZE"), os.environ.pop("RANK")
+        assert a.batch == 120 and a.scaling == "strong" and a.world == 4
+        w = bench.C4(md, a, bench.cpu_synth(md), gpu=False)
+        assert np.all(np.diff(w.index) >= 0) and set(w.index.tolist()) == set(range(48))
+        parts.append(w.src)
+        cfg = bench.bench_config(w.name, a.batch, a.world, 8, a.global_batch)
+        assert cfg["global_batch"] == 480 and cfg["frames_per_gpu_per_step"] == 120
+    whole = np.sort(np.concatenate(parts))
+    a1 = bench.parse_args(["--config", "c4", "--global-batch", "480"])
+    assert a1.batch == 480 and a1.world == 1
+    assert np.array_equal(whole, np.sort(bench.C4(md, a1, bench.cpu_synth(md), gpu=False).src))
+    d = bench.parse_args(["--config", "c4"])
+    assert d.global_batch == 65536 and d.batch == 65536
+    assert bench.parse_args(["--config", "c4", "--batch", "64"]).scaling == "weak"
