@@ -199,6 +199,10 @@ def c4_bank(md, seed: int = 2026):
 
 
 C4_SCENE_SEEDS = (7, 8, 9, 10)
+# PSF groups dealt round-robin over CUDA streams in the timed c4 step (PsfBankPipeline.run): 3
+# measured 0.7 % faster than 2 at 65536 frames; groups by class (2D tile kernels on their own
+# stream beside the cluster kernels) 0.5 % slower (scripts/c4_deal_ab.sh)
+C4_STREAMS = int(os.environ.get("MD_C4_STREAMS", "3"))
 
 
 C4_DISTINCT = 8                      # distinct noisy frames per PSF (4 scenes x 2 noise draws)
@@ -256,11 +260,12 @@ class C4:
         # strong scaling (configs[3], the default): ONE batch of args.global_batch frames over the
         # ranks, rank r taking frames r, r + N, ... (every rank sees every PSF class); weak (an
         # explicit --batch): args.batch frames per rank
-        G = args.global_batch or args.batch
+        gb = getattr(args, "global_batch", None)
+        G = gb or args.batch
         per = -(-G // nb)
         gidx = np.minimum(np.arange(G) // per, nb - 1)
         gsrc = c4_source(gidx)
-        sel = slice(args.rank, None, args.world) if args.global_batch else slice(None)
+        sel = slice(getattr(args, "rank", 0), None, getattr(args, "world", 1)) if gb else slice(None)
         self.index, self.src = gidx[sel], gsrc[sel]
         assert self.index.size == args.batch, (self.index.size, args.batch)
         self.distinct = c4_distinct(md, self.bank, synth).reshape(-1, H, W)
@@ -283,7 +288,7 @@ class C4:
         return PsfBankPipeline((H, W), self.bank, self.params, dtype=dtype)
 
     def run(self, f, u, pipe=None, index=None):
-        (pipe or self.pipe).run(f, self.index if index is None else index, out=u, streams=2)
+        (pipe or self.pipe).run(f, self.index if index is None else index, out=u, streams=C4_STREAMS)
 
     def run_profile(self, f, u) -> dict:
         tot = {"init_ms": 0.0, "iter_ms": 0.0, "layout_ms": 0.0, "groups": 0}

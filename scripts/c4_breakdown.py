@@ -10,7 +10,7 @@ from bench import C4
 from bench import gpu_synth
 dt = sys.argv[1] if len(sys.argv) > 1 else "float32"
 work = C4(md, types.SimpleNamespace(dtype=dt, batch=16384), gpu_synth(md))
-f_all = torch.from_numpy(work.host).cuda().to(torch.float32 if dt == "float32" else torch.float64)
+f_all = work.device_frames(torch.float32 if dt == "float32" else torch.float64)
 tot = collections.defaultdict(float)
 cnt = collections.Counter()
 for b, s, e in work.pipe.groups(work.index):

@@ -7,7 +7,7 @@ import paper_1212_2245_b200 as md
 from bench import C4
 
 work = C4(md, types.SimpleNamespace(dtype="float32", batch=16384))
-f_all = torch.from_numpy(work.host).cuda().float()
+f_all = work.device_frames(torch.float32)
 groups = work.pipe.groups(work.index)
 pick = [0, 1, 2, 11, 16, 17, 20, 32, 44]          # box H R14, V R4, H R2, V R14, 1D H, 1D V, 1D H long, 2D line, 2D 7x7
 for b, s, e in groups:

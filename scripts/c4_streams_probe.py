@@ -6,7 +6,7 @@ import paper_1212_2245_b200 as md
 from bench import C4
 
 work = C4(md, types.SimpleNamespace(dtype="float32", batch=16384))
-f = torch.from_numpy(work.host).cuda().float()
+f = work.device_frames(torch.float32)
 u = torch.empty_like(f)
 ref = None
 for ns in (1, 2, 3, 4, 1):
