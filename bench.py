@@ -324,7 +324,94 @@ class C4:
         return (2 + 8 * self.params.iterations) * PX * esz
 
 
-WORKLOADS = {"c1": C1, "c4": C4}
+class Single:
+    """configs[1] / configs[2]: one large frame geometry with one 2D PSF, a batch of frames per
+    step through one DeblurPipeline (FOURIER_2D: direct taps for the line PSF, the 2D-FFT
+    convolver for the dense 31x31 one). Noise-free inputs, as SURVEY 8(d) states them."""
+
+    profile_in_loop = True
+    fused = False
+    cpu_frames_per_core = 1
+
+    def __init__(self, md, args, synth, gpu: bool = True):
+        self.md = md
+        self.params = md.DeconvParams(iterations=self.iterations)
+        self.psf = self.make_psf(md)
+        n = self.side
+        base = np.stack([synth(md.make_test_image(n, n, seed=s).values, self.psf) for s in (7, 8, 9, 10)])
+        self.base = base
+        self.src = np.arange(args.batch) % base.shape[0]
+        self.cpu_items = [("fourier2d", self.psf, base[i]) for i in range(base.shape[0])]
+        if gpu:
+            self.pipe = self.make_pipe(args.dtype)
+            self.describe = self.pipe.plan.describe
+            self.latency_plan = self.pipe.plan
+
+    def make_pipe(self, dtype, fused="auto"):
+        return self.md.DeblurPipeline((self.side, self.side), self.psf, self.params, self.md.Scenario.FOURIER_2D,
+                                      dtype=dtype)
+
+    def device_frames(self, dtype):
+        import torch
+        d = torch.from_numpy(self.base).to(device="cuda", dtype=dtype)
+        return d[torch.from_numpy(self.src).cuda()].contiguous()
+
+    def run(self, f, u):
+        self.pipe.plan.run(f, out=u)
+
+    def run_profile(self, f, u) -> dict:
+        return self.pipe.plan.run_profile(f, out=u)
+
+    def e2e_set(self, nb):
+        return self.base[self.src[:nb]], None
+
+    def run_host(self, hin, hout, ctx):
+        self.pipe.run_batch(hin, out=hout, out_dtype=hout.dtype)
+
+    @staticmethod
+    def e2e_entry(src, dst) -> str:
+        return f"DeblurPipeline.run_batch({src}) -> {dst} (md_run_host_ex, copies pipelined over 3 streams)"
+
+    def launches(self, n) -> int:
+        return self.pipe.plan.launch_count(n)
+
+    def frames_per_iter_launch(self, n):
+        return None
+
+    def iter_bytes(self, n, esz) -> float:
+        return self.passes_per_iteration * self.params.iterations * self.side ** 2 * esz * n
+
+    def frame_bytes(self, esz) -> float:
+        return (7 + self.passes_per_iteration * self.params.iterations) * self.side ** 2 * esz
+
+
+class C2(Single):
+    name = ("c2: 512x512 line PSF L=21 @30 deg (sub-pixel, 63 taps), noise-free, Wiener + 10 RRRL, direct taps "
+            "(BASELINE.json configs[1])")
+    side, iterations, batch = 512, 10, 256
+    metric = "c2: deblurred 512^2 frames/s (line PSF, Wiener + 10 RRRL); % HBM roofline"
+    passes_per_iteration = 8            # SURVEY 8(d): line direct = 7 + 10 x 8 field passes per frame
+    cpu_frames_per_core = 2
+
+    @staticmethod
+    def make_psf(md):
+        return md.Psf.line(21.0, 30.0)
+
+
+class C3(Single):
+    name = ("c3: 1024x1024 dense 31x31 PSF exp(-r^2/50) x U(0.2, 1) (seed 3), noise-free, 2D-FFT Wiener + 5 RRRL "
+            "(BASELINE.json configs[2])")
+    side, iterations, batch = 1024, 5, 64
+    metric = "c3: deblurred 1024^2 frames/s (dense 31x31 PSF, 2D-FFT Wiener + 5 RRRL); % HBM roofline"
+    passes_per_iteration = 18           # SURVEY 8(d): 2D-FFT convolver = 7 + 5 x 18 field passes per frame
+
+    @staticmethod
+    def make_psf(md):
+        yy, xx = np.mgrid[-15:16, -15:16]
+        return md.Psf.general_2d(np.exp(-(yy ** 2 + xx ** 2) / 50.0) * np.random.default_rng(3).uniform(0.2, 1.0, (31, 31)))
+
+
+WORKLOADS = {"c1": C1, "c2": C2, "c3": C3, "c4": C4}
 
 
 def bench_config(work_name: str, batch: int, world: int, esz: int, global_batch=None) -> dict:
@@ -526,8 +613,8 @@ def _cpu_worker(job):
     """Time the oracle port of the reference pipeline on a list of (kind, psf-spec, frame)."""
     from oracle import wr3l_oracle as O
     t0 = time.perf_counter()
-    for kind, spec, f in job:
-        O.pipeline(f, spec, O.OParams(), kind)
+    for kind, spec, f, iters in job:
+        O.pipeline(f, spec, O.OParams(iterations=iters), kind)
     return time.perf_counter() - t0
 
 
@@ -542,7 +629,8 @@ def oracle_spec(psf):
 
 def cpu_jobs(work, per_core: int, cores: int):
     """Per-core frame lists with the workload's class mix."""
-    items = [(k, oracle_spec(p), f) for k, p, f in work.cpu_items]
+    iters = work.params.iterations
+    items = [(k, oracle_spec(p), f, iters) for k, p, f in work.cpu_items]
     return [[items[(c * per_core + i) % len(items)] for i in range(per_core)] for c in range(cores)]
 
 
@@ -577,7 +665,7 @@ def run_reference(args, rank: int, world: int) -> None:
               "through oracle/wr3l_oracle.pipeline (NumPy float64 restatement of the reference's "
               "DeblurPipeline.run: its radix-2 FFT and cumsum box filter), one process per host core")
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
+        "impl": "reference", "metric": getattr(work, "metric", METRIC), "value": value, "unit": "frames/s", "n_gpus": world,
         "devices": "host CPU cores only (n_gpus echoes the launch's N; no device work)",
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(walls) / args.steps,
         "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
@@ -610,7 +698,8 @@ def parse_args(argv=None):
     ap.add_argument("--global-batch", type=int, default=None,
                     help="c4: frames per step over ALL ranks (strong scaling; default 65536, configs[3])")
     ap.add_argument("--e2e-batch", type=int, default=2048)
-    ap.add_argument("--cpu-frames-per-core", type=int, default=24)
+    ap.add_argument("--cpu-frames-per-core", type=int, default=None,
+                    help="CPU sample frames per host core (default: 24 for c1 / c4, 2 for c2, 1 for c3)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip latency / extra e2e / f32 context legs")
     ap.add_argument("--fused", default="auto", choices=["auto", "on", "off"])
@@ -628,7 +717,9 @@ def parse_args(argv=None):
             ap.error(f"--global-batch {args.global_batch} does not split over {args.world} ranks")
         args.batch = args.global_batch // args.world
     elif args.batch is None:
-        args.batch = 4096
+        args.batch = WORKLOADS[args.config].batch if args.config in ("c2", "c3") else 4096
+    if args.cpu_frames_per_core is None:
+        args.cpu_frames_per_core = getattr(WORKLOADS.get(args.config), "cpu_frames_per_core", 24)
     args.scaling = "strong" if args.global_batch else "weak"
     return args
 
@@ -900,7 +991,8 @@ def run_frames(args, rank: int, world: int, local: int, cuda: bool) -> None:
         if geom:
             geom["sms"] = torch.cuda.get_device_properties(local).multi_processor_count
         line = {
-            "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+            "metric": getattr(work, "metric", METRIC), "value": value, "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
             "scaling": args.scaling, "vs_baseline": None, "dtype": "f32" if args.dtype == "float32" else "f64",
             "data": DATA,

@@ -82,3 +82,20 @@ def test_c4_strong_scaling_split():
     d = bench.parse_args(["--config", "c4"])
     assert d.global_batch == 65536 and d.batch == 65536
     assert bench.parse_args(["--config", "c4", "--batch", "64"]).scaling == "weak"
+
+
+def test_c2_c3_workloads_host_side():
+    """configs[1] / configs[2] bench lines: batch defaults, the SURVEY 8(d) bytes model, CPU
+    sample sizing, and the device-free frames the reference arm uses."""
+    sys.path.insert(0, ROOT)
+    import bench
+    import paper_1212_2245_b200 as md
+    a2 = bench.parse_args(["--config", "c2"])
+    assert a2.batch == 256 and a2.cpu_frames_per_core == 2 and a2.scaling == "weak"
+    w2 = bench.C2(md, a2, bench.cpu_synth(md), gpu=False)
+    assert w2.frame_bytes(8) == 182452224 and w2.params.iterations == 10
+    assert w2.base.shape == (4, 512, 512) and w2.src.size == 256
+    a3 = bench.parse_args(["--config", "c3", "--batch", "8"])
+    assert a3.batch == 8 and a3.cpu_frames_per_core == 1
+    assert bench.C3.passes_per_iteration == 18 and (7 + 18 * 5) * 1024 ** 2 * 8 == 813694976
+    assert bench.parse_args(["--config", "c1"]).cpu_frames_per_core == 24
