@@ -262,7 +262,7 @@ cudaError_t launch_fft2_rows(const Fft2Args &a, int64_t batch, cudaStream_t st) 
         smem = ((size_t)rb * fpad_len<sizeof(cx_t<T>)>(a.W) + a.W / 2 + 1) * sizeof(cx_t<T>);
         staged = 0;
     }
-    cudaError_t e = cudaFuncSetAttribute(k_fft2_rows<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = func_smem_attr((const void *)k_fft2_rows<T>, smem);
     if (e != cudaSuccess) return e;
     // `batch` counts complex fields; with pairing the real pointers advance two frames per field
     const int64_t fr = (int64_t)a.H * a.W;
@@ -297,7 +297,7 @@ cudaError_t launch_fft2_cols(const Fft2Args &a, int64_t batch, cudaStream_t st) 
     int lcw = 0;
     while ((1 << lcw) < cw) ++lcw;
     const size_t smem = ((size_t)cw * fline_stride<sizeof(cx_t<T>)>(a.H) + a.H + 1) * sizeof(cx_t<T>);
-    cudaError_t e = cudaFuncSetAttribute(k_fft2_cols<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = func_smem_attr((const void *)k_fft2_cols<T>, smem);
     if (e != cudaSuccess) return e;
     const int64_t fr = (int64_t)a.H * a.W;
     for (int64_t b0 = 0; b0 < batch; b0 += 65535) {

@@ -83,7 +83,7 @@ cudaError_t launch_fft_lines_nat(void *z, int n, int64_t lines, const void *tw, 
     while ((1 << log2n) < n) ++log2n;
     const int G = std::max(1, std::min(16, 2048 / n));
     const size_t smem = ((size_t)G * fline_stride<sizeof(C)>(n) + n + 1) * sizeof(C);
-    cudaError_t e = cudaFuncSetAttribute(k_fft_lines_nat<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = func_smem_attr((const void *)k_fft_lines_nat<T>, smem);
     if (e != cudaSuccess) return e;
     const int64_t blocks = (lines + G - 1) / G;
     if (blocks > 0x7fffffff) return cudaErrorInvalidValue;

@@ -370,7 +370,7 @@ cudaError_t launch_wiener_lines(const WienerLinesArgs &a0, int64_t batch, cudaSt
     WienerLinesArgs a = a0;
     a.lp = wiener_lines_lp<T>(a.n);
     const size_t smem = wiener_lines_smem<T>(a.n, a.lp, a.in_vert, a.fpos != nullptr);
-    cudaError_t e = cudaFuncSetAttribute(k_wiener_lines<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = func_smem_attr((const void *)k_wiener_lines<T>, smem);
     if (e != cudaSuccess) return e;
     const int groups = (a.m + 2 * a.lp - 1) / (2 * a.lp);
     for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
@@ -404,7 +404,7 @@ cudaError_t launch_iter_lines(const IterLinesArgs &a0, bool robust, int64_t batc
     a.tl = iter_lines_tl<T>(a.n);
     const size_t smem = iter_lines_smem<T>(a.n, a.tl, a.blur.ntaps + a.adj.ntaps);
     auto kern = robust ? k_iter_lines<T, true> : k_iter_lines<T, false>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = func_smem_attr((const void *)kern, smem);
     if (e != cudaSuccess) return e;
     const int tiles = (a.m + a.tl - 1) / a.tl;
     for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
@@ -425,7 +425,7 @@ cudaError_t launch_conv_lines(const ConvLinesArgs &a0, int64_t batch, cudaStream
     a.tl = 8;
     while (a.tl > 1 && ((size_t)a.tl * padded_len<T>(a.n) + a.c.ntaps) * sizeof(T) > 96 * 1024) a.tl >>= 1;
     const size_t smem = ((size_t)a.tl * padded_len<T>(a.n) + a.c.ntaps) * sizeof(T);
-    cudaError_t e = cudaFuncSetAttribute(k_conv_lines<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = func_smem_attr((const void *)k_conv_lines<T>, smem);
     if (e != cudaSuccess) return e;
     const int tiles = (a.m + a.tl - 1) / a.tl;
     for (int64_t b0 = 0; b0 < batch; b0 += 65535) {

@@ -378,8 +378,8 @@ cudaError_t launch_stage_plane(const StagePlaneArgs &a, bool robust, int64_t bat
     const size_t sb = stage_b_smem<T>(a.adj, robust);
     auto ka = robust ? k_stage_a_plane<T, true> : k_stage_a_plane<T, false>;
     auto kb = robust ? k_stage_b_plane<T, true> : k_stage_b_plane<T, false>;
-    cudaError_t e = cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sa);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+    cudaError_t e = func_smem_attr((const void *)ka, sa);
+    if (e == cudaSuccess) e = func_smem_attr((const void *)kb, sb);
     if (e != cudaSuccess) return e;
     const int64_t fb = (int64_t)a.H * a.W * sizeof(T);
     for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
@@ -403,7 +403,7 @@ template <typename T>
 cudaError_t launch_conv_plane(const ConvPlaneArgs &a, int64_t batch, cudaStream_t st) {
     const size_t sm = a.h.nt * sizeof(PlaneTap) +
                       (size_t)(PT + a.h.ht + a.h.hb) * (PT + a.h.hl + a.h.hr + 1) * sizeof(T);
-    cudaError_t e = cudaFuncSetAttribute(k_conv_plane<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaError_t e = func_smem_attr((const void *)k_conv_plane<T>, sm);
     if (e != cudaSuccess) return e;
     const int64_t fb = (int64_t)a.H * a.W * sizeof(T);
     for (int64_t b0 = 0; b0 < batch; b0 += 65535) {

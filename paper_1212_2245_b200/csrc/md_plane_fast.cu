@@ -480,8 +480,8 @@ cudaError_t launch_plane_fast(const PlaneFastDesc &d, bool robust, int64_t batch
     if (!(c)) return cudaErrorInvalidValue
     auto ka = robust ? k_plane_a_fast<T, true> : k_plane_a_fast<T, false>;
     auto kb = robust ? k_plane_b_fast<T, true> : k_plane_b_fast<T, false>;
-    cudaError_t e = cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sa);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+    cudaError_t e = func_smem_attr((const void *)ka, sa);
+    if (e == cudaSuccess) e = func_smem_attr((const void *)kb, sb);
     if (e != cudaSuccess) return e;
     const CUtensorMap no_map{};                      // slab launches: per-element tile loads
     a.tma_a = a.tma_b = a.tma_pw = 0;
