@@ -202,6 +202,24 @@ k_fft2_cols(Fft2Args a, int lcw) {
     // be hoisted above it: z may alias as far as the compiler knows)
     constexpr int U = 4;
     const int n = cw * H, bd = blockDim.x;
+#ifndef MD_FFT2_COLS_CP_ASYNC
+#define MD_FFT2_COLS_CP_ASYNC 1
+#endif
+#if MD_FFT2_COLS_CP_ASYNC
+    // cp.async (global -> shared, no register round trip): the whole block of columns in flight at
+    // once, columns past the frame zero-filled
+    for (int idx = threadIdx.x; idx < n; idx += bd) {
+        const int y = idx >> lcw, c = idx & (cw - 1);
+        const bool ok = x0 + c < W;
+        const C *src = ok ? z + base + (int64_t)y * W + x0 + c : z;
+        const uint32_t d = (uint32_t)__cvta_generic_to_shared(&s[c * cs + fpad<sizeof(C)>(y)]);
+        if (sizeof(C) == 16)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(ok ? 16 : 0) : "memory");
+        else
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(ok ? 8 : 0) : "memory");
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+#else
     for (int i0 = threadIdx.x; i0 < n; i0 += U * bd) {
         C v[U];
 #pragma unroll
@@ -218,6 +236,7 @@ k_fft2_cols(Fft2Args a, int lcw) {
             s[c * cs + fpad<sizeof(C)>(y)] = v[k];
         }
     }
+#endif
     __syncthreads();
     if (a.log2H > 0) fft_dif_lines<true>(s, a.log2H, cw, cs, tw);
     if (a.filt) {
