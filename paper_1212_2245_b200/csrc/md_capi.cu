@@ -803,9 +803,10 @@ int64_t auto_chunk(const md_plan &P, int64_t batch) {
 }
 
 template <typename T>
-FusedLinesArgs fused_args(md_plan &P, const void *A, const void *FP, void *u) {
+FusedLinesArgs fused_args(md_plan &P, const void *A, const void *FP, void *u, bool raw_f = false) {
     FusedLinesArgs fa{};
     fa.u_in = A; fa.fpos = FP; fa.u_out = u; fa.n = P.n; fa.m = P.m; fa.iterations = P.d.iterations;
+    fa.floor_f = raw_f ? 1 : 0; fa.floor = P.d.floor;
     fa.out_vert = P.vert; fa.blur = P.lblur; fa.adj = P.ladj;
     fa.taps_blur_host = P.w.data(); fa.taps_adj_host = P.wrev.data();
     fa.alpha = P.d.alpha; fa.eps_d2 = P.d.eps_data * P.d.eps_data; fa.eps_r2 = P.d.eps_reg * P.d.eps_reg;
@@ -813,10 +814,21 @@ FusedLinesArgs fused_args(md_plan &P, const void *A, const void *FP, void *u) {
     return fa;
 }
 
+// float64 cluster kernel on horizontal lines: it floors the raw observation itself (the input is
+// already line-major), so the Wiener step writes no fpos field -- one field pass fewer per frame
+// (MD_F64_RAW_F=0: the fpos field as before, for A/B runs)
+template <typename T>
+bool lines_raw_f(const md_plan &P) {
+    static const bool on = [] { const char *v = std::getenv("MD_F64_RAW_F"); return !v || std::atoi(v) != 0; }();
+    return on && sizeof(T) == 8 && !P.vert && P.d.init == MD_INIT_WIENER &&
+           std::max(line_radius(P.lblur), line_radius(P.ladj)) <= 16;
+}
+
 // the whole RRRL loop of nb frames: one launch of the cluster kernel
 template <typename T>
-int lines_fused_launch(md_plan &P, const void *A, const void *FP, void *u, int64_t nb, cudaStream_t st) {
-    FusedLinesArgs fa = fused_args<T>(P, A, FP, u);
+int lines_fused_launch(md_plan &P, const void *A, const void *FP, void *u, int64_t nb, cudaStream_t st,
+                       bool raw_f = false) {
+    FusedLinesArgs fa = fused_args<T>(P, A, FP, u, raw_f);
     CU(launch_fused_lines<T>(fa, nb, st));
     return MD_OK;
 }
@@ -867,15 +879,16 @@ int run_lines_pipelined(md_plan &P, const void *f, void *u, int64_t batch, cudaS
     auto uout = [&](int64_t c) { return static_cast<char *>(u) + c * chunk * fe * (int64_t)sizeof(T); };
     const int64_t C = (batch + chunk - 1) / chunk;
     auto nbof = [&](int64_t c) { return std::min(chunk, batch - c * chunk); };
-    rc = lines_wiener<T>(P, fin(0), A[0], 0, FP[0], nbof(0), st, false);
+    const bool raw = lines_raw_f<T>(P);
+    rc = lines_wiener<T>(P, fin(0), A[0], 0, raw ? nullptr : FP[0], nbof(0), st, false);
     if (rc) return rc;
     prof_mark(st, PK_INIT);
     for (int64_t c = 0; c < C; ++c) {
         const int s = (int)(c & 1);
-        rc = lines_fused_launch<T>(P, A[s], FP[s], uout(c), nbof(c), st);
+        rc = lines_fused_launch<T>(P, A[s], raw ? fin(c) : FP[s], uout(c), nbof(c), st, raw);
         if (rc) return rc;
         if (c + 1 < C) {
-            rc = lines_wiener<T>(P, fin(c + 1), A[s ^ 1], 0, FP[s ^ 1], nbof(c + 1), st, true);
+            rc = lines_wiener<T>(P, fin(c + 1), A[s ^ 1], 0, raw ? nullptr : FP[s ^ 1], nbof(c + 1), st, true);
             if (rc) return rc;
         }
     }
@@ -889,8 +902,10 @@ int run_lines(md_plan &P, const void *f, void *u, int64_t nb, char *scr, cudaStr
     void *FP = scr, *A = scr + fb, *B = scr + 2 * fb;
     const int K = P.d.iterations;
     const bool wiener = P.d.init == MD_INIT_WIENER;
+    const bool raw = P.fused && lines_raw_f<T>(P);
     if (wiener) {
-        const int rc = K == 0 ? lines_wiener<T>(P, f, u, P.vert, nullptr, nb, st) : lines_wiener<T>(P, f, A, 0, FP, nb, st);
+        const int rc = K == 0 ? lines_wiener<T>(P, f, u, P.vert, nullptr, nb, st)
+                              : lines_wiener<T>(P, f, A, 0, raw ? nullptr : FP, nb, st);
         if (rc) return rc;
         prof_mark(st, PK_INIT);
         if (K == 0) return MD_OK;
@@ -905,7 +920,7 @@ int run_lines(md_plan &P, const void *f, void *u, int64_t nb, char *scr, cudaStr
         prof_mark(st, PK_INIT);
     }
     if (P.fused) {
-        const int rc = lines_fused_launch<T>(P, A, FP, u, nb, st);
+        const int rc = lines_fused_launch<T>(P, A, raw ? f : FP, u, nb, st, raw);
         if (rc) return rc;
         prof_mark(st, PK_ITER);
         return MD_OK;

@@ -25,6 +25,7 @@ template <typename T>
 cudaError_t launch_fused_lines(const FusedLinesArgs &d, int64_t batch, cudaStream_t st) {
     const int r = std::max(line_radius(d.blur), line_radius(d.adj));
     if (sizeof(T) == 8 && r <= 16) return launch_fused64(d, batch, st);
+    if (d.floor_f) return cudaErrorNotSupported;          // the raw-observation mode is float64-kernel only
     // boxes (odd, even, fractional length): O(1) sliding sum + end corrections
     if (d.blur.kind == LINE_BOX && d.adj.kind == LINE_BOX && r >= 1 && r <= 15 && d.robust) {
         const cudaError_t e = launch_fused_box<T>(d, r, batch, st);

@@ -17,6 +17,8 @@ struct FusedLinesArgs {
     LutView lut;
     int *query;            // non-null: store the resident cluster count, launch nothing
     int *query_geom;       // with query: [cluster CTAs, CTAs per SM] of that launch (optional)
+    int floor_f;           // float64 kernel: `fpos` is the raw line-major observation, floored in the
+    double floor;          // kernel (max(f, floor) exactly as the Wiener epilogue: no fpos field)
 };
 
 // radius: max(blur, adjoint) line radius (line_radius, md_lines_fast.h)

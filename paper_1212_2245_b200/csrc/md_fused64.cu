@@ -42,6 +42,7 @@ cudaError_t launch_fused64(const FusedLinesArgs &d, int64_t batch, cudaStream_t 
         fill_dense<double, RR>(a.wa, d.adj, d.taps_adj_host);
         a.alpha = d.alpha; a.eps_d2 = d.eps_d2; a.eps_r2 = d.eps_r2; a.has_d = d.has_d;
         a.lut = d.lut;
+        a.floor = d.floor; a.floor_f = d.floor_f;
         return launch_fused64_t<RR, F64_NW, F64_LPW>(d.robust ? k_fused_lines64<RR, F64_NW, F64_LPW, true, 0, false>
                                                               : k_fused_lines64<RR, F64_NW, F64_LPW, false, 0, false>,
                                                      a, d.lut.p64, batch, st, d.query_geom);

@@ -365,6 +365,11 @@ k_fused_lines64(FusedKArgs<double, R> a, const double2 *__restrict__ lut64) {
                     fv[2 * i + 1] = x.y;
                 }
             }
+            if (a.floor_f) {
+                // the raw observation: max(f, floor) as the Wiener epilogue forms it (no fpos field)
+#pragma unroll
+                for (int r = 0; r < SEG; ++r) fv[r] = fv[r] > a.floor ? fv[r] : a.floor;
+            }
             T pv[SEG], wv[SEG];
             {
                 T v[WIN];
@@ -639,6 +644,7 @@ cudaError_t launch_fused64_box_r(const FusedLinesArgs &d, int64_t batch, cudaStr
     a.cl = 0;                                    // picked at launch (pick_cluster)
     a.alpha = d.alpha; a.eps_d2 = d.eps_d2; a.eps_r2 = d.eps_r2; a.has_d = d.has_d;
     a.lut = d.lut;
+    a.floor = d.floor; a.floor_f = d.floor_f;
     a.box_wi = d.blur.wi;
     a.alpha_w = d.alpha / d.blur.wi; a.guard_w = kGuard / d.blur.wi; a.one_w = 1.0 / d.blur.wi;
     if (!box_corrections<double, RR>(d.blur, d.blur.wi, a.box_cb) || !box_corrections<double, RR>(d.adj, d.blur.wi, a.box_ca))

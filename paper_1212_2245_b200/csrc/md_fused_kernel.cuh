@@ -42,6 +42,8 @@ template <typename T, int R> struct FusedKArgs {
     T box_wi;           // box specialisation: interior weight
     T alpha_w, guard_w, one_w;   // alpha, the division guard and 1 divided by box_wi
     T box_cb[4], box_ca[4];   // weight corrections at k = -R, -R+1, R-1, R (blur, adjoint)
+    T floor;            // floor_f: fpos holds the raw observation, floored on load (float64 kernel)
+    int floor_f;
 };
 
 __device__ __forceinline__ int fu_wrap(int j, int n, int periodic) {
