@@ -264,7 +264,9 @@ k_plane_a_fast(PlaneFastArgs<T> a, const __grid_constant__ CUtensorMap tmu) {
     }
 }
 
-template <typename T, bool ROBUST>
+// GALIAS: the diffusivity is computed after the column walk, into the (p, W) tile's memory -- one
+// shared region fewer, used where that fits one more block per SM (launch_plane_fast)
+template <typename T, bool ROBUST, bool GALIAS>
 __global__ void __launch_bounds__(256)
 k_plane_b_fast(PlaneFastArgs<T> a, const __grid_constant__ CUtensorMap tmu, const __grid_constant__ CUtensorMap tmpw) {
     constexpr int PR = PlaneMap<MD_PLANE_ROWS_B>::PR, PJ = PlaneMap<MD_PLANE_ROWS_B>::PJ, PX = PlaneMap<MD_PLANE_ROWS_B>::PX;
@@ -277,8 +279,10 @@ k_plane_b_fast(PlaneFastArgs<T> a, const __grid_constant__ CUtensorMap tmu, cons
     // (FY+4) x PS: u with a 2-pixel halo, 128-byte aligned (a TMA destination)
     T *su_box = reinterpret_cast<T *>(smem_raw + ((rows * ss * sizeof(T2) + 127) & ~size_t(127)));
     T *su = su_box + pf_xoff_b<T>();                 // column 0 = x0 - 2 (TMA boxes start 16-byte aligned)
-    T *sg = su_box + (FY + 4) * PS;                  // (FY+2) x PS: diffusivity
-    uint64_t *bar = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(sg + (FY + 2) * PS) + 7) & ~uintptr_t(7));
+    // (FY+2) x PS: diffusivity -- behind the u tile, or (GALIAS) over the (p, W) tile
+    T *sg = GALIAS ? reinterpret_cast<T *>(smem_raw) : su_box + (FY + 4) * PS;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(
+        (reinterpret_cast<uintptr_t>(su_box + (GALIAS ? FY + 4 : 2 * FY + 6) * PS) + 7) & ~uintptr_t(7));
     const int64_t fsz = (int64_t)H * W;
     const int64_t fr = blockIdx.z;
     const T *u = a.u + fr * fsz;
@@ -374,7 +378,7 @@ k_plane_b_fast(PlaneFastArgs<T> a, const __grid_constant__ CUtensorMap tmu, cons
         __syncthreads();
     }
     const T eps_r2 = a.eps_r2;
-    if (a.has_d) {
+    auto diffusivity = [&]() {
         for (int i = threadIdx.x / 32; i < FY + 2; i += 8) {
             const int yy = y0 - 1 + i;
             const int gyy = gy0 + yy;
@@ -393,12 +397,23 @@ k_plane_b_fast(PlaneFastArgs<T> a, const __grid_constant__ CUtensorMap tmu, cons
             }
         }
         __syncthreads();
-    }
+    };
     const int tp = threadIdx.x / PX, cx = threadIdx.x % PX;
     const int ty0 = PR * tp;
-    if (y0 + ty0 >= H) return;
     T2 nd[PR][PJ];
-    col_taps_rows2<T, PR, PJ, PX>(sp + (ty0 + a.ha.ht) * ss + a.ha.hl + cx, ss, a.ta, nd);
+    if (GALIAS) {
+        const bool active = y0 + ty0 < H;
+        if (active) col_taps_rows2<T, PR, PJ, PX>(sp + (ty0 + a.ha.ht) * ss + a.ha.hl + cx, ss, a.ta, nd);
+        if (a.has_d) {
+            __syncthreads();                         // every warp is done with the (p, W) tile
+            diffusivity();
+        }
+        if (!active) return;
+    } else {
+        if (a.has_d) diffusivity();
+        if (y0 + ty0 >= H) return;
+        col_taps_rows2<T, PR, PJ, PX>(sp + (ty0 + a.ha.ht) * ss + a.ha.hl + cx, ss, a.ta, nd);
+    }
     const T alpha = a.alpha;
 #pragma unroll
     for (int k = 0; k < PR; ++k) {
@@ -442,9 +457,13 @@ k_plane_b_fast(PlaneFastArgs<T> a, const __grid_constant__ CUtensorMap tmu, cons
 static size_t smem_a(const PlaneHalo &hb, size_t es, int ssa) {
     return (((size_t)(FY + hb.ht + hb.hb) * ssa * es + 7) & ~size_t(7)) + 8;
 }
-static size_t smem_b(const PlaneHalo &ha, size_t es, int ssb) {
-    return (((size_t)(FY + ha.ht + ha.hb) * ssb * 2 * es + 127) & ~size_t(127)) + (size_t)(2 * FY + 6) * PS * es + 16 + 8;
+static size_t smem_b(const PlaneHalo &ha, size_t es, int ssb, bool galias = false) {
+    const size_t pw = ((size_t)(FY + ha.ht + ha.hb) * ssb * 2 * es + 127) & ~size_t(127);
+    // galias: the diffusivity over the (p, W) tile (always larger: >= 32 x 64 pairs against 34 x 72)
+    return pw + (size_t)(galias ? FY + 4 : 2 * FY + 6) * PS * es + 16 + 8;
 }
+// blocks of `smem` bytes that fit one SM (228 KB, 1 KB reserved per block)
+static int blocks_per_sm(size_t smem) { return (int)((228 * 1024) / (smem + 1024)); }
 
 bool plane_fast_supported(const PlaneHalo &hb, const PlaneHalo &ha, const std::vector<PlaneTap> &taps_blur,
                           const std::vector<PlaneTap> &taps_adj, int dtype) {
@@ -475,11 +494,18 @@ cudaError_t launch_plane_fast(const PlaneFastDesc &d, bool robust, int64_t batch
         return cudaErrorNotSupported;
     a.alpha = T(d.alpha); a.eps_d2 = T(d.eps_d2); a.eps_r2 = T(d.eps_r2); a.has_d = d.has_d;
     a.lut = d.lut;
-    const size_t sa = smem_a(d.hb, sizeof(T), a.ssa), sb = smem_b(d.ha, sizeof(T), a.ssb);
+    const size_t sa = smem_a(d.hb, sizeof(T), a.ssa);
+    size_t sb = smem_b(d.ha, sizeof(T), a.ssb);
 #define MD_CHECK_HOST(c) \
     if (!(c)) return cudaErrorInvalidValue
     auto ka = robust ? k_plane_a_fast<T, true> : k_plane_a_fast<T, false>;
-    auto kb = robust ? k_plane_b_fast<T, true> : k_plane_b_fast<T, false>;
+    // the diffusivity over the (p, W) tile only where that fits one more block per SM: the extra
+    // barrier costs 13 % on c5's 59 KB tiles (2 blocks either way), the third block wins 3.5 % on
+    // the c4 lines (scripts/plane_ab.sh)
+    const bool galias = blocks_per_sm(smem_b(d.ha, sizeof(T), a.ssb, true)) > blocks_per_sm(sb);
+    if (galias) sb = smem_b(d.ha, sizeof(T), a.ssb, true);
+    auto kb = galias ? (robust ? k_plane_b_fast<T, true, true> : k_plane_b_fast<T, false, true>)
+                     : (robust ? k_plane_b_fast<T, true, false> : k_plane_b_fast<T, false, false>);
     cudaError_t e = func_smem_attr((const void *)ka, sa);
     if (e == cudaSuccess) e = func_smem_attr((const void *)kb, sb);
     if (e != cudaSuccess) return e;
