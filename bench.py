@@ -132,7 +132,10 @@ class C1:
 
     def make_pipe(self, dtype, fused="auto"):
         fz = None if fused == "auto" else fused == "on"
-        return self.md.DeblurPipeline((H, W), self.psf, self.params, self.md.Scenario.BOX_1D, dtype=dtype, fused=fz)
+        pipe = self.md.DeblurPipeline((H, W), self.psf, self.params, self.md.Scenario.BOX_1D, dtype=dtype, fused=fz)
+        if os.environ.get("MD_C1_CHUNK"):                 # measurement knob: frames per pipelined chunk
+            pipe.plan.set_chunk(int(os.environ["MD_C1_CHUNK"]))
+        return pipe
 
     def frames_per_iter_launch(self, n) -> float:
         """Frames one launch of the iteration kernel covers: the fused kernel runs every

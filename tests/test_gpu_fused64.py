@@ -109,3 +109,25 @@ def test_fused64_matches_per_iteration_kernel(md):
     f = md.quantize(md.add_gaussian_noise(md.synth_blur(g, psf), 5.0, seed=2))
     a, b = fused.run(f).values, plain.run(f).values
     assert float(np.abs(a - b).max()) <= 1e-9
+
+
+@pytest.mark.parametrize("psf_kind", ["box15", "box21.5", "gen1d"])
+def test_fused64_raw_observation_bitwise(md, psf_kind):
+    """Horizontal lines run the cluster kernel on the raw observation (floored on load, no fpos
+    field); vertical lines keep the transposing Wiener's fpos field. Same arithmetic either way:
+    the horizontal result equals the transposed vertical one bit for bit."""
+    ax_h, ax_v = md.BlurAxis.HORIZONTAL, md.BlurAxis.VERTICAL
+    if psf_kind == "gen1d":
+        w = np.exp(-0.5 * ((np.arange(13) - 6) / 2.5) ** 2)
+        ph, pv = md.Psf.general_1d(w, ax_h), md.Psf.general_1d(w, ax_v)
+    else:
+        L = 15.0 if psf_kind == "box15" else 21.5
+        ph, pv = md.Psf.uniform_box(ax_h, L), md.Psf.uniform_box(ax_v, L)
+    g = md.make_test_image(256, 256, seed=4)
+    f = md.quantize(md.add_gaussian_noise(md.synth_blur(g, ph), 5.0, seed=6))
+    dh = md.DeblurPipeline((256, 256), ph, md.DeconvParams(), dtype="float64")
+    dv = md.DeblurPipeline((256, 256), pv, md.DeconvParams(), dtype="float64")
+    assert dh.plan.fused and dv.plan.fused
+    a = dh.run(f).values
+    b = dv.run(md.Image(np.ascontiguousarray(f.values.T))).values.T
+    assert np.array_equal(a, b)
