@@ -814,6 +814,13 @@ FusedLinesArgs fused_args(md_plan &P, const void *A, const void *FP, void *u, bo
     return fa;
 }
 
+// 2D-FFT convolver iterations: the TV divergence from k_diffusion (MD_FFT2_DPRE=0: evaluated in
+// the update pass, five diffusivities per pixel -- for A/B runs)
+inline bool fft2_dpre() {
+    static const bool on = [] { const char *v = std::getenv("MD_FFT2_DPRE"); return !v || std::atoi(v) != 0; }();
+    return on;
+}
+
 // float64 cluster kernel on horizontal lines: it floors the raw observation itself (the input is
 // already line-major), so the Wiener step writes no fpos field -- one field pass fewer per frame
 // (MD_F64_RAW_F=0: the fpos field as before, for A/B runs)
@@ -1066,6 +1073,12 @@ int run_plane(md_plan &P, const void *f, void *u, int64_t nb, char *scr, cudaStr
             a.conj_filt = 1;
             CU(launch_fft2_cols<T>(a, nb, st));                       // adjoint pair: x conj(h)
             a.epi = R_EPI_STAGE_B; a.u = cur; a.oa = dst; a.fwd_after = !last;
+            if (P.has_d && fft2_dpre()) {
+                // the TV divergence of u in one tiled pass, into dst: the update pass reads each
+                // pixel's d before it writes u' there (same thread, same position)
+                CU(launch_diffusion<T>(cur, dst, nb, P.d.height, P.d.width, P.d.eps_reg * P.d.eps_reg, st));
+                a.dpre = dst;
+            }
             CU(launch_fft2_rows<T>(a, nb, st));                       // update, fwd of u'
         } else if (P.fast_plane) {
             PlaneFastDesc s{};

@@ -118,6 +118,7 @@ k_fft2_rows(Fft2Args a, int rb, int staged) {
                     g0[k] = static_cast<const T *>(a.f)[base + i];
                 } else if (a.epi == R_EPI_STAGE_B) {
                     g0[k] = static_cast<const T *>(a.u)[base + i];
+                    if (a.dpre) g1[k] = static_cast<const T *>(a.dpre)[base + i];
                 }
             }
 #pragma unroll
@@ -158,7 +159,9 @@ k_fft2_rows(Fft2Args a, int rb, int staged) {
                     const T *u = static_cast<const T *>(a.u) + fr * fsz;
                     const int y = y0 + (i >> lw), x = i & (W - 1);
                     const T uv = g0[k];
-                    const T d = a.has_d ? tv_div_global<T>(u, H, W, y, x, eps_r2) : T(0);
+                    // the divergence from one pass over the frame (k_diffusion: each diffusivity
+                    // once, not five times per pixel) or evaluated here from global memory
+                    const T d = !a.has_d ? T(0) : (a.dpre ? g1[k] : tv_div_global<T>(u, H, W, y, x, eps_r2));
                     const T un = a.robust ? combine_px<T, true>(uv, v.x * scale, v.y * scale, d, alpha, a.has_d != 0)
                                           : combine_px<T, false>(uv, v.x * scale, T(0), d, alpha, a.has_d != 0);
                     static_cast<T *>(a.oa)[o] = un;

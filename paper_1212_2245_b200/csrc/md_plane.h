@@ -75,6 +75,7 @@ struct Fft2Args {
     void *oa, *ob;              // epilogue real outputs
     const void *f;              // observation (stage A: floored; Wiener: raw -> writes fpos to ob)
     const void *u;              // current iterate (stage B)
+    const void *dpre;           // stage B: the TV divergence precomputed per pixel (k_diffusion), or null
     double floor, alpha, eps_d2, eps_r2, scale;
     int has_d, robust;
     LutView lut;
