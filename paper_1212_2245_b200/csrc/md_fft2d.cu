@@ -12,6 +12,7 @@
 //   rows(inv, stage A: b -> W, p; pack p + iW; fwd) -> cols(x conj h) ->
 //   rows(inv, stage B: adjoint pair + TV + update; pack u'; fwd) -> cols(x h)
 #include "md_fft.cuh"
+#include <cstdlib>
 #include "md_plane.h"
 
 namespace md {
@@ -314,8 +315,12 @@ cudaError_t launch_fft2_cols(const Fft2Args &a, int64_t batch, cudaStream_t st) 
     // columns) -- 16 float64 columns (78 KB of shared memory, 2 blocks/SM) ran the 256^2
     // Wiener column pass 20 % slower than 8 (39 KB); 4 was slower again
     constexpr int kColW = 128 / (int)sizeof(cx_t<T>);
-    int cw = 4096 / a.H;
+    // 1024-high columns: 2 per block (32 KB, 4 blocks/SM) measured 1.8 % faster on the c3 iterations
+    // than 4 (64 KB); 8 and 1 slower (MD_FFT2_COLW, scripts/c3_hash_probe.py)
+    int cw = a.H >= 1024 ? 2048 / a.H : 4096 / a.H;
     cw = cw > kColW ? kColW : (cw < 1 ? 1 : cw);          // a power of two (H is)
+    static const int cw_env = [] { const char *v = std::getenv("MD_FFT2_COLW"); return v ? std::atoi(v) : 0; }();
+    if (cw_env > 0) cw = cw_env;                          // measurement knob (a power of two)
     int lcw = 0;
     while ((1 << lcw) < cw) ++lcw;
     const size_t smem = ((size_t)cw * fline_stride<sizeof(cx_t<T>)>(a.H) + a.H + 1) * sizeof(cx_t<T>);
