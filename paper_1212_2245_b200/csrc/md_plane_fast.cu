@@ -264,9 +264,11 @@ k_plane_a_fast(PlaneFastArgs<T> a, const __grid_constant__ CUtensorMap tmu) {
     }
 }
 
-// GALIAS: the diffusivity is computed after the column walk, into the (p, W) tile's memory -- one
-// shared region fewer, used where that fits one more block per SM (launch_plane_fast)
-template <typename T, bool ROBUST, bool GALIAS>
+// MODE (shared layout, picked per launch in launch_plane_fast for the most blocks per SM):
+//  0: (p, W) tile | u tile | diffusivity
+//  1: (p, W) tile, the diffusivity computed after the column walk over it | u tile
+//  2: (p, W) tile only: after the walk the u tile is loaded, and the diffusivity computed, over it
+template <typename T, bool ROBUST, int MODE>
 __global__ void __launch_bounds__(256)
 k_plane_b_fast(PlaneFastArgs<T> a, const __grid_constant__ CUtensorMap tmu, const __grid_constant__ CUtensorMap tmpw) {
     constexpr int PR = PlaneMap<MD_PLANE_ROWS_B>::PR, PJ = PlaneMap<MD_PLANE_ROWS_B>::PJ, PX = PlaneMap<MD_PLANE_ROWS_B>::PX;
@@ -276,13 +278,16 @@ k_plane_b_fast(PlaneFastArgs<T> a, const __grid_constant__ CUtensorMap tmu, cons
     const int ss = a.ssb;
     const int rows = FY + a.ha.ht + a.ha.hb;
     T2 *spw = reinterpret_cast<T2 *>(smem_raw);
+    const size_t pw_bytes = (rows * ss * sizeof(T2) + 127) & ~size_t(127);
     // (FY+4) x PS: u with a 2-pixel halo, 128-byte aligned (a TMA destination)
-    T *su_box = reinterpret_cast<T *>(smem_raw + ((rows * ss * sizeof(T2) + 127) & ~size_t(127)));
+    T *su_box = reinterpret_cast<T *>(smem_raw + (MODE == 2 ? 0 : pw_bytes));
     T *su = su_box + pf_xoff_b<T>();                 // column 0 = x0 - 2 (TMA boxes start 16-byte aligned)
-    // (FY+2) x PS: diffusivity -- behind the u tile, or (GALIAS) over the (p, W) tile
-    T *sg = GALIAS ? reinterpret_cast<T *>(smem_raw) : su_box + (FY + 4) * PS;
-    uint64_t *bar = reinterpret_cast<uint64_t *>(
-        (reinterpret_cast<uintptr_t>(su_box + (GALIAS ? FY + 4 : 2 * FY + 6) * PS) + 7) & ~uintptr_t(7));
+    // (FY+2) x PS: diffusivity
+    T *sg = MODE == 0 ? su_box + (FY + 4) * PS : (MODE == 1 ? reinterpret_cast<T *>(smem_raw) : su_box + (FY + 4) * PS);
+    unsigned char *end = MODE == 0 ? reinterpret_cast<unsigned char *>(sg + (FY + 2) * PS)
+                                   : (MODE == 1 ? reinterpret_cast<unsigned char *>(su_box + (FY + 4) * PS) : smem_raw + pw_bytes);
+    uint64_t *bar = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(end) + 7) & ~uintptr_t(7));
+    uint64_t *bar2 = bar + 1;                        // MODE 2: the late u tile
     const int64_t fsz = (int64_t)H * W;
     const int64_t fr = blockIdx.z;
     const T *u = a.u + fr * fsz;
@@ -292,7 +297,8 @@ k_plane_b_fast(PlaneFastArgs<T> a, const __grid_constant__ CUtensorMap tmu, cons
     T2 *sp = spw + xpw;                              // the (p, W) tile's column 0 (x0 - hl)
     poison_smem(smem_raw);
     MD_CHECK((smem_addr_of(spw) & 127) == 0 && (smem_addr_of(su_box) & 127) == 0 &&
-             (size_t)(reinterpret_cast<unsigned char *>(bar + 1) - smem_raw) <= dyn_smem_bytes() &&
+             (size_t)(reinterpret_cast<unsigned char *>(bar + (MODE == 2 ? 2 : 1)) - smem_raw) <= dyn_smem_bytes() &&
+             (MODE != 2 || reinterpret_cast<unsigned char *>(sg + (FY + 2) * PS) <= smem_raw + pw_bytes) &&
              ((x0 - a.ha.hl - xpw) * 2 * (int)sizeof(T)) % 16 == 0 && ((x0 - 2 - pf_xoff_b<T>()) * (int)sizeof(T)) % 16 == 0);
     // interleaved (p, W) and an interior tile: the whole pair tile as one TMA box (rows x ss
     // pairs, started on a 16-byte boundary); otherwise per element (wrap / clamp at the edges)
@@ -301,79 +307,44 @@ k_plane_b_fast(PlaneFastArgs<T> a, const __grid_constant__ CUtensorMap tmu, cons
     if (!pw_tma) {
         const T *pp = a.p + fr * fsz, *ww = a.w + fr * fsz;
         const T2 *ppw = a.pwi ? reinterpret_cast<const T2 *>(a.p) + fr * fsz : nullptr;
-#if MD_PLANE_CP_ASYNC
         // (p, W) tile by cp.async: issued here, in flight while the u tile loads below
         pf_load_async<T, T2>(sp, ss, H, W, y0, x0, a.ha, a.periodic, a.slab, a.ylo, a.yhi, pp, ROBUST ? ww : nullptr, ppw);
-#else
-        pf_load<T>(sp, ss, H, W, y0, x0, a.ha, a.periodic, a.slab, a.ylo, a.yhi, [&](int64_t o) {
-            if (ppw) return ppw[o];
-            T2 v;
-            v.x = pp[o];
-            v.y = ROBUST ? ww[o] : T(0);
-            return v;
-        });
-#endif
     }
     const int gy0 = a.gy0, Hg = a.Hg;
-    if (threadIdx.x == 0 && (a.tma_b || pw_tma)) {
+    // u with a 2-pixel halo (zero outside the frame / slab): one TMA box (whole-frame launches,
+    // the map's zero fill = the zero halo) or cp.async with zero-fill
+    auto load_u = [&](bool tma_issued) {
+        if (!a.tma_b) {
+            constexpr int UC = FX + 4;
+            const int n = (FY + 4) * UC;
+            for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
+                const int i = idx / UC, j = idx - i * UC;
+                const int yy = y0 - 2 + i, xx = x0 - 2 + j;
+                const bool ok = gy0 + yy >= 0 && gy0 + yy < Hg && (a.slab ? (yy >= a.ylo && yy < a.yhi) : (yy >= 0 && yy < H)) &&
+                                xx >= 0 && xx < W;
+                const uint32_t d = (uint32_t)__cvta_generic_to_shared(su + i * PS + j);
+                const T *src = ok ? u + (int64_t)yy * W + xx : u;
+                if (sizeof(T) == 8)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(ok ? 8 : 0) : "memory");
+                else
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(ok ? 4 : 0) : "memory");
+            }
+        }
+        (void)tma_issued;
+    };
+    if (threadIdx.x == 0 && ((MODE != 2 && a.tma_b) || pw_tma)) {
         // TMA boxes on one barrier: u (FY+4) x PS at (x0-2, y0-2), positions outside the frame
         // arriving as zeros (whole-frame launches only: a slab reads its halo rows as they are);
         // the (p, W) pairs as 2 ss elements per row
-        tma_bar_arm(bar, (uint32_t)((a.tma_b ? (FY + 4) * PS * sizeof(T) : 0) + (pw_tma ? rows * ss * sizeof(T2) : 0)));
-        if (a.tma_b) tma_load_3d(su_box, &tmu, x0 - 2 - pf_xoff_b<T>(), y0 - 2, (int)blockIdx.z, bar);
+        const bool ub = MODE != 2 && a.tma_b;
+        tma_bar_arm(bar, (uint32_t)((ub ? (FY + 4) * PS * sizeof(T) : 0) + (pw_tma ? rows * ss * sizeof(T2) : 0)));
+        if (ub) tma_load_3d(su_box, &tmu, x0 - 2 - pf_xoff_b<T>(), y0 - 2, (int)blockIdx.z, bar);
         if (pw_tma) tma_load_3d(spw, &tmpw, 2 * (x0 - a.ha.hl - xpw), y0 - a.ha.ht, (int)blockIdx.z, bar);
     }
-#if MD_PLANE_CP_ASYNC
-    if (!a.tma_b) {
-        // u with a 2-pixel halo (zero outside the frame / slab): cp.async as well (zero-fill
-        // for the outside positions), so the whole tile set is in flight before one wait
-        constexpr int UC = FX + 4;
-        const int n = (FY + 4) * UC;
-        for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
-            const int i = idx / UC, j = idx - i * UC;
-            const int yy = y0 - 2 + i, xx = x0 - 2 + j;
-            const bool ok = gy0 + yy >= 0 && gy0 + yy < Hg && (a.slab ? (yy >= a.ylo && yy < a.yhi) : (yy >= 0 && yy < H)) &&
-                            xx >= 0 && xx < W;
-            const uint32_t d = (uint32_t)__cvta_generic_to_shared(su + i * PS + j);
-            const T *src = ok ? u + (int64_t)yy * W + xx : u;
-            if (sizeof(T) == 8)
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(ok ? 8 : 0) : "memory");
-            else
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(ok ? 4 : 0) : "memory");
-        }
-    }
-#else
-    if (!a.tma_b) {
-        constexpr int U = 4, UC = FX + 4;
-        const int n = (FY + 4) * UC, bd = blockDim.x;
-        for (int i0 = threadIdx.x; i0 < n; i0 += U * bd) {
-            T v[U];
-#pragma unroll
-            for (int k = 0; k < U; ++k) {
-                const int idx = i0 + k * bd;
-                v[k] = T(0);
-                if (idx >= n) continue;
-                const int i = idx / UC, j = idx - i * UC;
-                const int yy = y0 - 2 + i, xx = x0 - 2 + j;
-                const bool rok = gy0 + yy >= 0 && gy0 + yy < Hg &&
-                                 (a.slab ? (yy >= a.ylo && yy < a.yhi) : (yy >= 0 && yy < H));
-                if (rok && xx >= 0 && xx < W) v[k] = u[(int64_t)yy * W + xx];
-            }
-#pragma unroll
-            for (int k = 0; k < U; ++k) {
-                const int idx = i0 + k * bd;
-                if (idx >= n) break;
-                const int i = idx / UC, j = idx - i * UC;
-                su[i * PS + j] = v[k];
-            }
-        }
-    }
-#endif
-#if MD_PLANE_CP_ASYNC
+    if (MODE != 2) load_u(false);
     cp_async_wait_all();
-#endif
     __syncthreads();                                 // (also: the TMA barrier is initialised)
-    if (a.tma_b || pw_tma) {
+    if ((MODE != 2 && a.tma_b) || pw_tma) {
         tma_bar_wait(bar);
         __syncthreads();
     }
@@ -401,18 +372,35 @@ k_plane_b_fast(PlaneFastArgs<T> a, const __grid_constant__ CUtensorMap tmu, cons
     const int tp = threadIdx.x / PX, cx = threadIdx.x % PX;
     const int ty0 = PR * tp;
     T2 nd[PR][PJ];
-    if (GALIAS) {
+    if (MODE == 0) {
+        if (a.has_d) diffusivity();
+        if (y0 + ty0 >= H) return;
+        col_taps_rows2<T, PR, PJ, PX>(sp + (ty0 + a.ha.ht) * ss + a.ha.hl + cx, ss, a.ta, nd);
+    } else {
         const bool active = y0 + ty0 < H;
         if (active) col_taps_rows2<T, PR, PJ, PX>(sp + (ty0 + a.ha.ht) * ss + a.ha.hl + cx, ss, a.ta, nd);
-        if (a.has_d) {
+        if (MODE == 2) {
+            // the (p, W) tile is done with: the u tile over it, then the diffusivity behind it
+            __syncthreads();
+            if (threadIdx.x == 0 && a.tma_b) {
+                // generic-proxy reads of this memory (the walk) before the async-proxy writes
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                tma_bar_arm(bar2, (uint32_t)((FY + 4) * PS * sizeof(T)));
+                tma_load_3d(su_box, &tmu, x0 - 2 - pf_xoff_b<T>(), y0 - 2, (int)blockIdx.z, bar2);
+            }
+            load_u(true);
+            cp_async_wait_all();
+            __syncthreads();
+            if (a.tma_b) {
+                tma_bar_wait(bar2);
+                __syncthreads();
+            }
+            if (a.has_d) diffusivity();
+        } else if (a.has_d) {
             __syncthreads();                         // every warp is done with the (p, W) tile
             diffusivity();
         }
         if (!active) return;
-    } else {
-        if (a.has_d) diffusivity();
-        if (y0 + ty0 >= H) return;
-        col_taps_rows2<T, PR, PJ, PX>(sp + (ty0 + a.ha.ht) * ss + a.ha.hl + cx, ss, a.ta, nd);
     }
     const T alpha = a.alpha;
 #pragma unroll
@@ -457,10 +445,12 @@ k_plane_b_fast(PlaneFastArgs<T> a, const __grid_constant__ CUtensorMap tmu, cons
 static size_t smem_a(const PlaneHalo &hb, size_t es, int ssa) {
     return (((size_t)(FY + hb.ht + hb.hb) * ssa * es + 7) & ~size_t(7)) + 8;
 }
-static size_t smem_b(const PlaneHalo &ha, size_t es, int ssb, bool galias = false) {
+static size_t smem_b(const PlaneHalo &ha, size_t es, int ssb, int mode = 0) {
     const size_t pw = ((size_t)(FY + ha.ht + ha.hb) * ssb * 2 * es + 127) & ~size_t(127);
-    // galias: the diffusivity over the (p, W) tile (always larger: >= 32 x 64 pairs against 34 x 72)
-    return pw + (size_t)(galias ? FY + 4 : 2 * FY + 6) * PS * es + 16 + 8;
+    const size_t ug = (size_t)(2 * FY + 6) * PS * es;        // u tile + diffusivity
+    if (mode == 2) return pw < ug ? 0 : pw + 16 + 16;        // both over the (p, W) tile (0: does not fit)
+    // mode 1: the diffusivity over the (p, W) tile (always larger: >= 32 x 64 pairs against 34 x 72)
+    return pw + (mode == 1 ? (size_t)(FY + 4) * PS * es : ug) + 16 + 8;
 }
 // blocks of `smem` bytes that fit one SM (228 KB, 1 KB reserved per block)
 static int blocks_per_sm(size_t smem) { return (int)((228 * 1024) / (smem + 1024)); }
@@ -499,13 +489,24 @@ cudaError_t launch_plane_fast(const PlaneFastDesc &d, bool robust, int64_t batch
 #define MD_CHECK_HOST(c) \
     if (!(c)) return cudaErrorInvalidValue
     auto ka = robust ? k_plane_a_fast<T, true> : k_plane_a_fast<T, false>;
-    // the diffusivity over the (p, W) tile only where that fits one more block per SM: the extra
-    // barrier costs 13 % on c5's 59 KB tiles (2 blocks either way), the third block wins 3.5 % on
-    // the c4 lines (scripts/plane_ab.sh)
-    const bool galias = blocks_per_sm(smem_b(d.ha, sizeof(T), a.ssb, true)) > blocks_per_sm(sb);
-    if (galias) sb = smem_b(d.ha, sizeof(T), a.ssb, true);
-    auto kb = galias ? (robust ? k_plane_b_fast<T, true, true> : k_plane_b_fast<T, false, true>)
-                     : (robust ? k_plane_b_fast<T, true, false> : k_plane_b_fast<T, false, false>);
+    // the shared layout: mode 1 where it fits one more block per SM than mode 0, mode 2 where it
+    // fits two more -- the extra barriers cost 13 % (mode 1) on c5's tiles at an equal block count,
+    // and mode 2's late u tile about what one extra block gains (c5: 3 vs 2 blocks, 1.8 % slower);
+    // the c4 line PSFs run 4 blocks per SM in mode 2 against 2 in mode 0 (2D class -9 %,
+    // scripts/plane_mode_ab.sh). MD_PLANE_B_MODE forces a mode (A/B runs).
+    int mode = 0;
+    {
+        static const int m_env = [] { const char *v = std::getenv("MD_PLANE_B_MODE"); return v ? std::atoi(v) : -1; }();
+        const int b0 = blocks_per_sm(sb);
+        const size_t s1 = smem_b(d.ha, sizeof(T), a.ssb, 1), s2 = smem_b(d.ha, sizeof(T), a.ssb, 2);
+        if (m_env >= 0) mode = (m_env == 2 && s2 == 0) ? 0 : (m_env > 2 ? 0 : m_env);
+        else if (s2 && blocks_per_sm(s2) >= b0 + 2) mode = 2;
+        else if (blocks_per_sm(s1) > b0) mode = 1;
+        if (mode) sb = mode == 2 ? s2 : s1;
+    }
+    auto kb = mode == 2 ? (robust ? k_plane_b_fast<T, true, 2> : k_plane_b_fast<T, false, 2>)
+            : mode == 1 ? (robust ? k_plane_b_fast<T, true, 1> : k_plane_b_fast<T, false, 1>)
+                        : (robust ? k_plane_b_fast<T, true, 0> : k_plane_b_fast<T, false, 0>);
     cudaError_t e = func_smem_attr((const void *)ka, sa);
     if (e == cudaSuccess) e = func_smem_attr((const void *)kb, sb);
     if (e != cudaSuccess) return e;
