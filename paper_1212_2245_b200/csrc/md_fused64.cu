@@ -49,6 +49,8 @@ cudaError_t launch_fused64(const FusedLinesArgs &d, int64_t batch, cudaStream_t 
     };
     if (r <= 4) return go(std::integral_constant<int, 4>{});
     if (r <= 8) return go(std::integral_constant<int, 8>{});
+    // radius 9-12 (e.g. a 17-tap kernel centred off the middle): 25 dense taps instead of 33
+    if (r <= 12) return go(std::integral_constant<int, 12>{});
     return go(std::integral_constant<int, 16>{});
 }
 
