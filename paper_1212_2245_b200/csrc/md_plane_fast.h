@@ -25,6 +25,25 @@ template <typename T> struct PlaneFastArgs {
     int tma_a, tma_b;   // the u tiles come by TMA (md_tma.cuh): stage A's interior tiles, all of stage B's
     int pwi;            // p and W interleaved as pairs in the p buffer (2 elements per pixel; w unused)
     int tma_pw;         // ... and stage B's interior (p, W) tiles come by TMA
+    int pw_split;       // ... stored parity-split per row (even columns, then odd: k_plane_b_adj)
+};
+
+// Stage B with two ADJACENT output columns per thread (float64): the (p, W) pair tile is stored
+// de-interleaved by column parity ([parity][row][column pair]: stage A writes the pair field
+// parity-split per row, so each half is one plain TMA box), and a lane's input column 2l + e sits
+// at l + (e >> 1) of half (e & 1) -- consecutive across lanes, conflict-free for any tap offset.
+// A merged column d walks the union of the dy-runs of tap columns d (for output 2l) and d - 1
+// (for output 2l + 1): each loaded pair feeds up to 8 outputs (4 rows x 2 columns)
+// instead of 4. Weights outside a tap column's run are zero (an FMA of +0 leaves the sum bitwise
+// unchanged), so every output still sums its taps in the column-walk order: results are the
+// same bit for bit.
+constexpr int kAdjColMax = 72;
+constexpr int kAdjWeights = 320;
+template <typename T> struct AdjTaps {
+    int ncol;
+    int hle, hh;                            // tile starts at x0 - hle (hle even >= hl); hh pairs per half row
+    int2 c[kAdjColMax];                     // .x = tile offset (half * rows * hh + lo * hh + col), .y = len | (w0 << 16)
+    typename Vec2<T>::type w[kAdjWeights];  // (weight for output 2l, weight for output 2l + 1) per step
 };
 
 struct PlaneFastDesc {
