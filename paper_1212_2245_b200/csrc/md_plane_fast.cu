@@ -541,8 +541,10 @@ __device__ __forceinline__ void adj_walk(const T2 *s, int ss, const AT &tp, T2 (
 
 // LATE: shared memory holds only the (p, W) tile; after the walk the u tile is loaded, and the
 // diffusivity computed, over it (k_plane_b_fast's mode 2)
-template <typename T, bool ROBUST, bool LATE>
-__global__ void __launch_bounds__(256)
+// B4: compiled for 4 blocks per SM (64 registers, a few spilled) -- the c4 wide line PSFs, whose
+// late layout fits 4 blocks; otherwise for 3 (at most 80 registers: 84 would leave 2)
+template <typename T, bool ROBUST, bool LATE, bool B4>
+__global__ void __launch_bounds__(256, B4 ? 4 : 3)
 k_plane_b_adj(PlaneFastArgs<T> a, const __grid_constant__ AdjTaps<T> t, const __grid_constant__ CUtensorMap tmu,
               const __grid_constant__ CUtensorMap tmpw) {
     static_assert(sizeof(T) == 8, "float64 only (the TV loads pair two columns in 16 bytes)");
@@ -848,34 +850,38 @@ cudaError_t launch_plane_fast(const PlaneFastDesc &d, bool robust, int64_t batch
     // float64: stage B with adjacent output columns over a de-interleaved (p, W) tile where its
     // merged tap columns fit (MD_PLANE_ADJ=0 at run time: the stride-32 kernel, for A/B runs)
     // float64 stage B with two ADJACENT output columns per thread (k_plane_b_adj, the (p, W) tile
-    // de-interleaved by column parity, the u tile loaded over it after the walk) where it fits
-    // more blocks per SM than the stride-32 kernel's layout (at an equal count it is slower): 34 % fewer shared wavefronts
-    // for 21 % more (zero-weight) FMAs and 80 registers (3 blocks per SM at most) -- c5 / c2 line
-    // PSF 3 blocks against 2 (iterations 41.7 -> 38.3 ms); the c4 line PSFs keep the stride-32
-    // kernel at 4 blocks (scripts/plane_adjmode_ab.sh). MD_PLANE_ADJ: -1 (default) that pick, 0
-    // off, 2 adjacent columns with separate regions, 3 with the late layout (A/B runs).
+    // de-interleaved by column parity, the u tile loaded over it after the walk) for PSFs wider
+    // than tall whose merged columns all take the unrolled walks (<= 8 steps), where it fits at
+    // least as many blocks per SM as the stride-32 kernel's layout: 34 % fewer shared wavefronts
+    // for 21 % more (zero-weight) FMAs -- c5 / c2 line PSF 3 blocks against 2 (iterations
+    // 41.7 -> 38.3 ms), the wide c4 lines 4 blocks each way (2D PSFs 0.3-0.65 us/frame faster); tall
+    // PSFs (long columns, which the stride-32 kernel's 4-row walk already shares) keep it
+    // (scripts/plane_adjmode_ab.sh). MD_PLANE_ADJ: -1 (default) that pick, 0 off, 2 adjacent
+    // columns with separate regions, 3 with the late layout (A/B runs).
     static const int adj_env = [] { const char *v = std::getenv("MD_PLANE_ADJ"); return v ? std::atoi(v) : -1; }();
     AdjTaps<T> at;
     int hle = 0, hh = 0;
     adj_geometry(d.ha, &hle, &hh);
     const size_t sb_sep = smem_b_adj(d.ha, hh, false), sb_late = smem_b_adj(d.ha, hh, true);
     const int blocks_fast = std::min(4, blocks_per_sm(sb));                      // 64 registers
-    const int blocks_adj = sb_late ? std::min(3, blocks_per_sm(sb_late)) : 0;   // 80 registers
+    const int smem_late = sb_late ? blocks_per_sm(sb_late) : 0;
+    const bool b4 = smem_late >= 4;                                             // 64 / 80 registers
+    const int blocks_adj = std::min(b4 ? 4 : 3, smem_late);
     const bool late = adj_env == 2 ? false : sb_late != 0;
-    const bool want_adj = adj_env == -1 ? (sb_late != 0 && blocks_adj > blocks_fast) : adj_env >= 2;
+    const bool wide = d.ha.hl + d.ha.hr > d.ha.ht + d.ha.hb;
+    const bool want_adj = adj_env == -1 ? (wide && sb_late != 0 && blocks_adj >= blocks_fast) : adj_env >= 2;
     const size_t sb_adj = late ? sb_late : sb_sep;
     bool use_adj = sizeof(T) == 8 && want_adj && (d.W & 1) == 0 && FX + hle + d.ha.hr <= 32 * PF_CJ &&
                    sb_adj <= 200 * 1024 && build_adj_taps<T>(*d.taps_adj, hle, hh, FY + d.ha.ht + d.ha.hb, &at);
-    if (use_adj && adj_env == -1) {
-        // only PSFs whose merged columns all take the unrolled walks (<= 8 steps): tall PSFs (long
-        // columns) keep the stride-32 kernel, whose 4-row column walk already shares their loads
+    if (use_adj && adj_env == -1)
         for (int c = 0; c < at.ncol; ++c) use_adj = use_adj && (at.c[c].y & 0xffff) <= 8;
-    }
     using KB = void (*)(PlaneFastArgs<T>, AdjTaps<T>, CUtensorMap, CUtensorMap);
     KB kb_adj = nullptr;
-    if constexpr (sizeof(T) == 8)
-        kb_adj = late ? (robust ? k_plane_b_adj<T, true, true> : k_plane_b_adj<T, false, true>)
-                      : (robust ? k_plane_b_adj<T, true, false> : k_plane_b_adj<T, false, false>);
+    if constexpr (sizeof(T) == 8) {
+        if (!late) kb_adj = robust ? k_plane_b_adj<T, true, false, false> : k_plane_b_adj<T, false, false, false>;
+        else if (b4) kb_adj = robust ? k_plane_b_adj<T, true, true, true> : k_plane_b_adj<T, false, true, true>;
+        else kb_adj = robust ? k_plane_b_adj<T, true, true, false> : k_plane_b_adj<T, false, true, false>;
+    }
     if (use_adj) {
         e = func_smem_attr((const void *)kb_adj, sb_adj);
         if (e != cudaSuccess) return e;
