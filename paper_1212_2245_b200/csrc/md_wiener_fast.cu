@@ -144,7 +144,25 @@ k_wiener_lines_reg(WienerLinesArgs a) {
             if (v1) fpos[(int64_t)l1 * N + j] = v[j2].y > floor ? v[j2].y : floor;
         }
     }
-    __syncthreads();                            // twiddle table ready
+    constexpr int NP = N + 1;
+    const int lbase = 2 * blockIdx.x * PB;
+    if (fpos && a.in_vert) {
+        // vertical input: fpos line-major from the loaded registers, staged through the (still
+        // free) transpose buffer so that consecutive threads store consecutive samples of a line
+        T *st = reinterpret_cast<T *>(tr);
+#pragma unroll
+        for (int j2 = 0; j2 < S; ++j2) {
+            const int j = q + S * j2;
+            st[(2 * p) * NP + j] = v[j2].x > floor ? v[j2].x : floor;
+            st[(2 * p + 1) * NP + j] = v[j2].y > floor ? v[j2].y : floor;
+        }
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < 2 * PB * N; idx += blockDim.x) {
+            const int li = idx / N, j = idx - li * N;
+            if (lbase + li < m) fpos[(int64_t)(lbase + li) * N + j] = st[li * NP + j];
+        }
+    }
+    __syncthreads();                            // twiddle table ready (and the staging read)
     // ---- forward: DFT over j2 (X[k2] lands at v[rev(k2)]), twiddle W_n^{j1 k2}, transpose
     dif_reg<T, S>(v);
 #pragma unroll
@@ -194,7 +212,6 @@ k_wiener_lines_reg(WienerLinesArgs a) {
     // that consecutive threads write consecutive samples of a line. Staged lines are NP = N + 1
     // apart: the column-order writes (consecutive threads = consecutive lines) then hit distinct
     // banks instead of one (a stride of N words is a multiple of 32)
-    constexpr int NP = N + 1;
     __syncthreads();
     T *st = reinterpret_cast<T *>(tr);          // 2 PB lines x NP reals (fits: PB (S TS + 1) complex)
 #pragma unroll
@@ -206,23 +223,9 @@ k_wiener_lines_reg(WienerLinesArgs a) {
         st[(2 * p + 1) * NP + j] = y1;
     }
     __syncthreads();
-    const int lbase = 2 * blockIdx.x * PB;
     for (int idx = threadIdx.x; idx < 2 * PB * N; idx += blockDim.x) {
         const int li = idx / N, j = idx - li * N;
         if (lbase + li < m) out[(int64_t)(lbase + li) * N + j] = st[li * NP + j];
-    }
-    if (fpos) {
-        __syncthreads();
-        for (int idx = threadIdx.x; idx < 2 * PB * N; idx += blockDim.x) {
-            const int j = idx / (2 * PB), li = idx - j * (2 * PB);
-            if (lbase + li < m) st[li * NP + j] = in[(int64_t)j * m + lbase + li];
-        }
-        __syncthreads();
-        for (int idx = threadIdx.x; idx < 2 * PB * N; idx += blockDim.x) {
-            const int li = idx / N, j = idx - li * N;
-            const T x = st[li * NP + j];
-            if (lbase + li < m) fpos[(int64_t)(lbase + li) * N + j] = x > floor ? x : floor;
-        }
     }
 }
 
