@@ -169,6 +169,9 @@ __device__ __forceinline__ void lane_window(const double (&x)[SEG], double (&w)[
 // MD_F64_SKIP_SHADOW=1: a warp whose last line slot lies past RL (ragged split: 28-29 lines on
 // 16 warps x 2 slots in 9-CTA clusters) skips that slot's arithmetic instead of recomputing line
 // RL - 1 (the branch is warp-uniform, so the shuffles inside stay full-warp)
+#ifndef MD_F64_GROT
+#define MD_F64_GROT g_rot           // measurement knob: (NW - 2) restores the fixed rotation
+#endif
 #ifndef MD_F64_SKIP_SHADOW
 #define MD_F64_SKIP_SHADOW 1
 #endif
@@ -313,9 +316,15 @@ k_fused_lines64(FusedKArgs<double, R> a, const double2 *__restrict__ lut64) {
     };
     // wait for the neighbours' lines of parity `par` (phase `use` of that barrier), re-arm it,
     // then the diffusivity of the halo-dependent lines
+    // interior diffusivity lines 1 .. RL-2 dealt so that warps 0-3, which take the four
+    // halo-dependent lines after the neighbours' wait, are among the warps with one interior line:
+    // NW - min(4, ones) with `ones` warps holding a single interior line (RL = 28 / 29 in 9-CTA
+    // clusters: 6 / 5 such warps; RL = 32: 2 -- the former fixed NW - 2)
+    const int g_ones = 2 * NW - (RL - 2);
+    const int g_rot = NW - (g_ones < 4 ? (g_ones > 0 ? g_ones : 0) : 4);
     auto publish_and_g = [&](int par, int use) {
         __syncthreads();
-        g_lines(1, RL - 2, par, (warp + NW - 2) % NW);
+        g_lines(1, RL - 2, par, (warp + MD_F64_GROT) % NW);
         if (warp < 4) {
             mb_wait(smem_addr(&mbar[par]), (uint32_t)(use & 1));
             if (threadIdx.x == 0) mb_arm(smem_addr(&mbar[par]), expect);
