@@ -374,11 +374,6 @@ k_fused_lines64(FusedKArgs<double, R> a, const double2 *__restrict__ lut64) {
                     fv[2 * i + 1] = x.y;
                 }
             }
-            if (a.floor_f) {
-                // the raw observation: max(f, floor) as the Wiener epilogue forms it (no fpos field)
-#pragma unroll
-                for (int r = 0; r < SEG; ++r) fv[r] = fv[r] > a.floor ? fv[r] : a.floor;
-            }
             T pv[SEG], wv[SEG];
             {
                 T v[WIN];
@@ -388,6 +383,12 @@ k_fused_lines64(FusedKArgs<double, R> a, const double2 *__restrict__ lut64) {
                 conv_window<T, R, BOXR, BOXC>(v, a.wb, a.box_wi, a.box_cb, bl);
 #pragma unroll
                 for (int r = 0; r < SEG; ++r) bl[r] = MD_F64_MAX(bl[r], T(kGuard));   // b
+                if (a.floor_f) {
+                    // the raw observation: max(f, floor) as the Wiener epilogue forms it (no fpos
+                    // field) -- here, after the blur, so the loads' latency hides behind it
+#pragma unroll
+                    for (int r = 0; r < SEG; ++r) fv[r] = fv[r] > a.floor ? fv[r] : a.floor;
+                }
                 if (ROBUST) {
                     // r1(b / fpos) for the lane's 8 pixels: all 8 table pairs requested before any
                     // is used (no branch between them), the rare direct-log branch (x < 1/2) taken
